@@ -1,0 +1,7 @@
+"""B200-native executor for batched execution of re-aligned DNN fragment groups.
+
+Drop-in for the fragment-execution step of fragserve (the reference for arXiv 2312.10636):
+plans come in through the reference's plan types / plan JSON, per-request outputs come out.
+All compute runs in libgx (`_gx.so`, hand-written sm_100a CUDA); there is no CPU fallback.
+"""
+__version__ = "0.1.0"

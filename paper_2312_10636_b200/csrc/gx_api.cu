@@ -1,0 +1,275 @@
+// libgx C ABI: contexts, unit chains (models), stage instances, and the debug op entry.
+// See include/graft_exec.h for the mapping onto the reference's interfaces.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "gx_internal.h"
+#include "gx_ptx.cuh"
+#include "gx_runtime.h"
+
+namespace gx {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  g_last_error = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+  return GX_ECUDA;
+}
+
+// ---------------------------------------------------------------- tensor maps
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled_t encode_fn() {
+  static PFN_encodeTiled_t fn = nullptr;
+  if (fn == nullptr) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled_t>(p);
+  }
+  return fn;
+}
+
+bool encode_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                         uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer) {
+  PFN_encodeTiled_t fn = encode_fn();
+  if (fn == nullptr) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_stride_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// ---------------------------------------------------------------- op planning
+int elem_size(int dtype) { return dtype == GX_F32 ? 4 : 2; }
+int64_t tensor_elems(const gx_tensor& t) { return static_cast<int64_t>(t.H) * t.W * t.C; }
+
+static int pick_bn(int Cout, int m_tiles, int sm_budget) {
+  int bn;
+  if (Cout <= 256) {
+    bn = Cout;
+  } else {
+    bn = 256;
+    // prefer a tile width that divides Cout (Inception 320/384/448 -> 160/192/224)
+    for (int cand = 256; cand >= 64; cand -= 16)
+      if (Cout % cand == 0) {
+        bn = cand;
+        break;
+      }
+  }
+  while (m_tiles * ((Cout + bn - 1) / bn) < sm_budget && bn > 64 && (bn / 2) % 16 == 0) bn /= 2;
+  return bn;
+}
+
+static uint32_t tmem_cols_for(int bn) {
+  uint32_t need = 2u * static_cast<uint32_t>(bn);
+  uint32_t c = 32;
+  while (c < need) c <<= 1;
+  return c;
+}
+
+int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint8_t* wbase, int k, int sm_budget,
+              ConvLaunch* out) {
+  const gx_tensor& ti = T[op.in];
+  const gx_tensor& to = T[op.out];
+  const int R = op.kind == GX_OP_LINEAR ? 1 : op.R;
+  const int S = op.kind == GX_OP_LINEAR ? 1 : op.S;
+  if (ti.dtype != GX_BF16) return fail(GX_EINVAL, "conv input must be bf16");
+  if ((op.Cin & 7) || (ti.C & 7) || op.Cin > ti.C) return fail(GX_EINVAL, "conv Cin must be a multiple of 8");
+  if (op.Cout & 15) return fail(GX_EINVAL, "conv Cout must be a multiple of 16");
+  if ((to.C & 7) || (op.out_coff & 7)) return fail(GX_EINVAL, "conv output pitch/offset must be multiples of 8");
+  ConvArgs& a = out->args;
+  memset(&a, 0, sizeof(a));
+  a.x = static_cast<const __nv_bfloat16*>(ptrs[op.in]);
+  a.N = k;
+  a.H = ti.H;
+  a.W = ti.W;
+  a.x_ld = ti.C;
+  a.Cin = op.Cin;
+  a.Ho = to.H;
+  a.Wo = to.W;
+  a.R = R;
+  a.S = S;
+  a.sh = op.kind == GX_OP_LINEAR ? 1 : op.sh;
+  a.sw = op.kind == GX_OP_LINEAR ? 1 : op.sw;
+  a.ph = op.kind == GX_OP_LINEAR ? 0 : op.ph;
+  a.pw = op.kind == GX_OP_LINEAR ? 0 : op.pw;
+  a.K = R * S * op.Cin;
+  a.num_kb = (a.K + kBK - 1) / kBK;
+  a.M = k * a.Ho * a.Wo;
+  a.Cout = op.Cout;
+  a.m_tiles = (a.M + kBM - 1) / kBM;
+  a.BN = pick_bn(op.Cout, a.m_tiles, sm_budget);
+  a.n_tiles = (a.Cout + a.BN - 1) / a.BN;
+  a.num_tiles = a.m_tiles * a.n_tiles;
+  a.bias = reinterpret_cast<const float*>(wbase + op.b_off);
+  a.res = op.in2 >= 0 ? static_cast<const __nv_bfloat16*>(ptrs[op.in2]) : nullptr;
+  a.res_ld = op.in2 >= 0 ? T[op.in2].C : 0;
+  a.y = ptrs[op.out];
+  a.y_ld = to.C;
+  a.y_coff = op.out_coff;
+  a.y_f32 = to.dtype == GX_F32;
+  a.act = op.act;
+  a.idesc = umma_idesc_bf16(kBM, a.BN);
+  a.stages = conv_pick_stages(a.BN, a.num_kb);
+  a.tmem_cols = tmem_cols_for(a.BN);
+  if (a.res && (T[op.in2].dtype != GX_BF16 || (a.res_ld & 7))) return fail(GX_EINVAL, "bad residual tensor");
+  const int kpad = a.num_kb * kBK;
+  if (!encode_tmap_2d_bf16(&out->wmap, wbase + op.w_off, kpad, op.Cout, static_cast<uint64_t>(kpad) * 2, kBK, a.BN))
+    return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for conv weights");
+  out->grid = std::min(a.num_tiles, std::max(1, sm_budget));
+  return GX_OK;
+}
+
+int launch_op(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint8_t* wbase, int k, int sm_budget,
+              cudaStream_t s, bool pdl, const ConvLaunch* pre, int* kernels) {
+  const int bw_grid = std::max(1, sm_budget) * 8;
+  switch (op.kind) {
+    case GX_OP_CONV:
+    case GX_OP_LINEAR: {
+      ConvLaunch cl;
+      if (pre == nullptr) {
+        int rc = plan_conv(op, T, ptrs, wbase, k, sm_budget, &cl);
+        if (rc != GX_OK) return rc;
+        pre = &cl;
+      }
+      GX_CUDA(launch_conv(pre->wmap, pre->args, pre->grid, s, pdl));
+      break;
+    }
+    case GX_OP_MAXPOOL:
+    case GX_OP_AVGPOOL: {
+      const gx_tensor& ti = T[op.in];
+      const gx_tensor& to = T[op.out];
+      GX_CUDA(launch_pool(op.kind == GX_OP_MAXPOOL ? 0 : 1, static_cast<const __nv_bfloat16*>(ptrs[op.in]), k, ti.H,
+                          ti.W, ti.C, ti.C, static_cast<__nv_bfloat16*>(ptrs[op.out]), to.H, to.W, to.C, op.out_coff,
+                          op.R, op.S, op.sh, op.sw, op.ph, op.pw, op.flags & 1, bw_grid, s));
+      break;
+    }
+    case GX_OP_GAP: {
+      const gx_tensor& ti = T[op.in];
+      GX_CUDA(launch_gap(static_cast<const __nv_bfloat16*>(ptrs[op.in]), k, ti.H * ti.W, ti.C,
+                         static_cast<__nv_bfloat16*>(ptrs[op.out]), bw_grid, s));
+      break;
+    }
+    case GX_OP_FC: {
+      const gx_tensor& ti = T[op.in];
+      const gx_tensor& to = T[op.out];
+      const int K = static_cast<int>(tensor_elems(ti));
+      if (op.Cin != K) return fail(GX_EINVAL, "FC Cin must equal the flattened input size");
+      GX_CUDA(launch_fc(static_cast<const __nv_bfloat16*>(ptrs[op.in]), k, K,
+                        reinterpret_cast<const __nv_bfloat16*>(wbase + op.w_off),
+                        op.b_off >= 0 ? reinterpret_cast<const float*>(wbase + op.b_off) : nullptr, ptrs[op.out],
+                        op.Cout, to.dtype == GX_F32, op.act, bw_grid, s));
+      break;
+    }
+    case GX_OP_COPY: {
+      const gx_tensor& ti = T[op.in];
+      const gx_tensor& to = T[op.out];
+      GX_CUDA(launch_copy_channels(static_cast<const __nv_bfloat16*>(ptrs[op.in]),
+                                   static_cast<int64_t>(k) * ti.H * ti.W, op.Cin, ti.C, op.ph,
+                                   static_cast<__nv_bfloat16*>(ptrs[op.out]), to.C, op.out_coff, bw_grid, s));
+      break;
+    }
+    default:
+      return fail(GX_EINVAL, "unsupported op kind " + std::to_string(op.kind));
+  }
+  if (kernels) ++*kernels;
+  return GX_OK;
+}
+
+}  // namespace gx
+
+using namespace gx;
+
+// ==================================================================== C ABI
+extern "C" {
+
+int gx_abi_version(void) { return GX_ABI_VERSION; }
+
+int gx_last_error(char* buf, size_t n) {
+  if (buf && n) {
+    std::strncpy(buf, g_last_error.c_str(), n - 1);
+    buf[n - 1] = 0;
+  }
+  return static_cast<int>(g_last_error.size());
+}
+
+int gx_init(int device, gx_ctx** out) {
+  if (!out) return fail(GX_EINVAL, "null out");
+  GX_CUDA(cudaSetDevice(device));
+  int sms = 0;
+  GX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  int major = 0, minor = 0;
+  GX_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+  GX_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
+  if (major != 10 || minor != 0)
+    return fail(GX_EINFEASIBLE, "libgx is built for sm_100a (B200); device is sm_" + std::to_string(major) +
+                                    std::to_string(minor));
+  if (encode_fn() == nullptr) return fail(GX_ECUDA, "driver entry point cuTensorMapEncodeTiled unavailable");
+  gx_ctx* c = new gx_ctx();
+  c->device = device;
+  c->sm_count = sms;
+  *out = c;
+  return GX_OK;
+}
+
+int gx_destroy(gx_ctx* ctx) {
+  delete ctx;
+  return GX_OK;
+}
+
+int gx_sm_count(gx_ctx* ctx, int* out) {
+  if (!ctx || !out) return fail(GX_EINVAL, "null arg");
+  *out = ctx->sm_count;
+  return GX_OK;
+}
+
+int gx_run_op(gx_ctx* ctx, const gx_op* op, const gx_tensor* tensors, void* const* tensor_ptrs, const void* weights,
+              int k, int sm_budget, void* stream) {
+  if (!ctx || !op || !tensors || !tensor_ptrs) return fail(GX_EINVAL, "null arg");
+  if (k < 1) return fail(GX_EINVAL, "batch must be >= 1");
+  GX_CUDA(cudaSetDevice(ctx->device));
+  if (sm_budget <= 0 || sm_budget > ctx->sm_count) sm_budget = ctx->sm_count;
+  return launch_op(*op, tensors, tensor_ptrs, static_cast<const uint8_t*>(weights), k, sm_budget,
+                   static_cast<cudaStream_t>(stream), false, nullptr, nullptr);
+}
+
+int gx_gather(gx_ctx* ctx, int k, const void* const* src, const int32_t* src_dtype, int64_t pixels, int32_t c_src,
+              int32_t c_dst, void* dst, int sm_budget, void* stream) {
+  if (!ctx) return fail(GX_EINVAL, "null ctx");
+  if (k < 1 || k > 64) return fail(GX_EINVAL, "gather batch must be in 1..64");
+  if (sm_budget <= 0 || sm_budget > ctx->sm_count) sm_budget = ctx->sm_count;
+  GX_CUDA(launch_gather(k, src, src_dtype, pixels, c_src, c_dst, static_cast<__nv_bfloat16*>(dst), sm_budget * 8,
+                        static_cast<cudaStream_t>(stream)));
+  return GX_OK;
+}
+
+int gx_scatter(gx_ctx* ctx, int k, const void* src, int32_t src_dtype, int64_t row_elems, void* const* dst,
+               int32_t dst_dtype, int sm_budget, void* stream) {
+  if (!ctx) return fail(GX_EINVAL, "null ctx");
+  if (k < 1 || k > 64) return fail(GX_EINVAL, "scatter batch must be in 1..64");
+  if (sm_budget <= 0 || sm_budget > ctx->sm_count) sm_budget = ctx->sm_count;
+  GX_CUDA(launch_scatter(k, src, src_dtype, row_elems, dst, dst_dtype, sm_budget * 8,
+                         static_cast<cudaStream_t>(stream)));
+  return GX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,77 @@
+// Internal declarations shared by the libgx translation units.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "graft_exec.h"
+
+namespace gx {
+
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define GX_CUDA(call)                                   \
+  do {                                                  \
+    cudaError_t _e = (call);                            \
+    if (_e != cudaSuccess) return ::gx::cuda_fail(_e, #call); \
+  } while (0)
+
+// Driver entry point for cuTensorMapEncodeTiled (resolved once through the runtime).
+bool encode_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                         uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);
+
+// ------------------------------------------------------------------ implicit-GEMM conv (K2)
+// GEMM view: M = k*Ho*Wo output pixels, N = Cout, K = R*S*Cin (ordered r, s, cin).
+struct ConvArgs {
+  const __nv_bfloat16* x;  // input NHWC, pixel pitch x_ld elements
+  int N, H, W, x_ld, Cin;
+  int Ho, Wo, R, S, sh, sw, ph, pw;
+  int K, num_kb;  // num_kb = ceil(K / 64)
+  int M, Cout, BN, m_tiles, n_tiles, num_tiles;
+  const float* bias;
+  const __nv_bfloat16* res;  // residual [M][res_ld] or null
+  int res_ld;
+  void* y;  // output [M][y_ld] at column offset y_coff (bf16, or fp32 if y_f32)
+  int y_ld, y_coff, y_f32;
+  int act;
+  uint32_t idesc;
+  int stages;
+  uint32_t tmem_cols;
+};
+constexpr int kConvThreads = 320;  // 4 A-producer warps, TMA warp, MMA warp, 4 epilogue warps
+constexpr int kBM = 128;
+constexpr int kBK = 64;
+size_t conv_smem_bytes(int BN, int stages, int num_kb);
+int conv_pick_stages(int BN, int num_kb);
+cudaError_t launch_conv(const CUtensorMap& wmap, const ConvArgs& a, int grid, cudaStream_t s, bool pdl);
+
+// ------------------------------------------------------------------ bandwidth-bound kernels
+cudaError_t launch_gather(int k, const void* const* src, const int32_t* src_dtype, int64_t pixels,
+                          int c_src, int c_dst, __nv_bfloat16* dst, int grid, cudaStream_t s);
+cudaError_t launch_scatter(int k, const void* src, int src_dtype, int64_t row_elems, void* const* dst,
+                           int dst_dtype, int grid, cudaStream_t s);
+cudaError_t launch_pool(int mode, const __nv_bfloat16* x, int N, int H, int W, int C, int x_ld,
+                        __nv_bfloat16* y, int Ho, int Wo, int y_ld, int y_coff, int R, int S, int sh,
+                        int sw, int ph, int pw, int count_include_pad, int grid, cudaStream_t s);
+cudaError_t launch_gap(const __nv_bfloat16* x, int N, int HW, int C, __nv_bfloat16* y, int grid,
+                       cudaStream_t s);
+cudaError_t launch_fc(const __nv_bfloat16* x, int N, int K, const __nv_bfloat16* w, const float* b,
+                      void* y, int Nout, int y_f32, int act, int grid, cudaStream_t s);
+cudaError_t launch_copy_channels(const __nv_bfloat16* x, int64_t pixels, int C, int x_ld, int x_coff,
+                                 __nv_bfloat16* y, int y_ld, int y_coff, int grid, cudaStream_t s);
+cudaError_t launch_flatten_nchw(const __nv_bfloat16* x, int N, int HW, int C, __nv_bfloat16* y, int grid,
+                                cudaStream_t s);
+cudaError_t launch_layernorm(const __nv_bfloat16* x, const __nv_bfloat16* res, int rows, int C,
+                             const float* gamma, const float* beta, float eps, __nv_bfloat16* y, int grid,
+                             cudaStream_t s);
+cudaError_t launch_attention(const __nv_bfloat16* qkv, int N, int S, int heads, int dh,
+                             __nv_bfloat16* out, int grid, cudaStream_t s);
+cudaError_t launch_embed(const void* ids, int N, int S, int C, const __nv_bfloat16* word,
+                         const __nv_bfloat16* pos, const __nv_bfloat16* type, __nv_bfloat16* y,
+                         int grid, cudaStream_t s);
+
+}  // namespace gx

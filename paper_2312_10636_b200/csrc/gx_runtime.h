@@ -1,0 +1,62 @@
+// Runtime objects behind the opaque C handles.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "gx_internal.h"
+
+struct gx_ctx {
+  int device = 0;
+  int sm_count = 0;
+};
+
+namespace gx {
+struct ConvLaunch {
+  CUtensorMap wmap;
+  ConvArgs args;
+  int grid;
+};
+
+int elem_size(int dtype);
+int64_t tensor_elems(const gx_tensor& t);
+int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint8_t* wbase, int k, int sm_budget,
+              ConvLaunch* out);
+int launch_op(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint8_t* wbase, int k, int sm_budget,
+              cudaStream_t s, bool pdl, const ConvLaunch* pre, int* kernels);
+}  // namespace gx
+
+struct gx_model {
+  gx_ctx* ctx = nullptr;
+  std::string id;
+  std::vector<gx_tensor> tensors;
+  std::vector<gx_op> ops;
+  std::vector<int32_t> unit_first_op;  // n_units + 1
+  std::vector<int32_t> boundary;       // n_units + 1
+  void* wdev = nullptr;
+  size_t wbytes = 0;
+  int n_units() const { return static_cast<int>(boundary.size()) - 1; }
+};
+
+struct gx_stage {
+  gx_model* m = nullptr;
+  int start = 0, end = 0, max_batch = 0, sm_budget = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::vector<int> ops;         // op indices of the span, in order
+  std::vector<void*> tptr;      // device pointer per tensor id (workspace), nullptr if unused
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  int in_tid = -1, out_tid = -1;
+  struct PerK {
+    cudaGraphExec_t exec = nullptr;
+    int kernels = 0;
+  };
+  std::map<int, PerK> graphs;
+  // profiling scratch
+  void* prof_src = nullptr;
+  void* prof_dst = nullptr;
+};

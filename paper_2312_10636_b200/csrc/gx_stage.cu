@@ -1,0 +1,321 @@
+// Unit chains (gx_model) and stage instances (gx_stage): workspace planning, CUDA-graph capture of
+// a span per batch size k, and the gather -> span -> scatter dispatch that replaces
+// _StageRT.latency_for (simulator.py:95-100).
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "gx_internal.h"
+#include "gx_runtime.h"
+
+using namespace gx;
+
+namespace {
+
+size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// Greedy liveness-based workspace assignment for the tensors a span touches.
+int plan_workspace(gx_stage* st) {
+  gx_model* m = st->m;
+  const int nt = static_cast<int>(m->tensors.size());
+  std::vector<int> first(nt, INT32_MAX), last(nt, -2);
+  auto use = [&](int t, int pos) {
+    if (t < 0) return;
+    if (t >= nt) return;
+    last[t] = std::max(last[t], pos);
+  };
+  auto def = [&](int t, int pos) {
+    if (t < 0 || t >= nt) return;
+    first[t] = std::min(first[t], pos);
+    last[t] = std::max(last[t], pos);
+  };
+  def(st->in_tid, -1);
+  const int n = static_cast<int>(st->ops.size());
+  for (int i = 0; i < n; ++i) {
+    const gx_op& op = m->ops[st->ops[i]];
+    use(op.in, i);
+    use(op.in2, i);
+    def(op.out, i);
+  }
+  last[st->out_tid] = n;  // the span output lives until the scatter
+  for (int i = 0; i < n; ++i) {
+    const gx_op& op = m->ops[st->ops[i]];
+    if ((op.in >= 0 && first[op.in] == INT32_MAX) || (op.in2 >= 0 && first[op.in2] == INT32_MAX))
+      return fail(GX_EINVAL, "span reads a tensor no earlier op of the span produces");
+  }
+  struct Buf {
+    size_t bytes;
+    int free_at;  // position after which the buffer is free again
+  };
+  std::vector<Buf> bufs;
+  std::vector<int> assign(nt, -1);
+  for (int pos = -1; pos < n; ++pos) {
+    for (int t = 0; t < nt; ++t) {
+      if (first[t] != pos || assign[t] >= 0) continue;
+      const size_t need =
+          round_up(static_cast<size_t>(st->max_batch) * tensor_elems(m->tensors[t]) * elem_size(m->tensors[t].dtype), 256);
+      int best = -1;
+      for (int b = 0; b < static_cast<int>(bufs.size()); ++b)
+        if (bufs[b].free_at < pos && bufs[b].bytes >= need && (best < 0 || bufs[b].bytes < bufs[best].bytes)) best = b;
+      if (best < 0) {
+        bufs.push_back({need, INT32_MAX});
+        best = static_cast<int>(bufs.size()) - 1;
+      }
+      bufs[best].free_at = last[t];
+      assign[t] = best;
+    }
+  }
+  std::vector<size_t> off(bufs.size());
+  size_t total = 0;
+  for (size_t b = 0; b < bufs.size(); ++b) {
+    off[b] = total;
+    total += bufs[b].bytes;
+  }
+  GX_CUDA(cudaMalloc(&st->ws, std::max<size_t>(total, 256)));
+  st->ws_bytes = total;
+  st->tptr.assign(nt, nullptr);
+  for (int t = 0; t < nt; ++t)
+    if (assign[t] >= 0) st->tptr[t] = static_cast<uint8_t*>(st->ws) + off[assign[t]];
+  return GX_OK;
+}
+
+int capture_span(gx_stage* st, int k, gx_stage::PerK* out) {
+  gx_model* m = st->m;
+  const uint8_t* wbase = static_cast<const uint8_t*>(m->wdev);
+  // Plan every conv first so capture only records launches.
+  std::vector<ConvLaunch> plans(st->ops.size());
+  for (size_t i = 0; i < st->ops.size(); ++i) {
+    const gx_op& op = m->ops[st->ops[i]];
+    if (op.kind == GX_OP_CONV || op.kind == GX_OP_LINEAR) {
+      int rc = plan_conv(op, m->tensors.data(), st->tptr.data(), wbase, k, st->sm_budget, &plans[i]);
+      if (rc != GX_OK) return rc;
+    }
+  }
+  cudaGraph_t graph = nullptr;
+  GX_CUDA(cudaStreamBeginCapture(st->stream, cudaStreamCaptureModeThreadLocal));
+  int kernels = 0;
+  int rc = GX_OK;
+  for (size_t i = 0; i < st->ops.size() && rc == GX_OK; ++i) {
+    const gx_op& op = m->ops[st->ops[i]];
+    const bool is_conv = op.kind == GX_OP_CONV || op.kind == GX_OP_LINEAR;
+    rc = launch_op(op, m->tensors.data(), st->tptr.data(), wbase, k, st->sm_budget, st->stream, /*pdl=*/true,
+                   is_conv ? &plans[i] : nullptr, &kernels);
+  }
+  cudaError_t e = cudaStreamEndCapture(st->stream, &graph);
+  if (rc != GX_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return rc;
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+  e = cudaGraphInstantiate(&out->exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+  out->kernels = kernels;
+  return GX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gx_model_create(gx_ctx* ctx, const char* model_id, int n_tensors, const gx_tensor* tensors, int n_ops,
+                    const gx_op* ops, int n_units, const int32_t* unit_first_op, const int32_t* boundary,
+                    const void* weight_blob, size_t blob_bytes, gx_model** out) {
+  if (!ctx || !out || !tensors || !ops || !unit_first_op || !boundary) return fail(GX_EINVAL, "null arg");
+  if (n_units < 1 || n_tensors < 1 || n_ops < 1) return fail(GX_EINVAL, "empty unit chain");
+  if (unit_first_op[0] != 0 || unit_first_op[n_units] != n_ops) return fail(GX_EINVAL, "bad unit op ranges");
+  for (int u = 0; u < n_units; ++u)
+    if (unit_first_op[u + 1] < unit_first_op[u]) return fail(GX_EINVAL, "unit op ranges must be non-decreasing");
+  for (int u = 0; u <= n_units; ++u)
+    if (boundary[u] < 0 || boundary[u] >= n_tensors) return fail(GX_EINVAL, "bad boundary tensor id");
+  for (int i = 0; i < n_ops; ++i) {
+    const gx_op& op = ops[i];
+    if (op.in < 0 || op.in >= n_tensors || op.out < 0 || op.out >= n_tensors || op.in2 >= n_tensors)
+      return fail(GX_EINVAL, "op " + std::to_string(i) + " has a bad tensor id");
+    if ((op.w_off >= 0 && static_cast<size_t>(op.w_off) >= blob_bytes) ||
+        (op.b_off >= 0 && static_cast<size_t>(op.b_off) >= blob_bytes))
+      return fail(GX_EINVAL, "op " + std::to_string(i) + " weight offset outside the blob");
+  }
+  GX_CUDA(cudaSetDevice(ctx->device));
+  gx_model* m = new gx_model();
+  m->ctx = ctx;
+  m->id = model_id ? model_id : "";
+  m->tensors.assign(tensors, tensors + n_tensors);
+  m->ops.assign(ops, ops + n_ops);
+  m->unit_first_op.assign(unit_first_op, unit_first_op + n_units + 1);
+  m->boundary.assign(boundary, boundary + n_units + 1);
+  m->wbytes = blob_bytes;
+  cudaError_t e = cudaMalloc(&m->wdev, std::max<size_t>(blob_bytes, 256));
+  if (e == cudaSuccess && blob_bytes) e = cudaMemcpy(m->wdev, weight_blob, blob_bytes, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    if (m->wdev) cudaFree(m->wdev);
+    delete m;
+    return cuda_fail(e, "weight upload");
+  }
+  *out = m;
+  return GX_OK;
+}
+
+int gx_model_destroy(gx_model* m) {
+  if (!m) return GX_OK;
+  cudaSetDevice(m->ctx->device);
+  if (m->wdev) cudaFree(m->wdev);
+  delete m;
+  return GX_OK;
+}
+
+int gx_model_tensor_elems(gx_model* m, int tid, int64_t* out) {
+  if (!m || !out || tid < 0 || tid >= static_cast<int>(m->tensors.size())) return fail(GX_EINVAL, "bad tensor id");
+  *out = tensor_elems(m->tensors[tid]);
+  return GX_OK;
+}
+
+int gx_stage_create(gx_model* m, int start, int end, int max_batch, int sm_budget, void* stream, gx_stage** out) {
+  if (!m || !out) return fail(GX_EINVAL, "null arg");
+  if (!(0 <= start && start < end && end <= m->n_units()))
+    return fail(GX_EINVAL, "bad span [" + std::to_string(start) + ", " + std::to_string(end) + ") for model " + m->id);
+  if (max_batch < 1 || max_batch > 64) return fail(GX_EINVAL, "max_batch must be in 1..64");
+  if (sm_budget < 1 || sm_budget > m->ctx->sm_count)
+    return fail(GX_EINFEASIBLE, "SM budget " + std::to_string(sm_budget) + " outside 1.." +
+                                    std::to_string(m->ctx->sm_count));
+  GX_CUDA(cudaSetDevice(m->ctx->device));
+  gx_stage* st = new gx_stage();
+  st->m = m;
+  st->start = start;
+  st->end = end;
+  st->max_batch = max_batch;
+  st->sm_budget = sm_budget;
+  for (int i = m->unit_first_op[start]; i < m->unit_first_op[end]; ++i) st->ops.push_back(i);
+  st->in_tid = m->boundary[start];
+  st->out_tid = m->boundary[end];
+  int rc = plan_workspace(st);
+  if (rc != GX_OK) {
+    delete st;
+    return rc;
+  }
+  if (stream) {
+    st->stream = static_cast<cudaStream_t>(stream);
+  } else {
+    cudaError_t e = cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      cudaFree(st->ws);
+      delete st;
+      return cuda_fail(e, "cudaStreamCreate");
+    }
+    st->own_stream = true;
+  }
+  *out = st;
+  return GX_OK;
+}
+
+int gx_stage_destroy(gx_stage* st) {
+  if (!st) return GX_OK;
+  cudaSetDevice(st->m->ctx->device);
+  cudaStreamSynchronize(st->stream);
+  for (auto& kv : st->graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  if (st->ws) cudaFree(st->ws);
+  if (st->prof_src) cudaFree(st->prof_src);
+  if (st->prof_dst) cudaFree(st->prof_dst);
+  if (st->own_stream) cudaStreamDestroy(st->stream);
+  delete st;
+  return GX_OK;
+}
+
+int gx_stage_stream(gx_stage* st, void** stream_out) {
+  if (!st || !stream_out) return fail(GX_EINVAL, "null arg");
+  *stream_out = st->stream;
+  return GX_OK;
+}
+
+static int stage_graph(gx_stage* st, int k, gx_stage::PerK** out) {
+  auto it = st->graphs.find(k);
+  if (it == st->graphs.end()) {
+    gx_stage::PerK pk;
+    int rc = capture_span(st, k, &pk);
+    if (rc != GX_OK) return rc;
+    it = st->graphs.emplace(k, pk).first;
+  }
+  *out = &it->second;
+  return GX_OK;
+}
+
+int gx_stage_run(gx_stage* st, int k, const void* const* src, const int32_t* src_dtype, int32_t src_channels,
+                 void* const* dst, int32_t dst_dtype) {
+  if (!st || !src || !src_dtype || !dst) return fail(GX_EINVAL, "null arg");
+  if (k < 1 || k > st->max_batch) return fail(GX_EINVAL, "batch k outside 1..max_batch");
+  gx_model* m = st->m;
+  const gx_tensor& tin = m->tensors[st->in_tid];
+  const gx_tensor& tout = m->tensors[st->out_tid];
+  const int c_src = src_channels > 0 ? src_channels : tin.C;
+  if (c_src > tin.C) return fail(GX_EINVAL, "source has more channels than the boundary tensor");
+  gx_stage::PerK* pk = nullptr;
+  int rc = stage_graph(st, k, &pk);
+  if (rc != GX_OK) return rc;
+  const int bw_grid = st->sm_budget * 8;
+  GX_CUDA(launch_gather(k, src, src_dtype, static_cast<int64_t>(tin.H) * tin.W, c_src, tin.C,
+                        static_cast<__nv_bfloat16*>(st->tptr[st->in_tid]), bw_grid, st->stream));
+  GX_CUDA(cudaGraphLaunch(pk->exec, st->stream));
+  GX_CUDA(launch_scatter(k, st->tptr[st->out_tid], tout.dtype, tensor_elems(tout), dst, dst_dtype, bw_grid,
+                         st->stream));
+  return GX_OK;
+}
+
+int gx_stage_kernel_count(gx_stage* st, int k, int* out) {
+  if (!st || !out) return fail(GX_EINVAL, "null arg");
+  gx_stage::PerK* pk = nullptr;
+  int rc = stage_graph(st, k, &pk);
+  if (rc != GX_OK) return rc;
+  *out = pk->kernels + 2;
+  return GX_OK;
+}
+
+int gx_stage_profile(gx_stage* st, int k, int iters, float* ms_out) {
+  if (!st || !ms_out) return fail(GX_EINVAL, "null arg");
+  if (k < 1 || k > st->max_batch || iters < 1) return fail(GX_EINVAL, "bad profile arguments");
+  gx_model* m = st->m;
+  const gx_tensor& tin = m->tensors[st->in_tid];
+  const gx_tensor& tout = m->tensors[st->out_tid];
+  const size_t in_bytes = static_cast<size_t>(tensor_elems(tin)) * 4;
+  const size_t out_bytes = static_cast<size_t>(tensor_elems(tout)) * 4;
+  GX_CUDA(cudaSetDevice(m->ctx->device));
+  if (!st->prof_src) {
+    GX_CUDA(cudaMalloc(&st->prof_src, in_bytes * st->max_batch));
+    GX_CUDA(cudaMemset(st->prof_src, 0, in_bytes * st->max_batch));
+    GX_CUDA(cudaMalloc(&st->prof_dst, out_bytes * st->max_batch));
+  }
+  std::vector<const void*> src(k);
+  std::vector<int32_t> dt(k, GX_F32);
+  std::vector<void*> dst(k);
+  for (int i = 0; i < k; ++i) {
+    src[i] = static_cast<uint8_t*>(st->prof_src) + i * in_bytes;
+    dst[i] = static_cast<uint8_t*>(st->prof_dst) + i * out_bytes;
+  }
+  const int32_t dst_dtype = st->end == m->n_units() ? GX_F32 : GX_BF16;
+  // warm-up (also captures the graph)
+  for (int w = 0; w < 3; ++w) {
+    int rc = gx_stage_run(st, k, src.data(), dt.data(), tin.C, dst.data(), dst_dtype);
+    if (rc != GX_OK) return rc;
+  }
+  cudaEvent_t e0, e1;
+  GX_CUDA(cudaEventCreate(&e0));
+  GX_CUDA(cudaEventCreate(&e1));
+  std::vector<float> t(iters);
+  for (int i = 0; i < iters; ++i) {
+    GX_CUDA(cudaEventRecord(e0, st->stream));
+    int rc = gx_stage_run(st, k, src.data(), dt.data(), tin.C, dst.data(), dst_dtype);
+    if (rc != GX_OK) return rc;
+    GX_CUDA(cudaEventRecord(e1, st->stream));
+    GX_CUDA(cudaEventSynchronize(e1));
+    GX_CUDA(cudaEventElapsedTime(&t[i], e0, e1));
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  std::sort(t.begin(), t.end());
+  *ms_out = t[iters / 2];
+  return GX_OK;
+}
+
+}  // extern "C"

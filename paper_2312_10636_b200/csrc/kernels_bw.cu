@@ -1,0 +1,349 @@
+// Bandwidth-bound kernels: ragged batch assembly (K1 gather/scatter), pooling (K4), the skinny
+// FC layer at small batch, and channel-slice copies.  All are grid-stride loops over 16-byte
+// vectors so one launch can be bounded to the stage's SM budget (grid = budget * blocks/SM).
+#include <cuda_bf16.h>
+
+#include "gx_internal.h"
+#include "gx_ptx.cuh"
+
+namespace gx {
+
+namespace {
+constexpr int kMaxRows = 64;  // max requests in one dispatched batch (profiles.py:200 caps at 127;
+                              // fixtures use 16-32)
+struct RowPtrs {
+  const void* p[kMaxRows];
+  int32_t dt[kMaxRows];
+};
+struct RowDst {
+  void* p[kMaxRows];
+};
+
+__device__ __forceinline__ uint4 f32x8_to_bf16x8(float4 a, float4 b) {
+  uint4 o;
+  o.x = pack_bf16x2(a.x, a.y);
+  o.y = pack_bf16x2(a.z, a.w);
+  o.z = pack_bf16x2(b.x, b.y);
+  o.w = pack_bf16x2(b.z, b.w);
+  return o;
+}
+
+// K1 gather: k entry activations (each fp32 from ingress or bf16 from an alignment stage) ->
+// one contiguous bf16 NHWC batch.  c_src == c_dst: 8-element vectors; otherwise per-element
+// with zero padding of the extra channels (the 3-channel image into the 8-channel stem input).
+__global__ void gather_kernel(RowPtrs src, int k, int64_t pixels, int c_src, int c_dst,
+                              __nv_bfloat16* __restrict__ dst) {
+  if (c_src == c_dst && (c_dst & 7) == 0) {
+    const int64_t vec_per_row = pixels * c_dst / 8;
+    const int64_t total = vec_per_row * k;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+      const int r = static_cast<int>(i / vec_per_row);
+      const int64_t v = i - r * vec_per_row;
+      uint4 o;
+      if (src.dt[r] == GX_F32) {
+        const float4* s = reinterpret_cast<const float4*>(src.p[r]) + 2 * v;
+        o = f32x8_to_bf16x8(__ldg(s), __ldg(s + 1));
+      } else {
+        o = __ldg(reinterpret_cast<const uint4*>(src.p[r]) + v);
+      }
+      reinterpret_cast<uint4*>(dst)[i] = o;
+    }
+  } else {
+    const int64_t per_row = pixels * c_dst;
+    const int64_t total = per_row * k;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+      const int r = static_cast<int>(i / per_row);
+      const int64_t e = i - r * per_row;
+      const int64_t px = e / c_dst;
+      const int c = static_cast<int>(e - px * c_dst);
+      float val = 0.0f;
+      if (c < c_src) {
+        const int64_t si = px * c_src + c;
+        val = src.dt[r] == GX_F32 ? __ldg(reinterpret_cast<const float*>(src.p[r]) + si)
+                                  : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(src.p[r])[si]);
+      }
+      dst[i] = __float2bfloat16_rn(val);
+    }
+  }
+}
+
+// K1 scatter: batch rows -> per-request destinations (bf16 activations or fp32 logits).
+__global__ void scatter_kernel(const void* __restrict__ src, int src_f32, int k, int64_t row_elems, RowDst dst,
+                               int dst_f32) {
+  const int64_t vec_per_row = row_elems / 8;
+  const int64_t total = vec_per_row * k;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = static_cast<int>(i / vec_per_row);
+    const int64_t v = i - r * vec_per_row;
+    if (src_f32) {
+      const float4* s = reinterpret_cast<const float4*>(src) + 2 * i;
+      const float4 a = __ldg(s), b = __ldg(s + 1);
+      if (dst_f32) {
+        float4* d = reinterpret_cast<float4*>(dst.p[r]) + 2 * v;
+        d[0] = a;
+        d[1] = b;
+      } else {
+        reinterpret_cast<uint4*>(dst.p[r])[v] = f32x8_to_bf16x8(a, b);
+      }
+      continue;
+    }
+    const uint4 val = __ldg(reinterpret_cast<const uint4*>(src) + i);
+    if (dst_f32) {
+      float4* d = reinterpret_cast<float4*>(dst.p[r]) + 2 * v;
+      const float2 a = unpack_bf16x2(val.x), b = unpack_bf16x2(val.y), c = unpack_bf16x2(val.z),
+                   e = unpack_bf16x2(val.w);
+      d[0] = make_float4(a.x, a.y, b.x, b.y);
+      d[1] = make_float4(c.x, c.y, e.x, e.y);
+    } else {
+      reinterpret_cast<uint4*>(dst.p[r])[v] = val;
+    }
+  }
+}
+
+// K4 pooling over NHWC, 8 channels per thread (C % 8 == 0).  mode 0 = max, 1 = average.
+__global__ void pool_kernel(int mode, const __nv_bfloat16* __restrict__ x, int N, int H, int W, int C, int x_ld,
+                            __nv_bfloat16* __restrict__ y, int Ho, int Wo, int y_ld, int y_coff, int R, int S,
+                            int sh, int sw, int ph, int pw, int count_include_pad) {
+  const int cv = C / 8;
+  const int64_t total = static_cast<int64_t>(N) * Ho * Wo * cv;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c8 = static_cast<int>(i % cv);
+    int64_t p = i / cv;
+    const int wo = static_cast<int>(p % Wo);
+    p /= Wo;
+    const int ho = static_cast<int>(p % Ho);
+    const int n = static_cast<int>(p / Ho);
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = mode == 0 ? -INFINITY : 0.0f;
+    int cnt = 0;
+    for (int r = 0; r < R; ++r) {
+      const int hi = ho * sh - ph + r;
+      if (hi < 0 || hi >= H) continue;
+      for (int s = 0; s < S; ++s) {
+        const int wi = wo * sw - pw + s;
+        if (wi < 0 || wi >= W) continue;
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(x + ((static_cast<int64_t>(n) * H + hi) * W + wi) * x_ld) + c8);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = unpack_bf16x2(w[j]);
+          if (mode == 0) {
+            acc[2 * j] = fmaxf(acc[2 * j], f.x);
+            acc[2 * j + 1] = fmaxf(acc[2 * j + 1], f.y);
+          } else {
+            acc[2 * j] += f.x;
+            acc[2 * j + 1] += f.y;
+          }
+        }
+        ++cnt;
+      }
+    }
+    if (mode == 1) {
+      // count_include_pad: divisor is the window clipped to the padded extent (PyTorch semantics)
+      int div = cnt;
+      if (count_include_pad) {
+        const int h0 = ho * sh - ph, w0 = wo * sw - pw;
+        const int h1 = min(h0 + R, H + ph), w1 = min(w0 + S, W + pw);
+        div = (h1 - h0) * (w1 - w0);
+      }
+      const float inv = 1.0f / static_cast<float>(div);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] *= inv;
+    }
+    uint4 o;
+    o.x = pack_bf16x2(acc[0], acc[1]);
+    o.y = pack_bf16x2(acc[2], acc[3]);
+    o.z = pack_bf16x2(acc[4], acc[5]);
+    o.w = pack_bf16x2(acc[6], acc[7]);
+    *reinterpret_cast<uint4*>(y + ((static_cast<int64_t>(n) * Ho + ho) * Wo + wo) * y_ld + y_coff + 8 * c8) = o;
+  }
+}
+
+// Global average pool: [N, HW, C] -> [N, C]; one thread per 8 channels.
+__global__ void gap_kernel(const __nv_bfloat16* __restrict__ x, int N, int HW, int C, __nv_bfloat16* __restrict__ y) {
+  const int cv = C / 8;
+  const int64_t total = static_cast<int64_t>(N) * cv;
+  const float inv = 1.0f / HW;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int n = static_cast<int>(i / cv);
+    const int c8 = static_cast<int>(i % cv);
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const uint4* base = reinterpret_cast<const uint4*>(x + static_cast<int64_t>(n) * HW * C) + c8;
+    for (int p = 0; p < HW; ++p) {
+      const uint4 v = __ldg(base + static_cast<int64_t>(p) * cv);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = unpack_bf16x2(w[j]);
+        acc[2 * j] += f.x;
+        acc[2 * j + 1] += f.y;
+      }
+    }
+    uint4 o;
+    o.x = pack_bf16x2(acc[0] * inv, acc[1] * inv);
+    o.y = pack_bf16x2(acc[2] * inv, acc[3] * inv);
+    o.z = pack_bf16x2(acc[4] * inv, acc[5] * inv);
+    o.w = pack_bf16x2(acc[6] * inv, acc[7] * inv);
+    reinterpret_cast<uint4*>(y + static_cast<int64_t>(n) * C)[c8] = o;
+  }
+}
+
+// Skinny FC at small batch (weight-streaming, HBM-bound): y[n][o] = x[n] . w[o] + b[o].
+// One warp per group of 4 output features; lanes stride K in 16-byte vectors; the batch rows are
+// processed 8 at a time so x stays in registers/L1 and each weight byte is read once.
+constexpr int kFcOut = 4;
+constexpr int kFcRows = 8;
+__global__ void fc_kernel(const __nv_bfloat16* __restrict__ x, int N, int K, const __nv_bfloat16* __restrict__ w,
+                          const float* __restrict__ b, void* __restrict__ y, int Nout, int y_f32, int act) {
+  const int lane = threadIdx.x & 31;
+  const int warps_total = gridDim.x * (blockDim.x >> 5);
+  const int groups = (Nout + kFcOut - 1) / kFcOut;
+  const int kv = K / 8;
+  for (int g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < groups; g += warps_total) {
+    const int o0 = g * kFcOut;
+    for (int n0 = 0; n0 < N; n0 += kFcRows) {
+      float acc[kFcOut][kFcRows];
+#pragma unroll
+      for (int a = 0; a < kFcOut; ++a)
+#pragma unroll
+        for (int r = 0; r < kFcRows; ++r) acc[a][r] = 0.0f;
+      for (int v = lane; v < kv; v += 32) {
+        float wf[kFcOut][8];
+#pragma unroll
+        for (int a = 0; a < kFcOut; ++a) {
+          uint4 wv = make_uint4(0, 0, 0, 0);
+          if (o0 + a < Nout) wv = __ldg(reinterpret_cast<const uint4*>(w + static_cast<int64_t>(o0 + a) * K) + v);
+          const uint32_t ww[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 f = unpack_bf16x2(ww[j]);
+            wf[a][2 * j] = f.x;
+            wf[a][2 * j + 1] = f.y;
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < kFcRows; ++r) {
+          if (n0 + r < N) {
+            const uint4 xv = __ldg(reinterpret_cast<const uint4*>(x + static_cast<int64_t>(n0 + r) * K) + v);
+            const uint32_t xx[4] = {xv.x, xv.y, xv.z, xv.w};
+            float xf[8];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float2 f = unpack_bf16x2(xx[j]);
+              xf[2 * j] = f.x;
+              xf[2 * j + 1] = f.y;
+            }
+#pragma unroll
+            for (int a = 0; a < kFcOut; ++a)
+#pragma unroll
+              for (int j = 0; j < 8; ++j) acc[a][r] = fmaf(wf[a][j], xf[j], acc[a][r]);
+          }
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < kFcOut; ++a)
+#pragma unroll
+        for (int r = 0; r < kFcRows; ++r) {
+          float s = acc[a][r];
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+          acc[a][r] = s;
+        }
+      if (lane == 0) {
+        for (int a = 0; a < kFcOut; ++a) {
+          const int o = o0 + a;
+          if (o >= Nout) break;
+          for (int r = 0; r < kFcRows && n0 + r < N; ++r) {
+            float v = acc[a][r] + (b ? b[o] : 0.0f);
+            if (act == GX_ACT_RELU) v = fmaxf(v, 0.0f);
+            const int64_t idx = static_cast<int64_t>(n0 + r) * Nout + o;
+            if (y_f32)
+              static_cast<float*>(y)[idx] = v;
+            else
+              static_cast<__nv_bfloat16*>(y)[idx] = __float2bfloat16_rn(v);
+          }
+        }
+      }
+    }
+  }
+}
+
+__global__ void copy_channels_kernel(const __nv_bfloat16* __restrict__ x, int64_t pixels, int C, int x_ld,
+                                     int x_coff, __nv_bfloat16* __restrict__ y, int y_ld, int y_coff) {
+  const int cv = C / 8;
+  const int64_t total = pixels * cv;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = i / cv;
+    const int c8 = static_cast<int>(i - p * cv);
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(x + p * x_ld + x_coff) + c8);
+    reinterpret_cast<uint4*>(y + p * y_ld + y_coff)[c8] = v;
+  }
+}
+
+inline int grid_for(int64_t work_items, int threads, int grid_cap) {
+  int64_t g = (work_items + threads - 1) / threads;
+  if (g > grid_cap) g = grid_cap;
+  if (g < 1) g = 1;
+  return static_cast<int>(g);
+}
+}  // namespace
+
+cudaError_t launch_gather(int k, const void* const* src, const int32_t* src_dtype, int64_t pixels, int c_src,
+                          int c_dst, __nv_bfloat16* dst, int grid, cudaStream_t s) {
+  if (k > kMaxRows) return cudaErrorInvalidValue;
+  RowPtrs rp;
+  for (int i = 0; i < k; ++i) {
+    rp.p[i] = src[i];
+    rp.dt[i] = src_dtype[i];
+  }
+  const int64_t work = (c_src == c_dst && (c_dst & 7) == 0) ? pixels * c_dst / 8 * k : pixels * c_dst * k;
+  gather_kernel<<<grid_for(work, 256, grid), 256, 0, s>>>(rp, k, pixels, c_src, c_dst, dst);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter(int k, const void* src, int src_dtype, int64_t row_elems, void* const* dst,
+                           int dst_dtype, int grid, cudaStream_t s) {
+  if (k > kMaxRows || (row_elems & 7)) return cudaErrorInvalidValue;
+  RowDst rd;
+  for (int i = 0; i < k; ++i) rd.p[i] = dst[i];
+  scatter_kernel<<<grid_for(row_elems / 8 * k, 256, grid), 256, 0, s>>>(src, src_dtype == GX_F32, k, row_elems, rd,
+                                                                     dst_dtype == GX_F32);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pool(int mode, const __nv_bfloat16* x, int N, int H, int W, int C, int x_ld, __nv_bfloat16* y,
+                        int Ho, int Wo, int y_ld, int y_coff, int R, int S, int sh, int sw, int ph, int pw,
+                        int count_include_pad, int grid, cudaStream_t s) {
+  if (C & 7) return cudaErrorInvalidValue;
+  const int64_t work = static_cast<int64_t>(N) * Ho * Wo * (C / 8);
+  pool_kernel<<<grid_for(work, 256, grid), 256, 0, s>>>(mode, x, N, H, W, C, x_ld, y, Ho, Wo, y_ld, y_coff, R, S, sh,
+                                                         sw, ph, pw, count_include_pad);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gap(const __nv_bfloat16* x, int N, int HW, int C, __nv_bfloat16* y, int grid, cudaStream_t s) {
+  if (C & 7) return cudaErrorInvalidValue;
+  gap_kernel<<<grid_for(static_cast<int64_t>(N) * (C / 8), 128, grid), 128, 0, s>>>(x, N, HW, C, y);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fc(const __nv_bfloat16* x, int N, int K, const __nv_bfloat16* w, const float* b, void* y, int Nout,
+                      int y_f32, int act, int grid, cudaStream_t s) {
+  if (K & 7) return cudaErrorInvalidValue;
+  const int groups = (Nout + kFcOut - 1) / kFcOut;
+  const int warps_per_block = 8;
+  fc_kernel<<<grid_for(groups, warps_per_block, grid), 32 * warps_per_block, 0, s>>>(x, N, K, w, b, y, Nout, y_f32,
+                                                                                       act);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy_channels(const __nv_bfloat16* x, int64_t pixels, int C, int x_ld, int x_coff,
+                                 __nv_bfloat16* y, int y_ld, int y_coff, int grid, cudaStream_t s) {
+  if ((C | x_ld | x_coff | y_ld | y_coff) & 7) return cudaErrorInvalidValue;
+  copy_channels_kernel<<<grid_for(pixels * (C / 8), 256, grid), 256, 0, s>>>(x, pixels, C, x_ld, x_coff, y, y_ld,
+                                                                             y_coff);
+  return cudaGetLastError();
+}
+
+}  // namespace gx

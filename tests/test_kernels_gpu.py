@@ -1,0 +1,175 @@
+"""Kernel parity on the B200: every libgx kernel vs a plain PyTorch fp32 reference of the same op.
+
+bf16 in, fp32 accumulate, bf16 out: tolerance is bf16 output rounding plus input rounding
+(relative 1.5e-2 on the max-norm, written per test).  Integer/byte work (gather/scatter) is
+bit-exact.
+"""
+import pytest
+import torch
+import torch.nn.functional as F
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2312_10636_b200 import _native as N
+    from paper_2312_10636_b200.device import WeightBlob, pack_conv_weight, run_op, tensor_desc
+
+
+def _rel(a, b):
+    return ((a.float() - b.float()).abs().max() / b.float().abs().max().clamp_min(1e-6)).item()
+
+
+def _conv_case(k, H, W, Cin, Cout, R, S, stride, pad, residual, relu, cin_pad=None, sm_budget=0, out_coff=0,
+               out_c=None, seed=0):
+    g = torch.Generator().manual_seed(seed)
+    dev = "cuda"
+    cin_pad = cin_pad or Cin
+    x = torch.randn(k, H, W, Cin, generator=g)
+    w = torch.randn(Cout, Cin, R, S, generator=g) / (Cin * R * S) ** 0.5
+    b = torch.randn(Cout, generator=g) * 0.1
+    Ho = (H + 2 * pad - R) // stride + 1
+    Wo = (W + 2 * pad - S) // stride + 1
+    xb = x.to(torch.bfloat16)
+    ref = F.conv2d(xb.float().permute(0, 3, 1, 2), w.to(torch.bfloat16).float(), b, stride=stride, padding=pad)
+    ref = ref.permute(0, 2, 3, 1)
+    res = None
+    if residual:
+        res = torch.randn(k, Ho, Wo, Cout, generator=g).to(torch.bfloat16)
+        ref = ref + res.float()
+    if relu:
+        ref = ref.clamp_min(0)
+    blob = WeightBlob()
+    w_off = blob.add_bf16(pack_conv_weight(w, cin_pad))
+    b_off = blob.add_f32(b)
+    wdev = torch.from_numpy(blob.bytes()).to(dev)
+    xin = torch.zeros(k, H, W, cin_pad, dtype=torch.bfloat16)
+    xin[..., :Cin] = xb
+    xin = xin.to(dev)
+    out_c = out_c or Cout
+    y = torch.full((k, Ho, Wo, out_c), float("nan"), dtype=torch.bfloat16, device=dev)
+    descs = [tensor_desc(H, W, cin_pad), tensor_desc(Ho, Wo, out_c), tensor_desc(Ho, Wo, Cout)]
+    tensors = [xin, y, res.to(dev) if residual else y]
+    op = N.make_op(N.GX_OP_CONV, 0, 1, in2=2 if residual else -1, out_coff=out_coff,
+                   act=N.GX_ACT_RELU if relu else N.GX_ACT_NONE, R=R, S=S, sh=stride, sw=stride, ph=pad, pw=pad,
+                   Cin=cin_pad, Cout=Cout, w_off=w_off, b_off=b_off)
+    run_op(op, tensors, descs, wdev, k, sm_budget)
+    torch.cuda.synchronize()
+    got = y[..., out_coff:out_coff + Cout].float().cpu()
+    assert torch.isfinite(got).all(), "conv left unwritten outputs"
+    return got, ref
+
+
+@pytest.mark.parametrize(
+    "k,H,W,Cin,Cout,R,S,stride,pad,residual,relu",
+    [
+        (1, 8, 8, 64, 64, 1, 1, 1, 0, False, False),     # smallest 1x1
+        (2, 14, 14, 64, 128, 3, 3, 1, 1, False, True),   # 3x3 s1 p1
+        (3, 28, 28, 128, 256, 1, 1, 1, 0, True, True),   # bottleneck expand + residual
+        (2, 56, 56, 64, 64, 3, 3, 1, 1, False, True),    # layer1 3x3
+        (2, 28, 28, 128, 128, 3, 3, 2, 1, False, True),  # stride-2 3x3
+        (2, 14, 14, 256, 512, 1, 1, 2, 0, False, False), # stride-2 downsample 1x1
+        (1, 7, 7, 512, 2048, 1, 1, 1, 0, True, True),    # layer4 expand, many N tiles
+        (5, 7, 7, 512, 512, 3, 3, 1, 1, False, True),    # M not a multiple of 128
+        (1, 17, 17, 192, 160, 1, 7, 1, 0, False, True),  # Inception 1x7 (pad handled below)
+    ],
+)
+def test_conv_matches_torch(k, H, W, Cin, Cout, R, S, stride, pad, residual, relu):
+    got, ref = _conv_case(k, H, W, Cin, Cout, R, S, stride, pad, residual, relu)
+    assert _rel(got, ref) < 1.5e-2
+
+
+def test_conv_stem_channel_padded():
+    # ResNet stem: 3-channel image zero-padded to 8 channels, 7x7 stride 2 pad 3
+    got, ref = _conv_case(2, 64, 64, 3, 64, 7, 7, 2, 3, False, True, cin_pad=8)
+    assert _rel(got, ref) < 1.5e-2
+
+
+def test_conv_bounded_sm_budget_and_concat_offset():
+    got, ref = _conv_case(4, 28, 28, 64, 96, 3, 3, 1, 1, False, True, sm_budget=5, out_coff=32, out_c=160)
+    assert _rel(got, ref) < 1.5e-2
+
+
+def test_conv_large_m_persistent():
+    got, ref = _conv_case(8, 56, 56, 256, 64, 1, 1, 1, 0, False, True, sm_budget=20)
+    assert _rel(got, ref) < 1.5e-2
+
+
+@pytest.mark.parametrize("mode,R,stride,pad", [("max", 3, 2, 1), ("max", 2, 2, 0), ("avg", 3, 1, 1),
+                                                ("max", 3, 2, 0)])
+def test_pool(mode, R, stride, pad):
+    g = torch.Generator().manual_seed(1)
+    k, H, W, Cc = 3, 15, 15, 64
+    x = torch.randn(k, H, W, Cc, generator=g).to(torch.bfloat16)
+    xn = x.float().permute(0, 3, 1, 2)
+    if mode == "max":
+        ref = F.max_pool2d(xn, R, stride, pad)
+    else:
+        ref = F.avg_pool2d(xn, R, stride, pad, count_include_pad=True)
+    ref = ref.permute(0, 2, 3, 1)
+    Ho, Wo = ref.shape[1], ref.shape[2]
+    y = torch.empty(k, Ho, Wo, Cc, dtype=torch.bfloat16, device="cuda")
+    op = N.make_op(N.GX_OP_MAXPOOL if mode == "max" else N.GX_OP_AVGPOOL, 0, 1, R=R, S=R, sh=stride, sw=stride,
+                   ph=pad, pw=pad, flags=1)
+    run_op(op, [x.cuda(), y], [tensor_desc(H, W, Cc), tensor_desc(Ho, Wo, Cc)], torch.zeros(256, device="cuda"), k)
+    torch.cuda.synchronize()
+    assert _rel(y.float().cpu(), ref) < 1e-2
+
+
+def test_gap_and_fc():
+    g = torch.Generator().manual_seed(2)
+    k, HW, Cc, O = 5, 49, 2048, 1000
+    x = torch.randn(k, 7, 7, Cc, generator=g).to(torch.bfloat16)
+    w = torch.randn(O, Cc, generator=g) / Cc ** 0.5
+    b = torch.randn(O, generator=g)
+    pooled_ref = x.float().mean(dim=(1, 2))
+    blob = WeightBlob()
+    w_off = blob.add_bf16(w)
+    b_off = blob.add_f32(b)
+    wdev = torch.from_numpy(blob.bytes()).cuda()
+    pooled = torch.empty(k, Cc, dtype=torch.bfloat16, device="cuda")
+    run_op(N.make_op(N.GX_OP_GAP, 0, 1), [x.cuda(), pooled], [tensor_desc(7, 7, Cc), tensor_desc(1, 1, Cc)], wdev, k)
+    logits = torch.empty(k, O, dtype=torch.float32, device="cuda")
+    run_op(N.make_op(N.GX_OP_FC, 0, 1, Cin=Cc, Cout=O, w_off=w_off, b_off=b_off), [pooled, logits],
+           [tensor_desc(1, 1, Cc), tensor_desc(1, 1, O, N.GX_F32)], wdev, k)
+    torch.cuda.synchronize()
+    assert _rel(pooled.float().cpu(), pooled_ref) < 1e-2
+    ref = pooled.float().cpu() @ w.to(torch.bfloat16).float().t() + b
+    assert _rel(logits.cpu(), ref) < 1e-3
+
+
+def test_gather_scatter_bit_exact():
+    import ctypes as C
+    from paper_2312_10636_b200.device import context
+    ctx = context(0)
+    k, pix, Cc = 6, 56 * 56, 64
+    srcs = []
+    dts = []
+    for i in range(k):
+        if i % 2:
+            srcs.append(torch.randn(pix * Cc, device="cuda"))
+            dts.append(N.GX_F32)
+        else:
+            srcs.append(torch.randn(pix * Cc, device="cuda").to(torch.bfloat16))
+            dts.append(N.GX_BF16)
+    dst = torch.empty(k, pix * Cc, dtype=torch.bfloat16, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    N.check(N.lib().gx_gather(ctx.handle, k, N.ptr_array([t.data_ptr() for t in srcs]), N.i32_array(dts), pix, Cc,
+                              Cc, C.c_void_p(dst.data_ptr()), 0, C.c_void_p(s)))
+    outs = [torch.empty(pix * Cc, dtype=torch.float32, device="cuda") for _ in range(k)]
+    N.check(N.lib().gx_scatter(ctx.handle, k, C.c_void_p(dst.data_ptr()), N.GX_BF16, pix * Cc,
+                               N.ptr_array([o.data_ptr() for o in outs]), N.GX_F32, 0, C.c_void_p(s)))
+    torch.cuda.synchronize()
+    for i in range(k):
+        exp = srcs[i].to(torch.bfloat16)
+        assert torch.equal(dst[i], exp)
+        assert torch.equal(outs[i], exp.float())
+    # 3 -> 8 channel padding of the raw image (stem ingress)
+    img = [torch.randn(224 * 224 * 3, device="cuda") for _ in range(2)]
+    d8 = torch.empty(2, 224 * 224 * 8, dtype=torch.bfloat16, device="cuda")
+    N.check(N.lib().gx_gather(ctx.handle, 2, N.ptr_array([t.data_ptr() for t in img]), N.i32_array([N.GX_F32] * 2),
+                              224 * 224, 3, 8, C.c_void_p(d8.data_ptr()), 0, C.c_void_p(s)))
+    torch.cuda.synchronize()
+    for i in range(2):
+        v = d8[i].view(224 * 224, 8)
+        assert torch.equal(v[:, :3], img[i].view(-1, 3).to(torch.bfloat16))
+        assert (v[:, 3:] == 0).all()
