@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -55,6 +56,41 @@ bool encode_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uin
   cuuint32_t es[2] = {1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+typedef CUresult (*PFN_encodeIm2col_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                       const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
+                                       const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                       CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeIm2col_t im2col_fn() {
+  static PFN_encodeIm2col_t fn = nullptr;
+  if (fn == nullptr) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeIm2col_t>(p);
+  }
+  return fn;
+}
+
+// NHWC input as a rank-4 (C, W, H, N) im2col map: 128 output pixels x 64 channels per load.
+// Box corners follow the fprop convention: lower = -pad, upper = pad - (filter - 1).
+bool encode_tmap_im2col_bf16(CUtensorMap* map, const void* base, int C, int W, int H, int N, int lower_w,
+                             int lower_h, int upper_w, int upper_h, int stride_w, int stride_h) {
+  PFN_encodeIm2col_t fn = im2col_fn();
+  if (fn == nullptr) return false;
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
+                        static_cast<cuuint64_t>(N)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(C) * 2, static_cast<cuuint64_t>(C) * 2 * W,
+                           static_cast<cuuint64_t>(C) * 2 * W * H};
+  int lower[2] = {lower_w, lower_h};
+  int upper[2] = {upper_w, upper_h};
+  cuuint32_t es[4] = {1, static_cast<cuuint32_t>(stride_w), static_cast<cuuint32_t>(stride_h), 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, lower, upper, kBK, kBM,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -129,12 +165,20 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
   a.y_f32 = to.dtype == GX_F32;
   a.act = op.act;
   a.idesc = umma_idesc_bf16(kBM, a.BN);
-  a.stages = conv_pick_stages(a.BN, a.num_kb);
+  a.stages = conv_pick_stages(a.BN, a.num_kb, a.res != nullptr);
   a.tmem_cols = tmem_cols_for(a.BN);
   if (a.res && (T[op.in2].dtype != GX_BF16 || (a.res_ld & 7))) return fail(GX_EINVAL, "bad residual tensor");
   const int kpad = a.num_kb * kBK;
+  memset(&out->amap, 0, sizeof(out->amap));
+  memset(&out->rmap, 0, sizeof(out->rmap));
   if (!encode_tmap_2d_bf16(&out->wmap, wbase + op.w_off, kpad, op.Cout, static_cast<uint64_t>(kpad) * 2, kBK, a.BN))
     return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for conv weights");
+  a.tma_a = (op.Cin % kBK) == 0 && getenv("GX_NO_TMA_IM2COL") == nullptr;
+  if (a.tma_a && !encode_tmap_im2col_bf16(&out->amap, a.x, ti.C, ti.W, ti.H, k, -a.pw, -a.ph, a.pw - (a.S - 1),
+                                          a.ph - (a.R - 1), a.sw, a.sh))
+    return fail(GX_ECUDA, "cuTensorMapEncodeIm2col failed for conv input");
+  if (a.res && !encode_tmap_2d_bf16(&out->rmap, a.res, a.res_ld, a.M, static_cast<uint64_t>(a.res_ld) * 2, 64, kBM))
+    return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for the residual");
   out->grid = std::min(a.num_tiles, std::max(1, sm_budget));
   return GX_OK;
 }
@@ -151,7 +195,7 @@ int launch_op(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
         if (rc != GX_OK) return rc;
         pre = &cl;
       }
-      GX_CUDA(launch_conv(pre->wmap, pre->args, pre->grid, s, pdl));
+      GX_CUDA(launch_conv(pre->wmap, pre->amap, pre->rmap, pre->args, pre->grid, s, pdl));
       break;
     }
     case GX_OP_MAXPOOL:

@@ -17,6 +17,8 @@ struct gx_ctx {
 namespace gx {
 struct ConvLaunch {
   CUtensorMap wmap;
+  CUtensorMap amap;  // im2col map of the input (args.tma_a)
+  CUtensorMap rmap;  // residual tile map (args.res)
   ConvArgs args;
   int grid;
 };

@@ -1,0 +1,112 @@
+"""Executor objects over libgx: a unit chain resident on one GPU and its stage instances.
+
+`DeviceModel` is a ModelSpec (profiles.py:31-87) made executable; `StageInstance` is one
+instance of a planned stage (StagePlan, realign.py:50-67; _StageRT, simulator.py:76-100): span
+[start, end), max batch b, SM budget from the plan's share.  `StageInstance.run` is the real
+execution behind _StageRT.latency_for(k).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _native as N
+from .device import context
+from .errors import ValidationError
+from .models import UnitChain
+
+
+class DeviceModel:
+    def __init__(self, chain: UnitChain, device: int = 0):
+        self.chain = chain
+        self.device = device
+        self.ctx = context(device)
+        descs = (N.GxTensor * len(chain.tensors))()
+        for i, (H, W, Cc, dt) in enumerate(chain.tensors):
+            descs[i].H, descs[i].W, descs[i].C, descs[i].dtype = H, W, Cc, dt
+        ops = (N.GxOp * len(chain.ops))(*chain.ops)
+        blob = chain.blob.bytes()
+        self.handle = C.c_void_p()
+        with torch.cuda.device(device):
+            N.check(N.lib().gx_model_create(
+                self.ctx.handle, chain.model_id.encode(), len(chain.tensors), descs, len(chain.ops), ops,
+                chain.n_units, N.i32_array(chain.unit_first_op), N.i32_array(chain.boundary),
+                blob.ctypes.data_as(C.c_void_p), blob.nbytes, C.byref(self.handle)), "gx_model_create")
+        self.weight_bytes = blob.nbytes
+
+    @property
+    def n_units(self) -> int:
+        return self.chain.n_units
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                N.lib().gx_model_destroy(h)
+            except Exception:  # noqa: BLE001 - interpreter teardown
+                pass
+            self.handle = None
+
+
+class StageInstance:
+    """One executor instance of span [start, end) bounded to `sm_budget` SMs."""
+
+    def __init__(self, model: DeviceModel, start: int, end: int, max_batch: int, sm_budget: int,
+                 stream: torch.cuda.Stream | None = None):
+        if not 0 <= start < end <= model.n_units:
+            raise ValidationError(f"bad span [{start}, {end}) for model {model.chain.model_id!r}")
+        self.model = model
+        self.start, self.end, self.max_batch, self.sm_budget = start, end, max_batch, sm_budget
+        self.handle = C.c_void_p()
+        # the stream is torch-owned so tensors freed on it are tracked by torch's allocator
+        self.stream = stream or torch.cuda.Stream(device=model.device)
+        with torch.cuda.device(model.device):
+            N.check(N.lib().gx_stage_create(model.handle, start, end, max_batch, sm_budget,
+                                            C.c_void_p(self.stream.cuda_stream), C.byref(self.handle)),
+                    "gx_stage_create")
+        chain = model.chain
+        self.in_channels = chain.boundary_shape(start)[2]
+        self.out_elems = chain.boundary_elems(end)
+        self.final = end == chain.n_units
+
+    def run_ptrs(self, k: int, src, src_dtypes, dst, dst_dtype: int, src_channels: int = 0):
+        N.check(N.lib().gx_stage_run(self.handle, k, N.ptr_array(src), N.i32_array(src_dtypes), src_channels,
+                                     N.ptr_array(dst), dst_dtype), "gx_stage_run")
+
+    def run(self, inputs: list[torch.Tensor], out_dtype: torch.dtype | None = None,
+            src_channels: int = 0) -> list[torch.Tensor]:
+        """Execute one batch: inputs are per-request entry activations (NHWC, fp32 or bf16)."""
+        k = len(inputs)
+        if not 1 <= k <= self.max_batch:
+            raise ValidationError(f"batch {k} outside 1..{self.max_batch}")
+        out_dtype = out_dtype or (torch.float32 if self.final else torch.bfloat16)
+        dev = torch.device("cuda", self.model.device)
+        outs = [torch.empty(self.out_elems, dtype=out_dtype, device=dev) for _ in range(k)]
+        cur = torch.cuda.current_stream(dev)
+        self.stream.wait_stream(cur)
+        self.run_ptrs(k, [t.data_ptr() for t in inputs],
+                      [N.GX_F32 if t.dtype == torch.float32 else N.GX_BF16 for t in inputs],
+                      [o.data_ptr() for o in outs], N.GX_F32 if out_dtype == torch.float32 else N.GX_BF16,
+                      src_channels)
+        cur.wait_stream(self.stream)
+        return outs
+
+    def profile(self, k: int, iters: int = 20) -> float:
+        ms = C.c_float()
+        N.check(N.lib().gx_stage_profile(self.handle, k, iters, C.byref(ms)), "gx_stage_profile")
+        return float(ms.value)
+
+    def kernel_count(self, k: int) -> int:
+        n = C.c_int()
+        N.check(N.lib().gx_stage_kernel_count(self.handle, k, C.byref(n)))
+        return n.value
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                N.lib().gx_stage_destroy(h)
+            except Exception:  # noqa: BLE001
+                pass
+            self.handle = None

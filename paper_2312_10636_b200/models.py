@@ -1,0 +1,397 @@
+"""Unit chains: the executor-side form of the reference's ModelSpec (profiles.py:31-87).
+
+A model is a linear chain of N units; boundary p is the input of unit p (boundary 0 = the raw
+input, boundary N = the output), exactly as ModelSpec.payload_bytes(p) counts them
+(profiles.py:67-74).  Each unit lowers to a short run of libgx ops over per-sample NHWC bf16
+tensors; BatchNorm is folded into the preceding conv at build time, ReLU / residual adds are
+fused into the conv epilogue, Inception branch outputs are written straight into their concat
+slice, and VGG's NCHW flatten is folded into fc1's column order.
+
+Weights are random-initialised parameters of the named architecture (torchvision /
+transformers definitions as the parameter source, seeded), so the CPU oracle can run the very
+same parameters in fp32.  Only parameter tensors are taken from torch; nothing here computes.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+import torch.nn as nn
+
+from . import _native as N
+from .device import WeightBlob, pack_conv_weight
+
+BF16, F32 = N.GX_BF16, N.GX_F32
+
+
+@dataclass
+class UnitChain:
+    model_id: str
+    tensors: list = field(default_factory=list)  # (H, W, C, dtype)
+    ops: list = field(default_factory=list)  # GxOp
+    unit_first_op: list = field(default_factory=list)
+    boundary: list = field(default_factory=list)
+    blob: WeightBlob = field(default_factory=WeightBlob)
+    input_channels: int = 3  # channels a client actually ships at boundary 0 (pre-padding)
+    unit_flops: list = field(default_factory=list)  # per-sample FLOPs of each unit
+    ingress_nchw: list = field(default_factory=list)  # torch-layout per-sample shape per boundary
+
+    @property
+    def n_units(self) -> int:
+        return len(self.boundary) - 1
+
+    def boundary_shape(self, p: int):
+        H, W, Cc, dt = self.tensors[self.boundary[p]]
+        return H, W, Cc, dt
+
+    def boundary_elems(self, p: int) -> int:
+        H, W, Cc, _ = self.boundary_shape(p)
+        return H * W * Cc
+
+    def ingress_channels(self, p: int) -> int:
+        """Channels per pixel a client ships at boundary p (the stem input is 3, padded to 8)."""
+        return self.input_channels if p == 0 else self.boundary_shape(p)[2]
+
+    def payload_bytes(self, p: int) -> int:
+        """fp32 wire bytes at boundary p (what ModelSpec.output_bytes records)."""
+        H, W, Cc, _ = self.boundary_shape(p)
+        return H * W * self.ingress_channels(p) * 4
+
+    def model_spec_doc(self, compute_weight=None) -> dict:
+        """A reference ModelSpec JSON document (profiles.py:89-101) for this chain."""
+        cw = compute_weight or [f / 1e9 for f in self.unit_flops]
+        return {
+            "model_id": self.model_id,
+            "input_bytes": self.payload_bytes(0),
+            "layers": [{"compute_weight": round(float(cw[u]), 6), "output_bytes": self.payload_bytes(u + 1)}
+                       for u in range(self.n_units)],
+        }
+
+
+class ChainBuilder:
+    def __init__(self, model_id: str):
+        self.c = UnitChain(model_id)
+        self._flops = 0.0
+
+    # -- tensors / units --------------------------------------------------
+    def tensor(self, H, W, Cc, dtype=BF16) -> int:
+        self.c.tensors.append((H, W, Cc, dtype))
+        return len(self.c.tensors) - 1
+
+    def shape(self, t):
+        return self.c.tensors[t]
+
+    def begin_unit(self, x: int):
+        if self.c.unit_first_op:
+            self.c.unit_flops.append(self._flops)
+        self._flops = 0.0
+        self.c.unit_first_op.append(len(self.c.ops))
+        self.c.boundary.append(x)
+
+    def finish(self, out: int) -> UnitChain:
+        self.c.unit_flops.append(self._flops)
+        self.c.unit_first_op.append(len(self.c.ops))
+        self.c.boundary.append(out)
+        return self.c
+
+    # -- ops ----------------------------------------------------------------
+    def conv(self, x, conv: nn.Conv2d, bn: nn.BatchNorm2d | None, relu=True, residual=-1, out=-1, out_coff=0,
+             cin_pad=None):
+        H, W, Cx, _ = self.shape(x)
+        w = conv.weight.detach().float()
+        cout, cin, R, S = w.shape
+        b = conv.bias.detach().float() if conv.bias is not None else torch.zeros(cout)
+        if bn is not None:
+            scale = bn.weight.detach().float() / torch.sqrt(bn.running_var.detach().float() + bn.eps)
+            w = w * scale[:, None, None, None]
+            b = (b - bn.running_mean.detach().float()) * scale + bn.bias.detach().float()
+        sh, sw = conv.stride
+        ph, pw = conv.padding
+        Ho = (H + 2 * ph - R) // sh + 1
+        Wo = (W + 2 * pw - S) // sw + 1
+        cin_pad = cin_pad or cin
+        assert cin_pad <= Cx, (cin_pad, Cx)
+        if out < 0:
+            out = self.tensor(Ho, Wo, cout)
+        else:
+            assert self.shape(out)[:2] == (Ho, Wo), (self.shape(out), Ho, Wo)
+        w_off = self.c.blob.add_bf16(pack_conv_weight(w, cin_pad))
+        b_off = self.c.blob.add_f32(b)
+        self.c.ops.append(N.make_op(N.GX_OP_CONV, x, out, in2=residual, out_coff=out_coff,
+                                    act=N.GX_ACT_RELU if relu else N.GX_ACT_NONE, R=R, S=S, sh=sh, sw=sw, ph=ph,
+                                    pw=pw, Cin=cin_pad, Cout=cout, w_off=w_off, b_off=b_off))
+        self._flops += 2.0 * Ho * Wo * cout * cin * R * S
+        return out
+
+    def pool(self, x, kind: str, k, s, p, out=-1, out_coff=0, count_include_pad=True):
+        H, W, Cx, _ = self.shape(x)
+        Ho = (H + 2 * p - k) // s + 1
+        Wo = (W + 2 * p - k) // s + 1
+        if out < 0:
+            out = self.tensor(Ho, Wo, Cx)
+        self.c.ops.append(N.make_op(N.GX_OP_MAXPOOL if kind == "max" else N.GX_OP_AVGPOOL, x, out, out_coff=out_coff,
+                                    R=k, S=k, sh=s, sw=s, ph=p, pw=p, flags=1 if count_include_pad else 0))
+        return out
+
+    def gap(self, x):
+        H, W, Cx, _ = self.shape(x)
+        out = self.tensor(1, 1, Cx)
+        self.c.ops.append(N.make_op(N.GX_OP_GAP, x, out))
+        return out
+
+    def fc(self, x, lin: nn.Linear, relu=False, out_dtype=BF16, weight=None):
+        H, W, Cx, _ = self.shape(x)
+        K = H * W * Cx
+        w = (weight if weight is not None else lin.weight).detach().float()
+        assert w.shape[1] == K, (w.shape, K)
+        out = self.tensor(1, 1, w.shape[0], out_dtype)
+        w_off = self.c.blob.add_bf16(w)
+        b_off = self.c.blob.add_f32(lin.bias.detach().float())
+        self.c.ops.append(N.make_op(N.GX_OP_FC, x, out, act=N.GX_ACT_RELU if relu else N.GX_ACT_NONE, Cin=K,
+                                    Cout=w.shape[0], w_off=w_off, b_off=b_off))
+        self._flops += 2.0 * K * w.shape[0]
+        return out
+
+
+# ---------------------------------------------------------------------------------------------
+# deterministic random-init parameters (the architectures' own initialisers, seeded)
+# ---------------------------------------------------------------------------------------------
+
+def _calibrate_bn(model: nn.Module, example: torch.Tensor, seed: int):
+    """Give every BatchNorm non-trivial, well-scaled statistics so folding is exercised.
+
+    Running mean/var come from a seeded calibration batch (cumulative averaging), affine
+    parameters are redrawn (gamma ~ U(0.5, 1.5), beta ~ N(0, 0.1)).  The BN closing each
+    residual branch gets gamma ~ U(0.1, 0.3), as in trained ResNets: at plain random init a
+    deep residual stack is chaotic (a 0.4% per-layer perturbation grows to ~10% at the logits
+    of ResNet-50), which no finite-precision path could be held to 2e-2 against.
+    """
+    g = torch.Generator().manual_seed(seed + 7)
+    last_bn = set()
+    for m in model.modules():
+        if hasattr(m, "bn3") and hasattr(m, "conv3"):
+            last_bn.add(id(m.bn3))
+        elif hasattr(m, "bn2") and hasattr(m, "conv2") and hasattr(m, "downsample"):
+            last_bn.add(id(m.bn2))
+    for m in model.modules():
+        if isinstance(m, nn.BatchNorm2d):
+            m.reset_running_stats()
+            m.momentum = None
+            with torch.no_grad():
+                if id(m) in last_bn:
+                    m.weight.copy_(torch.rand(m.num_features, generator=g) * 0.2 + 0.1)
+                else:
+                    m.weight.copy_(torch.rand(m.num_features, generator=g) + 0.5)
+                m.bias.copy_(torch.randn(m.num_features, generator=g) * 0.1)
+    model.train()
+    with torch.no_grad():
+        model(example)
+    model.eval()
+
+
+def torch_model(name: str, seed: int = 0) -> nn.Module:
+    """The fp32 parameter source for `name` (also what the CPU oracle runs)."""
+    import torchvision
+
+    torch.manual_seed(seed)
+    if name == "resnet50":
+        m = torchvision.models.resnet50(weights=None)
+        ex = torch.randn(8, 3, 224, 224, generator=torch.Generator().manual_seed(seed + 1))
+    elif name == "resnet18":
+        m = torchvision.models.resnet18(weights=None)
+        ex = torch.randn(8, 3, 224, 224, generator=torch.Generator().manual_seed(seed + 1))
+    elif name == "vgg16":
+        m = torchvision.models.vgg16(weights=None)
+        ex = None
+    elif name == "inception_v3":
+        m = torchvision.models.inception_v3(weights=None, aux_logits=False, init_weights=True)
+        ex = torch.randn(4, 3, 299, 299, generator=torch.Generator().manual_seed(seed + 1))
+    else:
+        raise KeyError(f"unknown model {name!r}")
+    if ex is not None:
+        _calibrate_bn(m, ex, seed)
+    m.eval()
+    return m
+
+
+# ---------------------------------------------------------------------------------------------
+# chain builders
+# ---------------------------------------------------------------------------------------------
+
+def _resnet_chain(name: str, m) -> UnitChain:
+    b = ChainBuilder(name)
+    x = b.tensor(224, 224, 8)  # 3-channel image, zero-padded to 8 channels by the gather
+    b.begin_unit(x)
+    y = b.conv(x, m.conv1, m.bn1, relu=True, cin_pad=8)
+    y = b.pool(y, "max", 3, 2, 1)
+    for layer in (m.layer1, m.layer2, m.layer3, m.layer4):
+        for blk in layer:
+            b.begin_unit(y)
+            idn = y
+            if blk.downsample is not None:
+                idn = b.conv(y, blk.downsample[0], blk.downsample[1], relu=False)
+            if hasattr(blk, "conv3"):  # bottleneck
+                t = b.conv(y, blk.conv1, blk.bn1, relu=True)
+                t = b.conv(t, blk.conv2, blk.bn2, relu=True)
+                y = b.conv(t, blk.conv3, blk.bn3, relu=True, residual=idn)
+            else:  # basic block
+                t = b.conv(y, blk.conv1, blk.bn1, relu=True)
+                y = b.conv(t, blk.conv2, blk.bn2, relu=True, residual=idn)
+    b.begin_unit(y)
+    p = b.gap(y)
+    out = b.fc(p, m.fc, out_dtype=F32)
+    return b.finish(out)
+
+
+def _vgg16_chain(m) -> UnitChain:
+    b = ChainBuilder("vgg16")
+    x = b.tensor(224, 224, 8)
+    y = x
+    first = True
+    b.begin_unit(x)
+    feats = list(m.features)
+    i = 0
+    while i < len(feats):
+        layer = feats[i]
+        if isinstance(layer, nn.Conv2d):
+            y = b.conv(y, layer, None, relu=True, cin_pad=8 if first else None)
+            first = False
+            i += 2  # conv + relu
+        elif isinstance(layer, nn.MaxPool2d):
+            y = b.pool(y, "max", 2, 2, 0)
+            i += 1
+            if i < len(feats):
+                b.begin_unit(y)
+        else:
+            i += 1
+    # classifier: torch flattens NCHW (c, h, w); our activations are NHWC (h, w, c)
+    fc1 = m.classifier[0]
+    H, W, Cc, _ = b.shape(y)
+    w1 = fc1.weight.detach().view(fc1.out_features, Cc, H, W).permute(0, 2, 3, 1).reshape(fc1.out_features, -1)
+    b.begin_unit(y)
+    y = b.fc(y, fc1, relu=True, weight=w1)
+    b.begin_unit(y)
+    y = b.fc(y, m.classifier[3], relu=True)
+    b.begin_unit(y)
+    y = b.fc(y, m.classifier[6], out_dtype=F32)
+    return b.finish(y)
+
+
+def _basic(b, x, bc, out=-1, out_coff=0):
+    return b.conv(x, bc.conv, bc.bn, relu=True, out=out, out_coff=out_coff)
+
+
+def _inception_chain(m) -> UnitChain:
+    b = ChainBuilder("inception_v3")
+    x = b.tensor(299, 299, 8)
+    b.begin_unit(x)
+    y = b.conv(x, m.Conv2d_1a_3x3.conv, m.Conv2d_1a_3x3.bn, relu=True, cin_pad=8)
+    b.begin_unit(y)
+    y = _basic(b, y, m.Conv2d_2a_3x3)
+    b.begin_unit(y)
+    y = _basic(b, y, m.Conv2d_2b_3x3)
+    b.begin_unit(y)
+    y = b.pool(y, "max", 3, 2, 0)
+    b.begin_unit(y)
+    y = _basic(b, y, m.Conv2d_3b_1x1)
+    b.begin_unit(y)
+    y = _basic(b, y, m.Conv2d_4a_3x3)
+    b.begin_unit(y)
+    y = b.pool(y, "max", 3, 2, 0)
+
+    def cat(H, W, Cc):
+        return b.tensor(H, W, Cc)
+
+    for blk in (m.Mixed_5b, m.Mixed_5c, m.Mixed_5d):  # InceptionA
+        b.begin_unit(y)
+        H, W, _, _ = b.shape(y)
+        pf = blk.branch_pool.conv.out_channels
+        out = cat(H, W, 64 + 64 + 96 + pf)
+        _basic(b, y, blk.branch1x1, out, 0)
+        t = _basic(b, y, blk.branch5x5_1)
+        _basic(b, t, blk.branch5x5_2, out, 64)
+        t = _basic(b, y, blk.branch3x3dbl_1)
+        t = _basic(b, t, blk.branch3x3dbl_2)
+        _basic(b, t, blk.branch3x3dbl_3, out, 128)
+        t = b.pool(y, "avg", 3, 1, 1)
+        _basic(b, t, blk.branch_pool, out, 224)
+        y = out
+    blk = m.Mixed_6a  # InceptionB
+    b.begin_unit(y)
+    H, W, Cc, _ = b.shape(y)
+    Ho, Wo = (H - 3) // 2 + 1, (W - 3) // 2 + 1
+    out = cat(Ho, Wo, 384 + 96 + Cc)
+    _basic(b, y, blk.branch3x3, out, 0)
+    t = _basic(b, y, blk.branch3x3dbl_1)
+    t = _basic(b, t, blk.branch3x3dbl_2)
+    _basic(b, t, blk.branch3x3dbl_3, out, 384)
+    b.pool(y, "max", 3, 2, 0, out=out, out_coff=480)
+    y = out
+    for blk in (m.Mixed_6b, m.Mixed_6c, m.Mixed_6d, m.Mixed_6e):  # InceptionC
+        b.begin_unit(y)
+        H, W, _, _ = b.shape(y)
+        out = cat(H, W, 768)
+        _basic(b, y, blk.branch1x1, out, 0)
+        t = _basic(b, y, blk.branch7x7_1)
+        t = _basic(b, t, blk.branch7x7_2)
+        _basic(b, t, blk.branch7x7_3, out, 192)
+        t = _basic(b, y, blk.branch7x7dbl_1)
+        t = _basic(b, t, blk.branch7x7dbl_2)
+        t = _basic(b, t, blk.branch7x7dbl_3)
+        t = _basic(b, t, blk.branch7x7dbl_4)
+        _basic(b, t, blk.branch7x7dbl_5, out, 384)
+        t = b.pool(y, "avg", 3, 1, 1)
+        _basic(b, t, blk.branch_pool, out, 576)
+        y = out
+    blk = m.Mixed_7a  # InceptionD
+    b.begin_unit(y)
+    H, W, Cc, _ = b.shape(y)
+    Ho, Wo = (H - 3) // 2 + 1, (W - 3) // 2 + 1
+    out = cat(Ho, Wo, 320 + 192 + Cc)
+    t = _basic(b, y, blk.branch3x3_1)
+    _basic(b, t, blk.branch3x3_2, out, 0)
+    t = _basic(b, y, blk.branch7x7x3_1)
+    t = _basic(b, t, blk.branch7x7x3_2)
+    t = _basic(b, t, blk.branch7x7x3_3)
+    _basic(b, t, blk.branch7x7x3_4, out, 320)
+    b.pool(y, "max", 3, 2, 0, out=out, out_coff=512)
+    y = out
+    for blk in (m.Mixed_7b, m.Mixed_7c):  # InceptionE
+        b.begin_unit(y)
+        H, W, _, _ = b.shape(y)
+        out = cat(H, W, 2048)
+        _basic(b, y, blk.branch1x1, out, 0)
+        t = _basic(b, y, blk.branch3x3_1)
+        _basic(b, t, blk.branch3x3_2a, out, 320)
+        _basic(b, t, blk.branch3x3_2b, out, 704)
+        t = _basic(b, y, blk.branch3x3dbl_1)
+        t = _basic(b, t, blk.branch3x3dbl_2)
+        _basic(b, t, blk.branch3x3dbl_3a, out, 1088)
+        _basic(b, t, blk.branch3x3dbl_3b, out, 1472)
+        t = b.pool(y, "avg", 3, 1, 1)
+        _basic(b, t, blk.branch_pool, out, 1856)
+        y = out
+    b.begin_unit(y)
+    p = b.gap(y)
+    out = b.fc(p, m.fc, out_dtype=F32)
+    return b.finish(out)
+
+
+def build_chain(name: str, seed: int = 0, module: nn.Module | None = None) -> UnitChain:
+    m = module if module is not None else torch_model(name, seed)
+    if name in ("resnet50", "resnet18"):
+        return _resnet_chain(name, m)
+    if name == "vgg16":
+        return _vgg16_chain(m)
+    if name == "inception_v3":
+        return _inception_chain(m)
+    if name == "bert_base":
+        from .bert import bert_chain
+
+        return bert_chain(m)
+    raise KeyError(f"unknown model {name!r}")
+
+
+MODELS = ("resnet18", "resnet50", "vgg16", "inception_v3", "bert_base")

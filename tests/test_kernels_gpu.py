@@ -27,10 +27,11 @@ def _conv_case(k, H, W, Cin, Cout, R, S, stride, pad, residual, relu, cin_pad=No
     x = torch.randn(k, H, W, Cin, generator=g)
     w = torch.randn(Cout, Cin, R, S, generator=g) / (Cin * R * S) ** 0.5
     b = torch.randn(Cout, generator=g) * 0.1
-    Ho = (H + 2 * pad - R) // stride + 1
-    Wo = (W + 2 * pad - S) // stride + 1
+    ph, pw = pad if isinstance(pad, tuple) else (pad, pad)
+    Ho = (H + 2 * ph - R) // stride + 1
+    Wo = (W + 2 * pw - S) // stride + 1
     xb = x.to(torch.bfloat16)
-    ref = F.conv2d(xb.float().permute(0, 3, 1, 2), w.to(torch.bfloat16).float(), b, stride=stride, padding=pad)
+    ref = F.conv2d(xb.float().permute(0, 3, 1, 2), w.to(torch.bfloat16).float(), b, stride=stride, padding=(ph, pw))
     ref = ref.permute(0, 2, 3, 1)
     res = None
     if residual:
@@ -50,7 +51,7 @@ def _conv_case(k, H, W, Cin, Cout, R, S, stride, pad, residual, relu, cin_pad=No
     descs = [tensor_desc(H, W, cin_pad), tensor_desc(Ho, Wo, out_c), tensor_desc(Ho, Wo, Cout)]
     tensors = [xin, y, res.to(dev) if residual else y]
     op = N.make_op(N.GX_OP_CONV, 0, 1, in2=2 if residual else -1, out_coff=out_coff,
-                   act=N.GX_ACT_RELU if relu else N.GX_ACT_NONE, R=R, S=S, sh=stride, sw=stride, ph=pad, pw=pad,
+                   act=N.GX_ACT_RELU if relu else N.GX_ACT_NONE, R=R, S=S, sh=stride, sw=stride, ph=ph, pw=pw,
                    Cin=cin_pad, Cout=Cout, w_off=w_off, b_off=b_off)
     run_op(op, tensors, descs, wdev, k, sm_budget)
     torch.cuda.synchronize()
@@ -70,7 +71,15 @@ def _conv_case(k, H, W, Cin, Cout, R, S, stride, pad, residual, relu, cin_pad=No
         (2, 14, 14, 256, 512, 1, 1, 2, 0, False, False), # stride-2 downsample 1x1
         (1, 7, 7, 512, 2048, 1, 1, 1, 0, True, True),    # layer4 expand, many N tiles
         (5, 7, 7, 512, 512, 3, 3, 1, 1, False, True),    # M not a multiple of 128
-        (1, 17, 17, 192, 160, 1, 7, 1, 0, False, True),  # Inception 1x7 (pad handled below)
+        (1, 17, 17, 192, 160, 1, 7, 1, 0, False, True),  # 1x7 unpadded
+        (2, 17, 17, 128, 192, 1, 7, 1, (0, 3), False, True),  # Inception 1x7, asymmetric pad
+        (2, 17, 17, 128, 128, 7, 1, 1, (3, 0), False, True),  # Inception 7x1
+        (3, 8, 8, 384, 384, 1, 3, 1, (0, 1), False, True),    # Inception E 1x3
+        (2, 35, 35, 288, 64, 1, 1, 1, 0, False, True),        # Cin % 64 != 0 -> cp.async path
+        (2, 35, 35, 288, 384, 3, 3, 2, 0, False, True),       # Mixed_6a 3x3 s2 on 288 ch
+        (2, 35, 35, 64, 96, 5, 5, 1, 2, False, True),         # 5x5
+        (16, 7, 7, 512, 512, 3, 3, 1, 1, True, True),         # tail tile + residual
+        (3, 14, 14, 1024, 2048, 1, 1, 2, 0, False, False),    # downsample into layer4
     ],
 )
 def test_conv_matches_torch(k, H, W, Cin, Cout, R, S, stride, pad, residual, relu):

@@ -1,0 +1,56 @@
+"""Host-side checks of the unit chains against the oracle (no GPU): boundary shapes, payload
+bytes, unit counts as SURVEY App. B lists them, and BN folding arithmetic."""
+import pytest
+import torch
+
+from oracle.units import run_span, units_for
+from paper_2312_10636_b200.models import build_chain, torch_model
+
+CASES = {"resnet18": (10, 224), "resnet50": (18, 224), "vgg16": (8, 224), "inception_v3": (19, 299)}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_chain_boundaries_match_oracle(name):
+    n_units, res = CASES[name]
+    m = torch_model(name)
+    chain = build_chain(name, module=m)
+    assert chain.n_units == n_units
+    units = units_for(name, m)
+    assert len(units) == n_units
+    x = torch.randn(1, 3, res, res)
+    for p in range(n_units):
+        if p > 0:
+            H, W, Cc, _ = chain.boundary_shape(p)
+            if x.dim() == 4:
+                assert tuple(x.shape[1:]) == (Cc, H, W), (p, x.shape, (H, W, Cc))
+            else:
+                assert x.shape[1] == H * W * Cc
+        x = run_span(units, p, p + 1, x)
+    assert x.shape == (1, 1000)
+    assert chain.boundary_elems(n_units) == 1000
+
+
+def test_resnet50_payloads_match_survey_appendix_b():
+    chain = build_chain("resnet50")
+    # SURVEY App. B lists bf16 bytes; the wire format is fp32 (PAPER.md:463, 588 KB input)
+    bf16 = {1: 401_408, 2: 1_605_632, 5: 802_816, 9: 401_408, 15: 200_704}
+    for p, b in bf16.items():
+        assert chain.payload_bytes(p) == 2 * b
+    assert chain.payload_bytes(0) == 3 * 224 * 224 * 4
+    gflop = sum(chain.unit_flops) / 1e9
+    assert abs(gflop - 8.18) < 0.05
+
+
+def test_bn_folding_matches_module():
+    from paper_2312_10636_b200.device import pack_conv_weight
+    m = torch_model("resnet18")
+    conv, bn = m.layer1[0].conv1, m.layer1[0].bn1
+    x = torch.randn(2, 64, 9, 9)
+    ref = bn(conv(x))
+    scale = bn.weight / torch.sqrt(bn.running_var + bn.eps)
+    w = conv.weight * scale[:, None, None, None]
+    b = bn.bias - bn.running_mean * scale
+    got = torch.nn.functional.conv2d(x, w, b, padding=1)
+    assert torch.allclose(got, ref, atol=1e-4, rtol=1e-4)
+    packed = pack_conv_weight(w.detach())
+    assert packed.shape == (64, 576)
