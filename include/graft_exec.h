@@ -177,19 +177,26 @@ typedef struct gx_serve_stage {
   int32_t out_final;    /* 1: the stage output is the chain output (logits)                 */
 } gx_serve_stage;
 
-typedef struct gx_serve_route { /* _Route (simulator.py:103-107) */
+typedef struct gx_serve_route { /* _Route (simulator.py:103-107) + the arrival terms of _gen_request */
   int32_t n_stages;
-  int32_t stage[2];
-  double worst_rem_ms;
-  double arrive_offset_ms; /* mobile(p) + transfer(payload(p)) at the client's bandwidth     */
-  const void* ingress;     /* WALL: device (or pinned host) fp32 entry activation template   */
+  int32_t stage[2];        /* align stage (if any) then shared stage                          */
+  double worst_rem_ms;     /* 2 * (d_align + d_shared), simulator.py:290                       */
+  double mobile_ms;        /* DeviceProfile.mobile_ms(model, point), profiles.py:126-131       */
+  int64_t payload_bytes;   /* ModelSpec.payload_bytes(point), profiles.py:67-74                */
+  const void* ingress;     /* WALL: entry activation template (device, or pinned host)         */
   int64_t ingress_bytes;
+  int32_t ingress_dtype;   /* GX_F32 (client wire format)                                      */
+  int32_t ingress_channels;/* channels per pixel the client ships (3 at the image boundary)    */
 } gx_serve_route;
 
-typedef struct gx_serve_client {
+typedef struct gx_serve_client { /* ClientSpec (workload.py:98-117), clients sorted by id */
   double rate_rps, slo_ms;
-  int32_t route; /* -1: no route (dropped at generation) */
-  const double* gen_ms; int64_t n_gen; /* pre-drawn generation times (Poisson) or NULL      */
+  int32_t route;              /* -1: no route (dropped at generation)                         */
+  const double* gen_gaps_ms;  /* Poisson: pre-drawn inter-arrival gaps, first from t=0; NULL = 1000/rate */
+  int64_t n_gaps;
+  const double* trace_t_s;    /* BandwidthTrace (workload.py:30-43)                           */
+  const double* trace_mbps;
+  int64_t n_trace;
 } gx_serve_client;
 
 typedef struct gx_serve_cfg {

@@ -54,12 +54,15 @@ class GxServeStage(C.Structure):
 
 class GxServeRoute(C.Structure):
     _fields_ = [("n_stages", C.c_int32), ("stage", C.c_int32 * 2), ("worst_rem_ms", C.c_double),
-                ("arrive_offset_ms", C.c_double), ("ingress", C.c_void_p), ("ingress_bytes", C.c_int64)]
+                ("mobile_ms", C.c_double), ("payload_bytes", C.c_int64), ("ingress", C.c_void_p),
+                ("ingress_bytes", C.c_int64), ("ingress_dtype", C.c_int32), ("ingress_channels", C.c_int32)]
 
 
 class GxServeClient(C.Structure):
     _fields_ = [("rate_rps", C.c_double), ("slo_ms", C.c_double), ("route", C.c_int32),
-                ("gen_ms", C.POINTER(C.c_double)), ("n_gen", C.c_int64)]
+                ("gen_gaps_ms", C.POINTER(C.c_double)), ("n_gaps", C.c_int64),
+                ("trace_t_s", C.POINTER(C.c_double)), ("trace_mbps", C.POINTER(C.c_double)),
+                ("n_trace", C.c_int64)]
 
 
 class GxServeCfg(C.Structure):

@@ -36,12 +36,14 @@ struct SmemPlan {
   uint64_t* empty;
   uint64_t* tfull;
   uint64_t* tempty;
-  uint64_t* efull;
+  uint64_t* rfull;  // [2] residual slot filled
+  uint64_t* bfull;  // bias vector staged
   uint32_t* tslot;
   int2* ktab;
 };
 
 __host__ __device__ inline int res_groups(int BN) { return (BN + 63) / 64; }
+__host__ __device__ inline uint32_t bias_alloc(int Cout) { return (static_cast<uint32_t>(Cout) * 4u + 1023u) & ~1023u; }
 
 template <bool kTmaA>
 __global__ void __launch_bounds__(kConvThreads, 1)
@@ -57,13 +59,15 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   sp.sA = smem;
   sp.sB = sp.sA + static_cast<size_t>(S_) * kATileBytes;
   sp.sRes = sp.sB + static_cast<size_t>(S_) * b_bytes;
-  sp.sBias = reinterpret_cast<float*>(sp.sRes + (has_res ? res_groups(BN) * kResGroupBytes : 0));
-  sp.full = reinterpret_cast<uint64_t*>(sp.sBias + 256);
+  const uint32_t res_slot_bytes = has_res ? res_groups(BN) * kResGroupBytes : 0u;
+  sp.sBias = reinterpret_cast<float*>(sp.sRes + a.nres * res_slot_bytes);
+  sp.full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sp.sBias) + bias_alloc(a.Cout));
   sp.empty = sp.full + S_;
   sp.tfull = sp.empty + S_;
   sp.tempty = sp.tfull + 2;
-  sp.efull = sp.tempty + 2;
-  sp.tslot = reinterpret_cast<uint32_t*>(sp.efull + 1);
+  sp.rfull = sp.tempty + 2;
+  sp.bfull = sp.rfull + 2;
+  sp.tslot = reinterpret_cast<uint32_t*>(sp.bfull + 1);
   sp.ktab = reinterpret_cast<int2*>(sp.tslot + 4);
 
   const int tid = threadIdx.x;
@@ -99,7 +103,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         mbar_init(&sp.tfull[i], 1);
         mbar_init(&sp.tempty[i], 128);
       }
-      mbar_init(sp.efull, 1);
+      mbar_init(&sp.rfull[0], 1);
+      mbar_init(&sp.rfull[1], 1);
+      mbar_init(sp.bfull, 1);
       fence_barrier_init();
     }
     __syncwarp();
@@ -173,21 +179,31 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           wc = (rem - ho0 * a.Wo) * a.sw - a.pw;
           hc = ho0 * a.sh - a.ph;
         }
-        int c0 = 0, r = 0, s = 0;  // filter tap / channel block of k-block kb
+        // (filter row r, filter col s, channel block c0) of the next im2col load; K is ordered
+        // (r, s, c).  Loads past the last tap (K padding) read real pixels, but the matching
+        // packed weights are zero, so they contribute nothing.
+        int c0 = 0, r = 0, s = 0;
+        const int cpl = a.cpl;
+        const uint32_t region = static_cast<uint32_t>(kBM * cpl * 2);
         for (int kb = 0; kb < a.num_kb; ++kb, ++it) {
           const int st = it % S_;
           const uint32_t ph = (it / S_) & 1;
           mbar_wait(&sp.empty[st], ph ^ 1);
           mbar_arrive_expect_tx(&sp.full[st], tx);
-          if (kTmaA) {
-            tma_load_im2col_4d(sp.sA + st * kATileBytes, &amap, &sp.full[st], c0, wc, hc, nimg,
-                               static_cast<uint16_t>(s), static_cast<uint16_t>(r));
-            c0 += kBK;
-            if (c0 == a.Cin) {
-              c0 = 0;
-              if (++s == a.S) {
-                s = 0;
-                ++r;
+          if (kTmaA && a.a2d) {
+            // 1x1 / stride 1 / no padding: A is the plain [M, C] activation matrix
+            tma_load_2d(sp.sA + st * kATileBytes, &amap, &sp.full[st], kb * kBK, m_blk * kBM);
+          } else if (kTmaA) {
+            for (int l = 0; l < kBK / cpl; ++l) {
+              tma_load_im2col_4d(sp.sA + st * kATileBytes + l * region, &amap, &sp.full[st], c0, wc, hc, nimg,
+                                 static_cast<uint16_t>(s), static_cast<uint16_t>(r));
+              c0 += cpl;
+              if (c0 == a.Cin) {
+                c0 = 0;
+                if (++s == a.S) {
+                  s = 0;
+                  ++r;
+                }
               }
             }
           }
@@ -210,10 +226,22 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           const uint32_t ph = (it / S_) & 1;
           mbar_wait(&sp.full[st], ph);
           tc_fence_after();
-          const uint64_t ad = umma_desc_sw128(sp.sA + st * kATileBytes);
+          const uint32_t abase = smem_u32(sp.sA + st * kATileBytes);
           const uint64_t bd = umma_desc_sw128(sp.sB + static_cast<size_t>(st) * b_bytes);
+          if (!kTmaA || a.cpl == 64) {
+            const uint64_t ad = umma_desc_kmajor(abase, 64, 0);
 #pragma unroll
-          for (int kk = 0; kk < kBK / 16; ++kk) umma_bf16(d, ad + 2 * kk, bd + 2 * kk, a.idesc, (kb | kk) != 0);
+            for (int kk = 0; kk < kBK / 16; ++kk) umma_bf16(d, ad + 2 * kk, bd + 2 * kk, a.idesc, (kb | kk) != 0);
+          } else {
+            // A stage = 64/cpl regions of 128 rows x cpl channels; MMA kk covers K [16kk, 16kk+16)
+            const uint32_t region = static_cast<uint32_t>(kBM * a.cpl * 2);
+#pragma unroll
+            for (int kk = 0; kk < kBK / 16; ++kk) {
+              const int e0 = kk * 16;
+              const uint32_t addr = abase + (e0 / a.cpl) * region + (e0 % a.cpl) * 2;
+              umma_bf16(d, umma_desc_kmajor(addr, a.cpl, region), bd + 2 * kk, a.idesc, (kb | kk) != 0);
+            }
+          }
           umma_commit(&sp.empty[st]);
         }
         umma_commit(&sp.tfull[acc]);
@@ -224,9 +252,27 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;
     const bool leader = warp == 6 && lane == 0;
+    const int nres = a.nres;
+    // residual tile of the t-th tile this CTA processes -> slot t % nres
+    auto issue_res = [&](int t_idx) {
+      const int tile = blockIdx.x + t_idx * gridDim.x;
+      if (tile >= a.num_tiles) return;
+      const int slot = t_idx % nres;
+      mbar_arrive_expect_tx(&sp.rfull[slot], res_slot_bytes);
+      for (int g = 0; g < res_groups(BN); ++g)
+        tma_load_2d(sp.sRes + slot * res_slot_bytes + g * kResGroupBytes, &rmap, &sp.rfull[slot],
+                    (tile % a.n_tiles) * BN + g * 64, (tile / a.n_tiles) * kBM);
+    };
     if (leader) {
-      tma_prefetch_desc(&rmap);
+      // the whole bias vector once per CTA; residual tiles run ahead by `nres` tiles
+      mbar_arrive_expect_tx(sp.bfull, static_cast<uint32_t>(a.Cout) * 4u);
+      bulk_load(sp.sBias, a.bias, static_cast<uint32_t>(a.Cout) * 4u, sp.bfull);
+      if (has_res) {
+        tma_prefetch_desc(&rmap);
+        for (int i = 0; i < nres; ++i) issue_res(i);
+      }
     }
+    mbar_wait(sp.bfull, 0);
     int t = 0;
     for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++t) {
       const int m_blk = tile / a.n_tiles;
@@ -234,21 +280,14 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       const int m0 = m_blk * kBM;
       const int nb0 = n_blk * BN;
       const int ncols = min(BN, a.Cout - nb0);
-      if (leader) {
-        // stage this tile's bias and residual while the MMAs run
-        const uint32_t bias_bytes = static_cast<uint32_t>(ncols) * 4u;
-        const uint32_t res_bytes = has_res ? res_groups(BN) * kResGroupBytes : 0u;
-        mbar_arrive_expect_tx(sp.efull, bias_bytes + res_bytes);
-        bulk_load(sp.sBias, a.bias + nb0, bias_bytes, sp.efull);
-        if (has_res)
-          for (int g = 0; g < res_groups(BN); ++g)
-            tma_load_2d(sp.sRes + g * kResGroupBytes, &rmap, sp.efull, nb0 + g * 64, m0);
-      }
+      const int slot = has_res ? t % nres : 0;
+      const float* bias = sp.sBias + nb0;
+      const uint8_t* res_base = sp.sRes + slot * res_slot_bytes;
       const int acc = t & 1;
       const uint32_t aph = (t >> 1) & 1;
       mbar_wait(&sp.tfull[acc], aph);
       tc_fence_after();
-      mbar_wait(sp.efull, t & 1);
+      if (has_res) mbar_wait(&sp.rfull[slot], (t / nres) & 1);
       const int m = m0 + row;
       const bool row_ok = m < a.M;
       const uint32_t tbase = tmem_base + acc * acc_stride + (static_cast<uint32_t>(q * 32) << 16);
@@ -260,9 +299,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           const int n0 = nb0 + c;
           float f[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]) + sp.sBias[c + i];
+          for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]) + bias[c + i];
           if (has_res) {
-            const uint8_t* rrow = sp.sRes + (c >> 6) * kResGroupBytes + row * 128;
+            const uint8_t* rrow = res_base + (c >> 6) * kResGroupBytes + row * 128;
             const int j0 = (c & 63) >> 3;
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
@@ -305,7 +344,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&sp.tempty[acc]);
-      named_bar_sync(1, 128);  // every epilogue thread is done with sBias/sRes of this tile
+      if (has_res) {
+        named_bar_sync(1, 128);  // every epilogue thread is done with this residual slot
+        if (leader) issue_res(t + nres);
+      }
     }
   }
   // Let the next kernel in the stream start its prologue.
@@ -319,19 +361,30 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 }
 }  // namespace
 
-size_t conv_smem_bytes(int BN, int stages, int num_kb, bool res) {
-  return 1024 + static_cast<size_t>(stages) * (kATileBytes + BN * 128) + (res ? res_groups(BN) * kResGroupBytes : 0) +
-         1024 /*bias*/ + (2 * stages + 5) * 8 + 16 + static_cast<size_t>(num_kb) * 8 * sizeof(int2);
+size_t conv_smem_bytes(int BN, int stages, int num_kb, int nres, int Cout) {
+  return 1024 + static_cast<size_t>(stages) * (kATileBytes + BN * 128) +
+         static_cast<size_t>(nres) * res_groups(BN) * kResGroupBytes + bias_alloc(Cout) + (2 * stages + 9) * 8 + 16 +
+         static_cast<size_t>(num_kb) * 8 * sizeof(int2);
 }
 
-int conv_pick_stages(int BN, int num_kb, bool res) {
-  const size_t fixed = 1024 + (res ? res_groups(BN) * kResGroupBytes : 0) + 1024 + 64 +
-                       static_cast<size_t>(num_kb) * 8 * sizeof(int2);
+// Pipeline depth and residual slots that fit in ~220 KB: prefer >= 3 stages with a double-
+// buffered residual, else a single residual slot.
+int conv_pick_stages(int BN, int num_kb, bool res, int Cout, int* nres_out) {
   const size_t budget = 220 * 1024;
-  int s = budget > fixed ? static_cast<int>((budget - fixed - 16 * 8) / (kATileBytes + BN * 128 + 16)) : 2;
-  if (s > 8) s = 8;
-  if (s < 2) s = 2;
-  return s;
+  const size_t per_stage = kATileBytes + BN * 128 + 16;
+  int best_s = 2, best_r = res ? 1 : 0;
+  for (int nres = res ? 2 : 0; nres >= (res ? 1 : 0); --nres) {
+    const size_t fixed = conv_smem_bytes(BN, 0, num_kb, nres, Cout);
+    int s = budget > fixed ? static_cast<int>((budget - fixed) / per_stage) : 0;
+    if (s > 8) s = 8;
+    if (s >= 3 || nres <= 1) {
+      best_s = s < 2 ? 2 : s;
+      best_r = nres;
+      break;
+    }
+  }
+  *nres_out = best_r;
+  return best_s;
 }
 
 cudaError_t launch_conv(const CUtensorMap& wmap, const CUtensorMap& amap, const CUtensorMap& rmap,
@@ -347,7 +400,7 @@ cudaError_t launch_conv(const CUtensorMap& wmap, const CUtensorMap& amap, const 
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);
   cfg.blockDim = dim3(kConvThreads, 1, 1);
-  cfg.dynamicSmemBytes = conv_smem_bytes(a.BN, a.stages, a.num_kb, a.res != nullptr);
+  cfg.dynamicSmemBytes = conv_smem_bytes(a.BN, a.stages, a.num_kb, a.nres, a.Cout);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

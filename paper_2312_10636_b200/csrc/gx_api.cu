@@ -79,7 +79,7 @@ static PFN_encodeIm2col_t im2col_fn() {
 // NHWC input as a rank-4 (C, W, H, N) im2col map: 128 output pixels x 64 channels per load.
 // Box corners follow the fprop convention: lower = -pad, upper = pad - (filter - 1).
 bool encode_tmap_im2col_bf16(CUtensorMap* map, const void* base, int C, int W, int H, int N, int lower_w,
-                             int lower_h, int upper_w, int upper_h, int stride_w, int stride_h) {
+                             int lower_h, int upper_w, int upper_h, int stride_w, int stride_h, int cpl) {
   PFN_encodeIm2col_t fn = im2col_fn();
   if (fn == nullptr) return false;
   cuuint64_t dims[4] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
@@ -89,8 +89,12 @@ bool encode_tmap_im2col_bf16(CUtensorMap* map, const void* base, int C, int W, i
   int lower[2] = {lower_w, lower_h};
   int upper[2] = {upper_w, upper_h};
   cuuint32_t es[4] = {1, static_cast<cuuint32_t>(stride_w), static_cast<cuuint32_t>(stride_h), 1};
-  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, lower, upper, kBK, kBM,
-            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+  const CUtensorMapSwizzle sw = cpl == 64   ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : cpl == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                : cpl == 16 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                            : CU_TENSOR_MAP_SWIZZLE_NONE;
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, lower, upper,
+            static_cast<cuuint32_t>(cpl), kBM, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -154,6 +158,10 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
   a.Cout = op.Cout;
   a.m_tiles = (a.M + kBM - 1) / kBM;
   a.BN = pick_bn(op.Cout, a.m_tiles, sm_budget);
+  if (const char* e = getenv("GX_BN")) {  // tuning override (development)
+    const int bn = atoi(e);
+    if (bn >= 16 && bn <= 256 && bn % 16 == 0) a.BN = bn;
+  }
   a.n_tiles = (a.Cout + a.BN - 1) / a.BN;
   a.num_tiles = a.m_tiles * a.n_tiles;
   a.bias = reinterpret_cast<const float*>(wbase + op.b_off);
@@ -165,7 +173,11 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
   a.y_f32 = to.dtype == GX_F32;
   a.act = op.act;
   a.idesc = umma_idesc_bf16(kBM, a.BN);
-  a.stages = conv_pick_stages(a.BN, a.num_kb, a.res != nullptr);
+  a.stages = conv_pick_stages(a.BN, a.num_kb, a.res != nullptr, a.Cout, &a.nres);
+  if (const char* e = getenv("GX_STAGES")) {
+    const int st = atoi(e);
+    if (st >= 1 && st <= a.stages) a.stages = st;
+  }
   a.tmem_cols = tmem_cols_for(a.BN);
   if (a.res && (T[op.in2].dtype != GX_BF16 || (a.res_ld & 7))) return fail(GX_EINVAL, "bad residual tensor");
   const int kpad = a.num_kb * kBK;
@@ -173,9 +185,15 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
   memset(&out->rmap, 0, sizeof(out->rmap));
   if (!encode_tmap_2d_bf16(&out->wmap, wbase + op.w_off, kpad, op.Cout, static_cast<uint64_t>(kpad) * 2, kBK, a.BN))
     return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for conv weights");
-  a.tma_a = (op.Cin % kBK) == 0 && getenv("GX_NO_TMA_IM2COL") == nullptr;
-  if (a.tma_a && !encode_tmap_im2col_bf16(&out->amap, a.x, ti.C, ti.W, ti.H, k, -a.pw, -a.ph, a.pw - (a.S - 1),
-                                          a.ph - (a.R - 1), a.sw, a.sh))
+  a.cpl = (op.Cin % 64 == 0) ? 64 : (op.Cin % 32 == 0) ? 32 : (op.Cin % 16 == 0) ? 16 : 8;
+  a.tma_a = getenv("GX_NO_TMA_IM2COL") == nullptr;
+  a.a2d = a.tma_a && a.R == 1 && a.S == 1 && a.sh == 1 && a.sw == 1 && a.ph == 0 && a.pw == 0 && a.cpl == 64 &&
+          a.Cin == ti.C && getenv("GX_NO_A2D") == nullptr;
+  if (a.a2d) {
+    if (!encode_tmap_2d_bf16(&out->amap, a.x, ti.C, a.M, static_cast<uint64_t>(ti.C) * 2, kBK, kBM))
+      return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for conv input");
+  } else if (a.tma_a && !encode_tmap_im2col_bf16(&out->amap, a.x, ti.C, ti.W, ti.H, k, -a.pw, -a.ph, a.pw - (a.S - 1),
+                                          a.ph - (a.R - 1), a.sw, a.sh, a.cpl))
     return fail(GX_ECUDA, "cuTensorMapEncodeIm2col failed for conv input");
   if (a.res && !encode_tmap_2d_bf16(&out->rmap, a.res, a.res_ld, a.M, static_cast<uint64_t>(a.res_ld) * 2, 64, kBM))
     return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for the residual");

@@ -1,6 +1,7 @@
 // Internal declarations shared by the libgx translation units.
 #pragma once
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -41,18 +42,21 @@ struct ConvArgs {
   uint32_t idesc;
   int stages;
   uint32_t tmem_cols;
-  int tma_a;  // A operand via im2col TMA (Cin % 64 == 0), else cp.async im2col producers
+  int tma_a;  // A operand via im2col TMA, else cp.async im2col producers
+  int cpl;    // channels per im2col TMA load (8/16/32/64): Cin % cpl == 0, cpl | 64
+  int nres;   // residual smem slots (0 without residual, else 1 or 2)
+  int a2d;    // A via a plain 2D tiled map over [M, C] (1x1, stride 1, no padding)
 };
 constexpr int kConvThreads = 320;  // 4 A-producer warps, TMA warp, MMA warp, 4 epilogue warps
 constexpr int kBM = 128;
 constexpr int kBK = 64;
-size_t conv_smem_bytes(int BN, int stages, int num_kb, bool res);
-int conv_pick_stages(int BN, int num_kb, bool res);
+size_t conv_smem_bytes(int BN, int stages, int num_kb, int nres, int Cout);
+int conv_pick_stages(int BN, int num_kb, bool res, int Cout, int* nres_out);
 // wmap: weights [Cout][Kpad]; amap: im2col map of the input (tma_a); rmap: residual [M][res_ld].
 cudaError_t launch_conv(const CUtensorMap& wmap, const CUtensorMap& amap, const CUtensorMap& rmap,
                         const ConvArgs& a, int grid, cudaStream_t s, bool pdl);
 bool encode_tmap_im2col_bf16(CUtensorMap* map, const void* base, int C, int W, int H, int N, int lower_w,
-                             int lower_h, int upper_w, int upper_h, int stride_w, int stride_h);
+                             int lower_h, int upper_w, int upper_h, int stride_w, int stride_h, int cpl);
 
 // ------------------------------------------------------------------ bandwidth-bound kernels
 cudaError_t launch_gather(int k, const void* const* src, const int32_t* src_dtype, int64_t pixels,

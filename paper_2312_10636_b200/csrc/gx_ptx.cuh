@@ -145,6 +145,25 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(const void* smem_tile) {
   const uint64_t addr = smem_u32(smem_tile);
   return ((addr >> 4) & 0x3FFFull) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
 }
+// K-major descriptor for an A region written by an im2col TMA with `cpl` channels per pixel:
+//   cpl 64 -> SWIZZLE_128B (rows 128 B, 8-row atoms 1024 B apart)
+//   cpl 32 -> SWIZZLE_64B  (rows 64 B, atoms 512 B)
+//   cpl 16 -> SWIZZLE_32B  (rows 32 B, atoms 256 B)
+//   cpl  8 -> no swizzle: core matrices 8 rows x 16 B (SBO 128 B); the next 8 K-elements are the
+//             next tap's region, `lbo` bytes further (LBO).
+__device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t saddr, int cpl, uint32_t lbo) {
+  uint64_t d = ((static_cast<uint64_t>(saddr) >> 4) & 0x3FFFull) | (1ull << 46);
+  switch (cpl) {
+    case 64:
+      return d | (1ull << 16) | (64ull << 32) | (2ull << 61);
+    case 32:
+      return d | (1ull << 16) | (32ull << 32) | (4ull << 61);
+    case 16:
+      return d | (1ull << 16) | (16ull << 32) | (6ull << 61);
+    default:
+      return d | (static_cast<uint64_t>(lbo >> 4) << 16) | (8ull << 32);
+  }
+}
 // Instruction descriptor for kind::f16: bf16 x bf16 -> fp32, both operands K-major.
 __host__ __device__ constexpr uint32_t umma_idesc_bf16(int M, int N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);

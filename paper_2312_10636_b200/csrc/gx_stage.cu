@@ -4,6 +4,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -97,10 +98,11 @@ int capture_span(gx_stage* st, int k, gx_stage::PerK* out) {
   GX_CUDA(cudaStreamBeginCapture(st->stream, cudaStreamCaptureModeThreadLocal));
   int kernels = 0;
   int rc = GX_OK;
+  const bool use_pdl = getenv("GX_NO_PDL") == nullptr;
   for (size_t i = 0; i < st->ops.size() && rc == GX_OK; ++i) {
     const gx_op& op = m->ops[st->ops[i]];
     const bool is_conv = op.kind == GX_OP_CONV || op.kind == GX_OP_LINEAR;
-    rc = launch_op(op, m->tensors.data(), st->tptr.data(), wbase, k, st->sm_budget, st->stream, /*pdl=*/true,
+    rc = launch_op(op, m->tensors.data(), st->tptr.data(), wbase, k, st->sm_budget, st->stream, use_pdl,
                    is_conv ? &plans[i] : nullptr, &kernels);
   }
   cudaError_t e = cudaStreamEndCapture(st->stream, &graph);

@@ -170,6 +170,7 @@ __global__ void gap_kernel(const __nv_bfloat16* __restrict__ x, int N, int HW, i
     const int c8 = static_cast<int>(i % cv);
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const uint4* base = reinterpret_cast<const uint4*>(x + static_cast<int64_t>(n) * HW * C) + c8;
+#pragma unroll 7
     for (int p = 0; p < HW; ++p) {
       const uint4 v = __ldg(base + static_cast<int64_t>(p) * cv);
       const uint32_t w[4] = {v.x, v.y, v.z, v.w};
@@ -190,79 +191,94 @@ __global__ void gap_kernel(const __nv_bfloat16* __restrict__ x, int N, int HW, i
 }
 
 // Skinny FC at small batch (weight-streaming, HBM-bound): y[n][o] = x[n] . w[o] + b[o].
-// One warp per group of 4 output features; lanes stride K in 16-byte vectors; the batch rows are
-// processed 8 at a time so x stays in registers/L1 and each weight byte is read once.
-constexpr int kFcOut = 4;
-constexpr int kFcRows = 8;
-__global__ void fc_kernel(const __nv_bfloat16* __restrict__ x, int N, int K, const __nv_bfloat16* __restrict__ w,
-                          const float* __restrict__ b, void* __restrict__ y, int Nout, int y_f32, int act) {
-  const int lane = threadIdx.x & 31;
-  const int warps_total = gridDim.x * (blockDim.x >> 5);
-  const int groups = (Nout + kFcOut - 1) / kFcOut;
-  const int kv = K / 8;
-  for (int g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < groups; g += warps_total) {
-    const int o0 = g * kFcOut;
+// Block = 8 warps; warp w owns OPW consecutive output features; lanes stride K in 16-byte
+// vectors.  The batch rows are staged in shared memory one K-chunk at a time (each weight byte is
+// read from HBM exactly once, x comes from smem), 16 rows per accumulator pass.
+constexpr int kFcWarps = 8;
+constexpr int kFcRows = 16;
+constexpr int kFcKChunk = 2048;
+template <int OPW>
+__global__ void __launch_bounds__(256) fc_kernel(const __nv_bfloat16* __restrict__ x, int N, int K,
+                                                 const __nv_bfloat16* __restrict__ w, const float* __restrict__ b,
+                                                 void* __restrict__ y, int Nout, int y_f32, int act) {
+  extern __shared__ uint4 xs[];  // [kFcRows][kFcKChunk / 8]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int groups = (Nout + kFcWarps * OPW - 1) / (kFcWarps * OPW);
+  for (int g = blockIdx.x; g < groups; g += gridDim.x) {
+    const int o0 = (g * kFcWarps + warp) * OPW;
     for (int n0 = 0; n0 < N; n0 += kFcRows) {
-      float acc[kFcOut][kFcRows];
+      const int rows = min(kFcRows, N - n0);
+      float acc[OPW][kFcRows];
 #pragma unroll
-      for (int a = 0; a < kFcOut; ++a)
+      for (int a = 0; a < OPW; ++a)
 #pragma unroll
         for (int r = 0; r < kFcRows; ++r) acc[a][r] = 0.0f;
-      for (int v = lane; v < kv; v += 32) {
-        float wf[kFcOut][8];
-#pragma unroll
-        for (int a = 0; a < kFcOut; ++a) {
-          uint4 wv = make_uint4(0, 0, 0, 0);
-          if (o0 + a < Nout) wv = __ldg(reinterpret_cast<const uint4*>(w + static_cast<int64_t>(o0 + a) * K) + v);
-          const uint32_t ww[4] = {wv.x, wv.y, wv.z, wv.w};
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float2 f = unpack_bf16x2(ww[j]);
-            wf[a][2 * j] = f.x;
-            wf[a][2 * j + 1] = f.y;
-          }
+      for (int k0 = 0; k0 < K; k0 += kFcKChunk) {
+        const int kc = min(kFcKChunk, K - k0) / 8;  // 16-byte vectors in this chunk
+        __syncthreads();
+        for (int i = threadIdx.x; i < rows * kc; i += blockDim.x) {
+          const int r = i / kc, v = i - r * kc;
+          xs[r * (kFcKChunk / 8) + v] = __ldg(reinterpret_cast<const uint4*>(x + static_cast<int64_t>(n0 + r) * K + k0) + v);
         }
+        __syncthreads();
+        for (int v = lane; v < kc; v += 32) {
+          float wf[OPW][8];
 #pragma unroll
-        for (int r = 0; r < kFcRows; ++r) {
-          if (n0 + r < N) {
-            const uint4 xv = __ldg(reinterpret_cast<const uint4*>(x + static_cast<int64_t>(n0 + r) * K) + v);
-            const uint32_t xx[4] = {xv.x, xv.y, xv.z, xv.w};
-            float xf[8];
+          for (int a = 0; a < OPW; ++a) {
+            uint4 wv = make_uint4(0, 0, 0, 0);
+            if (o0 + a < Nout)
+              wv = __ldg(reinterpret_cast<const uint4*>(w + static_cast<int64_t>(o0 + a) * K + k0) + v);
+            const uint32_t ww[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-              const float2 f = unpack_bf16x2(xx[j]);
-              xf[2 * j] = f.x;
-              xf[2 * j + 1] = f.y;
+              const float2 f = unpack_bf16x2(ww[j]);
+              wf[a][2 * j] = f.x;
+              wf[a][2 * j + 1] = f.y;
             }
+          }
 #pragma unroll
-            for (int a = 0; a < kFcOut; ++a)
+          for (int r = 0; r < kFcRows; ++r) {
+            if (r < rows) {
+              const uint4 xv = xs[r * (kFcKChunk / 8) + v];
+              const uint32_t xx[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
-              for (int j = 0; j < 8; ++j) acc[a][r] = fmaf(wf[a][j], xf[j], acc[a][r]);
+              for (int j = 0; j < 4; ++j) {
+                const float2 f = unpack_bf16x2(xx[j]);
+#pragma unroll
+                for (int a = 0; a < OPW; ++a) {
+                  acc[a][r] = fmaf(wf[a][2 * j], f.x, acc[a][r]);
+                  acc[a][r] = fmaf(wf[a][2 * j + 1], f.y, acc[a][r]);
+                }
+              }
+            }
           }
         }
       }
 #pragma unroll
-      for (int a = 0; a < kFcOut; ++a)
+      for (int a = 0; a < OPW; ++a)
 #pragma unroll
         for (int r = 0; r < kFcRows; ++r) {
-          float s = acc[a][r];
+          float v = acc[a][r];
 #pragma unroll
-          for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-          acc[a][r] = s;
+          for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+          acc[a][r] = v;
         }
-      if (lane == 0) {
-        for (int a = 0; a < kFcOut; ++a) {
-          const int o = o0 + a;
-          if (o >= Nout) break;
-          for (int r = 0; r < kFcRows && n0 + r < N; ++r) {
-            float v = acc[a][r] + (b ? b[o] : 0.0f);
-            if (act == GX_ACT_RELU) v = fmaxf(v, 0.0f);
-            const int64_t idx = static_cast<int64_t>(n0 + r) * Nout + o;
-            if (y_f32)
-              static_cast<float*>(y)[idx] = v;
-            else
-              static_cast<__nv_bfloat16*>(y)[idx] = __float2bfloat16_rn(v);
-          }
+      // lane r writes row r (r < 16) for each of the warp's outputs
+#pragma unroll
+      for (int a = 0; a < OPW; ++a) {
+        const int o = o0 + a;
+        float mine = 0.0f;
+#pragma unroll
+        for (int r = 0; r < kFcRows; ++r)
+          if (lane == r) mine = acc[a][r];
+        if (o < Nout && lane < rows) {
+          float v = mine + (b ? b[o] : 0.0f);
+          if (act == GX_ACT_RELU) v = fmaxf(v, 0.0f);
+          const int64_t idx = static_cast<int64_t>(n0 + lane) * Nout + o;
+          if (y_f32)
+            static_cast<float*>(y)[idx] = v;
+          else
+            static_cast<__nv_bfloat16*>(y)[idx] = __float2bfloat16_rn(v);
         }
       }
     }
@@ -324,17 +340,30 @@ cudaError_t launch_pool(int mode, const __nv_bfloat16* x, int N, int H, int W, i
 
 cudaError_t launch_gap(const __nv_bfloat16* x, int N, int HW, int C, __nv_bfloat16* y, int grid, cudaStream_t s) {
   if (C & 7) return cudaErrorInvalidValue;
-  gap_kernel<<<grid_for(static_cast<int64_t>(N) * (C / 8), 128, grid), 128, 0, s>>>(x, N, HW, C, y);
+  gap_kernel<<<grid_for(static_cast<int64_t>(N) * (C / 8), 32, grid), 32, 0, s>>>(x, N, HW, C, y);
   return cudaGetLastError();
 }
 
 cudaError_t launch_fc(const __nv_bfloat16* x, int N, int K, const __nv_bfloat16* w, const float* b, void* y, int Nout,
                       int y_f32, int act, int grid, cudaStream_t s) {
   if (K & 7) return cudaErrorInvalidValue;
-  const int groups = (Nout + kFcOut - 1) / kFcOut;
-  const int warps_per_block = 8;
-  fc_kernel<<<grid_for(groups, warps_per_block, grid), 32 * warps_per_block, 0, s>>>(x, N, K, w, b, y, Nout, y_f32,
-                                                                                       act);
+  const size_t smem = static_cast<size_t>(kFcRows) * kFcKChunk * 2;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(fc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(fc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(fc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    configured = true;
+  }
+  const int opw = Nout >= 4096 ? 4 : Nout >= 2048 ? 2 : 1;
+  const int groups = (Nout + kFcWarps * opw - 1) / (kFcWarps * opw);
+  const int g = grid_for(groups, 1, grid / 8 > 0 ? grid / 8 : 1);
+  if (opw == 4)
+    fc_kernel<4><<<g, 256, smem, s>>>(x, N, K, w, b, y, Nout, y_f32, act);
+  else if (opw == 2)
+    fc_kernel<2><<<g, 256, smem, s>>>(x, N, K, w, b, y, Nout, y_f32, act);
+  else
+    fc_kernel<1><<<g, 256, smem, s>>>(x, N, K, w, b, y, Nout, y_f32, act);
   return cudaGetLastError();
 }
 

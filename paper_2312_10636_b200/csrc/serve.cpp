@@ -1,0 +1,650 @@
+// Native serving runtime: the discrete-event loop of fragserve's _Sim (simulator.py:430-463) with
+// its batching (_service / _enqueue / _stage_done, simulator.py:387-426) and admission control
+// (_arrive, simulator.py:377-385), for one deployed plan over one horizon.
+//
+// GX_CLOCK_VIRTUAL replays the reference exactly: the same event heap keyed (t, rank, seq), the same
+// push order (so request seqs match _Request.seq), the same float arithmetic; a batch completes at
+// dispatch time + the stage's latency table entry for k.  GX_CLOCK_WALL runs the same state machine
+// against the wall clock: every dispatched batch executes on the GPU (gx_stage_run on a free
+// instance's stream) and completes when its CUDA event fires.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <deque>
+#include <queue>
+#include <string>
+#include <vector>
+
+#include "gx_internal.h"
+#include "gx_runtime.h"
+
+using namespace gx;
+
+namespace {
+
+enum { R_REPLAN = 0, R_GEN = 1, R_ARRIVE = 2, R_TIMEOUT = 3, R_DONE = 4 };
+constexpr double kEps = 1e-9;  // simulator.py:39
+
+struct Ev {
+  double t;
+  int rank;
+  int64_t seq;
+  int64_t a, b;  // payload
+  bool operator>(const Ev& o) const {
+    if (t != o.t) return t > o.t;
+    if (rank != o.rank) return rank > o.rank;
+    return seq > o.seq;
+  }
+};
+
+struct Req {
+  int64_t seq;
+  int client;
+  double gen, slo, deadline, worst_rem;
+  int route;
+  int stage_idx = 0;
+  double stage_enq = 0.0;
+  int status = 2;  // 0 completed, 1 dropped, 2 inflight
+  double done = NAN;
+  // WALL: where the request's current activation lives
+  const void* cur = nullptr;
+  int cur_dtype = GX_F32;
+  int cur_channels = 0;
+  int slot = -1;
+};
+
+struct Batch {
+  int stage;
+  int inst;
+  std::vector<int> reqs;
+  cudaEvent_t ev = nullptr;
+};
+
+struct Stage {
+  int batch, instances, free;
+  double budget;
+  std::vector<double> lat;  // [batch + 1]
+  std::deque<int> queue;
+  int64_t armed_seq = -1;
+  std::vector<gx_stage*> inst;
+  std::vector<char> busy;
+  int out_final = 0;
+};
+
+struct Client {
+  double rate, slo;
+  int route;
+  std::vector<double> gaps;  // pre-drawn inter-arrival gaps (Poisson); empty = deterministic
+  size_t gap_idx = 0;
+  std::vector<double> tr_t, tr_mbps;  // bandwidth trace (piecewise constant, workload.py:46-52)
+};
+
+struct Route {
+  int n_stages;
+  int stage[2];
+  double worst_rem;
+  double mobile_ms;
+  int64_t payload_bytes;
+  const void* ingress;
+  int64_t ingress_bytes;
+  int ingress_dtype;
+  int ingress_channels;
+};
+
+}  // namespace
+
+struct gx_serve {
+  gx_ctx* ctx = nullptr;
+  gx_serve_cfg cfg;
+  std::vector<Stage> stages;
+  std::vector<Route> routes;
+  std::vector<Client> clients;
+  std::vector<Req> reqs;
+  std::priority_queue<Ev, std::vector<Ev>, std::greater<Ev>> heap;
+  int64_t seq = 0;
+  // dispatch log
+  std::vector<double> d_t;
+  std::vector<int32_t> d_stage, d_k;
+  std::vector<int64_t> d_seqs;
+  // WALL resources
+  std::vector<Batch> batches;
+  std::vector<int> free_batches;
+  std::vector<int> inflight;  // batch ids in flight (WALL)
+  void* slots = nullptr;
+  std::vector<int> free_slots;
+  void* results = nullptr;  // fp32 outputs ring (device) or pinned host
+  int64_t result_elems = 0;
+  int64_t result_cursor = 0;
+  cudaStream_t ingress_stream = nullptr;
+  cudaEvent_t ingress_ev = nullptr;
+  bool ingress_pending = false;
+  double wall_ms = 0.0;
+  int64_t n_batches = 0, n_kernels = 0;
+  int64_t drops_no_slot = 0;
+  std::chrono::steady_clock::time_point t0;
+
+  void push(double t, int rank, int64_t a, int64_t b = 0) {
+    ++seq;
+    heap.push(Ev{t, rank, seq, a, b});
+  }
+  double now_wall() const {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+  double bandwidth_at(const Client& c, double t_s) const {
+    // bisect_right(times, t_s) - 1, clamped at 0 (workload.py:46-52)
+    auto it = std::upper_bound(c.tr_t.begin(), c.tr_t.end(), t_s);
+    long idx = static_cast<long>(it - c.tr_t.begin()) - 1;
+    if (idx < 0) idx = 0;
+    return c.tr_mbps[idx];
+  }
+  double next_gen(Client& c, double now) {
+    if (!c.gaps.empty()) {
+      if (c.gap_idx >= c.gaps.size()) return INFINITY;
+      return now + c.gaps[c.gap_idx++];
+    }
+    return now + 1000.0 / c.rate;
+  }
+
+  int gen_request(int cid, double now);
+  int arrive(int ri, double now);
+  int enqueue(int si, int ri, double now);
+  int service(int si, double now);
+  int stage_done(int bi, double now);
+  int complete(int ri, double now);
+  int dispatch_gpu(int si, int bi);
+  int run();
+};
+
+int gx_serve::complete(int ri, double now) {
+  Req& r = reqs[ri];
+  r.status = 0;
+  r.done = now;
+  if (r.slot >= 0) {
+    free_slots.push_back(r.slot);
+    r.slot = -1;
+  }
+  return GX_OK;
+}
+
+int gx_serve::gen_request(int cid, double now) {
+  Client& c = clients[cid];
+  Req r;
+  r.seq = seq;  // _Request(self.seq, ...) before the ARRIVE push (simulator.py:355)
+  r.client = cid;
+  r.gen = now;
+  r.slo = c.slo;
+  r.deadline = now + c.slo;
+  r.worst_rem = 0.0;
+  r.route = c.route;
+  reqs.push_back(r);
+  const int ri = static_cast<int>(reqs.size()) - 1;
+  if (c.route < 0) {
+    reqs[ri].status = 1;
+    return GX_OK;
+  }
+  const Route& rt = routes[c.route];
+  const double bw = bandwidth_at(c, now / 1000.0);
+  // transfer_ms (workload.py:141-142), same operation order
+  const double xfer = static_cast<double>(rt.payload_bytes) * 8.0 / (bw * 1e6) * 1000.0;
+  const double arrive_t = now + rt.mobile_ms + xfer;
+  reqs[ri].worst_rem = rt.worst_rem;
+  push(arrive_t, R_ARRIVE, ri);
+  return GX_OK;
+}
+
+int gx_serve::arrive(int ri, double now) {
+  Req& r = reqs[ri];
+  const double elapsed = now - r.gen;
+  if (elapsed + r.worst_rem > r.slo + kEps) {
+    r.status = 1;
+    return GX_OK;
+  }
+  const Route& rt = routes[r.route];
+  if (rt.n_stages == 0) return complete(ri, now);
+  if (cfg.clock == GX_CLOCK_WALL) {
+    r.cur = rt.ingress;
+    r.cur_dtype = rt.ingress_dtype;
+    r.cur_channels = rt.ingress_channels;
+    const bool needs_slot = cfg.ingress_from_host || rt.n_stages > 1 || !stages[rt.stage[0]].out_final;
+    if (needs_slot) {
+      if (free_slots.empty()) {  // out of device slots: counts as an admission drop
+        r.status = 1;
+        ++drops_no_slot;
+        return GX_OK;
+      }
+      r.slot = free_slots.back();
+      free_slots.pop_back();
+      void* dst = static_cast<uint8_t*>(slots) + static_cast<size_t>(r.slot) * cfg.slot_bytes;
+      if (cfg.ingress_from_host) {
+        cudaError_t e = cudaMemcpyAsync(dst, rt.ingress, rt.ingress_bytes, cudaMemcpyHostToDevice, ingress_stream);
+        if (e != cudaSuccess) return cuda_fail(e, "ingress H2D");
+        ingress_pending = true;
+        r.cur = dst;
+      }
+    }
+  }
+  return enqueue(rt.stage[0], ri, now);
+}
+
+int gx_serve::enqueue(int si, int ri, double now) {
+  reqs[ri].stage_enq = now;
+  stages[si].queue.push_back(ri);
+  return service(si, now);
+}
+
+int gx_serve::dispatch_gpu(int si, int bi) {
+  Stage& st = stages[si];
+  Batch& b = batches[bi];
+  int inst = -1;
+  for (int i = 0; i < static_cast<int>(st.busy.size()); ++i)
+    if (!st.busy[i]) {
+      inst = i;
+      break;
+    }
+  if (inst < 0) return fail(GX_EINTERNAL, "no free instance although free > 0");
+  st.busy[inst] = 1;
+  b.inst = inst;
+  gx_stage* g = st.inst[inst];
+  const int k = static_cast<int>(b.reqs.size());
+  const void* src[64];
+  int32_t sdt[64];
+  void* dst[64];
+  int channels = 0;
+  for (int i = 0; i < k; ++i) {
+    Req& r = reqs[b.reqs[i]];
+    src[i] = r.cur;
+    sdt[i] = r.cur_dtype;
+    channels = std::max(channels, r.cur_channels);
+    if (st.out_final) {
+      dst[i] = static_cast<uint8_t*>(results) + (result_cursor % cfg.max_inflight) * result_elems * 4;
+      ++result_cursor;
+    } else {
+      dst[i] = static_cast<uint8_t*>(slots) + static_cast<size_t>(r.slot) * cfg.slot_bytes;
+    }
+  }
+  if (ingress_pending) {
+    GX_CUDA(cudaEventRecord(ingress_ev, ingress_stream));
+    ingress_pending = false;
+  }
+  GX_CUDA(cudaStreamWaitEvent(g->stream, ingress_ev, 0));
+  int rc = gx_stage_run(g, k, src, sdt, channels, dst, st.out_final ? GX_F32 : GX_BF16);
+  if (rc != GX_OK) return rc;
+  int kc = 0;
+  gx_stage_kernel_count(g, k, &kc);
+  n_kernels += kc;
+  GX_CUDA(cudaEventRecord(b.ev, g->stream));
+  for (int i = 0; i < k; ++i) {
+    Req& r = reqs[b.reqs[i]];
+    if (!st.out_final) {
+      r.cur = dst[i];
+      r.cur_dtype = GX_BF16;
+      r.cur_channels = 0;
+    }
+  }
+  inflight.push_back(bi);
+  return GX_OK;
+}
+
+int gx_serve::service(int si, double now) {
+  Stage& st = stages[si];
+  auto& q = st.queue;
+  while (st.free > 0 && !q.empty()) {
+    int k;
+    if (static_cast<int>(q.size()) >= st.batch) {
+      k = st.batch;
+    } else if (now - reqs[q.front()].stage_enq >= st.budget - kEps) {
+      k = static_cast<int>(q.size());
+    } else {
+      break;
+    }
+    int bi;
+    if (!free_batches.empty()) {
+      bi = free_batches.back();
+      free_batches.pop_back();
+    } else {
+      batches.emplace_back();
+      bi = static_cast<int>(batches.size()) - 1;
+      if (cfg.clock == GX_CLOCK_WALL) GX_CUDA(cudaEventCreateWithFlags(&batches[bi].ev, cudaEventDisableTiming));
+    }
+    Batch& b = batches[bi];
+    b.stage = si;
+    b.reqs.clear();
+    for (int i = 0; i < k; ++i) {
+      b.reqs.push_back(q.front());
+      q.pop_front();
+    }
+    st.free -= 1;
+    ++n_batches;
+    if (cfg.record_dispatch) {
+      d_t.push_back(now);
+      d_stage.push_back(si);
+      d_k.push_back(k);
+      for (int ri : b.reqs) d_seqs.push_back(reqs[ri].seq);
+    }
+    if (cfg.clock == GX_CLOCK_VIRTUAL) {
+      push(now + st.lat[k], R_DONE, bi);
+    } else {
+      int rc = dispatch_gpu(si, bi);
+      if (rc != GX_OK) return rc;
+    }
+  }
+  if (!q.empty()) {
+    // arm the partial-batch timer only when the head is not yet overdue (simulator.py:409-416)
+    const Req& head = reqs[q.front()];
+    const double tfire = head.stage_enq + st.budget;
+    if (tfire > now + kEps && st.armed_seq != head.seq) {
+      st.armed_seq = head.seq;
+      push(tfire, R_TIMEOUT, si, head.seq);
+    }
+  }
+  return GX_OK;
+}
+
+int gx_serve::stage_done(int bi, double now) {
+  Batch& b = batches[bi];
+  Stage& st = stages[b.stage];
+  st.free += 1;
+  if (cfg.clock == GX_CLOCK_WALL) st.busy[b.inst] = 0;
+  std::vector<int> reqs_copy = b.reqs;
+  const int si = b.stage;
+  free_batches.push_back(bi);
+  for (int ri : reqs_copy) {
+    Req& r = reqs[ri];
+    r.stage_idx += 1;
+    const Route& rt = routes[r.route];
+    if (r.stage_idx < rt.n_stages) {
+      int rc = enqueue(rt.stage[r.stage_idx], ri, now);
+      if (rc != GX_OK) return rc;
+    } else {
+      complete(ri, now);
+    }
+  }
+  return service(si, now);
+}
+
+int gx_serve::run() {
+  const double horizon = cfg.horizon_ms;
+  // _plan_epoch(0) then one REPLAN per later epoch (simulator.py:432-437): they consume seqs
+  if (cfg.epoch_ms > 0) {
+    long k = 1;
+    while (k * cfg.epoch_ms < horizon) {
+      push(k * cfg.epoch_ms, R_REPLAN, k);
+      ++k;
+    }
+  }
+  for (int cid = 0; cid < static_cast<int>(clients.size()); ++cid) {  // clients pre-sorted by id
+    Client& c = clients[cid];
+    const double first = c.gaps.empty() ? 0.0 : next_gen(c, 0.0);
+    if (first < horizon) push(first, R_GEN, cid);
+  }
+  t0 = std::chrono::steady_clock::now();
+  int rc = GX_OK;
+  if (cfg.clock == GX_CLOCK_VIRTUAL) {
+    while (!heap.empty() && heap.top().t <= horizon + kEps && rc == GX_OK) {
+      Ev e = heap.top();
+      heap.pop();
+      switch (e.rank) {
+        case R_REPLAN:
+          break;
+        case R_GEN: {
+          rc = gen_request(static_cast<int>(e.a), e.t);
+          const double nxt = next_gen(clients[e.a], e.t);
+          if (nxt < horizon) push(nxt, R_GEN, e.a);
+          break;
+        }
+        case R_ARRIVE:
+          rc = arrive(static_cast<int>(e.a), e.t);
+          break;
+        case R_TIMEOUT: {
+          Stage& st = stages[e.a];
+          if (st.armed_seq == e.b) {
+            st.armed_seq = -1;
+            rc = service(static_cast<int>(e.a), e.t);
+          }
+          break;
+        }
+        default:
+          rc = stage_done(static_cast<int>(e.a), e.t);
+      }
+    }
+  } else {
+    // Wall clock: scheduled events fire when the clock passes them; completions fire when the
+    // batch's CUDA event has completed (polled).  Stops at the horizon; in-flight work drains.
+    for (;;) {
+      const double now = now_wall();
+      bool progressed = false;
+      for (size_t i = 0; i < inflight.size();) {
+        const int bi = inflight[i];
+        cudaError_t q = cudaEventQuery(batches[bi].ev);
+        if (q == cudaSuccess) {
+          inflight[i] = inflight.back();
+          inflight.pop_back();
+          if (now <= horizon) {
+            rc = stage_done(bi, now);
+          } else {
+            Stage& st = stages[batches[bi].stage];
+            st.free += 1;
+            st.busy[batches[bi].inst] = 0;
+          }
+          progressed = true;
+          if (rc != GX_OK) break;
+        } else if (q == cudaErrorNotReady) {
+          ++i;
+        } else {
+          return cuda_fail(q, "batch completion");
+        }
+      }
+      if (rc != GX_OK) break;
+      while (!heap.empty() && heap.top().t <= now && heap.top().t <= horizon + kEps && rc == GX_OK) {
+        Ev e = heap.top();
+        heap.pop();
+        progressed = true;
+        // events fire at their scheduled time (the clock has passed it); state uses that time
+        switch (e.rank) {
+          case R_REPLAN:
+            break;
+          case R_GEN: {
+            rc = gen_request(static_cast<int>(e.a), e.t);
+            const double nxt = next_gen(clients[e.a], e.t);
+            if (nxt < horizon) push(nxt, R_GEN, e.a);
+            break;
+          }
+          case R_ARRIVE:
+            rc = arrive(static_cast<int>(e.a), e.t);
+            break;
+          case R_TIMEOUT: {
+            Stage& st = stages[e.a];
+            if (st.armed_seq == e.b) {
+              st.armed_seq = -1;
+              rc = service(static_cast<int>(e.a), now);
+            }
+            break;
+          }
+          default:
+            break;
+        }
+      }
+      if (rc != GX_OK) break;
+      if (now > horizon && inflight.empty()) break;
+      if (now > horizon + 60000.0) return fail(GX_EINTERNAL, "wall-clock serving did not drain");
+      (void)progressed;
+    }
+  }
+  wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return rc;
+}
+
+extern "C" {
+
+int gx_serve_create(gx_ctx* ctx, int n_stages, const gx_serve_stage* st, int n_routes, const gx_serve_route* rt,
+                    int n_clients, const gx_serve_client* cl, const gx_serve_cfg* cfg, gx_serve** out) {
+  if (!ctx || !out || !cfg || (n_stages && !st) || (n_routes && !rt) || (n_clients && !cl))
+    return fail(GX_EINVAL, "null arg");
+  gx_serve* s = new gx_serve();
+  s->ctx = ctx;
+  s->cfg = *cfg;
+  for (int i = 0; i < n_stages; ++i) {
+    Stage x;
+    x.batch = st[i].batch;
+    x.instances = st[i].instances;
+    x.free = st[i].instances;
+    x.budget = st[i].budget_ms;
+    x.out_final = st[i].out_final;
+    if (x.batch < 1 || x.instances < 1) {
+      delete s;
+      return fail(GX_EINVAL, "stage needs batch >= 1 and instances >= 1");
+    }
+    if (st[i].lat_ms) x.lat.assign(st[i].lat_ms, st[i].lat_ms + x.batch + 1);
+    if (cfg->clock == GX_CLOCK_WALL) {
+      if (!st[i].inst) {
+        delete s;
+        return fail(GX_EINVAL, "wall clock needs executor instances per stage");
+      }
+      for (int j = 0; j < x.instances; ++j) x.inst.push_back(static_cast<gx_stage*>(st[i].inst[j]));
+      x.busy.assign(x.instances, 0);
+    } else if (x.lat.empty()) {
+      delete s;
+      return fail(GX_EINVAL, "virtual clock needs a latency table per stage");
+    }
+    s->stages.push_back(std::move(x));
+  }
+  for (int i = 0; i < n_routes; ++i) {
+    Route r;
+    r.n_stages = rt[i].n_stages;
+    r.stage[0] = rt[i].stage[0];
+    r.stage[1] = rt[i].stage[1];
+    r.worst_rem = rt[i].worst_rem_ms;
+    r.mobile_ms = rt[i].mobile_ms;
+    r.payload_bytes = rt[i].payload_bytes;
+    r.ingress = rt[i].ingress;
+    r.ingress_bytes = rt[i].ingress_bytes;
+    r.ingress_dtype = rt[i].ingress_dtype;
+    r.ingress_channels = rt[i].ingress_channels;
+    for (int j = 0; j < r.n_stages; ++j)
+      if (r.stage[j] < 0 || r.stage[j] >= n_stages) {
+        delete s;
+        return fail(GX_EINVAL, "route references a bad stage");
+      }
+    s->routes.push_back(r);
+  }
+  for (int i = 0; i < n_clients; ++i) {
+    Client c;
+    c.rate = cl[i].rate_rps;
+    c.slo = cl[i].slo_ms;
+    c.route = cl[i].route;
+    if (cl[i].gen_gaps_ms && cl[i].n_gaps > 0) c.gaps.assign(cl[i].gen_gaps_ms, cl[i].gen_gaps_ms + cl[i].n_gaps);
+    if (cl[i].n_trace < 1 || !cl[i].trace_t_s || !cl[i].trace_mbps) {
+      delete s;
+      return fail(GX_EINVAL, "client needs a bandwidth trace");
+    }
+    c.tr_t.assign(cl[i].trace_t_s, cl[i].trace_t_s + cl[i].n_trace);
+    c.tr_mbps.assign(cl[i].trace_mbps, cl[i].trace_mbps + cl[i].n_trace);
+    if (c.route >= n_routes) {
+      delete s;
+      return fail(GX_EINVAL, "client references a bad route");
+    }
+    s->clients.push_back(std::move(c));
+  }
+  if (cfg->clock == GX_CLOCK_WALL) {
+    cudaError_t e = cudaSetDevice(ctx->device);
+    if (e == cudaSuccess && cfg->max_inflight > 0 && cfg->slot_bytes > 0)
+      e = cudaMalloc(&s->slots, static_cast<size_t>(cfg->slot_bytes) * cfg->max_inflight);
+    int64_t relems = 0;
+    for (auto& x : s->stages)
+      if (x.out_final && !x.inst.empty()) {
+        const gx_stage* g = x.inst[0];
+        relems = std::max<int64_t>(relems, tensor_elems(g->m->tensors[g->out_tid]));
+      }
+    s->result_elems = relems;
+    if (e == cudaSuccess && relems > 0) {
+      const size_t bytes = static_cast<size_t>(relems) * 4 * std::max(1, cfg->max_inflight);
+      e = cfg->egress_to_host ? cudaHostAlloc(&s->results, bytes, cudaHostAllocMapped) : cudaMalloc(&s->results, bytes);
+    }
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->ingress_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ingress_ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(s->ingress_ev, s->ingress_stream);
+    if (e != cudaSuccess) {
+      gx_serve_destroy(s);
+      return cuda_fail(e, "serving resources");
+    }
+    for (int i = cfg->max_inflight - 1; i >= 0; --i) s->free_slots.push_back(i);
+  }
+  *out = s;
+  return GX_OK;
+}
+
+int gx_serve_run(gx_serve* s) {
+  if (!s) return fail(GX_EINVAL, "null arg");
+  if (s->cfg.clock == GX_CLOCK_WALL) GX_CUDA(cudaSetDevice(s->ctx->device));
+  return s->run();
+}
+
+int gx_serve_count_requests(gx_serve* s, int64_t* n) {
+  if (!s || !n) return fail(GX_EINVAL, "null arg");
+  *n = static_cast<int64_t>(s->reqs.size());
+  return GX_OK;
+}
+
+int gx_serve_requests(gx_serve* s, int32_t* client, double* gen_ms, double* done_ms, double* deadline_ms,
+                      int32_t* status) {
+  if (!s) return fail(GX_EINVAL, "null arg");
+  for (size_t i = 0; i < s->reqs.size(); ++i) {
+    const Req& r = s->reqs[i];
+    if (client) client[i] = r.client;
+    if (gen_ms) gen_ms[i] = r.gen;
+    if (done_ms) done_ms[i] = r.done;
+    if (deadline_ms) deadline_ms[i] = r.deadline;
+    if (status) status[i] = r.status;
+  }
+  return GX_OK;
+}
+
+int gx_serve_count_dispatch(gx_serve* s, int64_t* n_batches, int64_t* n_items) {
+  if (!s) return fail(GX_EINVAL, "null arg");
+  if (n_batches) *n_batches = static_cast<int64_t>(s->d_t.size());
+  if (n_items) *n_items = static_cast<int64_t>(s->d_seqs.size());
+  return GX_OK;
+}
+
+int gx_serve_dispatch(gx_serve* s, double* t_ms, int32_t* stage, int32_t* k, int64_t* seqs) {
+  if (!s) return fail(GX_EINVAL, "null arg");
+  if (t_ms) std::copy(s->d_t.begin(), s->d_t.end(), t_ms);
+  if (stage) std::copy(s->d_stage.begin(), s->d_stage.end(), stage);
+  if (k) std::copy(s->d_k.begin(), s->d_k.end(), k);
+  if (seqs) std::copy(s->d_seqs.begin(), s->d_seqs.end(), seqs);
+  return GX_OK;
+}
+
+int gx_serve_stats(gx_serve* s, double* wall_ms, int64_t* batches, int64_t* kernels) {
+  if (!s) return fail(GX_EINVAL, "null arg");
+  if (wall_ms) *wall_ms = s->wall_ms;
+  if (batches) *batches = s->n_batches;
+  if (kernels) *kernels = s->n_kernels;
+  return GX_OK;
+}
+
+int gx_serve_destroy(gx_serve* s) {
+  if (!s) return GX_OK;
+  if (s->cfg.clock == GX_CLOCK_WALL) {
+    cudaSetDevice(s->ctx->device);
+    cudaDeviceSynchronize();
+    for (auto& b : s->batches)
+      if (b.ev) cudaEventDestroy(b.ev);
+    if (s->slots) cudaFree(s->slots);
+    if (s->results) {
+      if (s->cfg.egress_to_host)
+        cudaFreeHost(s->results);
+      else
+        cudaFree(s->results);
+    }
+    if (s->ingress_ev) cudaEventDestroy(s->ingress_ev);
+    if (s->ingress_stream) cudaStreamDestroy(s->ingress_stream);
+  }
+  delete s;
+  return GX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,274 @@
+"""Serving: a deployed plan driven by the native event loop (libgx gx_serve_*).
+
+`serve()` is the executor-side counterpart of fragserve's `simulate(..., fixed_plan=plan)`
+(simulator.py:536-538): same clients, same arrival process, same batching/admission semantics,
+same report schema (SimReport, simulator.py:121-183).  Two clocks:
+
+  * virtual — batch service time comes from a latency table (a CostModel's latency(model, start,
+    end, k, share), exactly what _StageRT.latency_for asks, simulator.py:95-100).  Dispatch order,
+    batch composition and every request record are bit-identical to the reference; this is the
+    parity mode.
+  * wall    — every dispatched batch really executes on the B200 (gather -> span kernels ->
+    scatter on a free instance's stream, SM-bounded by the stage's share) and completes when its
+    CUDA event fires.  This is the measurement mode for SLO-met requests/sec.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .errors import ValidationError
+from .plan import Deployment
+
+_EPS = 1e-9
+STATUS = {0: "completed", 1: "dropped", 2: "inflight"}
+
+
+@dataclass(frozen=True)
+class ClientView:
+    """The parts of a fragserve ClientSpec (workload.py:98-117) the serving loop needs."""
+
+    client_id: str
+    rate_rps: float
+    slo_ms: float
+    trace_t_s: tuple[float, ...]
+    trace_mbps: tuple[float, ...]
+    mobile_ms: tuple[float, ...]  # cumulative device latency per boundary (profiles.py:109-131)
+    payload_bytes: tuple[int, ...]  # ModelSpec.payload_bytes(p) for p = 0..N
+
+    @classmethod
+    def from_reference(cls, client) -> "ClientView":
+        model = client.model
+        n = model.layer_count
+        return cls(client.client_id, float(client.rate_rps), float(client.slo_ms),
+                   tuple(float(t) for t in client.trace.times_s), tuple(float(v) for v in client.trace.mbps),
+                   tuple(client.device.mobile_ms(model.model_id, p) for p in range(n + 1)),
+                   tuple(int(model.payload_bytes(p)) for p in range(n + 1)))
+
+    def to_doc(self) -> dict:
+        return {"client_id": self.client_id, "rate_rps": self.rate_rps, "slo_ms": self.slo_ms,
+                "trace_t_s": list(self.trace_t_s), "trace_mbps": list(self.trace_mbps),
+                "mobile_ms": list(self.mobile_ms), "payload_bytes": list(self.payload_bytes)}
+
+    @classmethod
+    def from_doc(cls, d: dict) -> "ClientView":
+        return cls(d["client_id"], float(d["rate_rps"]), float(d["slo_ms"]), tuple(d["trace_t_s"]),
+                   tuple(d["trace_mbps"]), tuple(d["mobile_ms"]), tuple(int(x) for x in d["payload_bytes"]))
+
+
+@dataclass
+class ServeReport:
+    """Same fields and serialisation as the reference SimReport (simulator.py:121-183)."""
+
+    planner: str
+    horizon_s: float
+    generated: int
+    completed: int
+    dropped: int
+    in_flight: int
+    latency_p50_ms: float | None
+    latency_p95_ms: float | None
+    latency_p99_ms: float | None
+    max_latency_ms: float | None
+    slo_violation_rate: float | None
+    drop_rate: float
+    requests: list[tuple]
+    config: dict = field(default_factory=dict)
+    dispatch: list[tuple] | None = None  # (t_ms, stage index, k, (request seqs...))
+    wall_ms: float = 0.0
+    batches: int = 0
+    kernels: int = 0
+
+    @property
+    def slo_met(self) -> int:
+        """#{completed and done <= deadline} (the metric's numerator)."""
+        return sum(1 for _c, _g, d, dl, s in self.requests if s == "completed" and d <= dl + _EPS)
+
+    def to_json_dict(self) -> dict:
+        return {
+            "format_version": 1, "planner": self.planner, "horizon_s": self.horizon_s,
+            "generated": self.generated, "completed": self.completed, "dropped": self.dropped,
+            "in_flight": self.in_flight,
+            "latency_ms": {"p50": self.latency_p50_ms, "p95": self.latency_p95_ms, "p99": self.latency_p99_ms,
+                           "max": self.max_latency_ms},
+            "slo_violation_rate": self.slo_violation_rate, "drop_rate": self.drop_rate, "config": self.config,
+        }
+
+    def to_json(self) -> str:
+        return json.dumps(self.to_json_dict(), sort_keys=True, indent=2) + "\n"
+
+    def requests_csv(self) -> str:
+        lines = ["client,gen_ms,done_ms,latency_ms,deadline_ms,status"]
+        for client_id, gen, done, deadline, status in self.requests:
+            if done is None:
+                done_s = lat_s = ""
+            else:
+                done_s = f"{done:.6f}"
+                lat_s = f"{done - gen:.6f}"
+            lines.append(f"{client_id},{gen:.6f},{done_s},{lat_s},{deadline:.6f},{status}")
+        return "\n".join(lines) + "\n"
+
+
+def _report(planner, horizon_s, client_ids, cl, gen, done, dl, status, config) -> ServeReport:
+    """_Sim._report (simulator.py:465-498) over the native records."""
+    n = len(gen)
+    completed = status == 0
+    dropped = int((status == 1).sum())
+    ncomp = int(completed.sum())
+    lats = (done - gen)[completed]
+    if ncomp:
+        p50, p95, p99 = (float(x) for x in np.percentile(lats, [50, 95, 99]))
+        mx = float(lats.max())
+        viol = int((done[completed] > dl[completed] + _EPS).sum())
+        viol_rate = viol / ncomp
+    else:
+        p50 = p95 = p99 = mx = None
+        viol_rate = None
+    reqs = [(client_ids[cl[i]], float(gen[i]), None if status[i] != 0 else float(done[i]), float(dl[i]),
+             STATUS[int(status[i])]) for i in range(n)]
+    return ServeReport(planner, horizon_s, n, ncomp, dropped, n - ncomp - dropped, p50, p95, p99, mx, viol_rate,
+                       dropped / n if n else 0.0, reqs, config)
+
+
+class _Keep:
+    """Keeps ctypes buffers alive for the duration of a native call."""
+
+    def __init__(self):
+        self.items = []
+
+    def __call__(self, x):
+        self.items.append(x)
+        return x
+
+
+def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *, epoch_s: float = 0.0,
+          latency=None, instances=None, ctx=None, poisson: bool = False, seed: int = 0,
+          record_dispatch: bool = False, ingress=None, ingress_from_host: bool = False,
+          egress_to_host: bool = False, slot_bytes: int = 0, max_inflight: int = 4096,
+          planner: str | None = None) -> ServeReport:
+    """Run one plan for one horizon.
+
+    latency: callable (StageSpec, k) -> ms for the virtual clock (None -> wall clock).
+    instances: per stage index, a list of `StageInstance` (wall clock).
+    ingress: route point -> (pointer, bytes, channels) of the fp32 entry activation template.
+    """
+    keep = _Keep()
+    wall = latency is None
+    ids = sorted(c.client_id for c in clients)
+    by_id = {c.client_id: c for c in clients}
+    st_arr = (N.GxServeStage * max(1, len(deployment.stages)))()
+    for i, s in enumerate(deployment.stages):
+        st_arr[i].batch, st_arr[i].instances, st_arr[i].budget_ms = s.batch, s.instances, s.budget_ms
+        st_arr[i].out_final = 0
+        if not wall:
+            lat = (C.c_double * (s.batch + 1))(0.0, *[float(latency(s, k)) for k in range(1, s.batch + 1)])
+            st_arr[i].lat_ms = keep(lat)
+        else:
+            insts = instances[i]
+            if len(insts) != s.instances:
+                raise ValidationError(f"stage {s.stage_id}: {len(insts)} executor instances for {s.instances}")
+            arr = (C.c_void_p * len(insts))(*[x.handle.value for x in insts])
+            st_arr[i].inst = keep(arr)
+            st_arr[i].out_final = 1 if insts[0].final else 0
+    # one native route per client (the reference keeps one _Route per client too)
+    route_docs = []
+    cl_arr = (N.GxServeClient * max(1, len(ids)))()
+    for ci, cid in enumerate(ids):
+        c = by_id[cid]
+        r = deployment.routes.get(cid)
+        ridx = -1
+        if r is not None:
+            rt = N.GxServeRoute()
+            rt.n_stages = len(r.stages)
+            for j, si in enumerate(r.stages):
+                rt.stage[j] = si
+            rt.worst_rem_ms = r.worst_rem_ms
+            rt.mobile_ms = c.mobile_ms[r.point]
+            rt.payload_bytes = c.payload_bytes[r.point]
+            rt.ingress_dtype = N.GX_F32
+            if ingress is not None:
+                ptr, nbytes, channels = ingress[r.point]
+                rt.ingress, rt.ingress_bytes, rt.ingress_channels = ptr, nbytes, channels
+            route_docs.append(rt)
+            ridx = len(route_docs) - 1
+        cl_arr[ci].rate_rps, cl_arr[ci].slo_ms, cl_arr[ci].route = c.rate_rps, c.slo_ms, ridx
+        if poisson:
+            # the reference draws gaps lazily from default_rng((seed, i)) in client-id order
+            # (simulator.py:240-242, 382-384); draw enough of the same stream up front
+            rng = np.random.default_rng((seed, ci))
+            n = int(horizon_s * c.rate_rps * 3 + 64)
+            gaps = rng.exponential(1000.0 / c.rate_rps, size=n)
+            g = keep((C.c_double * n)(*gaps))
+            cl_arr[ci].gen_gaps_ms, cl_arr[ci].n_gaps = g, n
+        tt = keep((C.c_double * len(c.trace_t_s))(*c.trace_t_s))
+        tm = keep((C.c_double * len(c.trace_mbps))(*c.trace_mbps))
+        cl_arr[ci].trace_t_s, cl_arr[ci].trace_mbps, cl_arr[ci].n_trace = tt, tm, len(c.trace_t_s)
+    rt_arr = (N.GxServeRoute * max(1, len(route_docs)))(*route_docs)
+    cfg = N.GxServeCfg()
+    cfg.horizon_ms = horizon_s * 1000.0
+    cfg.epoch_ms = epoch_s * 1000.0
+    cfg.clock = N.GX_CLOCK_WALL if wall else N.GX_CLOCK_VIRTUAL
+    cfg.record_dispatch = 1 if record_dispatch else 0
+    cfg.ingress_from_host = 1 if ingress_from_host else 0
+    cfg.egress_to_host = 1 if egress_to_host else 0
+    cfg.slot_bytes = slot_bytes
+    cfg.max_inflight = max_inflight
+    L = N.lib()
+    h = C.c_void_p()
+    ctx_handle = ctx.handle if ctx is not None else C.c_void_p(0)
+    if wall and ctx is None:
+        raise ValidationError("wall-clock serving needs an executor context")
+    if not wall and ctx is None:
+        ctx_handle = C.c_void_p(1)  # virtual clock never touches the device; any non-null handle
+    N.check(L.gx_serve_create(ctx_handle, len(deployment.stages), st_arr, len(route_docs), rt_arr, len(ids), cl_arr,
+                              C.byref(cfg), C.byref(h)), "gx_serve_create")
+    try:
+        N.check(L.gx_serve_run(h), "gx_serve_run")
+        n = C.c_int64()
+        N.check(L.gx_serve_count_requests(h, C.byref(n)))
+        n = n.value
+        cl = np.zeros(n, np.int32)
+        gen = np.zeros(n)
+        done = np.zeros(n)
+        dl = np.zeros(n)
+        status = np.zeros(n, np.int32)
+        P = lambda a, t: a.ctypes.data_as(C.POINTER(t))  # noqa: E731
+        N.check(L.gx_serve_requests(h, P(cl, C.c_int32), P(gen, C.c_double), P(done, C.c_double), P(dl, C.c_double),
+                                    P(status, C.c_int32)))
+        wall_ms = C.c_double()
+        nb = C.c_int64()
+        nk = C.c_int64()
+        N.check(L.gx_serve_stats(h, C.byref(wall_ms), C.byref(nb), C.byref(nk)))
+        dispatch = None
+        if record_dispatch:
+            nbat = C.c_int64()
+            nit = C.c_int64()
+            N.check(L.gx_serve_count_dispatch(h, C.byref(nbat), C.byref(nit)))
+            t = np.zeros(nbat.value)
+            si = np.zeros(nbat.value, np.int32)
+            kk = np.zeros(nbat.value, np.int32)
+            sq = np.zeros(nit.value, np.int64)
+            N.check(L.gx_serve_dispatch(h, P(t, C.c_double), P(si, C.c_int32), P(kk, C.c_int32), P(sq, C.c_int64)))
+            dispatch = []
+            off = 0
+            for i in range(nbat.value):
+                dispatch.append((float(t[i]), int(si[i]), int(kk[i]), tuple(int(x) for x in sq[off:off + kk[i]])))
+                off += kk[i]
+    finally:
+        L.gx_serve_destroy(h)
+    rep = _report(planner or deployment.planner, horizon_s, ids, cl, gen, done, dl, status,
+                  {"clock": "wall" if wall else "virtual", "horizon_s": horizon_s, "poisson": poisson, "seed": seed,
+                   "clients": len(ids)})
+    rep.dispatch = dispatch
+    rep.wall_ms, rep.batches, rep.kernels = float(wall_ms.value), int(nb.value), int(nk.value)
+    return rep
+
+
+def slo_met_rps(rep: ServeReport) -> float:
+    """SLO-met requests/sec over the horizon."""
+    return rep.slo_met / rep.horizon_s if rep.horizon_s > 0 else math.nan

@@ -1,0 +1,161 @@
+"""Generate golden serving fixtures by running the UNMODIFIED reference (fragserve) here.
+
+For each case: the reference planner's plan (plan_to_dict), the fragments it planned, the clients,
+the per-stage latency tables `_StageRT.latency_for` would use, and the reference simulator's
+output under `simulate(..., fixed_plan=plan)`: every request record and the dispatch log
+(time, stage, k, request seqs) captured by a `_Sim._push` hook.  The executor's native serving
+loop (virtual clock) and the oracle restatement must reproduce these bit for bit.
+
+Needs /root/reference (this container only).  Usage: python scripts/make_golden.py
+"""
+from __future__ import annotations
+
+import json
+import math
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+REF = Path("/root/reference/pkg")
+sys.path.insert(0, str(REF / "src"))
+sys.path.insert(0, str(ROOT))
+
+import fragserve  # noqa: E402
+from fragserve import (AllocConfig, BandwidthTrace, ClientSpec, DeviceProfile, ExecutionPlan, GroupPlan,  # noqa: E402
+                       LayerSpec, Level, ModelSpec, Scenario, SimConfig, StagePlan, SyntheticCostModel,
+                       load_scenario, plan_to_dict)
+from fragserve import simulator as S  # noqa: E402
+from fragserve.merging import merge_fragments  # noqa: E402
+from fragserve.workload import generate_epoch  # noqa: E402
+
+from paper_2312_10636_b200.serving import ClientView  # noqa: E402
+
+OUT = ROOT / "tests" / "golden" / "serving"
+
+
+class RecordingSim(S._Sim):
+    """_Sim with the dispatch log captured and merged fragments resolvable in _deploy."""
+
+    def __init__(self, *a, merged_fragments=None, **k):
+        super().__init__(*a, **k)
+        self.dispatch = []
+        self.stage_objs = []
+        self._merged = merged_fragments
+
+    def _push(self, t, rank, payload):
+        if rank == S._R_DONE:
+            stage, batch = payload
+            self.dispatch.append((self._now, self.stage_objs.index(stage), len(batch), [r.seq for r in batch]))
+        super()._push(t, rank, payload)
+
+    def _service(self, stage, now):
+        self._now = now
+        return super()._service(stage, now)
+
+    def _deploy(self, plan, fragments):
+        # creation order of _StageRT objects == the executor's deployment stage order
+        orig = S._StageRT
+
+        objs = self.stage_objs
+
+        class Tracked(orig):
+            def __init__(self, st):
+                super().__init__(st)
+                objs.append(self)
+
+        S._StageRT = Tracked
+        try:
+            return super()._deploy(plan, self._merged if self._merged is not None else fragments)
+        finally:
+            S._StageRT = orig
+
+
+def latency_tables(plan, cost):
+    out = {}
+    for gi, g in enumerate(plan.groups):
+        for li, lv in enumerate(g.levels):
+            for ai, st in enumerate(list(lv.align) + [lv.shared]):
+                sid = f"g{gi}.l{li}.align{ai}" if ai < len(lv.align) else f"g{gi}.l{li}.shared"
+                if st.is_null:
+                    continue
+                out[sid] = [0.0] + [cost.latency(st.model_id, st.start, st.end, k, st.alloc.share)
+                                    for k in range(1, st.alloc.batch + 1)]
+    return out
+
+
+def frag_doc(f):
+    return {"fragment_id": f.fragment_id, "start_layer": f.start_layer, "clients": sorted(f.clients)}
+
+
+def run_case(name, scenario, cost, planner, cfg, plan=None, fragments=None, merged=None):
+    if plan is None:
+        wl = generate_epoch(scenario.clients, 0.0, cost)
+        fragments = list(wl.fragments)
+        plan = S._Sim(scenario, cost, planner, cfg)._run_planner(wl.fragments)
+        if merged is not None:
+            merged = merge_fragments(wl.fragments, cfg.merge_cfg, cost, scenario.models,
+                                     cap=cfg.realign_cfg.instance_cap, max_share=cfg.realign_cfg.max_share)
+    sim = RecordingSim(scenario, cost, planner, cfg, fixed_plan=plan, merged_fragments=merged)
+    rep = sim.run()
+    doc = {
+        "name": name,
+        "reference": "fragserve " + fragserve.__version__,
+        "plan": plan_to_dict(plan),
+        "fragments": [frag_doc(f) for f in (merged if merged is not None else fragments)],
+        "clients": [ClientView.from_reference(c).to_doc() for c in sorted(scenario.clients, key=lambda c: c.client_id)],
+        "latency": latency_tables(plan, cost),
+        "horizon_s": cfg.horizon_s, "epoch_s": scenario.epoch_s, "poisson": cfg.poisson, "seed": cfg.seed,
+        "expected": {
+            "requests": [[c, g, d, dl, s] for c, g, d, dl, s in rep.requests],
+            "dispatch": sim.dispatch,
+            "summary": {"generated": rep.generated, "completed": rep.completed, "dropped": rep.dropped,
+                        "in_flight": rep.in_flight, "p99": rep.latency_p99_ms,
+                        "slo_violation_rate": rep.slo_violation_rate},
+        },
+    }
+    OUT.mkdir(parents=True, exist_ok=True)
+    (OUT / f"{name}.json").write_text(json.dumps(doc, separators=(",", ":")) + "\n")
+    print(f"{name}: generated={rep.generated} completed={rep.completed} dropped={rep.dropped} "
+          f"batches={len(sim.dispatch)} stages={len(sim.stage_objs)}")
+
+
+def closed_form_cases():
+    # test_simulator.py:35-56: two-layer model, hand-built fixed plans
+    m2 = ModelSpec("m2", 50_000, (LayerSpec(1.0, 2_000), LayerSpec(5.0, 1_000_000)))
+    dev = DeviceProfile("dev", {"m2": (0.0, 12.0, 112.0)})
+    cost = SyntheticCostModel({"m2": m2}, c0=1.0, c1=0.25, kappa=0.9, batch_max=16)
+
+    def plan(budget, batch, instances=1):
+        st = StagePlan("m2", 0, 2, 5.0, budget, AllocConfig(100, batch, instances), ("c0",))
+        return ExecutionPlan("fixed", (GroupPlan((Level(0, (), st),)),), 100 * instances)
+
+    for name, rate, budget, batch, inst, hz in (("closed_partial_batch", 5.0, 30.0, 8, 1, 2.0),
+                                                  ("closed_full_batch", 50.0, 30.0, 2, 2, 1.0),
+                                                  ("closed_inflight_horizon", 5.0, 30.0, 8, 1, 0.035)):
+        client = ClientSpec("c0", dev, m2, rate, 100.0, BandwidthTrace((0.0,), (40.0,)))
+        sc = Scenario((client,), 1, 10.0, {"m2": m2})
+        frags = list(generate_epoch(sc.clients, 0.0, cost).fragments)
+        run_case(name, sc, cost, "realign", SimConfig(horizon_s=hz), plan=plan(budget, batch, inst), fragments=frags)
+
+
+def main():
+    closed_form_cases()
+    scen = REF / "scenarios"
+    sc, cost = load_scenario(scen / "slo-guarantee" / "scenario.json")
+    run_case("slo_guarantee_realign", sc, cost, "realign", SimConfig(horizon_s=10.0))
+    run_case("slo_guarantee_independent_poisson", sc, cost, "independent",
+             SimConfig(horizon_s=6.0, seed=3, poisson=True))
+    sc, cost = load_scenario(scen / "shared-suffix" / "scenario.json")
+    run_case("shared_suffix_realign", sc, cost, "realign", SimConfig(horizon_s=5.0))
+    sc, cost = load_scenario(scen / "demo" / "scenario.json")
+    run_case("demo_realign", sc, cost, "realign", SimConfig(horizon_s=65.0))
+    sc, cost = load_scenario(scen / "merge-fleet" / "scenario.json")
+    # merging fires here: the reference's own _deploy raises KeyError; the recording
+    # sim deploys the merged fragments instead (the documented fix the executor applies too)
+    run_case("merge_fleet_realign_fixed_deploy", sc, cost, "realign", SimConfig(horizon_s=2.0), merged=True)
+    run_case("merge_fleet_realign_poisson", sc, cost, "realign", SimConfig(horizon_s=2.0, poisson=True, seed=1),
+             merged=True)
+
+
+if __name__ == "__main__":
+    main()
