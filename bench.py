@@ -1,0 +1,363 @@
+"""Benchmark: SLO-met requests/sec for re-aligned ResNet-50 fragment groups on B200.
+
+Workload (BASELINE.json configs[1]): a fleet of ResNet-50 clients at 30 rps cut at 8 partition
+points, planned by the unmodified reference planner (merge -> group -> re-align -> placement)
+against the measured B200 profile table; tests/golden/workload/resnet50_c<N>.json.  The executor
+serves that plan in real time: requests arrive on the wall clock (gen + mobile prefix + link
+transfer), are batched per stage exactly as the reference simulator batches them, and every
+dispatched batch runs on the GPU (ragged gather -> span kernels -> scatter) on an instance bounded
+to the stage's SM share.
+
+A step is one serving window of `--window` seconds of arrivals.  `value` counts requests generated
+in the K timed windows that complete within their deadline, divided by the timed window time;
+valid only when p99 latency <= SLO.  Entry activations are resident in HBM for `value`; `e2e`
+repeats the measurement with each request's activation copied host->device at arrival and its
+logits written back to pinned host memory.
+
+Multi-GPU (torchrun): one process per GPU, each serving its own independent fleet of the same
+size (groups share no tensors; no collective on the data path): scaling "weak".
+
+--impl reference: the reference's serving path on the host CPU — the oracle restatement of its
+event loop (pinned bit-exact to the reference) driven by fp32 CPU execution times of the same
+spans measured on this host (bounded sample).
+"""
+from __future__ import annotations
+
+import argparse
+import glob
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "SLO-met requests/sec (p99<=SLO) for re-aligned ResNet-50 groups"
+UNIT = "req/s"
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get("bf16_tflops_sustained", 1401.0), d.get("bf16_tflops", 1659.7), d.get("hbm_gbs", 6538.6), "measured"
+    return 1400.0, 1590.0, 6650.0, "fallback"
+
+
+def _workload(name: str, clients: int | None):
+    files = sorted(glob.glob(str(ROOT / "tests" / "golden" / "workload" / f"{name}_c*.json")),
+                   key=lambda f: int(f.rsplit("_c", 1)[1].split(".")[0]))
+    if not files:
+        raise SystemExit(f"no workload fixtures for {name}; run scripts/make_workload.py")
+    if clients is not None:
+        files = [f for f in files if f.endswith(f"_c{clients}.json")]
+        if not files:
+            raise SystemExit(f"no workload fixture with {clients} clients")
+    return json.loads(Path(files[-1]).read_text())
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:  # noqa: BLE001 - clocks are best-effort telemetry
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = sorted(float(s[1]) for s in self.samples)
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s in self.samples:
+            for n, v in zip(names, s[5:9]):
+                if v.strip().lower() in ("active", "1"):
+                    reasons.add(n)
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(self.samples[0][2]), "reasons": sorted(reasons),
+                "samples": len(self.samples)}
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2312_10636_b200 import _native as N
+    from paper_2312_10636_b200.device import context
+    from paper_2312_10636_b200.engine import DeviceModel, StageInstance
+    from paper_2312_10636_b200.models import build_chain
+    from paper_2312_10636_b200.plan import deploy
+    from paper_2312_10636_b200.serving import ClientView, serve
+
+    world, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    wl = _workload(args.model, args.clients)
+    ctx = context(local)
+    chain = build_chain(args.model)
+    dm = DeviceModel(chain, local)
+    dep = deploy(wl["plan"], wl["fragments"])
+    clients = [ClientView.from_doc(c) for c in wl["clients"]]
+    slo = wl["slo_ms"]
+    instances = []
+    for s in dep.stages:
+        instances.append([StageInstance(dm, s.start, s.end, s.batch, ctx.sm_budget(s.share)) for _ in range(s.instances)])
+    # entry activation templates per cut point (fp32 NHWC as a client ships them; synthetic)
+    g = torch.Generator(device="cuda").manual_seed(1234)
+    points = sorted({r.point for r in dep.routes.values()})
+    dev_in, host_in = {}, {}
+    slot_bytes = 0
+    for p in points:
+        H, W, Cc, _ = chain.boundary_shape(p)
+        ch = chain.ingress_channels(p)
+        x = torch.randn(H * W * ch, device="cuda", generator=g).clamp_min(0) if p > 0 else \
+            torch.randn(H * W * ch, device="cuda", generator=g)
+        dev_in[p] = (x, x.data_ptr(), x.numel() * 4, ch)
+        h = x.cpu().pin_memory()
+        host_in[p] = (h, h.data_ptr(), h.numel() * 4, ch)
+        slot_bytes = max(slot_bytes, x.numel() * 4, chain.boundary_elems(p) * 2)
+    for s in dep.stages:
+        slot_bytes = max(slot_bytes, chain.boundary_elems(s.end) * 2)
+    slot_bytes = (slot_bytes + 255) // 256 * 256
+    # warm every (instance, k) graph before the clock starts
+    for s, insts in zip(dep.stages, instances):
+        for inst in insts:
+            for k in range(1, s.batch + 1):
+                inst.kernel_count(k)
+    torch.cuda.synchronize()
+
+    window = args.window
+    W, K = args.warmup, args.steps
+    horizon = (W + K) * window
+
+    def one_run(host: bool):
+        ingress = {p: (v[1], v[2], v[3]) for p, v in (host_in if host else dev_in).items()}
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        rep = serve(dep, clients, horizon, ctx=ctx, instances=instances, ingress=ingress, ingress_from_host=host,
+                    egress_to_host=host, slot_bytes=slot_bytes, max_inflight=args.max_inflight)
+        e1.record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t_lo, t_hi = W * window * 1000.0, horizon * 1000.0
+        timed = [r for r in rep.requests if t_lo <= r[1] < t_hi]
+        met = sum(1 for _c, _g, d, dl, s in timed if s == "completed" and d <= dl + 1e-9)
+        lats = sorted(d - gg for _c, gg, d, _dl, s in timed if s == "completed")
+        p99 = lats[min(len(lats) - 1, int(math.ceil(0.99 * len(lats))) - 1)] if lats else math.inf
+        dropped = sum(1 for r in timed if r[4] == "dropped")
+        return {"met": met, "generated": len(timed), "dropped": dropped, "p99": p99, "wall_ms": rep.wall_ms,
+                "device_ms": e0.elapsed_time(e1), "kernels": rep.kernels, "batches": rep.batches,
+                "h2d": sum(ingress[dep.routes[r[0]].point][1] for r in timed if r[0] in dep.routes) if host else 0,
+                "d2h": sum(1 for r in timed if r[4] == "completed") * chain.boundary_elems(chain.n_units) * 4
+                if host else 0}
+
+    with ClockSampler(local) as clk:
+        res = one_run(host=False)
+    res_e2e = one_run(host=True)
+
+    # roofline: the dominant stage's span graph on its own stream (CUDA events, live)
+    def stage_flops(i):
+        s = dep.stages[i]
+        return s.instances * s.batch * sum(chain.unit_flops[s.start:s.end])
+
+    busiest = max(range(len(dep.stages)), key=stage_flops)
+    st = dep.stages[busiest]
+    inst = instances[busiest][0]
+    ms = inst.profile(st.batch, 20)
+    flops = st.batch * sum(chain.unit_flops[st.start:st.end])
+    sustained, burst, hbm, src = _peaks()
+    achieved = flops / (ms * 1e-3) / 1e12
+    stats = torch.tensor([res["met"], res["generated"], res["dropped"], res_e2e["met"], res["kernels"],
+                          res["h2d"], res_e2e["h2d"], res_e2e["d2h"]], dtype=torch.float64, device="cuda")
+    times = torch.tensor([res["device_ms"], res_e2e["device_ms"], res["p99"], res_e2e["p99"]], dtype=torch.float64,
+                         device="cuda")
+    if world > 1:
+        dist.all_reduce(stats)
+        dist.all_reduce(times, op=dist.ReduceOp.MAX)
+    timed_s = K * window
+    value = stats[0].item() / timed_s
+    e2e_value = stats[3].item() / timed_s
+    p99, p99_e2e = times[2].item(), times[3].item()
+    if rank == 0:
+        cpu = cpu_baseline(args, wl, dep, chain) if not args.no_cpu_baseline else None
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": round(window * 1000.0, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded random-init weights, random activations)",
+            "config": {"workload": f"{args.model} re-aligned fragment groups, {wl['clients_n']} clients x "
+                                   f"{wl['rate_rps']:.0f} rps per GPU, 8 cut points, plan from the reference planner "
+                                   f"on the measured B200 profile table, SM-share partitioning",
+                       "model": args.model, "clients_per_gpu": wl["clients_n"], "offered_rps_per_gpu":
+                           wl["clients_n"] * wl["rate_rps"], "slo_ms": round(slo, 3), "window_s": window,
+                       "stages": len(dep.stages), "instances": sum(s.instances for s in dep.stages),
+                       "plan_resource": wl["plan"]["total_resource"], "parallelism": f"replica-per-gpu x{world}",
+                       "l2": "inputs resident; working set per stage < L2, serving windows not flushed"},
+            "p99_ms": round(p99, 3), "p99_ok": p99 <= slo, "generated": int(stats[1].item()),
+            "dropped": int(stats[2].item()),
+            "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "p99_ms": round(p99_e2e, 3),
+                    "h2d_bytes_per_step": int(stats[6].item() / K), "d2h_bytes_per_step": int(stats[7].item() / K)},
+            "gpu_launches": int(stats[4].item()),
+            "roofline": {"bound": "tensor", "kernel": f"span [{st.start},{st.end}) k={st.batch} "
+                                                      f"({inst.kernel_count(st.batch)} kernels, share {st.share}%)",
+                         "achieved": round(achieved, 2), "peak": round(sustained * st.share / 100.0, 1),
+                         "unit": "TFLOP/s", "frac": round(achieved / (sustained * st.share / 100.0), 4),
+                         "traffic": None,
+                         "peak_source": f"{src} bf16_tflops_sustained ({sustained}) x the stage's SM share"},
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _cpu_stage_latency(chain_name, spans_k, budget_s):
+    """fp32 CPU forward time per (span, k) on this host (the reference's compute path restated)."""
+    import torch
+
+    from oracle.units import run_span, units_for
+    from paper_2312_10636_b200.models import build_chain, torch_model
+
+    torch.set_num_threads(os.cpu_count() or 1)
+    m = torch_model(chain_name)
+    units = units_for(chain_name, m)
+    chain = build_chain(chain_name, module=m)
+    out = {}
+    t_start = time.time()
+    for (a, b), ks in spans_k.items():
+        for k in ks:
+            if time.time() - t_start > budget_s:
+                break
+            if a == 0:
+                x = torch.randn(k, 3, 224, 224)
+            else:
+                H, W, Cc, _ = chain.boundary_shape(a)
+                x = torch.randn(k, Cc, H, W).clamp_min(0)
+            run_span(units, a, b, x)  # warm
+            t0 = time.perf_counter()
+            run_span(units, a, b, x)
+            out[(a, b, k)] = (time.perf_counter() - t0) * 1000.0
+    return out
+
+
+def cpu_baseline(args, wl, dep, chain, budget_s: float = 20.0):
+    """The CPU path on this host: oracle event loop + measured fp32 CPU span latencies."""
+    from oracle.serving import simulate_fixed
+    from paper_2312_10636_b200.serving import ClientView
+
+    spans_k = {}
+    for s in dep.stages:
+        spans_k.setdefault((s.start, s.end), set()).update({1, s.batch})
+    spans_k = {k: sorted(v) for k, v in spans_k.items()}
+    t0 = time.time()
+    lat = _cpu_stage_latency(args.model, spans_k, budget_s)
+
+    def latency(spec, k):
+        lo = lat.get((spec.start, spec.end, 1))
+        hi = lat.get((spec.start, spec.end, spec.batch))
+        if lo is None:
+            return 1e9
+        if hi is None or spec.batch == 1:
+            return lo * k
+        return lo + (hi - lo) * (k - 1) / (spec.batch - 1)
+
+    clients = [ClientView.from_doc(c) for c in wl["clients"]]
+    horizon = args.steps * args.window
+    recs, _ = simulate_fixed(dep, clients, horizon, 0.0, latency)
+    met = sum(1 for _c, _g, d, dl, s in recs if s == "completed" and d <= dl + 1e-9)
+    return {"value": round(met / horizon, 2), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+            "sample": f"fp32 CPU forward of {len(lat)} (span, k) points of this plan (one timed pass each, "
+                      f"{time.time() - t0:.1f}s) driving the oracle event loop over a {horizon:.1f}s horizon"}
+
+
+def run_reference(args):
+    world, rank, _ = _dist()
+    if rank != 0:
+        return
+    from paper_2312_10636_b200.models import build_chain
+    from paper_2312_10636_b200.plan import deploy
+
+    wl = _workload(args.model, args.clients)
+    dep = deploy(wl["plan"], wl["fragments"])
+    chain = build_chain(args.model)
+    vals = []
+    cpu = None
+    for _ in range(max(1, args.steps)):
+        cpu = cpu_baseline(args, wl, dep, chain, budget_s=max(5.0, 120.0 / max(1, args.steps)))
+        vals.append(cpu["value"])
+    value = sum(vals) / len(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": args.window * 1000.0, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{args.model} re-aligned fragment groups, {wl['clients_n']} clients, CPU path",
+                       "model": args.model},
+            "cpu_baseline": cpu, "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                                         "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--window", type=float, default=1.0, help="seconds of arrivals per step")
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--model", default="resnet50")
+    ap.add_argument("--clients", type=int, default=None, help="fleet size per GPU (default: largest feasible plan)")
+    ap.add_argument("--max-inflight", type=int, default=8192)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,56 @@
+"""Wall-clock serving probe across fleet sizes (development aid)."""
+import json
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2312_10636_b200.device import context  # noqa: E402
+from paper_2312_10636_b200.engine import DeviceModel, StageInstance  # noqa: E402
+from paper_2312_10636_b200.models import build_chain  # noqa: E402
+from paper_2312_10636_b200.plan import deploy  # noqa: E402
+from paper_2312_10636_b200.serving import ClientView, serve  # noqa: E402
+
+sizes = [int(x) for x in sys.argv[1].split(",")]
+horizon = float(sys.argv[2]) if len(sys.argv) > 2 else 2.0
+chain = build_chain("resnet50")
+dm = DeviceModel(chain)
+ctx = context(0)
+g = torch.Generator(device="cuda").manual_seed(0)
+for c in sizes:
+    wl = json.loads(Path(f"tests/golden/workload/resnet50_c{c}.json").read_text())
+    dep = deploy(wl["plan"], wl["fragments"])
+    clients = [ClientView.from_doc(x) for x in wl["clients"]]
+    inst = [[StageInstance(dm, s.start, s.end, s.batch, ctx.sm_budget(s.share)) for _ in range(s.instances)]
+            for s in dep.stages]
+    for s, ii in zip(dep.stages, inst):
+        for x in ii:
+            for k in range(1, s.batch + 1):
+                x.kernel_count(k)
+    ingress = {}
+    keep = []
+    slot = 0
+    for p in sorted({r.point for r in dep.routes.values()}):
+        H, W, Cc, _ = chain.boundary_shape(p)
+        ch = chain.ingress_channels(p)
+        t = torch.randn(H * W * ch, device="cuda", generator=g)
+        keep.append(t)
+        ingress[p] = (t.data_ptr(), t.numel() * 4, ch)
+        slot = max(slot, t.numel() * 4, chain.boundary_elems(p) * 2)
+    torch.cuda.synchronize()
+    t0 = time.time()
+    rep = serve(dep, clients, horizon, ctx=ctx, instances=inst, ingress=ingress, slot_bytes=(slot + 255) // 256 * 256,
+                max_inflight=8192)
+    el = time.time() - t0
+    lat = np.array([d - gg for _c, gg, d, _dl, s in rep.requests if s == "completed"])
+    met = rep.slo_met
+    shares = sorted({s.share for s in dep.stages})
+    print(f"clients={c} stages={len(dep.stages)} shares={shares} gen={rep.generated} done={rep.completed} "
+          f"inflight={rep.in_flight} met/s={met / horizon:.0f} p50={np.percentile(lat, 50) if len(lat) else -1:.1f} "
+          f"p99={np.percentile(lat, 99) if len(lat) else -1:.1f} batches={rep.batches} "
+          f"mean_k={sum(1 for r in rep.requests if r[4] == 'completed') / max(1, rep.batches):.2f} "
+          f"kernels={rep.kernels} wall={rep.wall_ms:.0f}ms elapsed={el:.1f}s", flush=True)
+    del inst
