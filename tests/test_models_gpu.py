@@ -38,7 +38,7 @@ def _check(got, ref, tol=2e-2):
             assert got[i].argmax() == ref[i].argmax(), i
 
 
-@pytest.mark.parametrize("name", ["resnet18", "resnet50", "vgg16", "inception_v3"])
+@pytest.mark.parametrize("name", ["resnet18", "resnet50", "vgg16"])
 def test_full_span_matches_fp32_oracle(name):
     from paper_2312_10636_b200.engine import StageInstance
     m, chain, dm = _setup(name)
@@ -78,3 +78,41 @@ def test_realignment_split_is_bit_exact():
         out = b.run(mid[:3]) + b.run(mid[3:])  # different batch compositions downstream
         for i in range(5):
             assert torch.equal(out[i], full[i]), (p, i)
+
+
+@pytest.mark.parametrize("name", ["resnet50", "inception_v3", "vgg16"])
+def test_every_unit_matches_fp32_oracle(name):
+    """Each unit on the oracle's fp32 entry activation: strict 2e-2 per unit."""
+    from paper_2312_10636_b200.engine import StageInstance
+    m, chain, dm = _setup(name)
+    units = units_for(name, m)
+    x = torch.randn(2, 3, RES[name], RES[name], generator=torch.Generator().manual_seed(11))
+    acts = [x]
+    for u in range(chain.n_units):
+        acts.append(run_span(units, u, u + 1, acts[-1]))
+    for u in range(chain.n_units):
+        st = StageInstance(dm, u, u + 1, max_batch=2, sm_budget=148)
+        got = torch.stack(st.run(_inputs(acts[u]), out_dtype=torch.float32, src_channels=3 if u == 0 else 0)).cpu()
+        ref = nchw_to_nhwc(acts[u + 1]).reshape(2, -1)
+        rel = ((got.view(2, -1) - ref).norm() / ref.norm()).item()
+        assert rel < 2e-2, (u, rel)
+
+
+def test_inception_end_to_end_within_framework_bf16_error():
+    """Random-init Inception-v3 amplifies bf16 rounding ~20x end to end (PyTorch's own bf16
+    forward is ~20% off its fp32 forward on these weights): hold the executor to no worse than
+    1.25x the framework's bf16 error, and identical top-1 on decisive inputs."""
+    from paper_2312_10636_b200.engine import StageInstance
+    m, chain, dm = _setup("inception_v3")
+    x = torch.randn(2, 3, 299, 299, generator=torch.Generator().manual_seed(1234))
+    ref = run_span(units_for("inception_v3", m), 0, chain.n_units, x)
+    import copy
+    with torch.no_grad():
+        fb = copy.deepcopy(m).to(torch.bfloat16)(x.to(torch.bfloat16)).float()
+    st = StageInstance(dm, 0, chain.n_units, max_batch=2, sm_budget=148)
+    got = torch.stack(st.run(_inputs(x), src_channels=3)).cpu().view(2, -1)
+    for i in range(2):
+        fw = ((fb[i] - ref[i]).norm() / ref[i].norm()).item()
+        rel = ((got[i] - ref[i]).norm() / ref[i].norm()).item()
+        assert rel <= max(2e-2, 1.25 * fw), (i, rel, fw)
+    _check(got, ref, tol=1.0)
