@@ -35,6 +35,26 @@ class Context:
             raise ValueError(f"gpu share must be an integer in 1..100, got {share}")
         return max(1, -(-share * self.sm_count // 100))
 
+    def sm_budgets(self, shares_instances, capacity: int = 99, work_conserving: bool = True) -> list[int]:
+        """SM budget per instance for a whole deployment on this GPU.
+
+        The plan's share is a floor (what the planner was promised).  With
+        `work_conserving`, SMs the plan leaves idle are handed out in proportion to the planned
+        shares, so a plan using 32% of the GPU does not leave 68% of the SMs dark; the total never
+        exceeds `capacity`% of the SMs (placement capacity, placement.py:24)."""
+        total = sum(s * n for s, n in shares_instances)
+        if total <= 0:
+            return []
+        scale = max(1.0, capacity / total) if work_conserving else 1.0
+        cap = self.sm_count * capacity // 100
+        out = []
+        for s, n in shares_instances:
+            b = max(self.sm_budget(s) if not work_conserving else 1, int(s * scale * self.sm_count / 100))
+            out.extend([min(b, self.sm_count)] * n)
+        while sum(out) > cap and max(out) > 1:  # rounding can overshoot: trim the largest
+            out[out.index(max(out))] -= 1
+        return out
+
 
 def context(device: int = 0) -> Context:
     ctx = _CTXS.get(device)
