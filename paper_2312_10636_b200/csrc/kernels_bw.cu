@@ -204,6 +204,7 @@ __global__ void __launch_bounds__(256) fc_kernel(const __nv_bfloat16* __restrict
   extern __shared__ uint4 xs[];  // [kFcRows][kFcKChunk / 8]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int groups = (Nout + kFcWarps * OPW - 1) / (kFcWarps * OPW);
+  int64_t staged = -1;
   for (int g = blockIdx.x; g < groups; g += gridDim.x) {
     const int o0 = (g * kFcWarps + warp) * OPW;
     for (int n0 = 0; n0 < N; n0 += kFcRows) {
@@ -215,12 +216,17 @@ __global__ void __launch_bounds__(256) fc_kernel(const __nv_bfloat16* __restrict
         for (int r = 0; r < kFcRows; ++r) acc[a][r] = 0.0f;
       for (int k0 = 0; k0 < K; k0 += kFcKChunk) {
         const int kc = min(kFcKChunk, K - k0) / 8;  // 16-byte vectors in this chunk
-        __syncthreads();
-        for (int i = threadIdx.x; i < rows * kc; i += blockDim.x) {
-          const int r = i / kc, v = i - r * kc;
-          xs[r * (kFcKChunk / 8) + v] = __ldg(reinterpret_cast<const uint4*>(x + static_cast<int64_t>(n0 + r) * K + k0) + v);
+        const int64_t key = static_cast<int64_t>(n0) * K + k0;
+        if (key != staged) {  // block-uniform: re-stage only when the (rows, K-chunk) changes
+          __syncthreads();
+          for (int i = threadIdx.x; i < rows * kc; i += blockDim.x) {
+            const int r = i / kc, v = i - r * kc;
+            xs[r * (kFcKChunk / 8) + v] =
+                __ldg(reinterpret_cast<const uint4*>(x + static_cast<int64_t>(n0 + r) * K + k0) + v);
+          }
+          __syncthreads();
+          staged = key;
         }
-        __syncthreads();
         for (int v = lane; v < kc; v += 32) {
           float wf[OPW][8];
 #pragma unroll
@@ -357,7 +363,8 @@ cudaError_t launch_fc(const __nv_bfloat16* x, int N, int K, const __nv_bfloat16*
   }
   const int opw = Nout >= 4096 ? 4 : Nout >= 2048 ? 2 : 1;
   const int groups = (Nout + kFcWarps * opw - 1) / (kFcWarps * opw);
-  const int g = grid_for(groups, 1, grid / 8 > 0 ? grid / 8 : 1);
+  // up to 3 blocks (64 KB smem each) per SM of the budget: weight streaming needs many loads in flight
+  const int g = grid_for(groups, 1, grid / 8 > 0 ? 3 * (grid / 8) : 1);
   if (opw == 4)
     fc_kernel<4><<<g, 256, smem, s>>>(x, N, K, w, b, y, Nout, y_f32, act);
   else if (opw == 2)

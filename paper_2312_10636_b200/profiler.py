@@ -20,15 +20,76 @@ from .engine import DeviceModel, StageInstance
 PROFILE_HEADER = "model,start_layer,end_layer,batch,gpu_share,latency_ms"
 
 
-def sweep(dmodel: DeviceModel, spans, batches, shares, iters: int = 10, log=None) -> list[tuple]:
+class Background:
+    """Keeps the SMs outside the measured instance busy with a full-model batch-16 instance on its
+    own stream, so profiled latencies include HBM/L2 contention from co-located stages (the
+    serving condition: the placement packs a GPU to 99%, placement.py:24)."""
+
+    def __init__(self, dmodel: DeviceModel):
+        import threading
+
+        import torch
+
+        self.dm = dmodel
+        self.torch = torch
+        self.threading = threading
+        self.inst = {}
+        chain = dmodel.chain
+        self.src = torch.randn(chain.boundary_elems(0), device=f"cuda:{dmodel.device}")
+        self.dst = torch.empty(16 * chain.boundary_elems(chain.n_units), device=f"cuda:{dmodel.device}")
+        self.thread = None
+
+    def start(self, sm_budget: int):
+        from . import _native as N
+
+        if sm_budget < 1:
+            return
+        inst = self.inst.get(sm_budget)
+        if inst is None:
+            inst = StageInstance(self.dm, 0, self.dm.n_units, 16, sm_budget)
+            self.inst[sm_budget] = inst
+        chain = self.dm.chain
+        out = chain.boundary_elems(chain.n_units)
+        srcs = [self.src.data_ptr()] * 16
+        dsts = [self.dst.data_ptr() + i * out * 4 for i in range(16)]
+        self.stop_flag = False
+
+        def loop():
+            while not self.stop_flag:
+                for _ in range(3):
+                    inst.run_ptrs(16, srcs, [N.GX_F32] * 16, dsts, N.GX_F32, chain.input_channels)
+                inst.stream.synchronize()
+
+        self.thread = self.threading.Thread(target=loop, daemon=True)
+        self.thread.start()
+
+    def stop(self):
+        if self.thread is not None:
+            self.stop_flag = True
+            self.thread.join()
+            self.thread = None
+
+
+def sweep(dmodel: DeviceModel, spans, batches, shares, iters: int = 10, log=None, contended: bool = False,
+          capacity: int = 99) -> list[tuple]:
     ctx = context(dmodel.device)
+    bg = Background(dmodel) if contended else None
     rows = []
     for a, b in spans:
         grid = np.full((len(batches), len(shares)), np.nan)
         for j, share in enumerate(shares):
-            st = StageInstance(dmodel, a, b, max(batches), ctx.sm_budget(share))
-            for i, k in enumerate(batches):
-                grid[i, j] = st.profile(k, iters)
+            budget = ctx.sm_budget(share)
+            st = StageInstance(dmodel, a, b, max(batches), budget)
+            for k in batches:
+                st.kernel_count(k)  # capture before the background starts
+            if bg is not None:
+                bg.start(ctx.sm_count * capacity // 100 - budget)
+            try:
+                for i, k in enumerate(batches):
+                    grid[i, j] = st.profile(k, iters)
+            finally:
+                if bg is not None:
+                    bg.stop()
             del st
         # monotone upper envelope: non-decreasing in batch, non-increasing in share
         grid = np.maximum.accumulate(grid, axis=0)
