@@ -144,6 +144,11 @@ GX_API int gx_stage_profile(gx_stage* st, int k, int iters, float* ms_out);
 /* Number of kernels one gx_stage_run(k) launches (gather + span + scatter). */
 GX_API int gx_stage_kernel_count(gx_stage* st, int k, int* out);
 
+/* Diagnostics: run one batch of the persistent span kernel with its on-device timeline enabled
+ * (globaltimer ns per CTA per op: producer past the previous op's barrier, producer's last
+ * activation load, worker/epilogue start, arrival).  out: [sm_budget][n_ops][4]. */
+GX_API int gx_stage_span_trace(gx_stage* st, int k, int64_t* out, int64_t cap, int* n_ops_out);
+
 /* Per-sample element count of tensor `tid` of model m (boundary sizes for slot pools). */
 GX_API int gx_model_tensor_elems(gx_model* m, int tid, int64_t* out);
 

@@ -102,14 +102,14 @@ bool encode_tmap_im2col_bf16(CUtensorMap* map, const void* base, int C, int W, i
 int elem_size(int dtype) { return dtype == GX_F32 ? 4 : 2; }
 int64_t tensor_elems(const gx_tensor& t) { return static_cast<int64_t>(t.H) * t.W * t.C; }
 
-static int pick_bn(int Cout, int m_tiles, int sm_budget) {
+static int pick_bn(int Cout, int m_tiles, int sm_budget, int cap) {
   int bn;
-  if (Cout <= 256) {
+  if (Cout <= cap) {
     bn = Cout;
   } else {
-    bn = 256;
+    bn = cap;
     // prefer a tile width that divides Cout (Inception 320/384/448 -> 160/192/224)
-    for (int cand = 256; cand >= 64; cand -= 16)
+    for (int cand = cap; cand >= 64; cand -= 16)
       if (Cout % cand == 0) {
         bn = cand;
         break;
@@ -127,7 +127,7 @@ static uint32_t tmem_cols_for(int bn) {
 }
 
 int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint8_t* wbase, int k, int sm_budget,
-              ConvLaunch* out) {
+              ConvLaunch* out, int bn_cap) {
   const gx_tensor& ti = T[op.in];
   const gx_tensor& to = T[op.out];
   const int R = op.kind == GX_OP_LINEAR ? 1 : op.R;
@@ -157,7 +157,7 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
   a.M = k * a.Ho * a.Wo;
   a.Cout = op.Cout;
   a.m_tiles = (a.M + kBM - 1) / kBM;
-  a.BN = pick_bn(op.Cout, a.m_tiles, sm_budget);
+  a.BN = pick_bn(op.Cout, a.m_tiles, sm_budget, bn_cap);
   if (const char* e = getenv("GX_BN")) {  // tuning override (development)
     const int bn = atoi(e);
     if (bn >= 16 && bn <= 256 && bn % 16 == 0) a.BN = bn;

@@ -26,7 +26,7 @@ struct ConvLaunch {
 int elem_size(int dtype);
 int64_t tensor_elems(const gx_tensor& t);
 int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint8_t* wbase, int k, int sm_budget,
-              ConvLaunch* out);
+              ConvLaunch* out, int bn_cap = 256);
 int launch_op(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint8_t* wbase, int k, int sm_budget,
               cudaStream_t s, bool pdl, const ConvLaunch* pre, int* kernels);
 }  // namespace gx
@@ -56,8 +56,16 @@ struct gx_stage {
   struct PerK {
     cudaGraphExec_t exec = nullptr;
     int kernels = 0;
+    // persistent span program (span_kernel.cu)
+    void* d_ops = nullptr;    // SpanOp[n_ops]
+    void* d_tmaps = nullptr;  // CUtensorMap[3 * n_conv]
+    int n_ops = 0;
+    int span_stages = 0, bn_max = 0, has_res = 0, bias_bytes = 0;
   };
   std::map<int, PerK> graphs;
+  bool span_mode = true;                 // one persistent launch per batch (else per-op CUDA graph)
+  unsigned long long* bar = nullptr;     // grid-barrier arrival counter (device)
+  unsigned long long launches = 0;       // span launches so far (barrier base)
   // profiling scratch
   void* prof_src = nullptr;
   void* prof_dst = nullptr;

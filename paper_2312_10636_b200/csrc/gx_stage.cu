@@ -10,6 +10,7 @@
 
 #include "gx_internal.h"
 #include "gx_runtime.h"
+#include "gx_span.h"
 
 using namespace gx;
 
@@ -118,6 +119,122 @@ int capture_span(gx_stage* st, int k, gx_stage::PerK* out) {
   return GX_OK;
 }
 
+// Resolve the span's ops for batch k into the persistent kernel's device program: one SpanOp per
+// op, three tensor maps (weights, activation, residual) per conv, BN capped at 128 so the smem
+// ring, two residual slots and the bias vector fit next to each other.
+int build_span_program(gx_stage* st, int k, gx_stage::PerK* out) {
+  gx_model* m = st->m;
+  const uint8_t* wbase = static_cast<const uint8_t*>(m->wdev);
+  const gx_tensor* T = m->tensors.data();
+  std::vector<SpanOp> ops(st->ops.size());
+  std::vector<CUtensorMap> maps;
+  int bn_max = 16, has_res = 0, cout_max = 16;
+  for (size_t i = 0; i < st->ops.size(); ++i) {
+    const gx_op& op = m->ops[st->ops[i]];
+    SpanOp& s = ops[i];
+    memset(&s, 0, sizeof(s));
+    s.kind = op.kind;
+    const gx_tensor& ti = T[op.in];
+    const gx_tensor& to = T[op.out];
+    s.x = static_cast<const __nv_bfloat16*>(st->tptr[op.in]);
+    s.y = st->tptr[op.out];
+    s.N = k;
+    s.H = ti.H;
+    s.W = ti.W;
+    s.C = ti.C;
+    s.x_ld = ti.C;
+    s.Ho = to.H;
+    s.Wo = to.W;
+    s.y_ld = to.C;
+    s.y_coff = op.out_coff;
+    s.y_f32 = to.dtype == GX_F32;
+    s.act = op.act;
+    switch (op.kind) {
+      case GX_OP_CONV:
+      case GX_OP_LINEAR: {
+        ConvLaunch cl;
+        int rc = plan_conv(op, T, st->tptr.data(), wbase, k, st->sm_budget, &cl, 128);
+        if (rc != GX_OK) return rc;
+        const ConvArgs& a = cl.args;
+        if (!a.tma_a) return fail(GX_EINVAL, "span kernel needs the TMA im2col path");
+        s.tmap = static_cast<int>(maps.size());
+        maps.push_back(cl.wmap);
+        maps.push_back(cl.amap);
+        maps.push_back(cl.rmap);
+        s.BN = a.BN;
+        s.n_tiles = a.n_tiles;
+        s.num_tiles = a.num_tiles;
+        s.num_kb = a.num_kb;
+        s.Cin = a.Cin;
+        s.cpl = a.cpl;
+        s.a2d = a.a2d;
+        s.HoWo = a.Ho * a.Wo;
+        s.M = a.M;
+        s.Cout = a.Cout;
+        s.idesc = a.idesc;
+        s.R = a.R;
+        s.S = a.S;
+        s.sh = a.sh;
+        s.sw = a.sw;
+        s.ph = a.ph;
+        s.pw = a.pw;
+        s.res = a.res;
+        s.bias = a.bias;
+        bn_max = std::max(bn_max, a.BN);
+        cout_max = std::max(cout_max, a.Cout);
+        has_res |= a.res != nullptr;
+        break;
+      }
+      case GX_OP_MAXPOOL:
+      case GX_OP_AVGPOOL:
+        s.R = op.R;
+        s.S = op.S;
+        s.sh = op.sh;
+        s.sw = op.sw;
+        s.ph = op.ph;
+        s.pw = op.pw;
+        s.flags = op.flags;
+        if (ti.C & 7) return fail(GX_EINVAL, "pool channels must be a multiple of 8");
+        break;
+      case GX_OP_GAP:
+        break;
+      case GX_OP_FC:
+        s.K = static_cast<int>(tensor_elems(ti));
+        s.Cout = op.Cout;
+        s.w = reinterpret_cast<const __nv_bfloat16*>(wbase + op.w_off);
+        s.bias = op.b_off >= 0 ? reinterpret_cast<const float*>(wbase + op.b_off) : nullptr;
+        if (s.K & 7) return fail(GX_EINVAL, "FC input must be a multiple of 8");
+        break;
+      case GX_OP_COPY:
+        s.pixels = static_cast<int64_t>(k) * ti.H * ti.W;
+        s.C = op.Cin;
+        s.x_coff = op.ph;
+        break;
+      default:
+        return fail(GX_EINVAL, "op kind " + std::to_string(op.kind) + " not supported by the span kernel");
+    }
+  }
+  SpanSmem L;
+  L.bn_max = bn_max;
+  L.has_res = has_res;
+  L.bias_bytes = (cout_max * 4 + 15) & ~15;
+  L.stages = 8;
+  while (L.stages > 2 && span_smem_bytes(L) > 225 * 1024) --L.stages;
+  if (span_smem_bytes(L) > 227 * 1024) return fail(GX_EINVAL, "span kernel shared memory does not fit");
+  out->span_stages = L.stages;
+  out->bn_max = L.bn_max;
+  out->has_res = L.has_res;
+  out->bias_bytes = L.bias_bytes;
+  out->n_ops = static_cast<int>(ops.size());
+  GX_CUDA(cudaMalloc(&out->d_ops, std::max<size_t>(1, ops.size()) * sizeof(SpanOp)));
+  GX_CUDA(cudaMemcpy(out->d_ops, ops.data(), ops.size() * sizeof(SpanOp), cudaMemcpyHostToDevice));
+  GX_CUDA(cudaMalloc(&out->d_tmaps, std::max<size_t>(1, maps.size()) * sizeof(CUtensorMap)));
+  if (!maps.empty())
+    GX_CUDA(cudaMemcpy(out->d_tmaps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+  out->kernels = 1;
+  return GX_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -208,6 +325,14 @@ int gx_stage_create(gx_model* m, int start, int end, int max_batch, int sm_budge
     }
     st->own_stream = true;
   }
+  const char* mode = getenv("GX_EXEC");
+  st->span_mode = !(mode && std::string(mode) == "graph");
+  cudaError_t e = cudaMalloc(&st->bar, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(st->bar, 0, sizeof(unsigned long long));
+  if (e != cudaSuccess) {
+    gx_stage_destroy(st);
+    return cuda_fail(e, "grid barrier counter");
+  }
   *out = st;
   return GX_OK;
 }
@@ -216,8 +341,12 @@ int gx_stage_destroy(gx_stage* st) {
   if (!st) return GX_OK;
   cudaSetDevice(st->m->ctx->device);
   cudaStreamSynchronize(st->stream);
-  for (auto& kv : st->graphs)
+  for (auto& kv : st->graphs) {
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    if (kv.second.d_ops) cudaFree(kv.second.d_ops);
+    if (kv.second.d_tmaps) cudaFree(kv.second.d_tmaps);
+  }
+  if (st->bar) cudaFree(st->bar);
   if (st->ws) cudaFree(st->ws);
   if (st->prof_src) cudaFree(st->prof_src);
   if (st->prof_dst) cudaFree(st->prof_dst);
@@ -236,7 +365,7 @@ static int stage_graph(gx_stage* st, int k, gx_stage::PerK** out) {
   auto it = st->graphs.find(k);
   if (it == st->graphs.end()) {
     gx_stage::PerK pk;
-    int rc = capture_span(st, k, &pk);
+    int rc = st->span_mode ? build_span_program(st, k, &pk) : capture_span(st, k, &pk);
     if (rc != GX_OK) return rc;
     it = st->graphs.emplace(k, pk).first;
   }
@@ -259,9 +388,49 @@ int gx_stage_run(gx_stage* st, int k, const void* const* src, const int32_t* src
   const int bw_grid = st->sm_budget * 8;
   GX_CUDA(launch_gather(k, src, src_dtype, static_cast<int64_t>(tin.H) * tin.W, c_src, tin.C,
                         static_cast<__nv_bfloat16*>(st->tptr[st->in_tid]), bw_grid, st->stream));
-  GX_CUDA(cudaGraphLaunch(pk->exec, st->stream));
+  if (st->span_mode) {
+    SpanSmem L;
+    L.stages = pk->span_stages;
+    L.bn_max = pk->bn_max;
+    L.has_res = pk->has_res;
+    L.bias_bytes = pk->bias_bytes;
+    const unsigned long long base = st->launches * static_cast<unsigned long long>(pk->n_ops) * st->sm_budget;
+    GX_CUDA(launch_span(static_cast<const SpanOp*>(pk->d_ops), pk->n_ops, static_cast<const CUtensorMap*>(pk->d_tmaps),
+                        st->bar, base, L, st->sm_budget, st->stream));
+    ++st->launches;
+  } else {
+    GX_CUDA(cudaGraphLaunch(pk->exec, st->stream));
+  }
   GX_CUDA(launch_scatter(k, st->tptr[st->out_tid], tout.dtype, tensor_elems(tout), dst, dst_dtype, bw_grid,
                          st->stream));
+  return GX_OK;
+}
+
+int gx_stage_span_trace(gx_stage* st, int k, int64_t* out, int64_t cap, int* n_ops_out) {
+  if (!st || !out || !n_ops_out) return fail(GX_EINVAL, "null arg");
+  if (!st->span_mode) return fail(GX_EINVAL, "stage is not in span mode");
+  if (k < 1 || k > st->max_batch) return fail(GX_EINVAL, "bad k");
+  gx_stage::PerK* pk = nullptr;
+  int rc = stage_graph(st, k, &pk);
+  if (rc != GX_OK) return rc;
+  const int64_t n = static_cast<int64_t>(st->sm_budget) * pk->n_ops * 4;
+  if (cap < n) return fail(GX_EINVAL, "trace buffer too small");
+  unsigned long long* d = nullptr;
+  GX_CUDA(cudaMalloc(&d, n * sizeof(unsigned long long)));
+  GX_CUDA(cudaMemset(d, 0, n * sizeof(unsigned long long)));
+  SpanSmem L;
+  L.stages = pk->span_stages;
+  L.bn_max = pk->bn_max;
+  L.has_res = pk->has_res;
+  L.bias_bytes = pk->bias_bytes;
+  const unsigned long long base = st->launches * static_cast<unsigned long long>(pk->n_ops) * st->sm_budget;
+  GX_CUDA(launch_span(static_cast<const SpanOp*>(pk->d_ops), pk->n_ops, static_cast<const CUtensorMap*>(pk->d_tmaps),
+                      st->bar, base, L, st->sm_budget, st->stream, d));
+  ++st->launches;
+  GX_CUDA(cudaStreamSynchronize(st->stream));
+  GX_CUDA(cudaMemcpy(out, d, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  *n_ops_out = pk->n_ops;
   return GX_OK;
 }
 

@@ -86,6 +86,10 @@ def run_graph(name, k, H, W, Cin, Cout, R, S, stride, pad, budget=0, iters=50):
 
 SHAPES["tiny"] = (1, 8, 8, 64, 64, 1, 1, 1, 0)
 
+SHAPES["l1_3x3_k1"] = (1, 56, 56, 64, 64, 3, 3, 1, 1)
+SHAPES["l3_3x3_k1"] = (1, 14, 14, 256, 256, 3, 3, 1, 1)
+SHAPES["l1_1x1_576_k1"] = (1, 56, 56, 576, 64, 1, 1, 1, 0)
+
 
 if __name__ == "__main__":
     names = sys.argv[1].split(",") if len(sys.argv) > 1 else list(SHAPES)

@@ -1,2 +1,1 @@
-python scripts/probe_perf.py resnet50 148 1,16
-GX_NO_PDL=1 python scripts/probe_perf.py resnet50 148 1,16
+for st in 2 4 6 8; do GX_STAGES=$st GRAPH=1 python scripts/bench_conv.py l1_3x3_k1,l3_3x3_k1,l1_1x1_576_k1 4 | sed "s/^/st=$st /"; done
