@@ -156,9 +156,8 @@ def run_ours(args):
             self.dev_in, self.host_in = {}, {}
             slot = 0
             for p in sorted({r.point for r in self.dep.routes.values()}):
-                H, W, Cc, _ = chain.boundary_shape(p)
                 ch = chain.ingress_channels(p)
-                x = torch.randn(H * W * ch, device="cuda", generator=g)
+                x = torch.randn(chain.ingress_elems(p), device="cuda", generator=g)
                 if p > 0:
                     x = x.clamp_min(0)  # post-ReLU client activations
                 self.dev_in[p] = (x, x.data_ptr(), x.numel() * 4, ch)

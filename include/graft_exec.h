@@ -71,6 +71,8 @@ extern "C" {
 typedef struct gx_tensor {
   int32_t H, W, C;
   int32_t dtype; /* GX_BF16 or GX_F32 */
+  int32_t s2d;   /* >1: this (boundary) tensor is the space-to-depth(s2d) form of an [H*s2d, W*s2d, c]
+                    client image; the gather performs the rearrangement (stride-2 stems)          */
 } gx_tensor;
 
 /* One op. Tensor ids index the model's gx_tensor table; -1 = unused. Weight/bias offsets are
@@ -91,7 +93,8 @@ typedef struct gx_op {
   int32_t flags;        /* pool: 1 = count_include_pad (avg)                */
   int64_t w_off, b_off, w2_off, w3_off;
   float eps;            /* layernorm epsilon                               */
-  int32_t reserved[3];
+  int32_t ph_hi, pw_hi; /* conv bottom/right padding; -1 = same as ph / pw  */
+  int32_t reserved;
 } gx_op;
 
 typedef struct gx_ctx gx_ctx;     /* one per GPU: device, SM count, driver entry points    */

@@ -21,7 +21,7 @@ GX_CLOCK_VIRTUAL, GX_CLOCK_WALL = 0, 1
 
 
 class GxTensor(C.Structure):
-    _fields_ = [("H", C.c_int32), ("W", C.c_int32), ("C", C.c_int32), ("dtype", C.c_int32)]
+    _fields_ = [("H", C.c_int32), ("W", C.c_int32), ("C", C.c_int32), ("dtype", C.c_int32), ("s2d", C.c_int32)]
 
 
 class GxOp(C.Structure):
@@ -32,17 +32,19 @@ class GxOp(C.Structure):
         ("ph", C.c_int32), ("pw", C.c_int32), ("Cin", C.c_int32), ("Cout", C.c_int32),
         ("heads", C.c_int32), ("flags", C.c_int32),
         ("w_off", C.c_int64), ("b_off", C.c_int64), ("w2_off", C.c_int64), ("w3_off", C.c_int64),
-        ("eps", C.c_float), ("reserved", C.c_int32 * 3),
+        ("eps", C.c_float), ("ph_hi", C.c_int32), ("pw_hi", C.c_int32), ("reserved", C.c_int32),
     ]
 
 
 def make_op(kind, in_, out, in2=-1, out_coff=0, act=GX_ACT_NONE, R=1, S=1, sh=1, sw=1, ph=0, pw=0,
-            Cin=0, Cout=0, heads=0, flags=0, w_off=-1, b_off=-1, w2_off=-1, w3_off=-1, eps=0.0):
+            Cin=0, Cout=0, heads=0, flags=0, w_off=-1, b_off=-1, w2_off=-1, w3_off=-1, eps=0.0, ph_hi=-1,
+            pw_hi=-1):
     op = GxOp()
     op.kind, op.in_, op.in2, op.out, op.out_coff, op.act = kind, in_, in2, out, out_coff, act
     op.R, op.S, op.sh, op.sw, op.ph, op.pw = R, S, sh, sw, ph, pw
     op.Cin, op.Cout, op.heads, op.flags = Cin, Cout, heads, flags
     op.w_off, op.b_off, op.w2_off, op.w3_off, op.eps = w_off, b_off, w2_off, w3_off, eps
+    op.ph_hi, op.pw_hi = ph_hi, pw_hi
     return op
 
 

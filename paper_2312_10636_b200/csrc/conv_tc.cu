@@ -51,6 +51,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                    const __grid_constant__ CUtensorMap rmap, const ConvArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const CUtensorMap* WM = a.gmaps ? a.gmaps : &wmap;
+  const CUtensorMap* AM = a.gmaps ? a.gmaps + 1 : &amap;
+  const CUtensorMap* RM = a.gmaps ? a.gmaps + 2 : &rmap;
   const int S_ = a.stages;
   const int BN = a.BN;
   const bool has_res = a.res != nullptr;
@@ -163,8 +166,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   } else if (warp == 4) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      tma_prefetch_desc(&wmap);
-      if (kTmaA) tma_prefetch_desc(&amap);
+      tma_prefetch_desc(WM);
+      if (kTmaA) tma_prefetch_desc(AM);
       const uint32_t tx = b_bytes + (kTmaA ? kATileBytes : 0);
       int it = 0;
       for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
@@ -192,10 +195,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           mbar_arrive_expect_tx(&sp.full[st], tx);
           if (kTmaA && a.a2d) {
             // 1x1 / stride 1 / no padding: A is the plain [M, C] activation matrix
-            tma_load_2d(sp.sA + st * kATileBytes, &amap, &sp.full[st], kb * kBK, m_blk * kBM);
+            tma_load_2d(sp.sA + st * kATileBytes, AM, &sp.full[st], kb * kBK, m_blk * kBM);
           } else if (kTmaA) {
             for (int l = 0; l < kBK / cpl; ++l) {
-              tma_load_im2col_4d(sp.sA + st * kATileBytes + l * region, &amap, &sp.full[st], c0, wc, hc, nimg,
+              tma_load_im2col_4d(sp.sA + st * kATileBytes + l * region, AM, &sp.full[st], c0, wc, hc, nimg,
                                  static_cast<uint16_t>(s), static_cast<uint16_t>(r));
               c0 += cpl;
               if (c0 == a.Cin) {
@@ -207,7 +210,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
               }
             }
           }
-          tma_load_2d(sp.sB + static_cast<size_t>(st) * b_bytes, &wmap, &sp.full[st], kb * kBK, n_blk * BN);
+          tma_load_2d(sp.sB + static_cast<size_t>(st) * b_bytes, WM, &sp.full[st], kb * kBK, n_blk * BN);
         }
       }
     }
@@ -260,7 +263,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       const int slot = t_idx % nres;
       mbar_arrive_expect_tx(&sp.rfull[slot], res_slot_bytes);
       for (int g = 0; g < res_groups(BN); ++g)
-        tma_load_2d(sp.sRes + slot * res_slot_bytes + g * kResGroupBytes, &rmap, &sp.rfull[slot],
+        tma_load_2d(sp.sRes + slot * res_slot_bytes + g * kResGroupBytes, RM, &sp.rfull[slot],
                     (tile % a.n_tiles) * BN + g * 64, (tile / a.n_tiles) * kBM);
     };
     if (leader) {
@@ -268,7 +271,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       mbar_arrive_expect_tx(sp.bfull, static_cast<uint32_t>(a.Cout) * 4u);
       bulk_load(sp.sBias, a.bias, static_cast<uint32_t>(a.Cout) * 4u, sp.bfull);
       if (has_res) {
-        tma_prefetch_desc(&rmap);
+        tma_prefetch_desc(RM);
         for (int i = 0; i < nres; ++i) issue_res(i);
       }
     }

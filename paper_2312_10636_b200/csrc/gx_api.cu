@@ -192,12 +192,20 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
   if (a.a2d) {
     if (!encode_tmap_2d_bf16(&out->amap, a.x, ti.C, a.M, static_cast<uint64_t>(ti.C) * 2, kBK, kBM))
       return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for conv input");
-  } else if (a.tma_a && !encode_tmap_im2col_bf16(&out->amap, a.x, ti.C, ti.W, ti.H, k, -a.pw, -a.ph, a.pw - (a.S - 1),
-                                          a.ph - (a.R - 1), a.sw, a.sh, a.cpl))
+  } else if (a.tma_a && !encode_tmap_im2col_bf16(&out->amap, a.x, ti.C, ti.W, ti.H, k, -a.pw, -a.ph,
+                                                 (op.pw_hi >= 0 ? op.pw_hi : a.pw) - (a.S - 1),
+                                                 (op.ph_hi >= 0 ? op.ph_hi : a.ph) - (a.R - 1), a.sw, a.sh, a.cpl))
     return fail(GX_ECUDA, "cuTensorMapEncodeIm2col failed for conv input");
   if (a.res && !encode_tmap_2d_bf16(&out->rmap, a.res, a.res_ld, a.M, static_cast<uint64_t>(a.res_ld) * 2, 64, kBM))
     return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for the residual");
   out->grid = std::min(a.num_tiles, std::max(1, sm_budget));
+  a.gmaps = nullptr;
+  if (getenv("GX_GMAPS")) {  // experiment: maps in global memory (leaks one small buffer per plan)
+    CUtensorMap* d = nullptr;
+    CUtensorMap h[3] = {out->wmap, out->amap, out->rmap};
+    if (cudaMalloc(&d, sizeof(h)) == cudaSuccess && cudaMemcpy(d, h, sizeof(h), cudaMemcpyHostToDevice) == cudaSuccess)
+      a.gmaps = d;
+  }
   return GX_OK;
 }
 

@@ -46,6 +46,7 @@ struct ConvArgs {
   int cpl;    // channels per im2col TMA load (8/16/32/64): Cin % cpl == 0, cpl | 64
   int nres;   // residual smem slots (0 without residual, else 1 or 2)
   int a2d;    // A via a plain 2D tiled map over [M, C] (1x1, stride 1, no padding)
+  const CUtensorMap* gmaps;  // experiment: tensor maps read from global memory instead of params
 };
 constexpr int kConvThreads = 320;  // 4 A-producer warps, TMA warp, MMA warp, 4 epilogue warps
 constexpr int kBM = 128;
@@ -61,6 +62,8 @@ bool encode_tmap_im2col_bf16(CUtensorMap* map, const void* base, int C, int W, i
 // ------------------------------------------------------------------ bandwidth-bound kernels
 cudaError_t launch_gather(int k, const void* const* src, const int32_t* src_dtype, int64_t pixels,
                           int c_src, int c_dst, __nv_bfloat16* dst, int grid, cudaStream_t s);
+cudaError_t launch_gather_s2d(int k, const void* const* src, const int32_t* src_dtype, int Ho, int Wo, int f,
+                              int c_src, int c_dst, __nv_bfloat16* dst, int grid, cudaStream_t s);
 cudaError_t launch_scatter(int k, const void* src, int src_dtype, int64_t row_elems, void* const* dst,
                            int dst_dtype, int grid, cudaStream_t s);
 cudaError_t launch_pool(int mode, const __nv_bfloat16* x, int N, int H, int W, int C, int x_ld,

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <map>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -15,6 +16,7 @@ struct gx_ctx {
 };
 
 namespace gx {
+struct SpanMaps;
 struct ConvLaunch {
   CUtensorMap wmap;
   CUtensorMap amap;  // im2col map of the input (args.tma_a)
@@ -53,19 +55,23 @@ struct gx_stage {
   void* ws = nullptr;
   size_t ws_bytes = 0;
   int in_tid = -1, out_tid = -1;
+  struct SpanChunk {
+    void* d_ops = nullptr;  // SpanOp[n_ops] (device)
+    int n_ops = 0;
+    std::shared_ptr<gx::SpanMaps> maps;  // tensor maps, passed by value as a kernel parameter
+  };
   struct PerK {
     cudaGraphExec_t exec = nullptr;
     int kernels = 0;
-    // persistent span program (span_kernel.cu)
-    void* d_ops = nullptr;    // SpanOp[n_ops]
-    void* d_tmaps = nullptr;  // CUtensorMap[3 * n_conv]
+    // persistent span program (span_kernel.cu): consecutive launches, one per chunk
+    std::vector<SpanChunk> chunks;
     int n_ops = 0;
     int span_stages = 0, bn_max = 0, has_res = 0, bias_bytes = 0;
   };
   std::map<int, PerK> graphs;
   bool span_mode = true;                 // one persistent launch per batch (else per-op CUDA graph)
   unsigned long long* bar = nullptr;     // grid-barrier arrival counter (device)
-  unsigned long long launches = 0;       // span launches so far (barrier base)
+  unsigned long long arrivals = 0;       // barrier arrivals so far (base of the next launch)
   // profiling scratch
   void* prof_src = nullptr;
   void* prof_dst = nullptr;

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <vector>
 
 #include "gx_internal.h"
@@ -127,7 +128,9 @@ int build_span_program(gx_stage* st, int k, gx_stage::PerK* out) {
   const uint8_t* wbase = static_cast<const uint8_t*>(m->wdev);
   const gx_tensor* T = m->tensors.data();
   std::vector<SpanOp> ops(st->ops.size());
-  std::vector<CUtensorMap> maps;
+  // chunks of consecutive ops whose tensor maps fit one kernel parameter block
+  std::vector<std::shared_ptr<SpanMaps>> chunk_maps(1, std::make_shared<SpanMaps>());
+  std::vector<int> chunk_first(1, 0), chunk_used(1, 0);
   int bn_max = 16, has_res = 0, cout_max = 16;
   for (size_t i = 0; i < st->ops.size(); ++i) {
     const gx_op& op = m->ops[st->ops[i]];
@@ -157,10 +160,22 @@ int build_span_program(gx_stage* st, int k, gx_stage::PerK* out) {
         if (rc != GX_OK) return rc;
         const ConvArgs& a = cl.args;
         if (!a.tma_a) return fail(GX_EINVAL, "span kernel needs the TMA im2col path");
-        s.tmap = static_cast<int>(maps.size());
-        maps.push_back(cl.wmap);
-        maps.push_back(cl.amap);
-        maps.push_back(cl.rmap);
+        const int need = a.res ? 3 : 2;
+        if (chunk_used.back() + need > kMaxSpanMaps) {
+          chunk_maps.push_back(std::make_shared<SpanMaps>());
+          chunk_first.push_back(static_cast<int>(i));
+          chunk_used.push_back(0);
+        }
+        SpanMaps& cm = *chunk_maps.back();
+        int& used = chunk_used.back();
+        s.tmap = used;
+        cm.m[used++] = cl.wmap;
+        cm.m[used++] = cl.amap;
+        s.rmap = -1;
+        if (a.res) {
+          s.rmap = used;
+          cm.m[used++] = cl.rmap;
+        }
         s.BN = a.BN;
         s.n_tiles = a.n_tiles;
         s.num_tiles = a.num_tiles;
@@ -226,12 +241,16 @@ int build_span_program(gx_stage* st, int k, gx_stage::PerK* out) {
   out->has_res = L.has_res;
   out->bias_bytes = L.bias_bytes;
   out->n_ops = static_cast<int>(ops.size());
-  GX_CUDA(cudaMalloc(&out->d_ops, std::max<size_t>(1, ops.size()) * sizeof(SpanOp)));
-  GX_CUDA(cudaMemcpy(out->d_ops, ops.data(), ops.size() * sizeof(SpanOp), cudaMemcpyHostToDevice));
-  GX_CUDA(cudaMalloc(&out->d_tmaps, std::max<size_t>(1, maps.size()) * sizeof(CUtensorMap)));
-  if (!maps.empty())
-    GX_CUDA(cudaMemcpy(out->d_tmaps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
-  out->kernels = 1;
+  chunk_first.push_back(static_cast<int>(ops.size()));
+  for (size_t c = 0; c + 1 < chunk_first.size(); ++c) {
+    gx_stage::SpanChunk ch;
+    ch.n_ops = chunk_first[c + 1] - chunk_first[c];
+    ch.maps = chunk_maps[c];
+    GX_CUDA(cudaMalloc(&ch.d_ops, std::max(1, ch.n_ops) * sizeof(SpanOp)));
+    GX_CUDA(cudaMemcpy(ch.d_ops, ops.data() + chunk_first[c], ch.n_ops * sizeof(SpanOp), cudaMemcpyHostToDevice));
+    out->chunks.push_back(ch);
+  }
+  out->kernels = static_cast<int>(out->chunks.size());
   return GX_OK;
 }
 
@@ -343,8 +362,8 @@ int gx_stage_destroy(gx_stage* st) {
   cudaStreamSynchronize(st->stream);
   for (auto& kv : st->graphs) {
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
-    if (kv.second.d_ops) cudaFree(kv.second.d_ops);
-    if (kv.second.d_tmaps) cudaFree(kv.second.d_tmaps);
+    for (auto& ch : kv.second.chunks)
+      if (ch.d_ops) cudaFree(ch.d_ops);
   }
   if (st->bar) cudaFree(st->bar);
   if (st->ws) cudaFree(st->ws);
@@ -386,18 +405,25 @@ int gx_stage_run(gx_stage* st, int k, const void* const* src, const int32_t* src
   int rc = stage_graph(st, k, &pk);
   if (rc != GX_OK) return rc;
   const int bw_grid = st->sm_budget * 8;
-  GX_CUDA(launch_gather(k, src, src_dtype, static_cast<int64_t>(tin.H) * tin.W, c_src, tin.C,
-                        static_cast<__nv_bfloat16*>(st->tptr[st->in_tid]), bw_grid, st->stream));
+  if (tin.s2d > 1) {
+    if (src_channels <= 0) return fail(GX_EINVAL, "space-to-depth boundary needs the client's channel count");
+    GX_CUDA(launch_gather_s2d(k, src, src_dtype, tin.H, tin.W, tin.s2d, src_channels, tin.C,
+                              static_cast<__nv_bfloat16*>(st->tptr[st->in_tid]), bw_grid, st->stream));
+  } else {
+    GX_CUDA(launch_gather(k, src, src_dtype, static_cast<int64_t>(tin.H) * tin.W, c_src, tin.C,
+                          static_cast<__nv_bfloat16*>(st->tptr[st->in_tid]), bw_grid, st->stream));
+  }
   if (st->span_mode) {
     SpanSmem L;
     L.stages = pk->span_stages;
     L.bn_max = pk->bn_max;
     L.has_res = pk->has_res;
     L.bias_bytes = pk->bias_bytes;
-    const unsigned long long base = st->launches * static_cast<unsigned long long>(pk->n_ops) * st->sm_budget;
-    GX_CUDA(launch_span(static_cast<const SpanOp*>(pk->d_ops), pk->n_ops, static_cast<const CUtensorMap*>(pk->d_tmaps),
-                        st->bar, base, L, st->sm_budget, st->stream));
-    ++st->launches;
+    for (const auto& ch : pk->chunks) {
+      GX_CUDA(launch_span(static_cast<const SpanOp*>(ch.d_ops), ch.n_ops, *ch.maps, st->bar, st->arrivals, L,
+                          st->sm_budget, st->stream));
+      st->arrivals += static_cast<unsigned long long>(ch.n_ops) * st->sm_budget;
+    }
   } else {
     GX_CUDA(cudaGraphLaunch(pk->exec, st->stream));
   }
@@ -423,10 +449,11 @@ int gx_stage_span_trace(gx_stage* st, int k, int64_t* out, int64_t cap, int* n_o
   L.bn_max = pk->bn_max;
   L.has_res = pk->has_res;
   L.bias_bytes = pk->bias_bytes;
-  const unsigned long long base = st->launches * static_cast<unsigned long long>(pk->n_ops) * st->sm_budget;
-  GX_CUDA(launch_span(static_cast<const SpanOp*>(pk->d_ops), pk->n_ops, static_cast<const CUtensorMap*>(pk->d_tmaps),
-                      st->bar, base, L, st->sm_budget, st->stream, d));
-  ++st->launches;
+  if (pk->chunks.size() != 1) return fail(GX_EINVAL, "trace supports single-chunk spans");
+  const gx_stage::SpanChunk& ch = pk->chunks[0];
+  GX_CUDA(launch_span(static_cast<const SpanOp*>(ch.d_ops), ch.n_ops, *ch.maps, st->bar, st->arrivals, L,
+                      st->sm_budget, st->stream, d));
+  st->arrivals += static_cast<unsigned long long>(ch.n_ops) * st->sm_budget;
   GX_CUDA(cudaStreamSynchronize(st->stream));
   GX_CUDA(cudaMemcpy(out, d, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
   cudaFree(d);
@@ -465,9 +492,11 @@ int gx_stage_profile(gx_stage* st, int k, int iters, float* ms_out) {
     dst[i] = static_cast<uint8_t*>(st->prof_dst) + i * out_bytes;
   }
   const int32_t dst_dtype = st->end == m->n_units() ? GX_F32 : GX_BF16;
+  // a space-to-depth boundary takes the client image (same byte count, C / s2d^2 channels)
+  const int c_src = tin.s2d > 1 ? tin.C / (tin.s2d * tin.s2d) : tin.C;
   // warm-up (also captures the graph)
   for (int w = 0; w < 3; ++w) {
-    int rc = gx_stage_run(st, k, src.data(), dt.data(), tin.C, dst.data(), dst_dtype);
+    int rc = gx_stage_run(st, k, src.data(), dt.data(), c_src, dst.data(), dst_dtype);
     if (rc != GX_OK) return rc;
   }
   cudaEvent_t e0, e1;
@@ -476,7 +505,7 @@ int gx_stage_profile(gx_stage* st, int k, int iters, float* ms_out) {
   std::vector<float> t(iters);
   for (int i = 0; i < iters; ++i) {
     GX_CUDA(cudaEventRecord(e0, st->stream));
-    int rc = gx_stage_run(st, k, src.data(), dt.data(), tin.C, dst.data(), dst_dtype);
+    int rc = gx_stage_run(st, k, src.data(), dt.data(), c_src, dst.data(), dst_dtype);
     if (rc != GX_OK) return rc;
     GX_CUDA(cudaEventRecord(e1, st->stream));
     GX_CUDA(cudaEventSynchronize(e1));

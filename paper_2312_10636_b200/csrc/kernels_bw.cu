@@ -31,6 +31,31 @@ __device__ __forceinline__ uint4 f32x8_to_bf16x8(float4 a, float4 b) {
 // K1 gather: k entry activations (each fp32 from ingress or bf16 from an alignment stage) ->
 // one contiguous bf16 NHWC batch.  c_src == c_dst: 8-element vectors; otherwise per-element
 // with zero padding of the extra channels (the 3-channel image into the 8-channel stem input).
+// K1 gather into a space-to-depth boundary: client image [Ho*f, Wo*f, c_src] (fp32 or bf16) ->
+// [Ho, Wo, c_dst] with channel (dy*f + dx)*c_src + c = pixel (f*h + dy, f*w + dx), zero above.
+__global__ void gather_s2d_kernel(RowPtrs src, int k, int Ho, int Wo, int f, int c_src, int c_dst,
+                                  __nv_bfloat16* __restrict__ dst) {
+  const int64_t per_row = static_cast<int64_t>(Ho) * Wo * c_dst;
+  const int64_t total = per_row * k;
+  const int Wi = Wo * f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = static_cast<int>(i / per_row);
+    const int64_t e = i - r * per_row;
+    const int64_t px = e / c_dst;
+    const int cd = static_cast<int>(e - px * c_dst);
+    float val = 0.0f;
+    if (cd < f * f * c_src) {
+      const int blk = cd / c_src, c = cd - blk * c_src;
+      const int h = static_cast<int>(px / Wo) * f + blk / f;
+      const int w = static_cast<int>(px % Wo) * f + blk % f;
+      const int64_t si = (static_cast<int64_t>(h) * Wi + w) * c_src + c;
+      val = src.dt[r] == GX_F32 ? __ldg(reinterpret_cast<const float*>(src.p[r]) + si)
+                                : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(src.p[r])[si]);
+    }
+    dst[i] = __float2bfloat16_rn(val);
+  }
+}
+
 __global__ void gather_kernel(RowPtrs src, int k, int64_t pixels, int c_src, int c_dst,
                               __nv_bfloat16* __restrict__ dst) {
   if (c_src == c_dst && (c_dst & 7) == 0) {
@@ -321,6 +346,19 @@ cudaError_t launch_gather(int k, const void* const* src, const int32_t* src_dtyp
   }
   const int64_t work = (c_src == c_dst && (c_dst & 7) == 0) ? pixels * c_dst / 8 * k : pixels * c_dst * k;
   gather_kernel<<<grid_for(work, 256, grid), 256, 0, s>>>(rp, k, pixels, c_src, c_dst, dst);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_s2d(int k, const void* const* src, const int32_t* src_dtype, int Ho, int Wo, int f,
+                              int c_src, int c_dst, __nv_bfloat16* dst, int grid, cudaStream_t s) {
+  if (k > kMaxRows || f * f * c_src > c_dst) return cudaErrorInvalidValue;
+  RowPtrs rp;
+  for (int i = 0; i < k; ++i) {
+    rp.p[i] = src[i];
+    rp.dt[i] = src_dtype[i];
+  }
+  const int64_t work = static_cast<int64_t>(Ho) * Wo * c_dst * k;
+  gather_s2d_kernel<<<grid_for(work, 256, grid), 256, 0, s>>>(rp, k, Ho, Wo, f, c_src, c_dst, dst);
   return cudaGetLastError();
 }
 

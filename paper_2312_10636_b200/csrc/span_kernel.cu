@@ -60,7 +60,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 // 1 producer issued its last activation load of op j, 2 worker/epilogue leader started op j,
 // 3 worker/epilogue leader arrived for op j.
 __global__ void __launch_bounds__(kConvThreads, 1)
-    span_kernel(const SpanOp* __restrict__ ops, int n_ops, const CUtensorMap* __restrict__ tmaps,
+    span_kernel(const SpanOp* __restrict__ ops, int n_ops, const __grid_constant__ SpanMaps P,
                 unsigned long long* __restrict__ bar, unsigned long long bar_base, SpanSmem L,
                 unsigned long long* __restrict__ trace) {
   auto stamp = [&](int j, int slot) {
@@ -112,58 +112,44 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 
   if (warp == 4) {
     // ================================================================ TMA producer
+    // Incremental walkers: no divisions per k-block (a single thread issues every load).
     if (lane == 0) {
-      int it = 0;
+      int st = 0;
+      uint32_t ph = 0;  // ring position of the next stage to fill
       for (int j = 0; j < n_ops; ++j) {
         const SpanOp& op = ops[j];
         if (op.kind != GX_OP_CONV && op.kind != GX_OP_LINEAR) continue;
-        const CUtensorMap* wmap = tmaps + op.tmap;
-        const CUtensorMap* amap = wmap + 1;
+        const CUtensorMap* wmap = &P.m[op.tmap];
+        const CUtensorMap* amap = &P.m[op.tmap + 1];
         tma_prefetch_desc(wmap);
         tma_prefetch_desc(amap);
+        const int num_kb = op.num_kb, n_tiles = op.n_tiles, cpl = op.cpl, Cin = op.Cin, Sf = op.S;
         const uint32_t b_bytes = static_cast<uint32_t>(op.BN) * 128u;
-        const int n_iter = cta_tiles(op.num_tiles) * op.num_kb;
+        const int n_iter = cta_tiles(op.num_tiles) * num_kb;
         const int npre = n_iter < S_ ? n_iter : S_;
-        const uint32_t region = static_cast<uint32_t>(kBM * op.cpl * 2);
-        // k-block iteration i -> (tile, kb)
-        auto tile_of = [&](int i) { return static_cast<int>(blockIdx.x) + (i / op.num_kb) * static_cast<int>(gridDim.x); };
-        auto issue_b = [&](int i) {
-          const int st = (it + i) % S_;
-          const int tile = tile_of(i), kb = i % op.num_kb;
-          mbar_expect_tx_arrive(&full[st], b_bytes);
-          tma_load_2d(sB + static_cast<size_t>(st) * b_stage, wmap, &full[st], kb * kBK, (tile % op.n_tiles) * op.BN);
-        };
-        auto issue_a = [&](int i) {
-          const int st = (it + i) % S_;
-          const int tile = tile_of(i), kb = i % op.num_kb;
-          const int m0 = (tile / op.n_tiles) * kBM;
-          mbar_expect_tx_arrive(&full[st], kATile);
-          uint8_t* dst = sA + static_cast<size_t>(st) * kATile;
-          if (op.a2d) {
-            tma_load_2d(dst, amap, &full[st], kb * kBK, m0);
-            return;
-          }
-          const int nimg = m0 / op.HoWo;
-          const int rem = m0 - nimg * op.HoWo;
-          const int ho0 = rem / op.Wo;
-          const int wc = (rem - ho0 * op.Wo) * op.sw - op.pw;
-          const int hc = ho0 * op.sh - op.ph;
-          // K order (r, s, c): k-block kb covers K elements [64 kb, 64 kb + 64)
-          int e = kb * kBK;
-          for (int l = 0; l < kBK / op.cpl; ++l, e += op.cpl) {
-            const int tap = e / op.Cin;
-            const int c0 = e - tap * op.Cin;
-            const int r = tap / op.S;
-            const int s = tap - r * op.S;
-            tma_load_im2col_4d(dst + l * region, amap, &full[st], c0, wc, hc, nimg, static_cast<uint16_t>(s),
-                               static_cast<uint16_t>(r));
+        const uint32_t region = static_cast<uint32_t>(kBM * cpl * 2);
+        const int nloads = kBK / cpl;
+        // B walker: tile, k-block, weight row offset of the tile
+        int b_tile = blockIdx.x, b_kb = 0, b_row = (b_tile % n_tiles) * op.BN;
+        int b_st = st;
+        uint32_t b_ph = ph;
+        auto issue_b = [&](int stage) {
+          mbar_expect_tx_arrive(&full[stage], b_bytes);
+          tma_load_2d(sB + static_cast<size_t>(stage) * b_stage, wmap, &full[stage], b_kb * kBK, b_row);
+          if (++b_kb == num_kb) {
+            b_kb = 0;
+            b_tile += gridDim.x;
+            b_row = (b_tile % n_tiles) * op.BN;
           }
         };
         // 1) weights of the first `npre` k-blocks: independent of the previous op
         for (int i = 0; i < npre; ++i) {
-          const int st = (it + i) % S_;
-          mbar_wait(&empty[st], (((it + i) / S_) & 1) ^ 1);
-          issue_b(i);
+          mbar_wait(&empty[b_st], b_ph ^ 1);
+          issue_b(b_st);
+          if (++b_st == S_) {
+            b_st = 0;
+            b_ph ^= 1;
+          }
         }
         // 2) activations only once every CTA finished op j-1
         if (n_iter > 0) {
@@ -171,45 +157,89 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           fence_proxy_async_global();
         }
         stamp(j, 0);
-        for (int i = 0; i < npre; ++i) issue_a(i);
-        // 3) steady state
-        for (int i = npre; i < n_iter; ++i) {
-          const int st = (it + i) % S_;
-          mbar_wait(&empty[st], (((it + i) / S_) & 1) ^ 1);
-          issue_b(i);
-          issue_a(i);
+        // A walker: per tile (image, output row/col origin), per load (filter tap r, s, channel c0)
+        int a_tile = blockIdx.x, a_kb = 0, m0 = 0, nimg = 0, wc = 0, hc = 0, c0 = 0, r = 0, s = 0;
+        auto tile_origin = [&]() {
+          m0 = (a_tile / n_tiles) * kBM;
+          nimg = m0 / op.HoWo;
+          const int rem = m0 - nimg * op.HoWo;
+          const int ho0 = rem / op.Wo;
+          wc = (rem - ho0 * op.Wo) * op.sw - op.pw;
+          hc = ho0 * op.sh - op.ph;
+          c0 = r = s = 0;
+        };
+        if (n_iter > 0) tile_origin();
+        for (int i = 0; i < n_iter; ++i) {
+          if (i >= npre) {  // 3) steady state: both operands of this stage
+            mbar_wait(&empty[st], ph ^ 1);
+            issue_b(st);
+          }
+          mbar_expect_tx_arrive(&full[st], kATile);
+          uint8_t* dst = sA + static_cast<size_t>(st) * kATile;
+          if (op.a2d) {
+            tma_load_2d(dst, amap, &full[st], a_kb * kBK, m0);
+          } else {
+            for (int l = 0; l < nloads; ++l) {
+              tma_load_im2col_4d(dst + l * region, amap, &full[st], c0, wc, hc, nimg, static_cast<uint16_t>(s),
+                                 static_cast<uint16_t>(r));
+              c0 += cpl;  // K order (r, s, c); loads past the last tap hit zero weights
+              if (c0 == Cin) {
+                c0 = 0;
+                if (++s == Sf) {
+                  s = 0;
+                  ++r;
+                }
+              }
+            }
+          }
+          if (++a_kb == num_kb) {
+            a_kb = 0;
+            a_tile += gridDim.x;
+            if (i + 1 < n_iter) tile_origin();
+          }
+          if (++st == S_) {
+            st = 0;
+            ph ^= 1;
+          }
         }
         stamp(j, 1);
-        it += n_iter;
       }
     }
   } else if (warp == 5) {
     // ================================================================ MMA issuer
     if (lane == 0) {
-      int it = 0, t = 0;
+      int st = 0, t = 0;
+      uint32_t ph = 0;
       for (int j = 0; j < n_ops; ++j) {
         const SpanOp& op = ops[j];
         if (op.kind != GX_OP_CONV && op.kind != GX_OP_LINEAR) continue;
-        const uint32_t region = static_cast<uint32_t>(kBM * op.cpl * 2);
+        const int cpl = op.cpl, num_kb = op.num_kb;
+        const uint32_t idesc = op.idesc;
+        const uint32_t region = static_cast<uint32_t>(kBM * cpl * 2);
+        // per-op descriptor template and the A offset of each K=16 step inside a stage
+        const uint64_t dbits = umma_desc_kmajor(0, cpl, region);
+        uint32_t offs[kBK / 16];
+#pragma unroll
+        for (int kk = 0; kk < kBK / 16; ++kk) offs[kk] = (kk * 16 / cpl) * region + (kk * 16 % cpl) * 2;
         const int ntile = cta_tiles(op.num_tiles);
         for (int tt = 0; tt < ntile; ++tt, ++t) {
           const int acc = t & 1;
           mbar_wait(&tempty[acc], ((t >> 1) & 1) ^ 1);
           tc_fence_after();
           const uint32_t d = tmem_base + acc * acc_stride;
-          for (int kb = 0; kb < op.num_kb; ++kb, ++it) {
-            const int st = it % S_;
-            mbar_wait(&full[st], (it / S_) & 1);
+          for (int kb = 0; kb < num_kb; ++kb) {
+            mbar_wait(&full[st], ph);
             tc_fence_after();
             const uint32_t abase = smem_u32(sA + static_cast<size_t>(st) * kATile);
             const uint64_t bd = umma_desc_sw128(sB + static_cast<size_t>(st) * b_stage);
 #pragma unroll
-            for (int kk = 0; kk < kBK / 16; ++kk) {
-              const int e0 = kk * 16;
-              const uint32_t addr = abase + (e0 / op.cpl) * region + (e0 % op.cpl) * 2;
-              umma_bf16(d, umma_desc_kmajor(addr, op.cpl, region), bd + 2 * kk, op.idesc, (kb | kk) != 0);
-            }
+            for (int kk = 0; kk < kBK / 16; ++kk)
+              umma_bf16(d, dbits | (((abase + offs[kk]) >> 4) & 0x3FFFull), bd + 2 * kk, idesc, (kb | kk) != 0);
             umma_commit(&empty[st]);
+            if (++st == S_) {
+              st = 0;
+              ph ^= 1;
+            }
           }
           umma_commit(&tfull[acc]);
         }
@@ -273,7 +303,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       // warps 0-3 the odd ones, so small-K convs are not bound by one warp group's epilogue.
       const int ntile = cta_tiles(op.num_tiles);
       const bool has_res = op.res != nullptr;
-      const CUtensorMap* rmap = tmaps + op.tmap + 2;
+      const CUtensorMap* rmap = &P.m[op.rmap >= 0 ? op.rmap : 0];
       auto issue_res = [&](int tt) {
         const int tile = static_cast<int>(blockIdx.x) + tt * static_cast<int>(gridDim.x);
         const int slot = r_issued & 1;
@@ -294,7 +324,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           for (int tt = 0; tt < ntile && tt < 2; ++tt) issue_res(tt);
         }
       }
-      mbar_wait(bfull, conv_seen & 1);
+      mbar_wait_sleepy(bfull, conv_seen & 1);
       ++conv_seen;
       if (leader) stamp(j, 2);
       for (int tt = 0; tt < ntile; ++tt, ++t) {
@@ -303,12 +333,12 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         const int nb0 = (tile % op.n_tiles) * op.BN;
         const int ncols = min(op.BN, op.Cout - nb0);
         const int acc = t & 1;
-        mbar_wait(&tfull[acc], (t >> 1) & 1);
+        mbar_wait_sleepy(&tfull[acc], (t >> 1) & 1);
         tc_fence_after();
         int slot = 0;
         if (has_res) {
           slot = r_waited & 1;
-          mbar_wait(&rfull[slot], (r_waited >> 1) & 1);
+          mbar_wait_sleepy(&rfull[slot], (r_waited >> 1) & 1);
           ++r_waited;
         }
         const uint8_t* res_base = sRes + slot * res_slot;
@@ -400,7 +430,7 @@ size_t span_smem_bytes(const SpanSmem& L) {
          L.bias_bytes + (2 * L.stages + 9) * 8 + 16;
 }
 
-cudaError_t launch_span(const SpanOp* ops, int n_ops, const CUtensorMap* tmaps, unsigned long long* bar,
+cudaError_t launch_span(const SpanOp* ops, int n_ops, const SpanMaps& maps, unsigned long long* bar,
                         unsigned long long bar_base, const SpanSmem& L, int grid, cudaStream_t s,
                         unsigned long long* trace) {
   static bool configured = false;
@@ -409,7 +439,7 @@ cudaError_t launch_span(const SpanOp* ops, int n_ops, const CUtensorMap* tmaps, 
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  span_kernel<<<grid, kConvThreads, span_smem_bytes(L), s>>>(ops, n_ops, tmaps, bar, bar_base, L, trace);
+  span_kernel<<<grid, kConvThreads, span_smem_bytes(L), s>>>(ops, n_ops, maps, bar, bar_base, L, trace);
   return cudaGetLastError();
 }
 

@@ -25,6 +25,7 @@ class DeviceModel:
         descs = (N.GxTensor * len(chain.tensors))()
         for i, (H, W, Cc, dt) in enumerate(chain.tensors):
             descs[i].H, descs[i].W, descs[i].C, descs[i].dtype = H, W, Cc, dt
+            descs[i].s2d = chain.tensor_s2d.get(i, 0)
         ops = (N.GxOp * len(chain.ops))(*chain.ops)
         blob = chain.blob.bytes()
         self.handle = C.c_void_p()

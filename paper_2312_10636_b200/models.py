@@ -36,7 +36,7 @@ class UnitChain:
     blob: WeightBlob = field(default_factory=WeightBlob)
     input_channels: int = 3  # channels a client actually ships at boundary 0 (pre-padding)
     unit_flops: list = field(default_factory=list)  # per-sample FLOPs of each unit
-    ingress_nchw: list = field(default_factory=list)  # torch-layout per-sample shape per boundary
+    tensor_s2d: dict = field(default_factory=dict)  # tensor id -> space-to-depth factor (stride-2 stems)
 
     @property
     def n_units(self) -> int:
@@ -54,10 +54,15 @@ class UnitChain:
         """Channels per pixel a client ships at boundary p (the stem input is 3, padded to 8)."""
         return self.input_channels if p == 0 else self.boundary_shape(p)[2]
 
+    def ingress_elems(self, p: int) -> int:
+        """Elements of the client's wire tensor at boundary p (the raw image at a s2d stem)."""
+        H, W, _, _ = self.boundary_shape(p)
+        f = self.tensor_s2d.get(self.boundary[p], 1)
+        return H * f * W * f * self.ingress_channels(p)
+
     def payload_bytes(self, p: int) -> int:
         """fp32 wire bytes at boundary p (what ModelSpec.output_bytes records)."""
-        H, W, Cc, _ = self.boundary_shape(p)
-        return H * W * self.ingress_channels(p) * 4
+        return self.ingress_elems(p) * 4
 
     def model_spec_doc(self, compute_weight=None) -> dict:
         """A reference ModelSpec JSON document (profiles.py:89-101) for this chain."""
@@ -96,21 +101,39 @@ class ChainBuilder:
         self.c.boundary.append(out)
         return self.c
 
+    def s2d_input(self, H, W, Cc, f) -> int:
+        """A boundary tensor holding a [H*f, W*f, c] client image in space-to-depth form."""
+        t = self.tensor(H, W, Cc)
+        self.c.tensor_s2d[t] = f
+        return t
+
     # -- ops ----------------------------------------------------------------
-    def conv(self, x, conv: nn.Conv2d, bn: nn.BatchNorm2d | None, relu=True, residual=-1, out=-1, out_coff=0,
-             cin_pad=None):
-        H, W, Cx, _ = self.shape(x)
+    @staticmethod
+    def folded(conv: nn.Conv2d, bn: nn.BatchNorm2d | None):
+        """Conv weight/bias with the following BatchNorm folded in (fp32)."""
         w = conv.weight.detach().float()
-        cout, cin, R, S = w.shape
-        b = conv.bias.detach().float() if conv.bias is not None else torch.zeros(cout)
+        b = conv.bias.detach().float() if conv.bias is not None else torch.zeros(w.shape[0])
         if bn is not None:
             scale = bn.weight.detach().float() / torch.sqrt(bn.running_var.detach().float() + bn.eps)
             w = w * scale[:, None, None, None]
             b = (b - bn.running_mean.detach().float()) * scale + bn.bias.detach().float()
+        return w, b
+
+    def conv(self, x, conv: nn.Conv2d, bn: nn.BatchNorm2d | None, relu=True, residual=-1, out=-1, out_coff=0,
+             cin_pad=None):
+        w, b = self.folded(conv, bn)
         sh, sw = conv.stride
         ph, pw = conv.padding
-        Ho = (H + 2 * ph - R) // sh + 1
-        Wo = (W + 2 * pw - S) // sw + 1
+        return self.conv_w(x, w, b, (sh, sw), (ph, pw, ph, pw), relu, residual, out, out_coff, cin_pad)
+
+    def conv_w(self, x, w, b, stride, pad, relu=True, residual=-1, out=-1, out_coff=0, cin_pad=None, flops=None):
+        """Conv from explicit (folded) weights; pad = (top, left, bottom, right)."""
+        H, W, Cx, _ = self.shape(x)
+        cout, cin, R, S = w.shape
+        sh, sw = stride
+        ph, pw, ph_hi, pw_hi = pad
+        Ho = (H + ph + ph_hi - R) // sh + 1
+        Wo = (W + pw + pw_hi - S) // sw + 1
         cin_pad = cin_pad or cin
         assert cin_pad <= Cx, (cin_pad, Cx)
         if out < 0:
@@ -121,9 +144,32 @@ class ChainBuilder:
         b_off = self.c.blob.add_f32(b)
         self.c.ops.append(N.make_op(N.GX_OP_CONV, x, out, in2=residual, out_coff=out_coff,
                                     act=N.GX_ACT_RELU if relu else N.GX_ACT_NONE, R=R, S=S, sh=sh, sw=sw, ph=ph,
-                                    pw=pw, Cin=cin_pad, Cout=cout, w_off=w_off, b_off=b_off))
-        self._flops += 2.0 * Ho * Wo * cout * cin * R * S
+                                    pw=pw, Cin=cin_pad, Cout=cout, w_off=w_off, b_off=b_off,
+                                    ph_hi=ph_hi if ph_hi != ph else -1, pw_hi=pw_hi if pw_hi != pw else -1))
+        self._flops += flops if flops is not None else 2.0 * Ho * Wo * cout * cin * R * S
         return out
+
+    def s2d_stem(self, conv: nn.Conv2d, bn: nn.BatchNorm2d | None, image_hw: int, relu=True):
+        """A 7x7 stride-2 pad-3 stem as the equivalent 4x4 stride-1 conv over the 2x2
+        space-to-depth image (channel (dy*2+dx)*3 + c), padding (2, 2, 1, 1).
+
+        Output pixel ho reads image rows 2ho-3 .. 2ho+3; with j = r + 1 that is block row
+        ho - 2 + j // 2, sub-row j % 2, so tap r maps to (R' = (r+1) // 2, dy = (r+1) % 2)."""
+        w, b = self.folded(conv, bn)
+        cout, cin, R, S = w.shape
+        assert (R, S) == (7, 7) and conv.stride == (2, 2) and conv.padding == (3, 3)
+        w2 = torch.zeros(cout, 16, 4, 4)
+        for r in range(7):
+            for s in range(7):
+                Rp, dy = (r + 1) // 2, (r + 1) % 2
+                Sp, dx = (s + 1) // 2, (s + 1) % 2
+                for c in range(cin):
+                    w2[:, (dy * 2 + dx) * cin + c, Rp, Sp] = w[:, c, r, s]
+        x = self.s2d_input(image_hw // 2, image_hw // 2, 16, 2)
+        self.begin_unit(x)
+        Ho = image_hw // 2
+        y = self.conv_w(x, w2, b, (1, 1), (2, 2, 1, 1), relu=relu, flops=2.0 * Ho * Ho * cout * cin * R * S)
+        return y
 
     def pool(self, x, kind: str, k, s, p, out=-1, out_coff=0, count_include_pad=True):
         H, W, Cx, _ = self.shape(x)
@@ -222,9 +268,9 @@ def torch_model(name: str, seed: int = 0) -> nn.Module:
 
 def _resnet_chain(name: str, m) -> UnitChain:
     b = ChainBuilder(name)
-    x = b.tensor(224, 224, 8)  # 3-channel image, zero-padded to 8 channels by the gather
-    b.begin_unit(x)
-    y = b.conv(x, m.conv1, m.bn1, relu=True, cin_pad=8)
+    # boundary 0: the 3-channel 224x224 image, rearranged by the gather into 2x2 space-to-depth
+    # blocks (112x112x16) so the 7x7/2 stem runs as a 4x4/1 conv with 32-byte im2col pixels
+    y = b.s2d_stem(m.conv1, m.bn1, 224)
     y = b.pool(y, "max", 3, 2, 1)
     for layer in (m.layer1, m.layer2, m.layer3, m.layer4):
         for blk in layer:

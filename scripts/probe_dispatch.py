@@ -16,8 +16,7 @@ dm = DeviceModel(chain)
 L = N.lib()
 for (a, b) in ((0, 18), (9, 18), (15, 18), (17, 18)):
     st = StageInstance(dm, a, b, 16, 2)
-    H, W, Cc, _ = chain.boundary_shape(a)
-    x = torch.randn(H * W * chain.ingress_channels(a), device="cuda")
+    x = torch.randn(chain.ingress_elems(a), device="cuda")
     out = torch.empty(chain.boundary_elems(b), device="cuda")
     src = N.ptr_array([x.data_ptr()])
     dt = N.i32_array([N.GX_F32])

@@ -34,9 +34,8 @@ for c in sizes:
     keep = []
     slot = 0
     for p in sorted({r.point for r in dep.routes.values()}):
-        H, W, Cc, _ = chain.boundary_shape(p)
         ch = chain.ingress_channels(p)
-        t = torch.randn(H * W * ch, device="cuda", generator=g)
+        t = torch.randn(chain.ingress_elems(p), device="cuda", generator=g)
         keep.append(t)
         ingress[p] = (t.data_ptr(), t.numel() * 4, ch)
         slot = max(slot, t.numel() * 4, chain.boundary_elems(p) * 2)
