@@ -156,7 +156,7 @@ int build_span_program(gx_stage* st, int k, gx_stage::PerK* out) {
       case GX_OP_CONV:
       case GX_OP_LINEAR: {
         ConvLaunch cl;
-        int rc = plan_conv(op, T, st->tptr.data(), wbase, k, st->sm_budget, &cl, 128);
+        int rc = plan_conv(op, T, st->tptr.data(), wbase, k, st->sm_budget, &cl, 256);
         if (rc != GX_OK) return rc;
         const ConvArgs& a = cl.args;
         if (!a.tma_a) return fail(GX_EINVAL, "span kernel needs the TMA im2col path");
@@ -231,10 +231,14 @@ int build_span_program(gx_stage* st, int k, gx_stage::PerK* out) {
   }
   SpanSmem L;
   L.bn_max = bn_max;
-  L.has_res = has_res;
   L.bias_bytes = (cout_max * 4 + 15) & ~15;
-  L.stages = 8;
-  while (L.stages > 2 && span_smem_bytes(L) > 225 * 1024) --L.stages;
+  // residual slots: two (prefetch one tile ahead) unless that squeezes the ring below 3 stages
+  for (int nres = has_res ? 2 : 0; nres >= (has_res ? 1 : 0); --nres) {
+    L.has_res = nres;
+    L.stages = 8;
+    while (L.stages > 2 && span_smem_bytes(L) > 225 * 1024) --L.stages;
+    if (L.stages >= 3) break;
+  }
   if (span_smem_bytes(L) > 227 * 1024) return fail(GX_EINVAL, "span kernel shared memory does not fit");
   out->span_stages = L.stages;
   out->bn_max = L.bn_max;

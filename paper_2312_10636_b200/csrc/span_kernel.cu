@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   uint8_t* sB = sA + static_cast<size_t>(S_) * kATile;
   uint8_t* sRes = sB + static_cast<size_t>(S_) * b_stage;
   const uint32_t res_slot = static_cast<uint32_t>((L.bn_max + 63) / 64) * kResGroup;
-  float* sBias = reinterpret_cast<float*>(sRes + (L.has_res ? 2 * res_slot : 0));
+  float* sBias = reinterpret_cast<float*>(sRes + L.has_res * res_slot);
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sBias) + L.bias_bytes);
   uint64_t* empty = full + S_;
   uint64_t* tfull = empty + S_;
@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       fence_barrier_init();
     }
     __syncwarp();
-    tmem_alloc(tslot, 2 * L.bn_max <= 128 ? 128 : 256);
+    tmem_alloc(tslot, 2 * L.bn_max <= 128 ? 128 : (2 * L.bn_max <= 256 ? 256 : 512));
   }
   tc_fence_before();
   __syncthreads();
@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       const CUtensorMap* rmap = &P.m[op.rmap >= 0 ? op.rmap : 0];
       auto issue_res = [&](int tt) {
         const int tile = static_cast<int>(blockIdx.x) + tt * static_cast<int>(gridDim.x);
-        const int slot = r_issued & 1;
+        const int slot = L.has_res == 2 ? (r_issued & 1) : 0;
         const int groups = (op.BN + 63) / 64;
         mbar_arrive_expect_tx(&rfull[slot], static_cast<uint32_t>(groups) * kResGroup);
         for (int g = 0; g < groups; ++g)
@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           tma_prefetch_desc(rmap);
           grid_wait(bar, prev_done);  // the residual may be the previous op's output
           fence_proxy_async_global();
-          for (int tt = 0; tt < ntile && tt < 2; ++tt) issue_res(tt);
+          for (int tt = 0; tt < ntile && tt < L.has_res; ++tt) issue_res(tt);
         }
       }
       mbar_wait_sleepy(bfull, conv_seen & 1);
@@ -337,8 +337,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         tc_fence_after();
         int slot = 0;
         if (has_res) {
-          slot = r_waited & 1;
-          mbar_wait_sleepy(&rfull[slot], (r_waited >> 1) & 1);
+          slot = L.has_res == 2 ? (r_waited & 1) : 0;
+          mbar_wait_sleepy(&rfull[slot], (L.has_res == 2 ? (r_waited >> 1) : r_waited) & 1);
           ++r_waited;
         }
         const uint8_t* res_base = sRes + slot * res_slot;
@@ -401,7 +401,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         mbar_arrive(&tempty[acc]);
         if (has_res) {
           named_bar_sync(1, 256);  // all epilogue threads are done with this residual slot
-          if (leader && tt + 2 < ntile) issue_res(tt + 2);
+          if (leader && tt + L.has_res < ntile) issue_res(tt + L.has_res);
         }
       }
       // op done on this CTA: publish to the grid
@@ -419,14 +419,14 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   __syncthreads();
   if (warp == 4) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 2 * L.bn_max <= 128 ? 128 : 256);
+    tmem_dealloc(tmem_base, 2 * L.bn_max <= 128 ? 128 : (2 * L.bn_max <= 256 ? 256 : 512));
   }
 }
 }  // namespace
 
 size_t span_smem_bytes(const SpanSmem& L) {
   const size_t res_slot = static_cast<size_t>((L.bn_max + 63) / 64) * kResGroup;
-  return 1024 + static_cast<size_t>(L.stages) * (kATile + L.bn_max * 128) + (L.has_res ? 2 * res_slot : 0) +
+  return 1024 + static_cast<size_t>(L.stages) * (kATile + L.bn_max * 128) + L.has_res * res_slot +
          L.bias_bytes + (2 * L.stages + 9) * 8 + 16;
 }
 
