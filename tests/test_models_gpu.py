@@ -116,3 +116,20 @@ def test_inception_end_to_end_within_framework_bf16_error():
         rel = ((got[i] - ref[i]).norm() / ref[i].norm()).item()
         assert rel <= max(2e-2, 1.25 * fw), (i, rel, fw)
     _check(got, ref, tol=1.0)
+
+
+@pytest.mark.parametrize("budget", [4, 148])
+def test_span_kernel_matches_per_op_path(budget, monkeypatch):
+    """The single-launch persistent span kernel (GX_EXEC=span) and the per-op graph path run the
+    same tiles in the same K order: identical outputs."""
+    from paper_2312_10636_b200.engine import StageInstance
+    m, chain, dm = _setup("resnet50")
+    x = torch.randn(3, 3, 224, 224, generator=torch.Generator().manual_seed(5))
+    inp = _inputs(x)
+    monkeypatch.setenv("GX_EXEC", "graph")
+    ref = StageInstance(dm, 0, chain.n_units, max_batch=4, sm_budget=budget).run(inp, src_channels=3)
+    monkeypatch.setenv("GX_EXEC", "span")
+    got = StageInstance(dm, 0, chain.n_units, max_batch=4, sm_budget=budget).run(inp, src_channels=3)
+    for a, b in zip(got, ref):
+        rel = ((a - b).norm() / b.norm()).item()
+        assert rel < 1e-3, rel
