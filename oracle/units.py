@@ -42,17 +42,13 @@ def inception_units(m) -> list:
 
 
 def bert_units(m) -> list:
-    layers = m.encoder.layer
-
-    def unit(layer):
-        return lambda x: layer(x)[0] if isinstance(layer(x), tuple) else layer(x)
-
+    """Unit u = encoder layer u on [k, S, hidden] (transformers BertLayer, no attention mask:
+    the reference's profiled BERT runs full 128-token sequences)."""
     out = []
-    for layer in layers:
+    for layer in m.encoder.layer:
         def f(x, layer=layer):
-            r = layer(x.unsqueeze(0) if x.dim() == 2 else x)
-            r = r[0] if isinstance(r, tuple) else r
-            return r
+            r = layer(x)
+            return r[0] if isinstance(r, tuple) else r
         out.append(f)
     return out
 

@@ -1,0 +1,75 @@
+"""BERT-base as a unit chain (BASELINE.json configs[4]): 12 units = 12 encoder layers.
+
+Boundary p is the hidden state entering layer p, [S=128, hidden=768] per request (the client
+computes the embeddings; 393,216 B fp32 on the wire).  Per layer:
+  QKV (fused 768 -> 2304)  -> attention (12 heads x 64, online softmax)
+  -> output dense + residual -> LayerNorm -> FFN1 + GELU -> FFN2 + residual -> LayerNorm
+The linears run on the tcgen05 GEMM path; the pre-LN residual adds are fused into the linear
+epilogues.  Parameters come from transformers' BertModel(BertConfig()) (seeded, random init).
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _native as N
+from .device import pack_conv_weight
+from .models import ChainBuilder, UnitChain
+
+
+def _linear(b: ChainBuilder, x, weight, bias, act=N.GX_ACT_NONE, residual=-1):
+    S, W, K, _ = b.shape(x)
+    n_out = weight.shape[0]
+    out = b.tensor(S, W, n_out)
+    w_off = b.c.blob.add_bf16(pack_conv_weight(weight.detach().float().view(n_out, K, 1, 1)))
+    b_off = b.c.blob.add_f32(bias.detach().float())
+    b.c.ops.append(N.make_op(N.GX_OP_LINEAR, x, out, in2=residual, act=act, Cin=K, Cout=n_out, w_off=w_off,
+                             b_off=b_off))
+    b._flops += 2.0 * S * W * n_out * K
+    return out
+
+
+def _layernorm(b: ChainBuilder, x, ln):
+    S, W, C, _ = b.shape(x)
+    out = b.tensor(S, W, C)
+    g_off = b.c.blob.add_f32(ln.weight.detach().float())
+    be_off = b.c.blob.add_f32(ln.bias.detach().float())
+    b.c.ops.append(N.make_op(N.GX_OP_LAYERNORM, x, out, w_off=g_off, b_off=be_off, eps=float(ln.eps)))
+    return out
+
+
+def _attention(b: ChainBuilder, qkv, heads: int):
+    S, W, C3, _ = b.shape(qkv)
+    hidden = C3 // 3
+    out = b.tensor(S, W, hidden)
+    b.c.ops.append(N.make_op(N.GX_OP_ATTENTION, qkv, out, heads=heads, Cout=hidden))
+    b._flops += 4.0 * S * S * hidden
+    return out
+
+
+def bert_chain(m, seq_len: int = 128) -> UnitChain:
+    cfg = m.config
+    hidden = cfg.hidden_size
+    b = ChainBuilder("bert_base")
+    b.c.input_channels = hidden
+    x = b.tensor(seq_len, 1, hidden)
+    for layer in m.encoder.layer:
+        b.begin_unit(x)
+        att = layer.attention
+        sa = att.self
+        w = torch.cat([sa.query.weight, sa.key.weight, sa.value.weight], 0)
+        bias = torch.cat([sa.query.bias, sa.key.bias, sa.value.bias], 0)
+        qkv = _linear(b, x, w, bias)
+        ctx = _attention(b, qkv, cfg.num_attention_heads)
+        h = _linear(b, ctx, att.output.dense.weight, att.output.dense.bias, residual=x)
+        h = _layernorm(b, h, att.output.LayerNorm)
+        f = _linear(b, h, layer.intermediate.dense.weight, layer.intermediate.dense.bias, act=N.GX_ACT_GELU)
+        f = _linear(b, f, layer.output.dense.weight, layer.output.dense.bias, residual=h)
+        x = _layernorm(b, f, layer.output.LayerNorm)
+    return b.finish(x)
+
+
+def bert_model(seed: int = 0):
+    from transformers import BertConfig, BertModel
+
+    torch.manual_seed(seed)
+    return BertModel(BertConfig(), add_pooling_layer=False).eval()

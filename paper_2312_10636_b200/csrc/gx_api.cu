@@ -258,6 +258,23 @@ int launch_op(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
                                    static_cast<__nv_bfloat16*>(ptrs[op.out]), to.C, op.out_coff, bw_grid, s));
       break;
     }
+    case GX_OP_LAYERNORM: {
+      const gx_tensor& ti = T[op.in];
+      const int rows = k * ti.H * ti.W;
+      GX_CUDA(launch_layernorm(static_cast<const __nv_bfloat16*>(ptrs[op.in]), nullptr, rows, ti.C,
+                               reinterpret_cast<const float*>(wbase + op.w_off),
+                               reinterpret_cast<const float*>(wbase + op.b_off), op.eps,
+                               static_cast<__nv_bfloat16*>(ptrs[op.out]), bw_grid, s));
+      break;
+    }
+    case GX_OP_ATTENTION: {
+      const gx_tensor& ti = T[op.in];
+      const gx_tensor& to = T[op.out];
+      if (op.heads < 1 || to.C % op.heads || ti.C != 3 * to.C) return fail(GX_EINVAL, "bad attention shapes");
+      GX_CUDA(launch_attention(static_cast<const __nv_bfloat16*>(ptrs[op.in]), k, ti.H, op.heads, to.C / op.heads,
+                               static_cast<__nv_bfloat16*>(ptrs[op.out]), bw_grid, s));
+      break;
+    }
     default:
       return fail(GX_EINVAL, "unsupported op kind " + std::to_string(op.kind));
   }

@@ -241,6 +241,10 @@ def torch_model(name: str, seed: int = 0) -> nn.Module:
     """The fp32 parameter source for `name` (also what the CPU oracle runs)."""
     import torchvision
 
+    if name == "bert_base":
+        from .bert import bert_model
+
+        return bert_model(seed)
     torch.manual_seed(seed)
     if name == "resnet50":
         m = torchvision.models.resnet50(weights=None)

@@ -182,3 +182,65 @@ def test_gather_scatter_bit_exact():
         v = d8[i].view(224 * 224, 8)
         assert torch.equal(v[:, :3], img[i].view(-1, 3).to(torch.bfloat16))
         assert (v[:, 3:] == 0).all()
+
+
+@pytest.mark.parametrize("k,S,K,O,act,residual", [(1, 128, 768, 2304, "none", False), (3, 128, 768, 768, "none", True),
+                                                  (2, 128, 768, 3072, "gelu", False), (2, 128, 3072, 768, "none", True)])
+def test_linear_matches_torch(k, S, K, O, act, residual):
+    """BERT's four linears: [S, K] x W^T on the tcgen05 GEMM path (GX_OP_LINEAR, 1x1 over [S,1,K])."""
+    g = torch.Generator().manual_seed(11)
+    x = torch.randn(k, S, K, generator=g).to(torch.bfloat16)
+    w = torch.randn(O, K, generator=g) / K ** 0.5
+    b = torch.randn(O, generator=g) * 0.1
+    ref = x.float() @ w.to(torch.bfloat16).float().t() + b
+    res = torch.randn(k, S, O, generator=g).to(torch.bfloat16) if residual else None
+    if residual:
+        ref = ref + res.float()
+    if act == "gelu":
+        ref = F.gelu(ref)
+    blob = WeightBlob()
+    w_off = blob.add_bf16(pack_conv_weight(w.view(O, K, 1, 1)))
+    b_off = blob.add_f32(b)
+    wdev = torch.from_numpy(blob.bytes()).cuda()
+    y = torch.full((k, S, O), float("nan"), dtype=torch.bfloat16, device="cuda")
+    descs = [tensor_desc(S, 1, K), tensor_desc(S, 1, O), tensor_desc(S, 1, O)]
+    op = N.make_op(N.GX_OP_LINEAR, 0, 1, in2=2 if residual else -1,
+                   act=N.GX_ACT_GELU if act == "gelu" else N.GX_ACT_NONE, Cin=K, Cout=O, w_off=w_off, b_off=b_off)
+    run_op(op, [x.cuda(), y, res.cuda() if residual else y], descs, wdev, k, 40)
+    torch.cuda.synchronize()
+    assert _rel(y.float().cpu(), ref) < 1.5e-2
+
+
+@pytest.mark.parametrize("k,S,C", [(1, 128, 768), (5, 128, 768), (2, 33, 256), (1, 7, 1024)])
+def test_layernorm_matches_torch(k, S, C):
+    g = torch.Generator().manual_seed(12)
+    x = (torch.randn(k, S, C, generator=g) * 3 + 1).to(torch.bfloat16)
+    gamma = torch.randn(C, generator=g) * 0.2 + 1
+    beta = torch.randn(C, generator=g) * 0.1
+    ref = F.layer_norm(x.float(), (C,), gamma, beta, eps=1e-12)
+    blob = WeightBlob()
+    g_off, b_off = blob.add_f32(gamma), blob.add_f32(beta)
+    wdev = torch.from_numpy(blob.bytes()).cuda()
+    y = torch.full((k, S, C), float("nan"), dtype=torch.bfloat16, device="cuda")
+    op = N.make_op(N.GX_OP_LAYERNORM, 0, 1, w_off=g_off, b_off=b_off, eps=1e-12)
+    run_op(op, [x.cuda(), y], [tensor_desc(S, 1, C), tensor_desc(S, 1, C)], wdev, k, 16)
+    torch.cuda.synchronize()
+    assert _rel(y.float().cpu(), ref) < 1e-2
+
+
+@pytest.mark.parametrize("k,S,heads", [(1, 128, 12), (3, 128, 12), (2, 77, 4), (1, 512, 2)])
+def test_attention_matches_torch(k, S, heads):
+    """Non-causal multi-head attention on a packed [q|k|v] row (BertSelfAttention, no mask)."""
+    g = torch.Generator().manual_seed(13)
+    D = 64
+    hidden = heads * D
+    qkv = (torch.randn(k, S, 3 * hidden, generator=g) * 1.5).to(torch.bfloat16)
+    q, kk, v = qkv.float().split(hidden, dim=-1)
+    sh = lambda t: t.view(k, S, heads, D).transpose(1, 2)
+    ref = F.scaled_dot_product_attention(sh(q), sh(kk), sh(v)).transpose(1, 2).reshape(k, S, hidden)
+    y = torch.full((k, S, hidden), float("nan"), dtype=torch.bfloat16, device="cuda")
+    op = N.make_op(N.GX_OP_ATTENTION, 0, 1, heads=heads, Cout=hidden)
+    run_op(op, [qkv.cuda(), y], [tensor_desc(S, 1, 3 * hidden), tensor_desc(S, 1, hidden)],
+           torch.zeros(256, device="cuda"), k, 30)
+    torch.cuda.synchronize()
+    assert _rel(y.float().cpu(), ref) < 1.5e-2

@@ -133,3 +133,31 @@ def test_span_kernel_matches_per_op_path(budget, monkeypatch):
     for a, b in zip(got, ref):
         rel = ((a - b).norm() / b.norm()).item()
         assert rel < 1e-3, rel
+
+
+def test_bert_full_span_matches_fp32_oracle():
+    """configs[4]: 12 encoder layers on [128, 768] hidden states (client-side embeddings)."""
+    from paper_2312_10636_b200.engine import StageInstance
+    m, chain, dm = _setup("bert_base")
+    k = 3
+    x = torch.randn(k, 128, 768, generator=torch.Generator().manual_seed(5))
+    ref = run_span(units_for("bert_base", m), 0, chain.n_units, x)
+    st = StageInstance(dm, 0, chain.n_units, max_batch=4, sm_budget=148)
+    got = torch.stack(st.run([x[i].contiguous().cuda() for i in range(k)])).cpu().view(k, 128, 768)
+    for i in range(k):
+        rel = ((got[i] - ref[i]).norm() / ref[i].norm()).item()
+        assert rel < 2e-2, (i, rel)
+
+
+def test_bert_split_is_bit_exact():
+    from paper_2312_10636_b200.engine import StageInstance
+    m, chain, dm = _setup("bert_base")
+    x = torch.randn(4, 128, 768, generator=torch.Generator().manual_seed(6))
+    inp = [x[i].contiguous().cuda() for i in range(4)]
+    full = StageInstance(dm, 0, 12, max_batch=4, sm_budget=148).run(inp)
+    a = StageInstance(dm, 0, 5, max_batch=4, sm_budget=37)
+    b = StageInstance(dm, 5, 12, max_batch=4, sm_budget=100)
+    mid = a.run(inp)
+    out = b.run(mid[:1]) + b.run(mid[1:])
+    for i in range(4):
+        assert torch.equal(out[i], full[i]), i
