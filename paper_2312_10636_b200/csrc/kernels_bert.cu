@@ -66,88 +66,142 @@ __global__ void layernorm_kernel(const __nv_bfloat16* __restrict__ x, int rows, 
   }
 }
 
-// Self-attention of one (request, head) per CTA iteration: K and V of the head staged in shared
-// memory, one thread per query row with an online (streaming) softmax in fp32, so the S x S score
-// matrix never materialises.  qkv rows are [q | k | v] (3 x hidden), heads are D-wide slices.
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t ld_b32(const __nv_bfloat16* p) { return *reinterpret_cast<const uint32_t*>(p); }
+
+constexpr int kAttnQ = 64;  // query rows per CTA (4 warps x 16)
+
+// Self-attention of one (request, head, 64-query block) per CTA iteration.  The per-head products
+// are tiny (S x S x 64): QK^T and PV run on warp-level bf16 MMA (m16n8k16) with fp32
+// accumulators, each warp owning 16 query rows; K and V^T of the head are staged in shared memory
+// (row strides padded so the fragment loads are bank-conflict free) and keys are consumed in
+// 64-wide chunks with an online softmax, so the S x S score matrix never leaves registers.
+// qkv rows are [q | k | v] (3 x hidden); heads are D-wide slices; no mask.
 template <int D>
 __global__ void __launch_bounds__(128) attention_kernel(const __nv_bfloat16* __restrict__ qkv, int N, int S, int heads,
-                                                        int hidden, float scale, __nv_bfloat16* __restrict__ out) {
+                                                        int hidden, float scale_log2, __nv_bfloat16* __restrict__ out) {
   extern __shared__ uint4 smem_kv[];
-  __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(smem_kv);
-  __nv_bfloat16* Vs = Ks + static_cast<size_t>(S) * D;
-  const int pairs = N * heads;
-  for (int pr = blockIdx.x; pr < pairs; pr += gridDim.x) {
-    const int n = pr / heads, h = pr - n * heads;
-    const __nv_bfloat16* base = qkv + static_cast<int64_t>(n) * S * 3 * hidden;
-    __syncthreads();
-    for (int i = threadIdx.x; i < S * (D / 8); i += blockDim.x) {
+  const int SP = (S + 63) & ~63;
+  constexpr int KST = D + 8;
+  const int VST = SP + 8;
+  __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(smem_kv);  // [SP][KST]
+  __nv_bfloat16* Vt = Ks + static_cast<size_t>(SP) * KST;         // [D][VST]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int qblocks = (S + kAttnQ - 1) / kAttnQ;
+  const int items = N * heads * qblocks;
+  const int64_t row_ld = 3 * static_cast<int64_t>(hidden);
+  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+    const int qb = it % qblocks, nh = it / qblocks;
+    const int n = nh / heads, h = nh - n * heads;
+    const __nv_bfloat16* base = qkv + static_cast<int64_t>(n) * S * row_ld + h * D;
+    __syncthreads();  // the previous item is done with K / V^T
+    for (int i = threadIdx.x; i < SP * (D / 8); i += blockDim.x) {
       const int j = i / (D / 8), c = i - j * (D / 8);
-      const __nv_bfloat16* row = base + static_cast<int64_t>(j) * 3 * hidden + h * D + c * 8;
-      reinterpret_cast<uint4*>(Ks + j * D)[c] = __ldcg(reinterpret_cast<const uint4*>(row + hidden));
-      reinterpret_cast<uint4*>(Vs + j * D)[c] = __ldcg(reinterpret_cast<const uint4*>(row + 2 * hidden));
+      uint4 kv = make_uint4(0, 0, 0, 0), vv = kv;
+      if (j < S) {
+        const __nv_bfloat16* row = base + j * row_ld + c * 8;
+        kv = __ldcg(reinterpret_cast<const uint4*>(row + hidden));
+        vv = __ldcg(reinterpret_cast<const uint4*>(row + 2 * hidden));
+      }
+      *reinterpret_cast<uint4*>(Ks + j * KST + c * 8) = kv;
+      const __nv_bfloat16* v8 = reinterpret_cast<const __nv_bfloat16*>(&vv);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) Vt[(c * 8 + e) * VST + j] = v8[e];
     }
     __syncthreads();
-    for (int qi = threadIdx.x; qi < S; qi += blockDim.x) {
-      float q[D], o[D];
-      const uint4* qr = reinterpret_cast<const uint4*>(base + static_cast<int64_t>(qi) * 3 * hidden + h * D);
+    const int q0 = qb * kAttnQ + warp * 16;
+    if (q0 >= S) continue;  // warp-uniform; the loop-top barrier is reached by every warp
+    const int r0 = min(q0 + g, S - 1), r1 = min(q0 + g + 8, S - 1);
+    uint32_t qa[D / 16][4];
 #pragma unroll
-      for (int c = 0; c < D / 8; ++c) {
-        const uint4 t = __ldcg(qr + c);
-        const uint32_t w[4] = {t.x, t.y, t.z, t.w};
+    for (int kk = 0; kk < D / 16; ++kk) {
+      qa[kk][0] = __ldcg(reinterpret_cast<const unsigned int*>(base + r0 * row_ld + 16 * kk + 2 * t));
+      qa[kk][1] = __ldcg(reinterpret_cast<const unsigned int*>(base + r1 * row_ld + 16 * kk + 2 * t));
+      qa[kk][2] = __ldcg(reinterpret_cast<const unsigned int*>(base + r0 * row_ld + 16 * kk + 8 + 2 * t));
+      qa[kk][3] = __ldcg(reinterpret_cast<const unsigned int*>(base + r1 * row_ld + 16 * kk + 8 + 2 * t));
+    }
+    float o[D / 8][4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float2 f = unpack_bf16x2(w[j]);
-          q[8 * c + 2 * j] = f.x * scale;
-          q[8 * c + 2 * j + 1] = f.y * scale;
+    for (int j = 0; j < D / 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.0f;
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.0f, l1 = 0.0f;
+    for (int kc = 0; kc < SP; kc += 64) {
+      float sc[8][4];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        sc[j][0] = sc[j][1] = sc[j][2] = sc[j][3] = 0.0f;
+        const __nv_bfloat16* kr = Ks + (kc + 8 * j + g) * KST + 2 * t;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) mma_bf16_16816(sc[j], qa[kk], ld_b32(kr + 16 * kk), ld_b32(kr + 16 * kk + 8));
+      }
+      float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int key = kc + 8 * j + 2 * t + (e & 1);
+          sc[j][e] = key < S ? sc[j][e] * scale_log2 : -INFINITY;
         }
+        mx0 = fmaxf(mx0, fmaxf(sc[j][0], sc[j][1]));
+        mx1 = fmaxf(mx1, fmaxf(sc[j][2], sc[j][3]));
       }
 #pragma unroll
-      for (int d = 0; d < D; ++d) o[d] = 0.0f;
-      float m = -INFINITY, l = 0.0f;
-      for (int j = 0; j < S; ++j) {
-        const uint4* kr = reinterpret_cast<const uint4*>(Ks + j * D);
-        float sp[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // 4 independent FMA chains
+      for (int off = 1; off <= 2; off <<= 1) {
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+      }
+      const float n0 = fmaxf(m0, mx0), n1 = fmaxf(m1, mx1);  // finite: key kc < S is always valid
+      const float c0 = exp2f(m0 - n0), c1 = exp2f(m1 - n1);
+      m0 = n0;
+      m1 = n1;
+      l0 *= c0;
+      l1 *= c1;
 #pragma unroll
-        for (int c = 0; c < D / 8; ++c) {
-          const uint4 t = kr[c];
-          const uint32_t w[4] = {t.x, t.y, t.z, t.w};
+      for (int j = 0; j < D / 8; ++j) {
+        o[j][0] *= c0;
+        o[j][1] *= c0;
+        o[j][2] *= c1;
+        o[j][3] *= c1;
+      }
 #pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
-            const float2 f = unpack_bf16x2(w[jj]);
-            sp[jj] = fmaf(q[8 * c + 2 * jj], f.x, sp[jj]);
-            sp[jj] = fmaf(q[8 * c + 2 * jj + 1], f.y, sp[jj]);
-          }
-        }
-        const float s = (sp[0] + sp[1]) + (sp[2] + sp[3]);
-        const float mn = fmaxf(m, s);
-        const float corr = __expf(m - mn);
-        const float p = __expf(s - mn);
-        l = l * corr + p;
-        m = mn;
-        const uint4* vr = reinterpret_cast<const uint4*>(Vs + j * D);
+      for (int j = 0; j < 8; ++j) {
+        sc[j][0] = exp2f(sc[j][0] - n0);
+        sc[j][1] = exp2f(sc[j][1] - n0);
+        sc[j][2] = exp2f(sc[j][2] - n1);
+        sc[j][3] = exp2f(sc[j][3] - n1);
+        l0 += sc[j][0] + sc[j][1];
+        l1 += sc[j][2] + sc[j][3];
+      }
 #pragma unroll
-        for (int c = 0; c < D / 8; ++c) {
-          const uint4 t = vr[c];
-          const uint32_t w[4] = {t.x, t.y, t.z, t.w};
+      for (int kk = 0; kk < 4; ++kk) {  // P (16 x 64 keys) as the A operand, straight from registers
+        const uint32_t pa[4] = {pack_bf16x2(sc[2 * kk][0], sc[2 * kk][1]), pack_bf16x2(sc[2 * kk][2], sc[2 * kk][3]),
+                                pack_bf16x2(sc[2 * kk + 1][0], sc[2 * kk + 1][1]),
+                                pack_bf16x2(sc[2 * kk + 1][2], sc[2 * kk + 1][3])};
 #pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
-            const float2 f = unpack_bf16x2(w[jj]);
-            o[8 * c + 2 * jj] = fmaf(o[8 * c + 2 * jj], corr, p * f.x);
-            o[8 * c + 2 * jj + 1] = fmaf(o[8 * c + 2 * jj + 1], corr, p * f.y);
-          }
+        for (int j = 0; j < D / 8; ++j) {
+          const __nv_bfloat16* vr = Vt + (8 * j + g) * VST + kc + 16 * kk + 2 * t;
+          mma_bf16_16816(o[j], pa, ld_b32(vr), ld_b32(vr + 8));
         }
       }
-      const float il = 1.0f / l;
-      uint4* orow = reinterpret_cast<uint4*>(out + (static_cast<int64_t>(n) * S + qi) * hidden + h * D);
+    }
 #pragma unroll
-      for (int c = 0; c < D / 8; ++c) {
-        uint4 t;
-        t.x = pack_bf16x2(o[8 * c + 0] * il, o[8 * c + 1] * il);
-        t.y = pack_bf16x2(o[8 * c + 2] * il, o[8 * c + 3] * il);
-        t.z = pack_bf16x2(o[8 * c + 4] * il, o[8 * c + 5] * il);
-        t.w = pack_bf16x2(o[8 * c + 6] * il, o[8 * c + 7] * il);
-        orow[c] = t;
-      }
+    for (int off = 1; off <= 2; off <<= 1) {
+      l0 += __shfl_xor_sync(0xffffffffu, l0, off);
+      l1 += __shfl_xor_sync(0xffffffffu, l1, off);
+    }
+    const float i0 = 1.0f / l0, i1 = 1.0f / l1;
+    __nv_bfloat16* o0 = out + (static_cast<int64_t>(n) * S + q0 + g) * hidden + h * D + 2 * t;
+    __nv_bfloat16* o1 = o0 + 8 * static_cast<int64_t>(hidden);
+#pragma unroll
+    for (int j = 0; j < D / 8; ++j) {
+      if (q0 + g < S) *reinterpret_cast<uint32_t*>(o0 + 8 * j) = pack_bf16x2(o[j][0] * i0, o[j][1] * i0);
+      if (q0 + g + 8 < S) *reinterpret_cast<uint32_t*>(o1 + 8 * j) = pack_bf16x2(o[j][2] * i1, o[j][3] * i1);
     }
   }
 }
@@ -181,18 +235,19 @@ cudaError_t launch_layernorm(const __nv_bfloat16* x, const __nv_bfloat16* res, i
 
 cudaError_t launch_attention(const __nv_bfloat16* qkv, int N, int S, int heads, int dh, __nv_bfloat16* out, int grid,
                              cudaStream_t s) {
-  if (dh != 64 || S > 512) return cudaErrorInvalidValue;
-  const size_t smem = static_cast<size_t>(S) * dh * 2 * 2;
+  if (dh != 64 || S < 1 || S > 512) return cudaErrorInvalidValue;
+  const int SP = (S + 63) & ~63;
+  const size_t smem = (static_cast<size_t>(SP) * (dh + 8) + static_cast<size_t>(dh) * (SP + 8)) * 2;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(attention_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     configured = true;
   }
-  int blocks = N * heads;
+  int blocks = N * heads * ((S + kAttnQ - 1) / kAttnQ);
   if (blocks > grid) blocks = grid;
   if (blocks < 1) blocks = 1;
-  attention_kernel<64><<<blocks, 128, smem, s>>>(qkv, N, S, heads, heads * dh, 1.0f / sqrtf(static_cast<float>(dh)),
-                                                 out);
+  const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(dh));
+  attention_kernel<64><<<blocks, 128, smem, s>>>(qkv, N, S, heads, heads * dh, scale_log2, out);
   return cudaGetLastError();
 }
 
