@@ -18,11 +18,22 @@
 namespace gx {
 
 static thread_local std::string g_last_error;
+static thread_local std::string g_last_encode;  // detail of the last failed tensor-map encode
 
 void set_error(const std::string& msg) { g_last_error = msg; }
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
+}
+int bind_device(int device) {
+  static thread_local bool bound = false;
+  int cur = -1;
+  if (!bound || cudaGetDevice(&cur) != cudaSuccess || cur != device) {
+    const cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    bound = true;
+  }
+  return GX_OK;
 }
 int cuda_fail(cudaError_t e, const char* what) {
   g_last_error = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
@@ -54,9 +65,17 @@ bool encode_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uin
   cuuint64_t strides[1] = {row_stride_bytes};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t es[2] = {1, 1};
-  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  const CUresult rc = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (rc != CUDA_SUCCESS) {
+    char b[256];
+    snprintf(b, sizeof b, "CUresult %d: base=%p dims=(%llu,%llu) stride=%llu box=(%u,%u)", static_cast<int>(rc), base,
+             static_cast<unsigned long long>(inner), static_cast<unsigned long long>(outer),
+             static_cast<unsigned long long>(row_stride_bytes), box_inner, box_outer);
+    g_last_encode = b;
+  }
+  return rc == CUDA_SUCCESS;
 }
 
 typedef CUresult (*PFN_encodeIm2col_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -184,20 +203,20 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
   memset(&out->amap, 0, sizeof(out->amap));
   memset(&out->rmap, 0, sizeof(out->rmap));
   if (!encode_tmap_2d_bf16(&out->wmap, wbase + op.w_off, kpad, op.Cout, static_cast<uint64_t>(kpad) * 2, kBK, a.BN))
-    return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for conv weights");
+    return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for conv weights: " + g_last_encode);
   a.cpl = (op.Cin % 64 == 0) ? 64 : (op.Cin % 32 == 0) ? 32 : (op.Cin % 16 == 0) ? 16 : 8;
   a.tma_a = getenv("GX_NO_TMA_IM2COL") == nullptr;
   a.a2d = a.tma_a && a.R == 1 && a.S == 1 && a.sh == 1 && a.sw == 1 && a.ph == 0 && a.pw == 0 && a.cpl == 64 &&
           a.Cin == ti.C && getenv("GX_NO_A2D") == nullptr;
   if (a.a2d) {
     if (!encode_tmap_2d_bf16(&out->amap, a.x, ti.C, a.M, static_cast<uint64_t>(ti.C) * 2, kBK, kBM))
-      return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for conv input");
+      return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for conv input: " + g_last_encode);
   } else if (a.tma_a && !encode_tmap_im2col_bf16(&out->amap, a.x, ti.C, ti.W, ti.H, k, -a.pw, -a.ph,
                                                  (op.pw_hi >= 0 ? op.pw_hi : a.pw) - (a.S - 1),
                                                  (op.ph_hi >= 0 ? op.ph_hi : a.ph) - (a.R - 1), a.sw, a.sh, a.cpl))
     return fail(GX_ECUDA, "cuTensorMapEncodeIm2col failed for conv input");
   if (a.res && !encode_tmap_2d_bf16(&out->rmap, a.res, a.res_ld, a.M, static_cast<uint64_t>(a.res_ld) * 2, 64, kBM))
-    return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for the residual");
+    return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for the residual: " + g_last_encode);
   out->grid = std::min(a.num_tiles, std::max(1, sm_budget));
   a.gmaps = nullptr;
   if (getenv("GX_GMAPS")) {  // experiment: maps in global memory (leaks one small buffer per plan)
@@ -333,7 +352,7 @@ int gx_run_op(gx_ctx* ctx, const gx_op* op, const gx_tensor* tensors, void* cons
               int k, int sm_budget, void* stream) {
   if (!ctx || !op || !tensors || !tensor_ptrs) return fail(GX_EINVAL, "null arg");
   if (k < 1) return fail(GX_EINVAL, "batch must be >= 1");
-  GX_CUDA(cudaSetDevice(ctx->device));
+  if (int rc = bind_device(ctx->device)) return rc;
   if (sm_budget <= 0 || sm_budget > ctx->sm_count) sm_budget = ctx->sm_count;
   return launch_op(*op, tensors, tensor_ptrs, static_cast<const uint8_t*>(weights), k, sm_budget,
                    static_cast<cudaStream_t>(stream), false, nullptr, nullptr);
@@ -343,6 +362,7 @@ int gx_gather(gx_ctx* ctx, int k, const void* const* src, const int32_t* src_dty
               int32_t c_dst, void* dst, int sm_budget, void* stream) {
   if (!ctx) return fail(GX_EINVAL, "null ctx");
   if (k < 1 || k > 64) return fail(GX_EINVAL, "gather batch must be in 1..64");
+  if (int rc = bind_device(ctx->device)) return rc;
   if (sm_budget <= 0 || sm_budget > ctx->sm_count) sm_budget = ctx->sm_count;
   GX_CUDA(launch_gather(k, src, src_dtype, pixels, c_src, c_dst, static_cast<__nv_bfloat16*>(dst), sm_budget * 8,
                         static_cast<cudaStream_t>(stream)));
@@ -353,6 +373,7 @@ int gx_scatter(gx_ctx* ctx, int k, const void* src, int32_t src_dtype, int64_t r
                int32_t dst_dtype, int sm_budget, void* stream) {
   if (!ctx) return fail(GX_EINVAL, "null ctx");
   if (k < 1 || k > 64) return fail(GX_EINVAL, "scatter batch must be in 1..64");
+  if (int rc = bind_device(ctx->device)) return rc;
   if (sm_budget <= 0 || sm_budget > ctx->sm_count) sm_budget = ctx->sm_count;
   GX_CUDA(launch_scatter(k, src, src_dtype, row_elems, dst, dst_dtype, sm_budget * 8,
                          static_cast<cudaStream_t>(stream)));

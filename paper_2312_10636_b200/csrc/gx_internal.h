@@ -14,6 +14,9 @@ namespace gx {
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);
+// Make `device`'s primary context current on the calling thread (tensor-map encoding and graph
+// capture need one; a caller thread that never touched CUDA has none).  Cheap when already bound.
+int bind_device(int device);
 
 #define GX_CUDA(call)                                   \
   do {                                                  \

@@ -267,6 +267,7 @@ int gx_model_create(gx_ctx* ctx, const char* model_id, int n_tensors, const gx_t
                     const void* weight_blob, size_t blob_bytes, gx_model** out) {
   if (!ctx || !out || !tensors || !ops || !unit_first_op || !boundary) return fail(GX_EINVAL, "null arg");
   if (n_units < 1 || n_tensors < 1 || n_ops < 1) return fail(GX_EINVAL, "empty unit chain");
+  if (int rc = bind_device(ctx->device)) return rc;
   if (unit_first_op[0] != 0 || unit_first_op[n_units] != n_ops) return fail(GX_EINVAL, "bad unit op ranges");
   for (int u = 0; u < n_units; ++u)
     if (unit_first_op[u + 1] < unit_first_op[u]) return fail(GX_EINVAL, "unit op ranges must be non-decreasing");
@@ -319,6 +320,7 @@ int gx_stage_create(gx_model* m, int start, int end, int max_batch, int sm_budge
   if (!(0 <= start && start < end && end <= m->n_units()))
     return fail(GX_EINVAL, "bad span [" + std::to_string(start) + ", " + std::to_string(end) + ") for model " + m->id);
   if (max_batch < 1 || max_batch > 64) return fail(GX_EINVAL, "max_batch must be in 1..64");
+  if (int rc = bind_device(m->ctx->device)) return rc;
   if (sm_budget < 1 || sm_budget > m->ctx->sm_count)
     return fail(GX_EINFEASIBLE, "SM budget " + std::to_string(sm_budget) + " outside 1.." +
                                     std::to_string(m->ctx->sm_count));
@@ -402,6 +404,7 @@ int gx_stage_run(gx_stage* st, int k, const void* const* src, const int32_t* src
                  void* const* dst, int32_t dst_dtype) {
   if (!st || !src || !src_dtype || !dst) return fail(GX_EINVAL, "null arg");
   if (k < 1 || k > st->max_batch) return fail(GX_EINVAL, "batch k outside 1..max_batch");
+  if (int rc = bind_device(st->m->ctx->device)) return rc;
   gx_model* m = st->m;
   const gx_tensor& tin = m->tensors[st->in_tid];
   const gx_tensor& tout = m->tensors[st->out_tid];
@@ -442,6 +445,7 @@ int gx_stage_span_trace(gx_stage* st, int k, int64_t* out, int64_t cap, int* n_o
   if (!st || !out || !n_ops_out) return fail(GX_EINVAL, "null arg");
   if (!st->span_mode) return fail(GX_EINVAL, "stage is not in span mode");
   if (k < 1 || k > st->max_batch) return fail(GX_EINVAL, "bad k");
+  if (int rc = bind_device(st->m->ctx->device)) return rc;
   gx_stage::PerK* pk = nullptr;
   int rc = stage_graph(st, k, &pk);
   if (rc != GX_OK) return rc;
@@ -469,6 +473,7 @@ int gx_stage_span_trace(gx_stage* st, int k, int64_t* out, int64_t cap, int* n_o
 
 int gx_stage_kernel_count(gx_stage* st, int k, int* out) {
   if (!st || !out) return fail(GX_EINVAL, "null arg");
+  if (int rc = bind_device(st->m->ctx->device)) return rc;
   gx_stage::PerK* pk = nullptr;
   int rc = stage_graph(st, k, &pk);
   if (rc != GX_OK) return rc;
@@ -479,6 +484,7 @@ int gx_stage_kernel_count(gx_stage* st, int k, int* out) {
 int gx_stage_profile(gx_stage* st, int k, int iters, float* ms_out) {
   if (!st || !ms_out) return fail(GX_EINVAL, "null arg");
   if (k < 1 || k > st->max_batch || iters < 1) return fail(GX_EINVAL, "bad profile arguments");
+  if (int rc = bind_device(st->m->ctx->device)) return rc;
   gx_model* m = st->m;
   const gx_tensor& tin = m->tensors[st->in_tid];
   const gx_tensor& tout = m->tensors[st->out_tid];
