@@ -213,7 +213,8 @@ def run_ours(args):
     W, K = args.warmup, args.steps
     horizon = (W + K) * window
 
-    def one_run(host: bool):
+    def one_run(fleet, host: bool):
+        dep = fleet.dep
         ingress = {p: (v[1], v[2], v[3]) for p, v in (fleet.host_in if host else fleet.dev_in).items()}
         if world > 1:
             dist.barrier()
@@ -239,8 +240,27 @@ def run_ours(args):
                 if host else 0}
 
     with ClockSampler(local) as clk:
-        res = one_run(host=False)
-    res_e2e = one_run(host=True)
+        res = one_run(fleet, host=False)
+    # e2e: the same achievable-throughput rule through the host path (ingress read from pinned host
+    # memory by the gather kernels, logits written to mapped host memory), from this fleet down
+    e2e_fleet = fleet
+    res_e2e = one_run(fleet, host=True)
+    if args.clients is None:
+        for w in [w for w in reversed(_workloads(args.model)) if w["clients_n"] < wl["clients_n"]]:
+            ok = res_e2e["p99"] <= slo and res_e2e["dropped"] <= 0.01 * max(1, res_e2e["generated"])
+            if world > 1:
+                flag = torch.tensor([1 if ok else 0], device="cuda")
+                dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+                ok = bool(flag.item())
+            if rank == 0:
+                print(f"# e2e clients={e2e_fleet.wl['clients_n']}: p99={res_e2e['p99']:.1f} ms -> "
+                      f"{'ok' if ok else 'over'}", file=sys.stderr, flush=True)
+            if ok:
+                break
+            if e2e_fleet is not fleet:
+                del e2e_fleet
+            e2e_fleet = Fleet(w)
+            res_e2e = one_run(e2e_fleet, host=True)
 
     # roofline: the dominant stage's span graph on its own stream (CUDA events, live)
     def stage_flops(i):
@@ -283,6 +303,9 @@ def run_ours(args):
             "p99_ms": round(p99, 3), "p99_ok": p99 <= slo, "generated": int(stats[1].item()),
             "dropped": int(stats[2].item()),
             "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "p99_ms": round(p99_e2e, 3),
+                    "p99_ok": p99_e2e <= slo, "clients_per_gpu": e2e_fleet.wl["clients_n"],
+                    "path": "serve() with host ingress: gather kernels read fp32 entry activations from pinned "
+                            "host memory over PCIe (zero-copy), logits scattered to mapped host memory",
                     "h2d_bytes_per_step": int(stats[6].item() / K), "d2h_bytes_per_step": int(stats[7].item() / K)},
             "gpu_launches": int(stats[4].item()),
             "roofline": {"bound": "tensor", "kernel": f"span [{st.start},{st.end}) k={st.batch} "

@@ -207,11 +207,16 @@ typedef struct gx_serve_client { /* ClientSpec (workload.py:98-117), clients sor
   int64_t n_trace;
 } gx_serve_client;
 
+enum { GX_INGRESS_DEVICE = 0, GX_INGRESS_ZERO_COPY = 1, GX_INGRESS_DMA = 2 };
+
 typedef struct gx_serve_cfg {
   double horizon_ms, epoch_ms;
   int32_t clock;          /* GX_CLOCK_*                                                    */
   int32_t record_dispatch;/* keep (t, stage, k, seq...) dispatch log                       */
-  int32_t ingress_from_host; /* WALL: H2D copy of each request's ingress from pinned host   */
+  int32_t ingress_from_host; /* WALL: ingress lives in pinned host memory.  GX_INGRESS_ZERO_COPY:
+                                 the stage's gather kernel reads it over PCIe directly (decode
+                                 + cast fused into K1); GX_INGRESS_DMA: cudaMemcpyAsync into a
+                                 device slot at arrival; 0: ingress already in device memory  */
   int32_t egress_to_host;    /* WALL: D2H copy of each request's output                     */
   int64_t slot_bytes;     /* per-request activation slot size on the device                 */
   int32_t max_inflight;   /* slot pool size                                                 */

@@ -76,3 +76,9 @@ struct gx_stage {
   void* prof_src = nullptr;
   void* prof_dst = nullptr;
 };
+
+namespace gx {
+// gx_stage_run on an explicit stream (gx_stage.cu); used by the serving loop's stream pool.
+int stage_run_on(gx_stage* st, cudaStream_t stream, int k, const void* const* src, const int32_t* src_dtype,
+                 int32_t src_channels, void* const* dst, int32_t dst_dtype);
+}  // namespace gx

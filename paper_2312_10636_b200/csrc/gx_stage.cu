@@ -405,6 +405,16 @@ int gx_stage_run(gx_stage* st, int k, const void* const* src, const int32_t* src
   if (!st || !src || !src_dtype || !dst) return fail(GX_EINVAL, "null arg");
   if (k < 1 || k > st->max_batch) return fail(GX_EINVAL, "batch k outside 1..max_batch");
   if (int rc = bind_device(st->m->ctx->device)) return rc;
+  return gx::stage_run_on(st, st->stream, k, src, src_dtype, src_channels, dst, dst_dtype);
+}
+
+}  // extern "C"
+
+namespace gx {
+// The body of gx_stage_run on an explicit stream: the serving loop runs batches of any instance on
+// a pooled stream (an instance never has two batches in flight, so its workspace is never shared).
+int stage_run_on(gx_stage* st, cudaStream_t stream, int k, const void* const* src, const int32_t* src_dtype,
+                 int32_t src_channels, void* const* dst, int32_t dst_dtype) {
   gx_model* m = st->m;
   const gx_tensor& tin = m->tensors[st->in_tid];
   const gx_tensor& tout = m->tensors[st->out_tid];
@@ -417,10 +427,10 @@ int gx_stage_run(gx_stage* st, int k, const void* const* src, const int32_t* src
   if (tin.s2d > 1) {
     if (src_channels <= 0) return fail(GX_EINVAL, "space-to-depth boundary needs the client's channel count");
     GX_CUDA(launch_gather_s2d(k, src, src_dtype, tin.H, tin.W, tin.s2d, src_channels, tin.C,
-                              static_cast<__nv_bfloat16*>(st->tptr[st->in_tid]), bw_grid, st->stream));
+                              static_cast<__nv_bfloat16*>(st->tptr[st->in_tid]), bw_grid, stream));
   } else {
     GX_CUDA(launch_gather(k, src, src_dtype, static_cast<int64_t>(tin.H) * tin.W, c_src, tin.C,
-                          static_cast<__nv_bfloat16*>(st->tptr[st->in_tid]), bw_grid, st->stream));
+                          static_cast<__nv_bfloat16*>(st->tptr[st->in_tid]), bw_grid, stream));
   }
   if (st->span_mode) {
     SpanSmem L;
@@ -430,16 +440,19 @@ int gx_stage_run(gx_stage* st, int k, const void* const* src, const int32_t* src
     L.bias_bytes = pk->bias_bytes;
     for (const auto& ch : pk->chunks) {
       GX_CUDA(launch_span(static_cast<const SpanOp*>(ch.d_ops), ch.n_ops, *ch.maps, st->bar, st->arrivals, L,
-                          st->sm_budget, st->stream));
+                          st->sm_budget, stream));
       st->arrivals += static_cast<unsigned long long>(ch.n_ops) * st->sm_budget;
     }
   } else {
-    GX_CUDA(cudaGraphLaunch(pk->exec, st->stream));
+    GX_CUDA(cudaGraphLaunch(pk->exec, stream));
   }
   GX_CUDA(launch_scatter(k, st->tptr[st->out_tid], tout.dtype, tensor_elems(tout), dst, dst_dtype, bw_grid,
-                         st->stream));
+                         stream));
   return GX_OK;
 }
+}  // namespace gx
+
+extern "C" {
 
 int gx_stage_span_trace(gx_stage* st, int k, int64_t* out, int64_t cap, int* n_ops_out) {
   if (!st || !out || !n_ops_out) return fail(GX_EINVAL, "null arg");

@@ -12,6 +12,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <queue>
@@ -61,6 +63,8 @@ struct Batch {
   int inst;
   std::vector<int> reqs;
   cudaEvent_t ev = nullptr;
+  double t_disp = 0.0;  // wall ms at dispatch (diagnostics)
+  int lane = -1;        // stream-pool lane the batch runs on
 };
 
 struct Stage {
@@ -72,6 +76,9 @@ struct Stage {
   std::vector<gx_stage*> inst;
   std::vector<char> busy;
   int out_final = 0;
+  // wall-clock diagnostics (GX_SERVE_DEBUG): observed dispatch->completion time per batch
+  double obs_ms = 0.0, plan_ms = 0.0;
+  int64_t obs_n = 0, obs_k = 0;
 };
 
 struct Client {
@@ -119,11 +126,21 @@ struct gx_serve {
   int64_t result_elems = 0;
   int64_t result_cursor = 0;
   cudaStream_t ingress_stream = nullptr;
+  // Stream pool: a batch runs on an idle pooled stream rather than on its instance's own stream.
+  // The device has at most CUDA_DEVICE_MAX_CONNECTIONS (32) hardware queues; with one stream per
+  // instance, plans with > 32 instances alias streams onto shared queues and unrelated instances
+  // serialise.  Pooling keeps every in-flight batch on its own queue while <= pool size.
+  std::vector<cudaStream_t> pool;
+  std::vector<int> pool_n;        // batches in flight per lane
+  std::vector<double> pool_last;  // wall ms of the lane's last dispatch
   cudaEvent_t ingress_ev = nullptr;
   bool ingress_pending = false;
   double wall_ms = 0.0;
   int64_t n_batches = 0, n_kernels = 0;
   int64_t drops_no_slot = 0;
+  double host_dispatch_ms = 0.0, host_poll_ms = 0.0;  // diagnostics (GX_SERVE_DEBUG)
+  int64_t loop_iters = 0;
+  size_t max_inflight_seen = 0;
   std::chrono::steady_clock::time_point t0;
 
   void push(double t, int rank, int64_t a, int64_t b = 0) {
@@ -208,7 +225,10 @@ int gx_serve::arrive(int ri, double now) {
     r.cur = rt.ingress;
     r.cur_dtype = rt.ingress_dtype;
     r.cur_channels = rt.ingress_channels;
-    const bool needs_slot = cfg.ingress_from_host || rt.n_stages > 1 || !stages[rt.stage[0]].out_final;
+    // zero-copy ingress: r.cur stays the pinned host pointer (UVA) and the first stage's gather
+    // reads it over PCIe; only DMA ingress and multi-stage routes need a device slot
+    const bool needs_slot = cfg.ingress_from_host == GX_INGRESS_DMA || rt.n_stages > 1 ||
+                            !stages[rt.stage[0]].out_final;
     if (needs_slot) {
       if (free_slots.empty()) {  // out of device slots: counts as an admission drop
         r.status = 1;
@@ -218,7 +238,7 @@ int gx_serve::arrive(int ri, double now) {
       r.slot = free_slots.back();
       free_slots.pop_back();
       void* dst = static_cast<uint8_t*>(slots) + static_cast<size_t>(r.slot) * cfg.slot_bytes;
-      if (cfg.ingress_from_host) {
+      if (cfg.ingress_from_host == GX_INGRESS_DMA) {
         cudaError_t e = cudaMemcpyAsync(dst, rt.ingress, rt.ingress_bytes, cudaMemcpyHostToDevice, ingress_stream);
         if (e != cudaSuccess) return cuda_fail(e, "ingress H2D");
         ingress_pending = true;
@@ -269,13 +289,21 @@ int gx_serve::dispatch_gpu(int si, int bi) {
     GX_CUDA(cudaEventRecord(ingress_ev, ingress_stream));
     ingress_pending = false;
   }
-  GX_CUDA(cudaStreamWaitEvent(g->stream, ingress_ev, 0));
-  int rc = gx_stage_run(g, k, src, sdt, channels, dst, st.out_final ? GX_F32 : GX_BF16);
+  // an idle lane if there is one, else the lane with the fewest / oldest batches in flight
+  int lane = 0;
+  for (int i = 1; i < static_cast<int>(pool.size()); ++i)
+    if (pool_n[i] < pool_n[lane] || (pool_n[i] == pool_n[lane] && pool_last[i] < pool_last[lane])) lane = i;
+  cudaStream_t sm = pool[lane];
+  b.lane = lane;
+  pool_n[lane] += 1;
+  pool_last[lane] = b.t_disp;
+  GX_CUDA(cudaStreamWaitEvent(sm, ingress_ev, 0));
+  int rc = gx::stage_run_on(g, sm, k, src, sdt, channels, dst, st.out_final ? GX_F32 : GX_BF16);
   if (rc != GX_OK) return rc;
   int kc = 0;
   gx_stage_kernel_count(g, k, &kc);
   n_kernels += kc;
-  GX_CUDA(cudaEventRecord(b.ev, g->stream));
+  GX_CUDA(cudaEventRecord(b.ev, sm));
   for (int i = 0; i < k; ++i) {
     Req& r = reqs[b.reqs[i]];
     if (!st.out_final) {
@@ -327,7 +355,10 @@ int gx_serve::service(int si, double now) {
     if (cfg.clock == GX_CLOCK_VIRTUAL) {
       push(now + st.lat[k], R_DONE, bi);
     } else {
+      const double t_a = now_wall();
+      b.t_disp = t_a;
       int rc = dispatch_gpu(si, bi);
+      host_dispatch_ms += now_wall() - t_a;
       if (rc != GX_OK) return rc;
     }
   }
@@ -347,7 +378,13 @@ int gx_serve::stage_done(int bi, double now) {
   Batch& b = batches[bi];
   Stage& st = stages[b.stage];
   st.free += 1;
-  if (cfg.clock == GX_CLOCK_WALL) st.busy[b.inst] = 0;
+  if (cfg.clock == GX_CLOCK_WALL) {
+    st.busy[b.inst] = 0;
+    st.obs_ms += now - b.t_disp;
+    if (b.reqs.size() < st.lat.size()) st.plan_ms += st.lat[b.reqs.size()];
+    st.obs_n += 1;
+    st.obs_k += static_cast<int64_t>(b.reqs.size());
+  }
   std::vector<int> reqs_copy = b.reqs;
   const int si = b.stage;
   free_batches.push_back(bi);
@@ -416,12 +453,15 @@ int gx_serve::run() {
     for (;;) {
       const double now = now_wall();
       bool progressed = false;
+      ++loop_iters;
+      max_inflight_seen = std::max(max_inflight_seen, inflight.size());
       for (size_t i = 0; i < inflight.size();) {
         const int bi = inflight[i];
         cudaError_t q = cudaEventQuery(batches[bi].ev);
         if (q == cudaSuccess) {
           inflight[i] = inflight.back();
           inflight.pop_back();
+          pool_n[batches[bi].lane] -= 1;
           if (now <= horizon) {
             rc = stage_done(bi, now);
           } else {
@@ -474,6 +514,20 @@ int gx_serve::run() {
     }
   }
   wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  if (cfg.clock == GX_CLOCK_WALL && getenv("GX_SERVE_DEBUG")) {
+    fprintf(stderr, "[serve] wall=%.0fms batches=%lld host_dispatch=%.0fms (%.1fus/batch) loop_iters=%lld max_inflight=%zu\n",
+            wall_ms, static_cast<long long>(n_batches), host_dispatch_ms,
+            n_batches ? 1000.0 * host_dispatch_ms / n_batches : 0.0, static_cast<long long>(loop_iters),
+            max_inflight_seen);
+    for (size_t i = 0; i < stages.size(); ++i) {
+      const Stage& st = stages[i];
+      if (!st.obs_n) continue;
+      fprintf(stderr, "[serve] stage %zu: batches=%lld mean_k=%.2f obs=%.3fms plan=%.3fms ratio=%.2f busy=%.0f%%\n", i,
+              static_cast<long long>(st.obs_n), double(st.obs_k) / st.obs_n, st.obs_ms / st.obs_n,
+              st.plan_ms / st.obs_n, st.obs_ms / std::max(1e-9, st.plan_ms),
+              100.0 * st.obs_ms / std::max(1e-9, wall_ms * st.instances));
+    }
+  }
   return rc;
 }
 
@@ -564,6 +618,15 @@ int gx_serve_create(gx_ctx* ctx, int n_stages, const gx_serve_stage* st, int n_r
       e = cfg->egress_to_host ? cudaHostAlloc(&s->results, bytes, cudaHostAllocMapped) : cudaMalloc(&s->results, bytes);
     }
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->ingress_stream, cudaStreamNonBlocking);
+    int lanes = 30;  // leaves hardware queues for the ingress stream and the caller's streams
+    if (const char* v = getenv("GX_SERVE_STREAMS")) lanes = std::max(1, atoi(v));
+    for (int i = 0; i < lanes && e == cudaSuccess; ++i) {
+      cudaStream_t q = nullptr;
+      e = cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking);
+      if (e == cudaSuccess) s->pool.push_back(q);
+    }
+    s->pool_n.assign(s->pool.size(), 0);
+    s->pool_last.assign(s->pool.size(), 0.0);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ingress_ev, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventRecord(s->ingress_ev, s->ingress_stream);
     if (e != cudaSuccess) {
@@ -642,6 +705,7 @@ int gx_serve_destroy(gx_serve* s) {
     }
     if (s->ingress_ev) cudaEventDestroy(s->ingress_ev);
     if (s->ingress_stream) cudaStreamDestroy(s->ingress_stream);
+    for (cudaStream_t q : s->pool) cudaStreamDestroy(q);
   }
   delete s;
   return GX_OK;

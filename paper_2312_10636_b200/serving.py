@@ -150,12 +150,14 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
           latency=None, instances=None, ctx=None, poisson: bool = False, seed: int = 0,
           record_dispatch: bool = False, ingress=None, ingress_from_host: bool = False,
           egress_to_host: bool = False, slot_bytes: int = 0, max_inflight: int = 4096,
-          planner: str | None = None) -> ServeReport:
+          planner: str | None = None, plan_latency=None) -> ServeReport:
     """Run one plan for one horizon.
 
     latency: callable (StageSpec, k) -> ms for the virtual clock (None -> wall clock).
     instances: per stage index, a list of `StageInstance` (wall clock).
     ingress: route point -> (pointer, bytes, channels) of the fp32 entry activation template.
+    plan_latency: optional (StageSpec, k) -> ms the plan assumed; on the wall clock it is only
+    compared with the observed batch times in the GX_SERVE_DEBUG summary.
     """
     keep = _Keep()
     wall = latency is None
@@ -165,10 +167,11 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
     for i, s in enumerate(deployment.stages):
         st_arr[i].batch, st_arr[i].instances, st_arr[i].budget_ms = s.batch, s.instances, s.budget_ms
         st_arr[i].out_final = 0
-        if not wall:
-            lat = (C.c_double * (s.batch + 1))(0.0, *[float(latency(s, k)) for k in range(1, s.batch + 1)])
+        lat_fn = plan_latency if wall else latency
+        if lat_fn is not None:
+            lat = (C.c_double * (s.batch + 1))(0.0, *[float(lat_fn(s, k)) for k in range(1, s.batch + 1)])
             st_arr[i].lat_ms = keep(lat)
-        else:
+        if wall:
             insts = instances[i]
             if len(insts) != s.instances:
                 raise ValidationError(f"stage {s.stage_id}: {len(insts)} executor instances for {s.instances}")
@@ -214,7 +217,8 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
     cfg.epoch_ms = epoch_s * 1000.0
     cfg.clock = N.GX_CLOCK_WALL if wall else N.GX_CLOCK_VIRTUAL
     cfg.record_dispatch = 1 if record_dispatch else 0
-    cfg.ingress_from_host = 1 if ingress_from_host else 0
+    # True / "zero_copy": the gather reads pinned host memory over PCIe; "dma": copy at arrival
+    cfg.ingress_from_host = {False: 0, True: 1, "zero_copy": 1, "dma": 2}[ingress_from_host]
     cfg.egress_to_host = 1 if egress_to_host else 0
     cfg.slot_bytes = slot_bytes
     cfg.max_inflight = max_inflight
