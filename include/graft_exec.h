@@ -144,6 +144,15 @@ GX_API int gx_stage_run(gx_stage* st, int k, const void* const* src, const int32
  * Produces the rows a TableCostModel ingests (profiles.py:315-454, header profiles.py:24). */
 GX_API int gx_stage_profile(gx_stage* st, int k, int iters, float* ms_out);
 
+/* Per-op breakdown of gx_stage_profile (the per-kernel roofline evidence behind a profile row):
+ * each op of the span launched alone on the stage stream at batch k and SM budget, median of
+ * `iters` CUDA-event timings (ms[i]); flops[i] / bytes[i] = the op's algorithmic work (unpadded
+ * FLOPs; every logical input, weight, bias, residual and output byte once); kind[i] = GX_OP_*.
+ * Arrays hold at least gx_stage_op_count() entries. */
+GX_API int gx_stage_op_count(gx_stage* st, int* out);
+GX_API int gx_stage_profile_ops(gx_stage* st, int k, int iters, int cap, float* ms, double* flops, double* bytes,
+                                int32_t* kind);
+
 /* Number of kernels one gx_stage_run(k) launches (gather + span + scatter). */
 GX_API int gx_stage_kernel_count(gx_stage* st, int k, int* out);
 

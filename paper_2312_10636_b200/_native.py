@@ -104,6 +104,8 @@ def lib():
         "gx_stage_run": (i32, [vp, C.c_int, P(vp), P(i32), i32, P(vp), i32]),
         "gx_stage_profile": (i32, [vp, C.c_int, C.c_int, P(C.c_float)]),
         "gx_stage_kernel_count": (i32, [vp, C.c_int, P(C.c_int)]),
+        "gx_stage_op_count": (i32, [vp, P(C.c_int)]),
+        "gx_stage_profile_ops": (i32, [vp, C.c_int, C.c_int, C.c_int, P(C.c_float), P(dbl), P(dbl), P(i32)]),
         "gx_run_op": (i32, [vp, P(GxOp), P(GxTensor), P(vp), vp, C.c_int, C.c_int, vp]),
         "gx_gather": (i32, [vp, C.c_int, P(vp), P(i32), i64, i32, i32, vp, C.c_int, vp]),
         "gx_scatter": (i32, [vp, C.c_int, vp, i32, i64, P(vp), i32, C.c_int, vp]),

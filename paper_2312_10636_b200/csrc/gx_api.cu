@@ -228,6 +228,60 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
   return GX_OK;
 }
 
+// Algorithmic work of one op at batch k: FLOPs of the unpadded math and the bytes a perfect kernel
+// moves (every logical input, weight, bias, residual and output byte exactly once).
+void op_work(const gx_op& op, const gx_tensor* T, int k, double* flops, double* bytes) {
+  const gx_tensor& ti = T[op.in];
+  const gx_tensor& to = T[op.out];
+  const double es_in = elem_size(ti.dtype), es_out = elem_size(to.dtype);
+  const double in_px = static_cast<double>(k) * ti.H * ti.W;
+  const double out_px = static_cast<double>(k) * to.H * to.W;
+  double f = 0.0, b = 0.0;
+  switch (op.kind) {
+    case GX_OP_CONV:
+    case GX_OP_LINEAR: {
+      const int R = op.kind == GX_OP_LINEAR ? 1 : op.R, S = op.kind == GX_OP_LINEAR ? 1 : op.S;
+      const double K = static_cast<double>(R) * S * op.Cin;
+      f = 2.0 * out_px * op.Cout * K;
+      b = in_px * op.Cin * es_in + static_cast<double>(op.Cout) * K * 2.0 + op.Cout * 4.0 + out_px * op.Cout * es_out;
+      if (op.in2 >= 0) b += out_px * op.Cout * 2.0;
+      break;
+    }
+    case GX_OP_MAXPOOL:
+    case GX_OP_AVGPOOL:
+      f = out_px * ti.C * op.R * op.S;
+      b = in_px * ti.C * es_in + out_px * ti.C * es_out;
+      break;
+    case GX_OP_GAP:
+      f = in_px * ti.C;
+      b = in_px * ti.C * es_in + static_cast<double>(k) * to.C * es_out;
+      break;
+    case GX_OP_FC: {
+      const double K = static_cast<double>(tensor_elems(ti));
+      f = 2.0 * k * K * op.Cout;
+      b = K * op.Cout * 2.0 + op.Cout * 4.0 + k * K * es_in + static_cast<double>(k) * op.Cout * es_out;
+      break;
+    }
+    case GX_OP_COPY:
+      b = 2.0 * in_px * op.Cin * 2.0;
+      break;
+    case GX_OP_LAYERNORM:
+      f = 8.0 * in_px * ti.C;
+      b = in_px * ti.C * (es_in + es_out) + ti.C * 8.0;
+      break;
+    case GX_OP_ATTENTION: {
+      const double S = ti.H, D = to.C;  // D = heads * head_dim
+      f = 4.0 * k * S * S * D;
+      b = in_px * ti.C * es_in + out_px * to.C * es_out;
+      break;
+    }
+    default:
+      b = in_px * ti.C * es_in + out_px * to.C * es_out;
+  }
+  *flops = f;
+  *bytes = b;
+}
+
 int launch_op(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint8_t* wbase, int k, int sm_budget,
               cudaStream_t s, bool pdl, const ConvLaunch* pre, int* kernels) {
   const int bw_grid = std::max(1, sm_budget) * 8;

@@ -31,6 +31,7 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
               ConvLaunch* out, int bn_cap = 256);
 int launch_op(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint8_t* wbase, int k, int sm_budget,
               cudaStream_t s, bool pdl, const ConvLaunch* pre, int* kernels);
+void op_work(const gx_op& op, const gx_tensor* T, int k, double* flops, double* bytes);
 }  // namespace gx
 
 struct gx_model {

@@ -543,4 +543,55 @@ int gx_stage_profile(gx_stage* st, int k, int iters, float* ms_out) {
   return GX_OK;
 }
 
+int gx_stage_op_count(gx_stage* st, int* out) {
+  if (!st || !out) return fail(GX_EINVAL, "null arg");
+  *out = static_cast<int>(st->ops.size());
+  return GX_OK;
+}
+
+int gx_stage_profile_ops(gx_stage* st, int k, int iters, int cap, float* ms, double* flops, double* bytes,
+                         int32_t* kind) {
+  if (!st || !ms || !flops || !bytes || !kind) return fail(GX_EINVAL, "null arg");
+  if (k < 1 || k > st->max_batch || iters < 1) return fail(GX_EINVAL, "bad profile arguments");
+  if (cap < static_cast<int>(st->ops.size())) return fail(GX_EINVAL, "output arrays smaller than the span");
+  float whole = 0.0f;
+  // one full batch first: captures the graph and leaves real activations in every workspace tensor
+  if (int rc = gx_stage_profile(st, k, 3, &whole)) return rc;
+  gx_model* m = st->m;
+  const gx_tensor* T = m->tensors.data();
+  const uint8_t* wbase = static_cast<const uint8_t*>(m->wdev);
+  cudaEvent_t e0, e1;
+  GX_CUDA(cudaEventCreate(&e0));
+  GX_CUDA(cudaEventCreate(&e1));
+  std::vector<float> t(iters);
+  for (size_t i = 0; i < st->ops.size(); ++i) {
+    const gx_op& op = m->ops[st->ops[i]];
+    ConvLaunch cl;
+    const bool is_conv = op.kind == GX_OP_CONV || op.kind == GX_OP_LINEAR;
+    if (is_conv) {
+      if (int rc = plan_conv(op, T, st->tptr.data(), wbase, k, st->sm_budget, &cl)) return rc;
+    }
+    for (int w = 0; w < 2; ++w)
+      if (int rc = launch_op(op, T, st->tptr.data(), wbase, k, st->sm_budget, st->stream, false,
+                             is_conv ? &cl : nullptr, nullptr))
+        return rc;
+    for (int it = 0; it < iters; ++it) {
+      GX_CUDA(cudaEventRecord(e0, st->stream));
+      if (int rc = launch_op(op, T, st->tptr.data(), wbase, k, st->sm_budget, st->stream, false,
+                             is_conv ? &cl : nullptr, nullptr))
+        return rc;
+      GX_CUDA(cudaEventRecord(e1, st->stream));
+      GX_CUDA(cudaEventSynchronize(e1));
+      GX_CUDA(cudaEventElapsedTime(&t[it], e0, e1));
+    }
+    std::sort(t.begin(), t.end());
+    ms[i] = t[iters / 2];
+    op_work(op, T, k, &flops[i], &bytes[i]);
+    kind[i] = op.kind;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return GX_OK;
+}
+
 }  // extern "C"

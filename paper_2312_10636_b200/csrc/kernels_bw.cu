@@ -19,6 +19,15 @@ struct RowDst {
   void* p[kMaxRows];
 };
 
+// Read-once weight stream: non-coherent, no L1 allocation.
+__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
 __device__ __forceinline__ uint4 f32x8_to_bf16x8(float4 a, float4 b) {
   uint4 o;
   o.x = pack_bf16x2(a.x, a.y);
@@ -223,7 +232,7 @@ constexpr int kFcWarps = 8;
 constexpr int kFcRows = 16;
 constexpr int kFcKChunk = 2048;
 template <int OPW>
-__global__ void __launch_bounds__(256) fc_kernel(const __nv_bfloat16* __restrict__ x, int N, int K,
+__global__ void __launch_bounds__(256, 2) fc_kernel(const __nv_bfloat16* __restrict__ x, int N, int K,
                                                  const __nv_bfloat16* __restrict__ w, const float* __restrict__ b,
                                                  void* __restrict__ y, int Nout, int y_f32, int act) {
   extern __shared__ uint4 xs[];  // [kFcRows][kFcKChunk / 8]
@@ -252,33 +261,48 @@ __global__ void __launch_bounds__(256) fc_kernel(const __nv_bfloat16* __restrict
           __syncthreads();
           staged = key;
         }
-        for (int v = lane; v < kc; v += 32) {
-          float wf[OPW][8];
+        // 8 independent 16-byte weight loads in flight per lane (U vectors x OPW outputs) before
+        // any FMA: at a few-SM budget the kernel is latency-bound on L2/HBM, not FMA-bound
+        constexpr int U = OPW >= 4 ? 1 : 8 / OPW;
+        for (int v0 = lane; v0 < kc; v0 += 32 * U) {
+          uint4 wv[U][OPW];
 #pragma unroll
-          for (int a = 0; a < OPW; ++a) {
-            uint4 wv = make_uint4(0, 0, 0, 0);
-            if (o0 + a < Nout)
-              wv = __ldg(reinterpret_cast<const uint4*>(w + static_cast<int64_t>(o0 + a) * K + k0) + v);
-            const uint32_t ww[4] = {wv.x, wv.y, wv.z, wv.w};
+          for (int u = 0; u < U; ++u)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const float2 f = unpack_bf16x2(ww[j]);
-              wf[a][2 * j] = f.x;
-              wf[a][2 * j + 1] = f.y;
+            for (int a = 0; a < OPW; ++a) {
+              const int v = v0 + 32 * u;
+              wv[u][a] = (v < kc && o0 + a < Nout)
+                             ? ldg_stream(reinterpret_cast<const uint4*>(w + static_cast<int64_t>(o0 + a) * K + k0) + v)
+                             : make_uint4(0, 0, 0, 0);
             }
-          }
 #pragma unroll
-          for (int r = 0; r < kFcRows; ++r) {
-            if (r < rows) {
-              const uint4 xv = xs[r * (kFcKChunk / 8) + v];
-              const uint32_t xx[4] = {xv.x, xv.y, xv.z, xv.w};
+          for (int u = 0; u < U; ++u) {
+            const int v = v0 + 32 * u;
+            if (v >= kc) break;
+            float wf[OPW][8];
+#pragma unroll
+            for (int a = 0; a < OPW; ++a) {
+              const uint32_t ww[4] = {wv[u][a].x, wv[u][a].y, wv[u][a].z, wv[u][a].w};
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
-                const float2 f = unpack_bf16x2(xx[j]);
+                const float2 f = unpack_bf16x2(ww[j]);
+                wf[a][2 * j] = f.x;
+                wf[a][2 * j + 1] = f.y;
+              }
+            }
 #pragma unroll
-                for (int a = 0; a < OPW; ++a) {
-                  acc[a][r] = fmaf(wf[a][2 * j], f.x, acc[a][r]);
-                  acc[a][r] = fmaf(wf[a][2 * j + 1], f.y, acc[a][r]);
+            for (int r = 0; r < kFcRows; ++r) {
+              if (r < rows) {
+                const uint4 xv = xs[r * (kFcKChunk / 8) + v];
+                const uint32_t xx[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  const float2 f = unpack_bf16x2(xx[j]);
+#pragma unroll
+                  for (int a = 0; a < OPW; ++a) {
+                    acc[a][r] = fmaf(wf[a][2 * j], f.x, acc[a][r]);
+                    acc[a][r] = fmaf(wf[a][2 * j + 1], f.y, acc[a][r]);
+                  }
                 }
               }
             }

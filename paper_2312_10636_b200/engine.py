@@ -98,6 +98,17 @@ class StageInstance:
         N.check(N.lib().gx_stage_profile(self.handle, k, iters, C.byref(ms)), "gx_stage_profile")
         return float(ms.value)
 
+    def profile_ops(self, k: int, iters: int = 20) -> list[dict]:
+        """Each op of the span alone at batch k: median ms and algorithmic FLOPs / bytes."""
+        L = N.lib()
+        n = C.c_int()
+        N.check(L.gx_stage_op_count(self.handle, C.byref(n)))
+        n = n.value
+        ms, fl, by, kd = (C.c_float * n)(), (C.c_double * n)(), (C.c_double * n)(), (C.c_int32 * n)()
+        N.check(L.gx_stage_profile_ops(self.handle, k, iters, n, ms, fl, by, kd), "gx_stage_profile_ops")
+        return [{"op": i, "kind": int(kd[i]), "ms": float(ms[i]), "flops": float(fl[i]), "bytes": float(by[i])}
+                for i in range(n)]
+
     def kernel_count(self, k: int) -> int:
         n = C.c_int()
         N.check(N.lib().gx_stage_kernel_count(self.handle, k, C.byref(n)))
