@@ -161,6 +161,9 @@ GX_API int gx_stage_kernel_count(gx_stage* st, int k, int* out);
  * activation load, worker/epilogue start, arrival).  out: [sm_budget][n_ops][4]. */
 GX_API int gx_stage_span_trace(gx_stage* st, int k, int64_t* out, int64_t cap, int* n_ops_out);
 
+/* Development: clock64 trace of the conv kernel when GX_CONV_DBG has bit 16 (copied and cleared). */
+GX_API int gx_debug_trace(int64_t* out, int64_t n);
+
 /* Per-sample element count of tensor `tid` of model m (boundary sizes for slot pools). */
 GX_API int gx_model_tensor_elems(gx_model* m, int tid, int64_t* out);
 

@@ -11,7 +11,10 @@ from pathlib import Path
 
 from .errors import raise_for_status
 
-LIB_PATH = Path(__file__).resolve().parent / "_gx.so"
+import os
+
+# GX_LIB: alternative build of the same library (development A/B of compile-time variants)
+LIB_PATH = Path(os.environ.get("GX_LIB") or Path(__file__).resolve().parent / "_gx.so")
 
 GX_BF16, GX_F32 = 0, 1
 (GX_OP_CONV, GX_OP_MAXPOOL, GX_OP_AVGPOOL, GX_OP_GAP, GX_OP_FC, GX_OP_LINEAR, GX_OP_LAYERNORM,
@@ -105,6 +108,7 @@ def lib():
         "gx_stage_profile": (i32, [vp, C.c_int, C.c_int, P(C.c_float)]),
         "gx_stage_kernel_count": (i32, [vp, C.c_int, P(C.c_int)]),
         "gx_stage_op_count": (i32, [vp, P(C.c_int)]),
+        "gx_debug_trace": (i32, [P(i64), i64]),
         "gx_stage_profile_ops": (i32, [vp, C.c_int, C.c_int, C.c_int, P(C.c_float), P(dbl), P(dbl), P(i32)]),
         "gx_run_op": (i32, [vp, P(GxOp), P(GxTensor), P(vp), vp, C.c_int, C.c_int, vp]),
         "gx_gather": (i32, [vp, C.c_int, P(vp), P(i32), i64, i32, i32, vp, C.c_int, vp]),

@@ -45,24 +45,55 @@ struct SmemPlan {
 __host__ __device__ inline int res_groups(int BN) { return (BN + 63) / 64; }
 __host__ __device__ inline uint32_t bias_alloc(int Cout) { return (static_cast<uint32_t>(Cout) * 4u + 1023u) & ~1023u; }
 
-template <bool kTmaA>
-__global__ void __launch_bounds__(kConvThreads, 1)
+// How the many epilogue threads wait for the accumulator / residual / bias (development knob;
+// default: every thread polls with a short back-off).
+__device__ __forceinline__ void epi_wait(uint64_t* bar, uint32_t parity) {
+#if defined(GX_EPI_WAIT) && GX_EPI_WAIT == 0
+  mbar_wait(bar, parity);
+#elif defined(GX_EPI_WAIT) && GX_EPI_WAIT == 2
+  if ((threadIdx.x & 31) == 0) mbar_wait(bar, parity);
+  __syncwarp();
+  mbar_wait(bar, parity);  // completed phase: returns at once, gives every lane the acquire
+#else
+  mbar_wait_sleepy(bar, parity);
+#endif
+}
+
+// Producer / MMA warps: how the warp waits on a pipeline barrier (development knob).
+__device__ __forceinline__ void pipe_wait(uint64_t* bar, uint32_t parity, bool issuer) {
+#if defined(GX_WAIT1)
+  if (issuer) mbar_wait(bar, parity);
+  __syncwarp();
+#else
+  (void)issuer;
+  mbar_wait(bar, parity);
+#endif
+}
+
+template <bool kTmaA, int KPS>
+__global__ void __launch_bounds__(kConvTcThreads, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap amap,
-                   const __grid_constant__ CUtensorMap rmap, const ConvArgs a) {
+                   const __grid_constant__ CUtensorMap rmap, const __grid_constant__ CUtensorMap ymap,
+                   const ConvArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const CUtensorMap* WM = a.gmaps ? a.gmaps : &wmap;
   const CUtensorMap* AM = a.gmaps ? a.gmaps + 1 : &amap;
   const CUtensorMap* RM = a.gmaps ? a.gmaps + 2 : &rmap;
+  const CUtensorMap* YM = &ymap;
   const int S_ = a.stages;
   const int BN = a.BN;
   const bool has_res = a.res != nullptr;
+  const bool ystore = a.ystore != 0;
   const uint32_t b_bytes = static_cast<uint32_t>(BN) * 128u;
   SmemPlan sp;
   sp.sA = smem;
-  sp.sB = sp.sA + static_cast<size_t>(S_) * kATileBytes;
-  sp.sRes = sp.sB + static_cast<size_t>(S_) * b_bytes;
-  const uint32_t res_slot_bytes = has_res ? res_groups(BN) * kResGroupBytes : 0u;
+  // KPS: k-blocks per pipeline stage (TMA mode): one barrier round trip per KPS*64 of K
+  const uint32_t sa_bytes = KPS * kATileBytes, sb_bytes = KPS * b_bytes;
+  sp.sB = sp.sA + static_cast<size_t>(S_) * sa_bytes;
+  sp.sRes = sp.sB + static_cast<size_t>(S_) * sb_bytes;
+  // slots: the residual tile (TMA-loaded) and/or the staged output tile (TMA-stored), in place
+  const uint32_t res_slot_bytes = (has_res || ystore) ? res_groups(BN) * kResGroupBytes : 0u;
   sp.sBias = reinterpret_cast<float*>(sp.sRes + a.nres * res_slot_bytes);
   sp.full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sp.sBias) + bias_alloc(a.Cout));
   sp.empty = sp.full + S_;
@@ -99,12 +130,12 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   if (warp == 4) {
     if (lane == 0) {
       for (int i = 0; i < S_; ++i) {
-        mbar_init(&sp.full[i], kTmaA ? 1 : 128 + 1);
+        mbar_init(&sp.full[i], kTmaA ? 2 : 128 + 1);
         mbar_init(&sp.empty[i], 1);
       }
       for (int i = 0; i < 2; ++i) {
         mbar_init(&sp.tfull[i], 1);
-        mbar_init(&sp.tempty[i], 128);
+        mbar_init(&sp.tempty[i], kTmaA ? 256 : 128);
       }
       mbar_init(&sp.rfull[0], 1);
       mbar_init(&sp.rfull[1], 1);
@@ -124,8 +155,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   pdl_wait();
 
   const int HoWo = a.Ho * a.Wo;
-  if (warp < 4) {
-    if (!kTmaA) {
+  if (warp < 4 && !kTmaA) {
+    {
       // ---------------------------------------------------------- A producers (cp.async im2col)
       const int row = tid;
       int it = 0;
@@ -163,43 +194,67 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         }
       }
     }
-  } else if (warp == 4) {
-    // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      tma_prefetch_desc(WM);
-      if (kTmaA) tma_prefetch_desc(AM);
-      const uint32_t tx = b_bytes + (kTmaA ? kATileBytes : 0);
-      int it = 0;
-      for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
-        const int m_blk = tile / a.n_tiles;
-        const int n_blk = tile % a.n_tiles;
-        int wc = 0, hc = 0, nimg = 0;
-        if (kTmaA) {
-          const int m0 = m_blk * kBM;
-          nimg = m0 / HoWo;
-          const int rem = m0 - nimg * HoWo;
-          const int ho0 = rem / a.Wo;
-          wc = (rem - ho0 * a.Wo) * a.sw - a.pw;
-          hc = ho0 * a.sh - a.ph;
+  } else if (warp == 4 || warp == 10) {
+    // ------------------------------------------------------------ TMA producers
+    // Warp 4 issues the A operand (im2col / 2D TMA), warp 10 the B operand (weights), each on its
+    // own arrival of the stage's full barrier, so the two request streams overlap instead of
+    // queueing behind one issuing thread.  (cp.async mode: warps 0-3 build A, warp 4 loads B.)
+    // The whole warp walks the loop (waits, coordinates: warp-uniform values the compiler keeps in
+    // uniform registers); one elected lane issues each copy.
+    const bool issuer = elect_one();
+    const bool do_a = kTmaA && warp == 4;
+    const bool do_b = kTmaA ? warp == 10 : warp == 4;
+    const bool skipA = a.dbg & 1, skipB = a.dbg & 2;
+    if (issuer) {
+      if (do_b && !a.wsw) tma_prefetch_desc(WM);
+      if (do_a) tma_prefetch_desc(AM);
+    }
+    const uint32_t tx = (do_a && !skipA ? kATileBytes : 0u) + (do_b && !skipB ? b_bytes : 0u);
+    const int cpl = a.cpl;
+    const int nl = kBK / cpl;
+    const uint32_t region = static_cast<uint32_t>(kBM * cpl * 2);
+    int st = 0, it = 0;
+    uint32_t ph = 0;
+    for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
+      const int m_blk = tile / a.n_tiles;
+      const int n_blk = tile % a.n_tiles;
+      int wc = 0, hc = 0, nimg = 0;
+      if (do_a) {
+        const int m0 = m_blk * kBM;
+        nimg = m0 / HoWo;
+        const int rem = m0 - nimg * HoWo;
+        const int ho0 = rem / a.Wo;
+        wc = (rem - ho0 * a.Wo) * a.sw - a.pw;
+        hc = ho0 * a.sh - a.ph;
+      }
+      // (filter row r, filter col s, channel block c0) of the next im2col load; K is ordered
+      // (r, s, c).  Loads past the last tap (K padding) read real pixels, but the matching
+      // packed weights are zero, so they contribute nothing.
+      int c0 = 0, r = 0, s = 0;
+      const uint8_t* wsrc = a.wsw ? a.wsw + static_cast<size_t>(n_blk) * BN * 128u : nullptr;
+      for (int kb0 = 0; kb0 < a.num_kb; kb0 += KPS, ++it) {
+        pipe_wait(&sp.empty[st], ph ^ 1, issuer);
+        if (issuer && warp == 4 && a.trace && blockIdx.x == 0 && it < 8192) a.trace[it * 4 + 0] = clock64();
+        const int nk = min(KPS, a.num_kb - kb0);
+        if (issuer) {
+          if (tx)
+            mbar_arrive_expect_tx(&sp.full[st], tx * nk);
+          else
+            mbar_arrive(&sp.full[st]);
         }
-        // (filter row r, filter col s, channel block c0) of the next im2col load; K is ordered
-        // (r, s, c).  Loads past the last tap (K padding) read real pixels, but the matching
-        // packed weights are zero, so they contribute nothing.
-        int c0 = 0, r = 0, s = 0;
-        const int cpl = a.cpl;
-        const uint32_t region = static_cast<uint32_t>(kBM * cpl * 2);
-        for (int kb = 0; kb < a.num_kb; ++kb, ++it) {
-          const int st = it % S_;
-          const uint32_t ph = (it / S_) & 1;
-          mbar_wait(&sp.empty[st], ph ^ 1);
-          mbar_arrive_expect_tx(&sp.full[st], tx);
-          if (kTmaA && a.a2d) {
+        for (int j = 0; j < nk; ++j) {
+        const int kb = kb0 + j;
+        uint8_t* const sa = sp.sA + st * sa_bytes + j * kATileBytes;
+        uint8_t* const sb = sp.sB + static_cast<size_t>(st) * sb_bytes + j * b_bytes;
+        if (do_a) {
+          if (a.a2d) {
             // 1x1 / stride 1 / no padding: A is the plain [M, C] activation matrix
-            tma_load_2d(sp.sA + st * kATileBytes, AM, &sp.full[st], kb * kBK, m_blk * kBM);
-          } else if (kTmaA) {
-            for (int l = 0; l < kBK / cpl; ++l) {
-              tma_load_im2col_4d(sp.sA + st * kATileBytes + l * region, AM, &sp.full[st], c0, wc, hc, nimg,
-                                 static_cast<uint16_t>(s), static_cast<uint16_t>(r));
+            if (issuer && !skipA) tma_load_2d(sa, AM, &sp.full[st], kb * kBK, m_blk * kBM);
+          } else {
+            for (int l = 0; l < nl; ++l) {
+              if (issuer && !skipA)
+                tma_load_im2col_4d(sa + l * region, AM, &sp.full[st], c0, wc, hc, nimg, static_cast<uint16_t>(s),
+                                   static_cast<uint16_t>(r));
               c0 += cpl;
               if (c0 == a.Cin) {
                 c0 = 0;
@@ -210,52 +265,85 @@ __global__ void __launch_bounds__(kConvThreads, 1)
               }
             }
           }
-          tma_load_2d(sp.sB + static_cast<size_t>(st) * b_bytes, WM, &sp.full[st], kb * kBK, n_blk * BN);
+        }
+        if (do_b && !skipB && issuer) {
+          if (wsrc)  // pre-swizzled tile: one contiguous bulk copy (no tensor-map walk)
+            bulk_load(sb, wsrc + static_cast<size_t>(kb) * a.Cout * 128u, b_bytes, &sp.full[st]);
+          else
+            tma_load_2d(sb, WM, &sp.full[st], kb * kBK, n_blk * BN);
+        }
+        }
+        __syncwarp();
+        if (++st == S_) {
+          st = 0;
+          ph ^= 1;
         }
       }
     }
   } else if (warp == 5) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      int it = 0, t = 0;
-      for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++t) {
-        const int acc = t & 1;
-        const uint32_t aph = (t >> 1) & 1;
-        mbar_wait(&sp.tempty[acc], aph ^ 1);
+    // ------------------------------------------------------------ MMA issuer (warp-uniform loop)
+    const bool issuer = elect_one();
+    int it = 0, t = 0, st = 0;
+    uint32_t ph = 0;
+    for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++t) {
+      const int acc = t & 1;
+      const uint32_t aph = (t >> 1) & 1;
+      pipe_wait(&sp.tempty[acc], aph ^ 1, issuer);
+      tc_fence_after();
+      const uint32_t d = tmem_base + acc * acc_stride;
+      for (int kb0 = 0; kb0 < a.num_kb; kb0 += KPS, ++it, st = (st + 1 == S_) ? 0 : st + 1, ph ^= (st == 0)) {
+        pipe_wait(&sp.full[st], ph, issuer);
+        if (issuer && a.trace && blockIdx.x == 0 && it < 8192) a.trace[it * 4 + 1] = clock64();
         tc_fence_after();
-        const uint32_t d = tmem_base + acc * acc_stride;
-        for (int kb = 0; kb < a.num_kb; ++kb, ++it) {
-          const int st = it % S_;
-          const uint32_t ph = (it / S_) & 1;
-          mbar_wait(&sp.full[st], ph);
-          tc_fence_after();
-          const uint32_t abase = smem_u32(sp.sA + st * kATileBytes);
-          const uint64_t bd = umma_desc_sw128(sp.sB + static_cast<size_t>(st) * b_bytes);
-          if (!kTmaA || a.cpl == 64) {
-            const uint64_t ad = umma_desc_kmajor(abase, 64, 0);
+        if (a.dbg & 4) {
+          if (issuer) umma_commit(&sp.empty[st]);
+          __syncwarp();
+          continue;
+        }
+        const int nk = min(KPS, a.num_kb - kb0);
+        for (int jj = 0; jj < nk; ++jj) {
+        const int kb = kb0 + jj;
+        const uint32_t abase = smem_u32(sp.sA + st * sa_bytes + jj * kATileBytes);
+        const uint64_t bd = umma_desc_sw128(sp.sB + static_cast<size_t>(st) * sb_bytes + jj * b_bytes);
+        if (!kTmaA || a.cpl == 64) {
+          const uint64_t ad = umma_desc_kmajor(abase, 64, 0);
+          if (issuer) {
 #pragma unroll
             for (int kk = 0; kk < kBK / 16; ++kk) umma_bf16(d, ad + 2 * kk, bd + 2 * kk, a.idesc, (kb | kk) != 0);
-          } else {
-            // A stage = 64/cpl regions of 128 rows x cpl channels; MMA kk covers K [16kk, 16kk+16)
-            const uint32_t region = static_cast<uint32_t>(kBM * a.cpl * 2);
-#pragma unroll
-            for (int kk = 0; kk < kBK / 16; ++kk) {
-              const int e0 = kk * 16;
-              const uint32_t addr = abase + (e0 / a.cpl) * region + (e0 % a.cpl) * 2;
-              umma_bf16(d, umma_desc_kmajor(addr, a.cpl, region), bd + 2 * kk, a.idesc, (kb | kk) != 0);
-            }
           }
-          umma_commit(&sp.empty[st]);
+        } else {
+          // A stage = 64/cpl regions of 128 rows x cpl channels; MMA kk covers K [16kk, 16kk+16)
+          const uint32_t region = static_cast<uint32_t>(kBM * a.cpl * 2);
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk) {
+            const int e0 = kk * 16;
+            const uint32_t addr = abase + (e0 / a.cpl) * region + (e0 % a.cpl) * 2;
+            const uint64_t adk = umma_desc_kmajor(addr, a.cpl, region);
+            if (issuer) umma_bf16(d, adk, bd + 2 * kk, a.idesc, (kb | kk) != 0);
+          }
         }
-        umma_commit(&sp.tfull[acc]);
+        }
+        if (issuer) {
+          umma_commit(&sp.empty[st]);
+          if (a.trace && blockIdx.x == 0 && it < 8192) a.trace[it * 4 + 2] = clock64();
+        }
+        __syncwarp();
       }
+      if (issuer) umma_commit(&sp.tfull[acc]);
+      __syncwarp();
     }
-  } else {
+  } else if ((warp >= 6 && warp <= 9) || (kTmaA && warp < 4)) {
     // ------------------------------------------------------------ epilogue
+    // warps 6-9, plus warps 0-3 when TMA builds A (they have no producer work): two warps per
+    // TMEM lane quarter split the tile's 16-column chunks, two tcgen05.ld in flight per wait
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;
+    const int nepi = kTmaA ? 256 : 128;
+    const int half = (kTmaA && warp < 4) ? 1 : 0;
+    const int cstep = kTmaA ? 32 : 16;
     const bool leader = warp == 6 && lane == 0;
     const int nres = a.nres;
+    const int nslot = (has_res || ystore) ? nres : 1;
     // residual tile of the t-th tile this CTA processes -> slot t % nres
     auto issue_res = [&](int t_idx) {
       const int tile = blockIdx.x + t_idx * gridDim.x;
@@ -275,7 +363,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         for (int i = 0; i < nres; ++i) issue_res(i);
       }
     }
-    mbar_wait(sp.bfull, 0);
+    epi_wait(sp.bfull, 0);
     int t = 0;
     for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++t) {
       const int m_blk = tile / a.n_tiles;
@@ -283,22 +371,30 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       const int m0 = m_blk * kBM;
       const int nb0 = n_blk * BN;
       const int ncols = min(BN, a.Cout - nb0);
-      const int slot = has_res ? t % nres : 0;
+      const int slot = t % nslot;
       const float* bias = sp.sBias + nb0;
       const uint8_t* res_base = sp.sRes + slot * res_slot_bytes;
       const int acc = t & 1;
       const uint32_t aph = (t >> 1) & 1;
-      mbar_wait(&sp.tfull[acc], aph);
+      epi_wait(&sp.tfull[acc], aph);
       tc_fence_after();
-      if (has_res) mbar_wait(&sp.rfull[slot], (t / nres) & 1);
+      if (has_res) {
+        epi_wait(&sp.rfull[slot], (t / nres) & 1);
+      } else if (ystore) {
+        // the TMA store that last used this slot (tile t - nres) has finished reading it
+        if (leader) {
+          if (nres == 1)
+            bulk_wait_read<0>();
+          else
+            bulk_wait_read<1>();
+        }
+        named_bar_sync(1, nepi);
+      }
       const int m = m0 + row;
       const bool row_ok = m < a.M;
       const uint32_t tbase = tmem_base + acc * acc_stride + (static_cast<uint32_t>(q * 32) << 16);
-      for (int c = 0; c < BN; c += 16) {
-        uint32_t v[16];
-        tmem_ld16(tbase + c, v);
-        tmem_ld_wait();
-        if (row_ok && c < ncols) {
+      auto emit = [&](const int c, const uint32_t (&v)[16]) {
+        if ((row_ok || ystore) && c < ncols) {
           const int n0 = nb0 + c;
           float f[16];
 #pragma unroll
@@ -325,7 +421,20 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 #pragma unroll
             for (int i = 0; i < 16; ++i) f[i] = gelu_erf(f[i]);
           }
-          if (a.y_f32) {
+          if (ystore) {
+            // back into the slot, same swizzled position the residual came from
+            uint8_t* srow = const_cast<uint8_t*>(res_base) + (c >> 6) * kResGroupBytes + row * 128;
+            const int j0 = (c & 63) >> 3;
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              uint4 o;
+              o.x = pack_bf16x2(f[8 * i + 0], f[8 * i + 1]);
+              o.y = pack_bf16x2(f[8 * i + 2], f[8 * i + 3]);
+              o.z = pack_bf16x2(f[8 * i + 4], f[8 * i + 5]);
+              o.w = pack_bf16x2(f[8 * i + 6], f[8 * i + 7]);
+              *reinterpret_cast<uint4*>(srow + (((j0 + i) ^ (row & 7)) << 4)) = o;
+            }
+          } else if (a.y_f32) {
             float4* y4 = reinterpret_cast<float4*>(static_cast<float*>(a.y) + static_cast<size_t>(m) * a.y_ld +
                                                    a.y_coff + n0);
 #pragma unroll
@@ -344,15 +453,37 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             }
           }
         }
+      };
+      for (int c = half * 16; c < ((a.dbg & 8) ? 0 : BN); c += 2 * cstep) {
+        uint32_t v0[16], v1[16];
+        const int c1 = c + cstep;
+        tmem_ld16(tbase + c, v0);
+        if (c1 < BN) tmem_ld16(tbase + c1, v1);
+        tmem_ld_wait();
+        emit(c, v0);
+        if (c1 < BN) emit(c1, v1);
       }
       tc_fence_before();
       mbar_arrive(&sp.tempty[acc]);
-      if (has_res) {
-        named_bar_sync(1, 128);  // every epilogue thread is done with this residual slot
+      if (ystore) {
+        fence_proxy_async_smem();  // make the slot's generic-proxy writes visible to the TMA store
+        named_bar_sync(1, nepi);
+        if (leader) {
+          for (int g = 0; g < (ncols + 63) / 64; ++g)
+            tma_store_2d(YM, res_base + g * kResGroupBytes, a.y_coff + nb0 + g * 64, m0);
+          bulk_commit();
+          if (has_res) {
+            bulk_wait_read<0>();  // the slot is refilled by the next residual load
+            issue_res(t + nres);
+          }
+        }
+      } else if (has_res) {
+        named_bar_sync(1, nepi);  // every epilogue thread is done with this residual slot
         if (leader) issue_res(t + nres);
       }
     }
   }
+  if (ystore && warp == 6 && lane == 0) bulk_wait<0>();  // output stores complete before exit
   // Let the next kernel in the stream start its prologue.
   pdl_launch_dependents();
   tc_fence_before();
@@ -364,20 +495,20 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 }
 }  // namespace
 
-size_t conv_smem_bytes(int BN, int stages, int num_kb, int nres, int Cout) {
-  return 1024 + static_cast<size_t>(stages) * (kATileBytes + BN * 128) +
+size_t conv_smem_bytes(int BN, int stages, int num_kb, int nres, int Cout, int kps) {
+  return 1024 + static_cast<size_t>(stages) * kps * (kATileBytes + BN * 128) +
          static_cast<size_t>(nres) * res_groups(BN) * kResGroupBytes + bias_alloc(Cout) + (2 * stages + 9) * 8 + 16 +
          static_cast<size_t>(num_kb) * 8 * sizeof(int2);
 }
 
 // Pipeline depth and residual slots that fit in ~220 KB: prefer >= 3 stages with a double-
 // buffered residual, else a single residual slot.
-int conv_pick_stages(int BN, int num_kb, bool res, int Cout, int* nres_out) {
+int conv_pick_stages(int BN, int num_kb, bool res, int Cout, int* nres_out, int kps) {
   const size_t budget = 220 * 1024;
-  const size_t per_stage = kATileBytes + BN * 128 + 16;
+  const size_t per_stage = static_cast<size_t>(kps) * (kATileBytes + BN * 128) + 16;
   int best_s = 2, best_r = res ? 1 : 0;
   for (int nres = res ? 2 : 0; nres >= (res ? 1 : 0); --nres) {
-    const size_t fixed = conv_smem_bytes(BN, 0, num_kb, nres, Cout);
+    const size_t fixed = conv_smem_bytes(BN, 0, num_kb, nres, Cout, kps);
     int s = budget > fixed ? static_cast<int>((budget - fixed) / per_stage) : 0;
     if (s > 8) s = 8;
     if (s >= 3 || nres <= 1) {
@@ -391,27 +522,30 @@ int conv_pick_stages(int BN, int num_kb, bool res, int Cout, int* nres_out) {
 }
 
 cudaError_t launch_conv(const CUtensorMap& wmap, const CUtensorMap& amap, const CUtensorMap& rmap,
-                        const ConvArgs& a, int grid, cudaStream_t s, bool pdl) {
+                        const CUtensorMap& ymap, const ConvArgs& a, int grid, cudaStream_t s, bool pdl) {
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(conv_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+      e = cudaFuncSetAttribute(conv_tc_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(conv_tc_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     if (e != cudaSuccess) return e;
     configured = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);
-  cfg.blockDim = dim3(kConvThreads, 1, 1);
-  cfg.dynamicSmemBytes = conv_smem_bytes(a.BN, a.stages, a.num_kb, a.nres, a.Cout);
+  cfg.blockDim = dim3(kConvTcThreads, 1, 1);
+  cfg.dynamicSmemBytes = conv_smem_bytes(a.BN, a.stages, a.num_kb, a.nres, a.Cout, a.kps);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  if (a.tma_a) return cudaLaunchKernelEx(&cfg, conv_tc_kernel<true>, wmap, amap, rmap, a);
-  return cudaLaunchKernelEx(&cfg, conv_tc_kernel<false>, wmap, amap, rmap, a);
+  if (a.tma_a && a.kps == 2) return cudaLaunchKernelEx(&cfg, conv_tc_kernel<true, 2>, wmap, amap, rmap, ymap, a);
+  if (a.tma_a) return cudaLaunchKernelEx(&cfg, conv_tc_kernel<true, 1>, wmap, amap, rmap, ymap, a);
+  return cudaLaunchKernelEx(&cfg, conv_tc_kernel<false, 1>, wmap, amap, rmap, ymap, a);
 }
 
 }  // namespace gx

@@ -117,6 +117,17 @@ bool encode_tmap_im2col_bf16(CUtensorMap* map, const void* base, int C, int W, i
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// ---------------------------------------------------------------- development trace buffer
+static unsigned long long* g_trace = nullptr;
+constexpr int kTraceEntries = 1 << 20;
+unsigned long long* debug_trace_buffer() {
+  if (!g_trace) {
+    cudaMalloc(&g_trace, kTraceEntries * sizeof(unsigned long long));
+    cudaMemset(g_trace, 0, kTraceEntries * sizeof(unsigned long long));
+  }
+  return g_trace;
+}
+
 // ---------------------------------------------------------------- op planning
 int elem_size(int dtype) { return dtype == GX_F32 ? 4 : 2; }
 int64_t tensor_elems(const gx_tensor& t) { return static_cast<int64_t>(t.H) * t.W * t.C; }
@@ -146,7 +157,7 @@ static uint32_t tmem_cols_for(int bn) {
 }
 
 int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint8_t* wbase, int k, int sm_budget,
-              ConvLaunch* out, int bn_cap) {
+              ConvLaunch* out, int bn_cap, const uint8_t* wsw) {
   const gx_tensor& ti = T[op.in];
   const gx_tensor& to = T[op.out];
   const int R = op.kind == GX_OP_LINEAR ? 1 : op.R;
@@ -192,16 +203,38 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
   a.y_f32 = to.dtype == GX_F32;
   a.act = op.act;
   a.idesc = umma_idesc_bf16(kBM, a.BN);
-  a.stages = conv_pick_stages(a.BN, a.num_kb, a.res != nullptr, a.Cout, &a.nres);
+  // bf16 output through smem + TMA store when every 64-column group of a tile is whole (a tile
+  // never writes past its own channel slice of a concat tensor)
+  a.ystore = !a.y_f32 && a.BN % 64 == 0 && a.Cout % 64 == 0 && to.C >= 64 && getenv("GX_NO_YSTORE") == nullptr &&
+             getenv("GX_GMAPS") == nullptr;
+  // two k-blocks per pipeline stage halve the barrier round trips per unit of K; worth it when the
+  // per-k-block MMA time (2*BN cycles) is below the ~500-cycle stage round trip and >= 3 stages fit
+  a.kps = 1;
+  {
+    const bool tma = getenv("GX_NO_TMA_IM2COL") == nullptr;
+    const char* e = getenv("GX_KPS");
+    const int want = e ? atoi(e) : (a.BN <= 64 ? 2 : 1);
+    if (tma && want == 2 && a.num_kb >= 2) {
+      int nres2 = 0;
+      if (conv_pick_stages(a.BN, a.num_kb, a.res != nullptr || a.ystore, a.Cout, &nres2, 2) >= 3) a.kps = 2;
+    }
+  }
+  a.stages = conv_pick_stages(a.BN, a.num_kb, a.res != nullptr || a.ystore, a.Cout, &a.nres, a.kps);
   if (const char* e = getenv("GX_STAGES")) {
     const int st = atoi(e);
     if (st >= 1 && st <= a.stages) a.stages = st;
   }
   a.tmem_cols = tmem_cols_for(a.BN);
+  a.wsw = getenv("GX_NO_WBULK") ? nullptr : wsw;
+  a.dbg = getenv("GX_CONV_DBG") ? atoi(getenv("GX_CONV_DBG")) : 0;
+  a.trace = (a.dbg & 16) ? debug_trace_buffer() : nullptr;
   if (a.res && (T[op.in2].dtype != GX_BF16 || (a.res_ld & 7))) return fail(GX_EINVAL, "bad residual tensor");
   const int kpad = a.num_kb * kBK;
   memset(&out->amap, 0, sizeof(out->amap));
   memset(&out->rmap, 0, sizeof(out->rmap));
+  memset(&out->ymap, 0, sizeof(out->ymap));
+  if (a.ystore && !encode_tmap_2d_bf16(&out->ymap, a.y, to.C, a.M, static_cast<uint64_t>(to.C) * 2, 64, kBM))
+    return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for the conv output: " + g_last_encode);
   if (!encode_tmap_2d_bf16(&out->wmap, wbase + op.w_off, kpad, op.Cout, static_cast<uint64_t>(kpad) * 2, kBK, a.BN))
     return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for conv weights: " + g_last_encode);
   a.cpl = (op.Cin % 64 == 0) ? 64 : (op.Cin % 32 == 0) ? 32 : (op.Cin % 16 == 0) ? 16 : 8;
@@ -294,7 +327,7 @@ int launch_op(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
         if (rc != GX_OK) return rc;
         pre = &cl;
       }
-      GX_CUDA(launch_conv(pre->wmap, pre->amap, pre->rmap, pre->args, pre->grid, s, pdl));
+      GX_CUDA(launch_conv(pre->wmap, pre->amap, pre->rmap, pre->ymap, pre->args, pre->grid, s, pdl));
       break;
     }
     case GX_OP_MAXPOOL:
@@ -363,6 +396,16 @@ using namespace gx;
 extern "C" {
 
 int gx_abi_version(void) { return GX_ABI_VERSION; }
+
+// Development: copy the conv kernel's clock64 trace (GX_CONV_DBG & 16) to the host and clear it.
+int gx_debug_trace(int64_t* out, int64_t n) {
+  if (!g_trace || !out || n <= 0) return fail(GX_EINVAL, "no trace");
+  if (n > kTraceEntries) n = kTraceEntries;
+  GX_CUDA(cudaDeviceSynchronize());
+  GX_CUDA(cudaMemcpy(out, g_trace, n * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  GX_CUDA(cudaMemset(g_trace, 0, kTraceEntries * sizeof(unsigned long long)));
+  return GX_OK;
+}
 
 int gx_last_error(char* buf, size_t n) {
   if (buf && n) {

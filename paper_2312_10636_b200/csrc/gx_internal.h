@@ -50,15 +50,25 @@ struct ConvArgs {
   int nres;   // residual smem slots (0 without residual, else 1 or 2)
   int a2d;    // A via a plain 2D tiled map over [M, C] (1x1, stride 1, no padding)
   const CUtensorMap* gmaps;  // experiment: tensor maps read from global memory instead of params
+  int ystore;  // bf16 output staged in the smem slots and written by TMA stores (ymap), else st.global
+  int dbg;  // GX_CONV_DBG timing attribution (results invalid): 1 skip A loads, 2 skip B loads,
+            // 4 skip MMAs, 8 skip the epilogue's TMEM reads and stores
+  int kps;  // k-blocks per pipeline stage (1 or 2; 2 only with TMA-built A)
+  unsigned long long* trace;  // dbg & 16: per-iteration clock64 stamps of CTA 0 (development)
+  const uint8_t* wsw;  // B tiles by plain bulk copy from the pre-swizzled [kb][Cout][64] layout (or null)
 };
-constexpr int kConvThreads = 320;  // 4 A-producer warps, TMA warp, MMA warp, 4 epilogue warps
+constexpr int kConvThreads = 320;  // span kernel: 4 A-producer warps, TMA warp, MMA warp, 4 epilogue warps
+// conv_tc: warps 0-3 cp.async A producers (or epilogue when TMA builds A), 4 A/B TMA, 5 MMA,
+// 6-9 epilogue, 10 B TMA (TMA mode)
+constexpr int kConvTcThreads = 352;
 constexpr int kBM = 128;
 constexpr int kBK = 64;
-size_t conv_smem_bytes(int BN, int stages, int num_kb, int nres, int Cout);
-int conv_pick_stages(int BN, int num_kb, bool res, int Cout, int* nres_out);
-// wmap: weights [Cout][Kpad]; amap: im2col map of the input (tma_a); rmap: residual [M][res_ld].
+size_t conv_smem_bytes(int BN, int stages, int num_kb, int nres, int Cout, int kps = 1);
+int conv_pick_stages(int BN, int num_kb, bool res, int Cout, int* nres_out, int kps = 1);
+// wmap: weights [Cout][Kpad]; amap: im2col map of the input (tma_a); rmap: residual [M][res_ld];
+// ymap: output [M][y_ld] (ystore).
 cudaError_t launch_conv(const CUtensorMap& wmap, const CUtensorMap& amap, const CUtensorMap& rmap,
-                        const ConvArgs& a, int grid, cudaStream_t s, bool pdl);
+                        const CUtensorMap& ymap, const ConvArgs& a, int grid, cudaStream_t s, bool pdl);
 bool encode_tmap_im2col_bf16(CUtensorMap* map, const void* base, int C, int W, int H, int N, int lower_w,
                              int lower_h, int upper_w, int upper_h, int stride_w, int stride_h, int cpl);
 

@@ -21,16 +21,20 @@ struct ConvLaunch {
   CUtensorMap wmap;
   CUtensorMap amap;  // im2col map of the input (args.tma_a)
   CUtensorMap rmap;  // residual tile map (args.res)
+  CUtensorMap ymap;  // output tile map (args.ystore)
   ConvArgs args;
   int grid;
 };
 
 int elem_size(int dtype);
 int64_t tensor_elems(const gx_tensor& t);
+// wsw: the op's weights pre-tiled and pre-swizzled for bulk copies ([kb][Cout][64] bf16, 128B
+// swizzle), or null to load them with a tiled TMA from the [Cout][Kpad] blob.
 int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint8_t* wbase, int k, int sm_budget,
-              ConvLaunch* out, int bn_cap = 256);
+              ConvLaunch* out, int bn_cap = 256, const uint8_t* wsw = nullptr);
 int launch_op(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint8_t* wbase, int k, int sm_budget,
               cudaStream_t s, bool pdl, const ConvLaunch* pre, int* kernels);
+unsigned long long* debug_trace_buffer();
 void op_work(const gx_op& op, const gx_tensor* T, int k, double* flops, double* bytes);
 }  // namespace gx
 
@@ -43,6 +47,11 @@ struct gx_model {
   std::vector<int32_t> boundary;       // n_units + 1
   void* wdev = nullptr;
   size_t wbytes = 0;
+  void* wsw = nullptr;                // conv/linear weights re-laid for bulk copies (see plan_conv)
+  std::vector<int64_t> wsw_off;       // per op: byte offset into wsw, -1 if none
+  const uint8_t* op_wsw(int op) const {
+    return wsw && wsw_off[op] >= 0 ? static_cast<const uint8_t*>(wsw) + wsw_off[op] : nullptr;
+  }
   int n_units() const { return static_cast<int>(boundary.size()) - 1; }
 };
 

@@ -92,7 +92,8 @@ int capture_span(gx_stage* st, int k, gx_stage::PerK* out) {
   for (size_t i = 0; i < st->ops.size(); ++i) {
     const gx_op& op = m->ops[st->ops[i]];
     if (op.kind == GX_OP_CONV || op.kind == GX_OP_LINEAR) {
-      int rc = plan_conv(op, m->tensors.data(), st->tptr.data(), wbase, k, st->sm_budget, &plans[i]);
+      int rc = plan_conv(op, m->tensors.data(), st->tptr.data(), wbase, k, st->sm_budget, &plans[i], 256,
+                         m->op_wsw(st->ops[i]));
       if (rc != GX_OK) return rc;
     }
   }
@@ -258,6 +259,45 @@ int build_span_program(gx_stage* st, int k, gx_stage::PerK* out) {
   return GX_OK;
 }
 
+// Conv / linear weights re-laid for the conv kernel's B operand: [kb][Cout][64] bf16 with the
+// 128-byte swizzle already applied (16-byte chunk j of row n stored at chunk j ^ (n & 7)), so a
+// BN x 64 tile of k-block kb is one contiguous BN*128-byte run that a plain bulk copy drops into
+// shared memory exactly as a SWIZZLE_128B tensor-map load would (tiles start at multiples of 16
+// rows).  One extra k-block of slack lets a partial last N tile over-read harmlessly.
+cudaError_t build_bulk_weights(gx_model* m, const uint8_t* blob) {
+  const int n = static_cast<int>(m->ops.size());
+  m->wsw_off.assign(n, -1);
+  size_t total = 0;
+  for (int i = 0; i < n; ++i) {
+    const gx_op& op = m->ops[i];
+    if (op.kind != GX_OP_CONV && op.kind != GX_OP_LINEAR) continue;
+    const int R = op.kind == GX_OP_LINEAR ? 1 : op.R, S = op.kind == GX_OP_LINEAR ? 1 : op.S;
+    const size_t kpad = (static_cast<size_t>(R) * S * op.Cin + 63) / 64 * 64;
+    m->wsw_off[i] = static_cast<int64_t>(total);
+    total += kpad * op.Cout * 2;
+  }
+  if (total == 0) return cudaSuccess;
+  total += 256 * 128;
+  std::vector<uint8_t> h(total, 0);
+  for (int i = 0; i < n; ++i) {
+    if (m->wsw_off[i] < 0) continue;
+    const gx_op& op = m->ops[i];
+    const int R = op.kind == GX_OP_LINEAR ? 1 : op.R, S = op.kind == GX_OP_LINEAR ? 1 : op.S;
+    const size_t kpad = (static_cast<size_t>(R) * S * op.Cin + 63) / 64 * 64;
+    const size_t nkb = kpad / 64;
+    const uint8_t* src = blob + op.w_off;  // [Cout][kpad] bf16
+    uint8_t* dst = h.data() + m->wsw_off[i];
+    for (size_t kb = 0; kb < nkb; ++kb)
+      for (int row = 0; row < op.Cout; ++row)
+        for (int j = 0; j < 8; ++j)
+          std::memcpy(dst + ((kb * op.Cout + row) * 8 + (j ^ (row & 7))) * 16,
+                      src + (static_cast<size_t>(row) * kpad + kb * 64 + j * 8) * 2, 16);
+  }
+  cudaError_t e = cudaMalloc(&m->wsw, total);
+  if (e == cudaSuccess) e = cudaMemcpy(m->wsw, h.data(), total, cudaMemcpyHostToDevice);
+  return e;
+}
+
 }  // namespace
 
 extern "C" {
@@ -292,8 +332,10 @@ int gx_model_create(gx_ctx* ctx, const char* model_id, int n_tensors, const gx_t
   m->wbytes = blob_bytes;
   cudaError_t e = cudaMalloc(&m->wdev, std::max<size_t>(blob_bytes, 256));
   if (e == cudaSuccess && blob_bytes) e = cudaMemcpy(m->wdev, weight_blob, blob_bytes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = build_bulk_weights(m, static_cast<const uint8_t*>(weight_blob));
   if (e != cudaSuccess) {
     if (m->wdev) cudaFree(m->wdev);
+    if (m->wsw) cudaFree(m->wsw);
     delete m;
     return cuda_fail(e, "weight upload");
   }
@@ -305,6 +347,7 @@ int gx_model_destroy(gx_model* m) {
   if (!m) return GX_OK;
   cudaSetDevice(m->ctx->device);
   if (m->wdev) cudaFree(m->wdev);
+  if (m->wsw) cudaFree(m->wsw);
   delete m;
   return GX_OK;
 }
@@ -569,7 +612,8 @@ int gx_stage_profile_ops(gx_stage* st, int k, int iters, int cap, float* ms, dou
     ConvLaunch cl;
     const bool is_conv = op.kind == GX_OP_CONV || op.kind == GX_OP_LINEAR;
     if (is_conv) {
-      if (int rc = plan_conv(op, T, st->tptr.data(), wbase, k, st->sm_budget, &cl)) return rc;
+      if (int rc = plan_conv(op, T, st->tptr.data(), wbase, k, st->sm_budget, &cl, 256, m->op_wsw(st->ops[i])))
+        return rc;
     }
     for (int w = 0; w < 2; ++w)
       if (int rc = launch_op(op, T, st->tptr.data(), wbase, k, st->sm_budget, st->stream, false,

@@ -85,6 +85,11 @@ def run_graph(name, k, H, W, Cin, Cout, R, S, stride, pad, budget=0, iters=50):
 
 
 SHAPES["tiny"] = (1, 8, 8, 64, 64, 1, 1, 1, 0)
+SHAPES["l1_1x1_64_256_k8"] = (8, 56, 56, 64, 256, 1, 1, 1, 0)
+SHAPES["l1_3x3_64_k8"] = (8, 56, 56, 64, 64, 3, 3, 1, 1)
+SHAPES["l3_3x3_256_k8"] = (8, 14, 14, 256, 256, 3, 3, 1, 1)
+SHAPES["l3_1x1_1024_256_k8"] = (8, 14, 14, 1024, 256, 1, 1, 1, 0)
+SHAPES["l4_3x3_512_k8"] = (8, 7, 7, 512, 512, 3, 3, 1, 1)
 
 SHAPES["l1_3x3_k1"] = (1, 56, 56, 64, 64, 3, 3, 1, 1)
 SHAPES["l3_3x3_k1"] = (1, 14, 14, 256, 256, 3, 3, 1, 1)
