@@ -187,6 +187,7 @@ GX_API int gx_scatter(gx_ctx* ctx, int k, const void* src, int32_t src_dtype, in
  * when its CUDA event fires.                                                                */
 #define GX_CLOCK_VIRTUAL 0
 #define GX_CLOCK_WALL 1
+#define GX_CLOCK_REPLAY 2 /* virtual clock + every batch really executed (numerics parity mode) */
 
 typedef struct gx_serve_stage {
   int32_t batch, instances;
@@ -251,6 +252,10 @@ GX_API int gx_serve_requests(gx_serve* s, int32_t* client, double* gen_ms, doubl
 GX_API int gx_serve_count_dispatch(gx_serve* s, int64_t* n_batches, int64_t* n_items);
 GX_API int gx_serve_dispatch(gx_serve* s, double* t_ms, int32_t* stage, int32_t* k, int64_t* seqs);
 GX_API int gx_serve_stats(gx_serve* s, double* wall_ms, int64_t* batches, int64_t* kernels);
+/* Per-request outputs (WALL / REPLAY): row i = request i's final-stage output (logits, fp32,
+ * `elems` values; NaN for requests that did not complete).  Rows are valid while no more than
+ * max_inflight requests completed (results are a ring of max_inflight rows). */
+GX_API int gx_serve_outputs(gx_serve* s, float* out, int64_t n_requests, int64_t elems);
 GX_API int gx_serve_destroy(gx_serve* s);
 
 #ifdef __cplusplus

@@ -20,7 +20,7 @@ GX_BF16, GX_F32 = 0, 1
 (GX_OP_CONV, GX_OP_MAXPOOL, GX_OP_AVGPOOL, GX_OP_GAP, GX_OP_FC, GX_OP_LINEAR, GX_OP_LAYERNORM,
  GX_OP_ATTENTION, GX_OP_EMBED, GX_OP_COPY, GX_OP_FLATTEN_NCHW) = range(1, 12)
 GX_ACT_NONE, GX_ACT_RELU, GX_ACT_GELU = 0, 1, 2
-GX_CLOCK_VIRTUAL, GX_CLOCK_WALL = 0, 1
+GX_CLOCK_VIRTUAL, GX_CLOCK_WALL, GX_CLOCK_REPLAY = 0, 1, 2
 
 
 class GxTensor(C.Structure):
@@ -122,6 +122,7 @@ def lib():
         "gx_serve_dispatch": (i32, [vp, P(dbl), P(i32), P(i32), P(i64)]),
         "gx_serve_stats": (i32, [vp, P(dbl), P(i64), P(i64)]),
         "gx_serve_destroy": (i32, [vp]),
+        "gx_serve_outputs": (i32, [vp, P(C.c_float), i64, i64]),
     }
     for name, (res, args) in sig.items():
         if not hasattr(L, name):

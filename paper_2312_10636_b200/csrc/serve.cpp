@@ -6,7 +6,10 @@
 // push order (so request seqs match _Request.seq), the same float arithmetic; a batch completes at
 // dispatch time + the stage's latency table entry for k.  GX_CLOCK_WALL runs the same state machine
 // against the wall clock: every dispatched batch executes on the GPU (gx_stage_run on a free
-// instance's stream) and completes when its CUDA event fires.
+// instance's stream) and completes when its CUDA event fires.  GX_CLOCK_REPLAY keeps the virtual
+// clock (so dispatch order and batch composition are the reference's, bit for bit) and also
+// executes every dispatched batch on the GPU, synchronously, with the real per-request
+// activations flowing align -> shared through the ragged gather: the numerics-parity mode.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -56,6 +59,7 @@ struct Req {
   int cur_dtype = GX_F32;
   int cur_channels = 0;
   int slot = -1;
+  int64_t result_idx = -1;  // row of `results` holding the request's output (final stage)
 };
 
 struct Batch {
@@ -143,6 +147,7 @@ struct gx_serve {
   size_t max_inflight_seen = 0;
   std::chrono::steady_clock::time_point t0;
 
+  bool gpu() const { return cfg.clock != GX_CLOCK_VIRTUAL; }
   void push(double t, int rank, int64_t a, int64_t b = 0) {
     ++seq;
     heap.push(Ev{t, rank, seq, a, b});
@@ -221,7 +226,7 @@ int gx_serve::arrive(int ri, double now) {
   }
   const Route& rt = routes[r.route];
   if (rt.n_stages == 0) return complete(ri, now);
-  if (cfg.clock == GX_CLOCK_WALL) {
+  if (gpu()) {
     r.cur = rt.ingress;
     r.cur_dtype = rt.ingress_dtype;
     r.cur_channels = rt.ingress_channels;
@@ -279,7 +284,8 @@ int gx_serve::dispatch_gpu(int si, int bi) {
     sdt[i] = r.cur_dtype;
     channels = std::max(channels, r.cur_channels);
     if (st.out_final) {
-      dst[i] = static_cast<uint8_t*>(results) + (result_cursor % cfg.max_inflight) * result_elems * 4;
+      r.result_idx = result_cursor % cfg.max_inflight;
+      dst[i] = static_cast<uint8_t*>(results) + r.result_idx * result_elems * 4;
       ++result_cursor;
     } else {
       dst[i] = static_cast<uint8_t*>(slots) + static_cast<size_t>(r.slot) * cfg.slot_bytes;
@@ -335,7 +341,7 @@ int gx_serve::service(int si, double now) {
     } else {
       batches.emplace_back();
       bi = static_cast<int>(batches.size()) - 1;
-      if (cfg.clock == GX_CLOCK_WALL) GX_CUDA(cudaEventCreateWithFlags(&batches[bi].ev, cudaEventDisableTiming));
+      if (gpu()) GX_CUDA(cudaEventCreateWithFlags(&batches[bi].ev, cudaEventDisableTiming));
     }
     Batch& b = batches[bi];
     b.stage = si;
@@ -353,6 +359,15 @@ int gx_serve::service(int si, double now) {
       for (int ri : b.reqs) d_seqs.push_back(reqs[ri].seq);
     }
     if (cfg.clock == GX_CLOCK_VIRTUAL) {
+      push(now + st.lat[k], R_DONE, bi);
+    } else if (cfg.clock == GX_CLOCK_REPLAY) {
+      // execute now and finish before anything else is dispatched (the next stage's gather reads
+      // this batch's outputs); completion stays on the virtual clock
+      int rc = dispatch_gpu(si, bi);
+      if (rc != GX_OK) return rc;
+      GX_CUDA(cudaStreamSynchronize(pool[b.lane]));
+      inflight.pop_back();
+      pool_n[b.lane] -= 1;
       push(now + st.lat[k], R_DONE, bi);
     } else {
       const double t_a = now_wall();
@@ -378,8 +393,8 @@ int gx_serve::stage_done(int bi, double now) {
   Batch& b = batches[bi];
   Stage& st = stages[b.stage];
   st.free += 1;
+  if (gpu()) st.busy[b.inst] = 0;
   if (cfg.clock == GX_CLOCK_WALL) {
-    st.busy[b.inst] = 0;
     st.obs_ms += now - b.t_disp;
     if (b.reqs.size() < st.lat.size()) st.plan_ms += st.lat[b.reqs.size()];
     st.obs_n += 1;
@@ -419,7 +434,7 @@ int gx_serve::run() {
   }
   t0 = std::chrono::steady_clock::now();
   int rc = GX_OK;
-  if (cfg.clock == GX_CLOCK_VIRTUAL) {
+  if (cfg.clock != GX_CLOCK_WALL) {
     while (!heap.empty() && heap.top().t <= horizon + kEps && rc == GX_OK) {
       Ev e = heap.top();
       heap.pop();
@@ -552,7 +567,11 @@ int gx_serve_create(gx_ctx* ctx, int n_stages, const gx_serve_stage* st, int n_r
       return fail(GX_EINVAL, "stage needs batch >= 1 and instances >= 1");
     }
     if (st[i].lat_ms) x.lat.assign(st[i].lat_ms, st[i].lat_ms + x.batch + 1);
-    if (cfg->clock == GX_CLOCK_WALL) {
+    if (cfg->clock == GX_CLOCK_REPLAY && x.lat.empty()) {
+      delete s;
+      return fail(GX_EINVAL, "replay clock needs a latency table per stage");
+    }
+    if (cfg->clock != GX_CLOCK_VIRTUAL) {
       if (!st[i].inst) {
         delete s;
         return fail(GX_EINVAL, "wall clock needs executor instances per stage");
@@ -602,7 +621,7 @@ int gx_serve_create(gx_ctx* ctx, int n_stages, const gx_serve_stage* st, int n_r
     }
     s->clients.push_back(std::move(c));
   }
-  if (cfg->clock == GX_CLOCK_WALL) {
+  if (cfg->clock != GX_CLOCK_VIRTUAL) {
     cudaError_t e = cudaSetDevice(ctx->device);
     if (e == cudaSuccess && cfg->max_inflight > 0 && cfg->slot_bytes > 0)
       e = cudaMalloc(&s->slots, static_cast<size_t>(cfg->slot_bytes) * cfg->max_inflight);
@@ -641,7 +660,7 @@ int gx_serve_create(gx_ctx* ctx, int n_stages, const gx_serve_stage* st, int n_r
 
 int gx_serve_run(gx_serve* s) {
   if (!s) return fail(GX_EINVAL, "null arg");
-  if (s->cfg.clock == GX_CLOCK_WALL) GX_CUDA(cudaSetDevice(s->ctx->device));
+  if (s->gpu()) GX_CUDA(cudaSetDevice(s->ctx->device));
   return s->run();
 }
 
@@ -689,9 +708,31 @@ int gx_serve_stats(gx_serve* s, double* wall_ms, int64_t* batches, int64_t* kern
   return GX_OK;
 }
 
+int gx_serve_outputs(gx_serve* s, float* out, int64_t n_requests, int64_t elems) {
+  if (!s || !out) return fail(GX_EINVAL, "null arg");
+  if (!s->gpu()) return fail(GX_EINVAL, "outputs exist only when batches execute on the GPU");
+  if (elems != s->result_elems) return fail(GX_EINVAL, "output row size mismatch");
+  if (n_requests < static_cast<int64_t>(s->reqs.size())) return fail(GX_EINVAL, "output array too small");
+  if (s->result_cursor > s->cfg.max_inflight)
+    return fail(GX_EINVAL, "outputs were overwritten (more completions than max_inflight result rows)");
+  GX_CUDA(cudaSetDevice(s->ctx->device));
+  GX_CUDA(cudaDeviceSynchronize());
+  for (size_t i = 0; i < s->reqs.size(); ++i) {
+    const Req& r = s->reqs[i];
+    float* dst = out + static_cast<int64_t>(i) * elems;
+    if (r.status != 0 || r.result_idx < 0) {
+      for (int64_t j = 0; j < elems; ++j) dst[j] = NAN;
+      continue;
+    }
+    const uint8_t* src = static_cast<const uint8_t*>(s->results) + r.result_idx * elems * 4;
+    GX_CUDA(cudaMemcpy(dst, src, elems * 4, cudaMemcpyDefault));
+  }
+  return GX_OK;
+}
+
 int gx_serve_destroy(gx_serve* s) {
   if (!s) return GX_OK;
-  if (s->cfg.clock == GX_CLOCK_WALL) {
+  if (s->gpu()) {
     cudaSetDevice(s->ctx->device);
     cudaDeviceSynchronize();
     for (auto& b : s->batches)

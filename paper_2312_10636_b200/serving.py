@@ -11,6 +11,9 @@ same report schema (SimReport, simulator.py:121-183).  Two clocks:
   * wall    — every dispatched batch really executes on the B200 (gather -> span kernels ->
     scatter on a free instance's stream, SM-bounded by the stage's share) and completes when its
     CUDA event fires.  This is the measurement mode for SLO-met requests/sec.
+  * replay  — the virtual clock's dispatch decisions (bit-identical to the reference) with every
+    batch also executed on the B200 and the real activations flowing align -> shared; per-request
+    outputs come back for numerics parity against the fp32 oracle.
 """
 from __future__ import annotations
 
@@ -80,6 +83,7 @@ class ServeReport:
     requests: list[tuple]
     config: dict = field(default_factory=dict)
     dispatch: list[tuple] | None = None  # (t_ms, stage index, k, (request seqs...))
+    outputs: np.ndarray | None = None  # replay / wall with return_outputs: [request, out elems]
     wall_ms: float = 0.0
     batches: int = 0
     kernels: int = 0
@@ -150,17 +154,20 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
           latency=None, instances=None, ctx=None, poisson: bool = False, seed: int = 0,
           record_dispatch: bool = False, ingress=None, ingress_from_host: bool = False,
           egress_to_host: bool = False, slot_bytes: int = 0, max_inflight: int = 4096,
-          planner: str | None = None, plan_latency=None) -> ServeReport:
+          planner: str | None = None, plan_latency=None, return_outputs: bool = False) -> ServeReport:
     """Run one plan for one horizon.
 
     latency: callable (StageSpec, k) -> ms for the virtual clock (None -> wall clock).
-    instances: per stage index, a list of `StageInstance` (wall clock).
-    ingress: route point -> (pointer, bytes, channels) of the fp32 entry activation template.
+    instances: per stage index, a list of `StageInstance` (wall clock; with `latency` too: replay).
+    ingress: route point (or client id, which wins) -> (pointer, bytes, channels) of the fp32
+    entry activation template.
     plan_latency: optional (StageSpec, k) -> ms the plan assumed; on the wall clock it is only
     compared with the observed batch times in the GX_SERVE_DEBUG summary.
     """
     keep = _Keep()
     wall = latency is None
+    replay = latency is not None and instances is not None
+    gpu = wall or replay
     ids = sorted(c.client_id for c in clients)
     by_id = {c.client_id: c for c in clients}
     st_arr = (N.GxServeStage * max(1, len(deployment.stages)))()
@@ -171,7 +178,7 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
         if lat_fn is not None:
             lat = (C.c_double * (s.batch + 1))(0.0, *[float(lat_fn(s, k)) for k in range(1, s.batch + 1)])
             st_arr[i].lat_ms = keep(lat)
-        if wall:
+        if gpu:
             insts = instances[i]
             if len(insts) != s.instances:
                 raise ValidationError(f"stage {s.stage_id}: {len(insts)} executor instances for {s.instances}")
@@ -195,7 +202,7 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
             rt.payload_bytes = c.payload_bytes[r.point]
             rt.ingress_dtype = N.GX_F32
             if ingress is not None:
-                ptr, nbytes, channels = ingress[r.point]
+                ptr, nbytes, channels = ingress[cid] if cid in ingress else ingress[r.point]
                 rt.ingress, rt.ingress_bytes, rt.ingress_channels = ptr, nbytes, channels
             route_docs.append(rt)
             ridx = len(route_docs) - 1
@@ -215,7 +222,7 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
     cfg = N.GxServeCfg()
     cfg.horizon_ms = horizon_s * 1000.0
     cfg.epoch_ms = epoch_s * 1000.0
-    cfg.clock = N.GX_CLOCK_WALL if wall else N.GX_CLOCK_VIRTUAL
+    cfg.clock = N.GX_CLOCK_WALL if wall else N.GX_CLOCK_REPLAY if replay else N.GX_CLOCK_VIRTUAL
     cfg.record_dispatch = 1 if record_dispatch else 0
     # True / "zero_copy": the gather reads pinned host memory over PCIe; "dma": copy at arrival
     cfg.ingress_from_host = {False: 0, True: 1, "zero_copy": 1, "dma": 2}[ingress_from_host]
@@ -225,9 +232,9 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
     L = N.lib()
     h = C.c_void_p()
     ctx_handle = ctx.handle if ctx is not None else C.c_void_p(0)
-    if wall and ctx is None:
-        raise ValidationError("wall-clock serving needs an executor context")
-    if not wall and ctx is None:
+    if gpu and ctx is None:
+        raise ValidationError("executing batches needs an executor context")
+    if not gpu and ctx is None:
         ctx_handle = C.c_void_p(1)  # virtual clock never touches the device; any non-null handle
     N.check(L.gx_serve_create(ctx_handle, len(deployment.stages), st_arr, len(route_docs), rt_arr, len(ids), cl_arr,
                               C.byref(cfg), C.byref(h)), "gx_serve_create")
@@ -248,6 +255,14 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
         nb = C.c_int64()
         nk = C.c_int64()
         N.check(L.gx_serve_stats(h, C.byref(wall_ms), C.byref(nb), C.byref(nk)))
+        outputs = None
+        if return_outputs and gpu:
+            final = [x for x in (instances or []) if x and x[0].final]
+            elems = final[0][0].out_elems if final else 0
+            outputs = np.zeros((max(1, n), max(1, elems)), np.float32)
+            if elems:
+                N.check(L.gx_serve_outputs(h, outputs.ctypes.data_as(C.POINTER(C.c_float)), outputs.shape[0], elems),
+                        "gx_serve_outputs")
         dispatch = None
         if record_dispatch:
             nbat = C.c_int64()
@@ -266,9 +281,10 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
     finally:
         L.gx_serve_destroy(h)
     rep = _report(planner or deployment.planner, horizon_s, ids, cl, gen, done, dl, status,
-                  {"clock": "wall" if wall else "virtual", "horizon_s": horizon_s, "poisson": poisson, "seed": seed,
-                   "clients": len(ids)})
+                  {"clock": "wall" if wall else "replay" if replay else "virtual", "horizon_s": horizon_s,
+                   "poisson": poisson, "seed": seed, "clients": len(ids)})
     rep.dispatch = dispatch
+    rep.outputs = outputs
     rep.wall_ms, rep.batches, rep.kernels = float(wall_ms.value), int(nb.value), int(nk.value)
     return rep
 

@@ -138,7 +138,42 @@ def closed_form_cases():
         run_case(name, sc, cost, "realign", SimConfig(horizon_s=hz), plan=plan(budget, batch, inst), fragments=frags)
 
 
+def resnet18_case():
+    """BASELINE.json configs[0]: ResNet-18 fragments at 3 partition points, plan from the reference
+    CPU planner.  One client per cut p in {2, 4, 6}; each client's device is cheap up to its cut and
+    prohibitively slow after it, so the reference's own partition_client (workload.py:145-176) picks
+    exactly that cut.  Server latency: the reference's SyntheticCostModel over the unit chain's
+    GFLOP weights, with a large per-batch fixed cost (c0) and a small per-request one (c1), at
+    300 rps per client: re-alignment pays and plan_realigned (planners.py:81-100) builds ONE level
+    at point 6 with alignment stages [2, 6) and [4, 6) feeding a shared [6, 10) suffix, i.e. the
+    align -> shared ragged gather the executor must get right.  The golden drives the GPU replay
+    test (tests/test_replay_gpu.py)."""
+    from fragserve.workload import partition_client
+
+    from paper_2312_10636_b200.models import build_chain
+
+    chain = build_chain("resnet18")
+    doc = chain.model_spec_doc()
+    spec = ModelSpec(doc["model_id"], doc["input_bytes"],
+                     tuple(LayerSpec(l["compute_weight"], l["output_bytes"]) for l in doc["layers"]))
+    cost = SyntheticCostModel({spec.model_id: spec}, c0=2.0, c1=0.05, kappa=0.9, batch_max=8)
+    n = spec.layer_count
+    clients = []
+    for j, p in enumerate((2, 4, 6)):
+        cum = [0.0]
+        for u in range(n):
+            cum.append(cum[-1] + (0.2 if u < p else 500.0))
+        dev = DeviceProfile(f"dev{j}", {spec.model_id: tuple(cum)})
+        c = ClientSpec(f"c{j}", dev, spec, 300.0, 100.0, BandwidthTrace((0.0,), (2000.0 + 100.0 * j,)))
+        frag = partition_client(c, 2000.0 + 100.0 * j, cost)
+        assert frag is not None and frag.start_layer == p, (j, p, frag)
+        clients.append(c)
+    sc = Scenario(tuple(clients), 1, 10.0, {spec.model_id: spec})
+    run_case("resnet18_3cuts_realign", sc, cost, "realign", SimConfig(horizon_s=0.15))
+
+
 def main():
+    resnet18_case()
     closed_form_cases()
     scen = REF / "scenarios"
     sc, cost = load_scenario(scen / "slo-guarantee" / "scenario.json")
