@@ -231,23 +231,23 @@ __global__ void gap_kernel(const __nv_bfloat16* __restrict__ x, int N, int HW, i
 constexpr int kFcWarps = 8;
 constexpr int kFcRows = 16;
 constexpr int kFcKChunk = 2048;
-template <int OPW>
+template <int OPW, int ROWS>
 __global__ void __launch_bounds__(256, 2) fc_kernel(const __nv_bfloat16* __restrict__ x, int N, int K,
                                                  const __nv_bfloat16* __restrict__ w, const float* __restrict__ b,
                                                  void* __restrict__ y, int Nout, int y_f32, int act) {
-  extern __shared__ uint4 xs[];  // [kFcRows][kFcKChunk / 8]
+  extern __shared__ uint4 xs[];  // [ROWS][kFcKChunk / 8]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int groups = (Nout + kFcWarps * OPW - 1) / (kFcWarps * OPW);
   int64_t staged = -1;
   for (int g = blockIdx.x; g < groups; g += gridDim.x) {
     const int o0 = (g * kFcWarps + warp) * OPW;
-    for (int n0 = 0; n0 < N; n0 += kFcRows) {
-      const int rows = min(kFcRows, N - n0);
-      float acc[OPW][kFcRows];
+    for (int n0 = 0; n0 < N; n0 += ROWS) {
+      const int rows = min(ROWS, N - n0);
+      float acc[OPW][ROWS];
 #pragma unroll
       for (int a = 0; a < OPW; ++a)
 #pragma unroll
-        for (int r = 0; r < kFcRows; ++r) acc[a][r] = 0.0f;
+        for (int r = 0; r < ROWS; ++r) acc[a][r] = 0.0f;
       for (int k0 = 0; k0 < K; k0 += kFcKChunk) {
         const int kc = min(kFcKChunk, K - k0) / 8;  // 16-byte vectors in this chunk
         const int64_t key = static_cast<int64_t>(n0) * K + k0;
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(256, 2) fc_kernel(const __nv_bfloat16* __restr
               }
             }
 #pragma unroll
-            for (int r = 0; r < kFcRows; ++r) {
+            for (int r = 0; r < ROWS; ++r) {
               if (r < rows) {
                 const uint4 xv = xs[r * (kFcKChunk / 8) + v];
                 const uint32_t xx[4] = {xv.x, xv.y, xv.z, xv.w};
@@ -309,14 +309,32 @@ __global__ void __launch_bounds__(256, 2) fc_kernel(const __nv_bfloat16* __restr
           }
         }
       }
+      // warm L2 with the next group's weight rows while this group reduces and stores
+      {
+        const int gn = g + gridDim.x;
+        if (gn < groups && n0 + ROWS >= N) {
+#pragma unroll
+          for (int a = 0; a < OPW; ++a) {
+            const int on = (gn * kFcWarps + warp) * OPW + a;
+            if (on < Nout) {
+              const char* rowp = reinterpret_cast<const char*>(w + static_cast<int64_t>(on) * K);
+              for (int64_t off = static_cast<int64_t>(lane) * 128; off < static_cast<int64_t>(K) * 2; off += 32 * 128)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(rowp + off));
+            }
+          }
+        }
+      }
+      // butterfly-reduce the rows this pass holds (ROWS = batch rounded up to a power of two)
 #pragma unroll
       for (int a = 0; a < OPW; ++a)
 #pragma unroll
-        for (int r = 0; r < kFcRows; ++r) {
-          float v = acc[a][r];
+        for (int r = 0; r < ROWS; ++r) {
+          if (r < rows) {
+            float v = acc[a][r];
 #pragma unroll
-          for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-          acc[a][r] = v;
+            for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+            acc[a][r] = v;
+          }
         }
       // lane r writes row r (r < 16) for each of the warp's outputs
 #pragma unroll
@@ -324,7 +342,7 @@ __global__ void __launch_bounds__(256, 2) fc_kernel(const __nv_bfloat16* __restr
         const int o = o0 + a;
         float mine = 0.0f;
 #pragma unroll
-        for (int r = 0; r < kFcRows; ++r)
+        for (int r = 0; r < ROWS; ++r)
           if (lane == r) mine = acc[a][r];
         if (o < Nout && lane < rows) {
           float v = mine + (b ? b[o] : 0.0f);
@@ -415,24 +433,42 @@ cudaError_t launch_gap(const __nv_bfloat16* x, int N, int HW, int C, __nv_bfloat
 cudaError_t launch_fc(const __nv_bfloat16* x, int N, int K, const __nv_bfloat16* w, const float* b, void* y, int Nout,
                       int y_f32, int act, int grid, cudaStream_t s) {
   if (K & 7) return cudaErrorInvalidValue;
-  const size_t smem = static_cast<size_t>(kFcRows) * kFcKChunk * 2;
+  // rows per accumulator pass = the batch rounded up to a power of two (<= 16): the unrolled
+  // per-row FMA / reduction work matches k instead of a fixed 16-row capacity
+  const int rows = N >= 16 ? 16 : N > 4 ? 8 : N > 2 ? 4 : N;
+  const size_t smem = static_cast<size_t>(rows) * kFcKChunk * 2;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(fc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    cudaFuncSetAttribute(fc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    cudaFuncSetAttribute(fc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    const int mx = static_cast<int>(static_cast<size_t>(kFcRows) * kFcKChunk * 2);
+#define GX_FC_ATTR(O, R) cudaFuncSetAttribute(fc_kernel<O, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    GX_FC_ATTR(1, 1) GX_FC_ATTR(1, 2) GX_FC_ATTR(1, 4) GX_FC_ATTR(1, 8) GX_FC_ATTR(1, 16)
+    GX_FC_ATTR(2, 1) GX_FC_ATTR(2, 2) GX_FC_ATTR(2, 4) GX_FC_ATTR(2, 8) GX_FC_ATTR(2, 16)
+    GX_FC_ATTR(4, 1) GX_FC_ATTR(4, 2) GX_FC_ATTR(4, 4) GX_FC_ATTR(4, 8) GX_FC_ATTR(4, 16)
+#undef GX_FC_ATTR
     configured = true;
   }
   const int opw = Nout >= 4096 ? 4 : Nout >= 2048 ? 2 : 1;
   const int groups = (Nout + kFcWarps * opw - 1) / (kFcWarps * opw);
-  // up to 3 blocks (64 KB smem each) per SM of the budget: weight streaming needs many loads in flight
+  // up to 3 blocks per SM of the budget: weight streaming needs many loads in flight
   const int g = grid_for(groups, 1, grid / 8 > 0 ? 3 * (grid / 8) : 1);
-  if (opw == 4)
-    fc_kernel<4><<<g, 256, smem, s>>>(x, N, K, w, b, y, Nout, y_f32, act);
-  else if (opw == 2)
-    fc_kernel<2><<<g, 256, smem, s>>>(x, N, K, w, b, y, Nout, y_f32, act);
-  else
-    fc_kernel<1><<<g, 256, smem, s>>>(x, N, K, w, b, y, Nout, y_f32, act);
+#define GX_FC_LAUNCH(O, R) fc_kernel<O, R><<<g, 256, smem, s>>>(x, N, K, w, b, y, Nout, y_f32, act)
+#define GX_FC_ROWS(O)               \
+  switch (rows) {                   \
+    case 1: GX_FC_LAUNCH(O, 1); break; \
+    case 2: GX_FC_LAUNCH(O, 2); break; \
+    case 4: GX_FC_LAUNCH(O, 4); break; \
+    case 8: GX_FC_LAUNCH(O, 8); break; \
+    default: GX_FC_LAUNCH(O, 16); break; \
+  }
+  if (opw == 4) {
+    GX_FC_ROWS(4)
+  } else if (opw == 2) {
+    GX_FC_ROWS(2)
+  } else {
+    GX_FC_ROWS(1)
+  }
+#undef GX_FC_ROWS
+#undef GX_FC_LAUNCH
   return cudaGetLastError();
 }
 

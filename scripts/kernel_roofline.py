@@ -21,6 +21,12 @@ KIND = {1: "conv", 2: "maxpool", 3: "avgpool", 4: "gap", 5: "fc", 6: "linear", 7
         9: "embed", 10: "copy", 11: "flatten"}
 
 
+# one SM's measured L2->SM feed (bulk copies, 2x64 KB in flight, scripts/native/sm_feed_probe.cu,
+# profiles/r01_sm_feed_probe.log): the memory roofline of a kernel confined to a few SMs, whose
+# working set (weights, activations) is L2-resident; HBM caps it for large budgets
+SM_FEED_GBS = 166.3
+
+
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -77,7 +83,8 @@ def main():
             tf = o["flops"] / t / 1e12 if t > 0 else 0.0
             gb = o["bytes"] / t / 1e9 if t > 0 else 0.0
             t_tc = o["flops"] / (tc_peak * scale * 1e12)
-            t_hbm = o["bytes"] / (hbm_peak * scale * 1e9)
+            mem_peak = min(hbm_peak, SM_FEED_GBS * budget)
+            t_hbm = o["bytes"] / (mem_peak * 1e9)
             bound = "tensor" if t_tc >= t_hbm else "hbm"
             frac = max(t_tc, t_hbm) / t if t > 0 else 0.0
             frac_w += frac * o["ms"]
@@ -85,11 +92,11 @@ def main():
                          "op": first + o["op"], "kind": KIND.get(o["kind"], str(o["kind"])),
                          "shape": describe(chain, first + o["op"]), "us": round(o["ms"] * 1000, 2),
                          "gflop": round(o["flops"] / 1e9, 4), "mbytes": round(o["bytes"] / 1e6, 4),
-                         "tflops": round(tf, 2), "gbs": round(gb, 1), "bound": bound,
+                         "tflops": round(tf, 2), "gbs": round(gb, 1), "bound": "tensor" if t_tc >= t_hbm else "memory",
                          "roofline_us": round(max(t_tc, t_hbm) * 1e6, 2), "frac": round(frac, 3)})
         print(f"# span [{a},{b}) k={k} budget={budget} SMs: graph {whole * 1000:.1f} us, sum of ops "
               f"{tot_ms * 1000:.1f} us over {len(ops)} ops, time-weighted roofline frac "
-              f"{frac_w / max(tot_ms, 1e-12):.3f} (peaks {src}: {tc_peak} TF/s, {hbm_peak} GB/s x {budget}/{sms})",
+              f"{frac_w / max(tot_ms, 1e-12):.3f} (peaks {src}: {tc_peak} TF/s x {budget}/{sms}; memory min({hbm_peak}, {SM_FEED_GBS} x {budget}) GB/s)",
               flush=True)
         by_kind = {}
         for r in rows[-len(ops):]:
