@@ -1,7 +1,7 @@
 """Per-kernel roofline table: every op of a span launched alone (gx_stage_profile_ops) at batch k on
 an SM budget, its algorithmic FLOPs / bytes (FLOPs = 2*M*N*K unpadded; bytes = every
 logical input, weight, bias, residual and output byte once) against the measured peaks scaled by
-budget/SMs.  Writes a CSV and prints a summary per operating point.
+budget/SMs (tensor) and min(HBM, per-SM L2 feed x budget) (memory).  Writes a CSV and prints a summary per operating point.
 
   python scripts/kernel_roofline.py --model resnet50 --points 0:18:16:148,0:18:8:3,2:18:1:2 \
       --out profiles/r01_kernel_roofline.csv
@@ -85,7 +85,6 @@ def main():
             t_tc = o["flops"] / (tc_peak * scale * 1e12)
             mem_peak = min(hbm_peak, SM_FEED_GBS * budget)
             t_hbm = o["bytes"] / (mem_peak * 1e9)
-            bound = "tensor" if t_tc >= t_hbm else "hbm"
             frac = max(t_tc, t_hbm) / t if t > 0 else 0.0
             frac_w += frac * o["ms"]
             rows.append({"model": args.model, "start": a, "end": b, "k": k, "sm_budget": budget,
