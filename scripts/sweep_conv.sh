@@ -1,4 +1,3 @@
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:fc_kernel -c 1 -o /tmp/fc python scripts/ncu_stage.py resnet50 15 18 1 1 > /dev/null 2>&1
-ncu -i /tmp/fc.ncu-rep --page source --csv --print-source sass > gpurun_out/fc_source.csv 2>/dev/null
-ncu -i /tmp/fc.ncu-rep --page raw --csv > gpurun_out/fc_raw.csv 2>/dev/null
-ls -la gpurun_out
+for c in 896 1024; do for m in zero_copy dma; do
+timeout 300 python bench.py --clients $c --e2e-ingress $m --no-cpu-baseline --steps 4 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('$c $m', d['value'], d['p99_ms'], 'e2e', d['e2e']['value'], d['e2e']['p99_ms'])"
+done; done
