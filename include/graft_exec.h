@@ -218,6 +218,12 @@ typedef struct gx_serve_client { /* ClientSpec (workload.py:98-117), clients sor
   const double* trace_t_s;    /* BandwidthTrace (workload.py:30-43)                           */
   const double* trace_mbps;
   int64_t n_trace;
+  /* Plan transitions (churn, simulator.py:297-349): route of this client in epoch e is
+   * epoch_route[e] (-1: no route that epoch -> requests dropped at generation), switched at each
+   * epoch's REPLAN event; in-flight requests keep the stages of the route they were generated on
+   * (drain-old / start-new).  NULL / 0: `route` for every epoch. */
+  const int32_t* epoch_route;
+  int64_t n_epoch_route;
 } gx_serve_client;
 
 enum { GX_INGRESS_DEVICE = 0, GX_INGRESS_ZERO_COPY = 1, GX_INGRESS_DMA = 2 };

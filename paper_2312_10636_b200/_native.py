@@ -67,7 +67,7 @@ class GxServeClient(C.Structure):
     _fields_ = [("rate_rps", C.c_double), ("slo_ms", C.c_double), ("route", C.c_int32),
                 ("gen_gaps_ms", C.POINTER(C.c_double)), ("n_gaps", C.c_int64),
                 ("trace_t_s", C.POINTER(C.c_double)), ("trace_mbps", C.POINTER(C.c_double)),
-                ("n_trace", C.c_int64)]
+                ("n_trace", C.c_int64), ("epoch_route", C.POINTER(C.c_int32)), ("n_epoch_route", C.c_int64)]
 
 
 class GxServeCfg(C.Structure):

@@ -91,6 +91,7 @@ struct Client {
   std::vector<double> gaps;  // pre-drawn inter-arrival gaps (Poisson); empty = deterministic
   size_t gap_idx = 0;
   std::vector<double> tr_t, tr_mbps;  // bandwidth trace (piecewise constant, workload.py:46-52)
+  std::vector<int> epoch_route;       // per-epoch route (plan transitions); empty = `route` always
 };
 
 struct Route {
@@ -116,6 +117,7 @@ struct gx_serve {
   std::vector<Req> reqs;
   std::priority_queue<Ev, std::vector<Ev>, std::greater<Ev>> heap;
   int64_t seq = 0;
+  int cur_epoch = 0;  // advanced by REPLAN events (simulator.py:457-458 -> _plan_epoch)
   // dispatch log
   std::vector<double> d_t;
   std::vector<int32_t> d_stage, d_k;
@@ -200,14 +202,16 @@ int gx_serve::gen_request(int cid, double now) {
   r.slo = c.slo;
   r.deadline = now + c.slo;
   r.worst_rem = 0.0;
-  r.route = c.route;
+  // self.routes.get(client_id) of the current epoch (simulator.py:360-365)
+  r.route = c.epoch_route.empty() ? c.route
+                                  : c.epoch_route[std::min<size_t>(static_cast<size_t>(cur_epoch), c.epoch_route.size() - 1)];
   reqs.push_back(r);
   const int ri = static_cast<int>(reqs.size()) - 1;
-  if (c.route < 0) {
+  if (reqs[ri].route < 0) {
     reqs[ri].status = 1;
     return GX_OK;
   }
-  const Route& rt = routes[c.route];
+  const Route& rt = routes[reqs[ri].route];
   const double bw = bandwidth_at(c, now / 1000.0);
   // transfer_ms (workload.py:141-142), same operation order
   const double xfer = static_cast<double>(rt.payload_bytes) * 8.0 / (bw * 1e6) * 1000.0;
@@ -440,6 +444,7 @@ int gx_serve::run() {
       heap.pop();
       switch (e.rank) {
         case R_REPLAN:
+          cur_epoch = static_cast<int>(e.a);
           break;
         case R_GEN: {
           rc = gen_request(static_cast<int>(e.a), e.t);
@@ -500,6 +505,7 @@ int gx_serve::run() {
         // events fire at their scheduled time (the clock has passed it); state uses that time
         switch (e.rank) {
           case R_REPLAN:
+            cur_epoch = static_cast<int>(e.a);
             break;
           case R_GEN: {
             rc = gen_request(static_cast<int>(e.a), e.t);
@@ -614,6 +620,14 @@ int gx_serve_create(gx_ctx* ctx, int n_stages, const gx_serve_stage* st, int n_r
       return fail(GX_EINVAL, "client needs a bandwidth trace");
     }
     c.tr_t.assign(cl[i].trace_t_s, cl[i].trace_t_s + cl[i].n_trace);
+    if (cl[i].epoch_route && cl[i].n_epoch_route > 0) {
+      c.epoch_route.assign(cl[i].epoch_route, cl[i].epoch_route + cl[i].n_epoch_route);
+      for (int rix : c.epoch_route)
+        if (rix >= n_routes) {
+          delete s;
+          return fail(GX_EINVAL, "client references a bad epoch route");
+        }
+    }
     c.tr_mbps.assign(cl[i].trace_mbps, cl[i].trace_mbps + cl[i].n_trace);
     if (c.route >= n_routes) {
       delete s;

@@ -138,3 +138,23 @@ def load_plan_json(path) -> dict:
     if "groups" not in doc:
         raise ValidationError(f"{path}: not a plan document")
     return doc
+
+
+def deploy_epochs(epoch_docs) -> list:
+    """Plan transitions under churn (_Sim._plan_epoch, simulator.py:297-349): one entry per epoch,
+    each {"kind": "deploy", "plan": plan JSON, "fragments": [...]} (a new plan is deployed at that
+    epoch's REPLAN), {"kind": "keep"} (cut points unchanged: the previous plan stays) or
+    {"kind": "infeasible"} (no routes).  Returns the `epochs` list `serving.serve` takes; stages of
+    earlier deployments stay alive so in-flight requests drain on them."""
+    out = []
+    for e in epoch_docs:
+        kind = e["kind"]
+        if kind == "deploy":
+            out.append(deploy(e["plan"], e["fragments"]))
+        elif kind == "keep":
+            out.append(None)
+        elif kind == "infeasible":
+            out.append("infeasible")
+        else:
+            raise ValidationError(f"unknown epoch kind {kind!r}")
+    return out

@@ -154,7 +154,8 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
           latency=None, instances=None, ctx=None, poisson: bool = False, seed: int = 0,
           record_dispatch: bool = False, ingress=None, ingress_from_host: bool = False,
           egress_to_host: bool = False, slot_bytes: int = 0, max_inflight: int = 4096,
-          planner: str | None = None, plan_latency=None, return_outputs: bool = False) -> ServeReport:
+          planner: str | None = None, plan_latency=None, return_outputs: bool = False,
+          epochs: list | None = None) -> ServeReport:
     """Run one plan for one horizon.
 
     latency: callable (StageSpec, k) -> ms for the virtual clock (None -> wall clock).
@@ -163,6 +164,9 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
     entry activation template.
     plan_latency: optional (StageSpec, k) -> ms the plan assumed; on the wall clock it is only
     compared with the observed batch times in the GX_SERVE_DEBUG summary.
+    epochs: plan transitions under churn, one entry per epoch (Deployment / None = keep /
+    "infeasible"); `deployment` is then ignored and stage indices (latency, instances, the
+    dispatch log) run over the concatenated stages of the deployments in epoch order.
     """
     keep = _Keep()
     wall = latency is None
@@ -170,8 +174,31 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
     gpu = wall or replay
     ids = sorted(c.client_id for c in clients)
     by_id = {c.client_id: c for c in clients}
-    st_arr = (N.GxServeStage * max(1, len(deployment.stages)))()
-    for i, s in enumerate(deployment.stages):
+    # plan transitions (simulator.py:297-349): epochs[e] is the Deployment put in place at epoch
+    # e's REPLAN, None keeps the previous one, "infeasible" clears the routes (simulator.py:320-324).
+    # Stages of every deployment stay alive (in-flight requests drain on the stages they were
+    # routed to); they are numbered in deployment order, as the reference creates _StageRT objects.
+    if epochs is None:
+        epochs = [deployment]
+    deps, eff, cur = [], [], -1
+    for e, d in enumerate(epochs):
+        if d is None:
+            if e == 0:
+                raise ValidationError("epoch 0 needs a deployment")
+        elif isinstance(d, str):
+            if d != "infeasible":
+                raise ValidationError(f"bad epoch entry {d!r}")
+            cur = -1
+        else:
+            deps.append(d)
+            cur = len(deps) - 1
+        eff.append(cur)
+    stages, offset = [], []
+    for d in deps:
+        offset.append(len(stages))
+        stages.extend(d.stages)
+    st_arr = (N.GxServeStage * max(1, len(stages)))()
+    for i, s in enumerate(stages):
         st_arr[i].batch, st_arr[i].instances, st_arr[i].budget_ms = s.batch, s.instances, s.budget_ms
         st_arr[i].out_final = 0
         lat_fn = plan_latency if wall else latency
@@ -185,28 +212,37 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
             arr = (C.c_void_p * len(insts))(*[x.handle.value for x in insts])
             st_arr[i].inst = keep(arr)
             st_arr[i].out_final = 1 if insts[0].final else 0
-    # one native route per client (the reference keeps one _Route per client too)
+    # one native route per (deployment, client): the reference keeps one _Route per client per plan
     route_docs = []
-    cl_arr = (N.GxServeClient * max(1, len(ids)))()
-    for ci, cid in enumerate(ids):
-        c = by_id[cid]
-        r = deployment.routes.get(cid)
-        ridx = -1
-        if r is not None:
+    route_of = {}
+    for di, d in enumerate(deps):
+        for cid in ids:
+            c = by_id[cid]
+            r = d.routes.get(cid)
+            if r is None:
+                continue
             rt = N.GxServeRoute()
             rt.n_stages = len(r.stages)
             for j, si in enumerate(r.stages):
-                rt.stage[j] = si
+                rt.stage[j] = offset[di] + si
             rt.worst_rem_ms = r.worst_rem_ms
             rt.mobile_ms = c.mobile_ms[r.point]
             rt.payload_bytes = c.payload_bytes[r.point]
             rt.ingress_dtype = N.GX_F32
             if ingress is not None:
-                ptr, nbytes, channels = ingress[cid] if cid in ingress else ingress[r.point]
+                key = (cid, r.point) if (cid, r.point) in ingress else cid if cid in ingress else r.point
+                ptr, nbytes, channels = ingress[key]
                 rt.ingress, rt.ingress_bytes, rt.ingress_channels = ptr, nbytes, channels
             route_docs.append(rt)
-            ridx = len(route_docs) - 1
-        cl_arr[ci].rate_rps, cl_arr[ci].slo_ms, cl_arr[ci].route = c.rate_rps, c.slo_ms, ridx
+            route_of[(di, cid)] = len(route_docs) - 1
+    cl_arr = (N.GxServeClient * max(1, len(ids)))()
+    for ci, cid in enumerate(ids):
+        c = by_id[cid]
+        per_epoch = [route_of.get((d, cid), -1) if d >= 0 else -1 for d in eff]
+        cl_arr[ci].rate_rps, cl_arr[ci].slo_ms, cl_arr[ci].route = c.rate_rps, c.slo_ms, per_epoch[0]
+        if len(per_epoch) > 1:
+            er = keep((C.c_int32 * len(per_epoch))(*per_epoch))
+            cl_arr[ci].epoch_route, cl_arr[ci].n_epoch_route = er, len(per_epoch)
         if poisson:
             # the reference draws gaps lazily from default_rng((seed, i)) in client-id order
             # (simulator.py:240-242, 382-384); draw enough of the same stream up front
@@ -236,7 +272,7 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
         raise ValidationError("executing batches needs an executor context")
     if not gpu and ctx is None:
         ctx_handle = C.c_void_p(1)  # virtual clock never touches the device; any non-null handle
-    N.check(L.gx_serve_create(ctx_handle, len(deployment.stages), st_arr, len(route_docs), rt_arr, len(ids), cl_arr,
+    N.check(L.gx_serve_create(ctx_handle, len(stages), st_arr, len(route_docs), rt_arr, len(ids), cl_arr,
                               C.byref(cfg), C.byref(h)), "gx_serve_create")
     try:
         N.check(L.gx_serve_run(h), "gx_serve_run")
@@ -280,7 +316,7 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
                 off += kk[i]
     finally:
         L.gx_serve_destroy(h)
-    rep = _report(planner or deployment.planner, horizon_s, ids, cl, gen, done, dl, status,
+    rep = _report(planner or deps[0].planner, horizon_s, ids, cl, gen, done, dl, status,
                   {"clock": "wall" if wall else "replay" if replay else "virtual", "horizon_s": horizon_s,
                    "poisson": poisson, "seed": seed, "clients": len(ids)})
     rep.dispatch = dispatch

@@ -40,6 +40,7 @@ class RecordingSim(S._Sim):
         super().__init__(*a, **k)
         self.dispatch = []
         self.stage_objs = []
+        self.epoch_log = []
         self._merged = merged_fragments
 
     def _push(self, t, rank, payload):
@@ -52,11 +53,30 @@ class RecordingSim(S._Sim):
         self._now = now
         return super()._service(stage, now)
 
+    def _plan_epoch(self, epoch, t_s):
+        self._epoch_kind = "keep"
+        super()._plan_epoch(epoch, t_s)
+        if self._epoch_kind == "keep" and not self.routes:
+            self._epoch_kind = "infeasible"
+        self.epoch_log.append(self._epoch_deploy if self._epoch_kind == "deploy" else {"kind": self._epoch_kind})
+
     def _deploy(self, plan, fragments):
         # creation order of _StageRT objects == the executor's deployment stage order
         orig = S._StageRT
 
         objs = self.stage_objs
+        if self._merged is None and getattr(self, "remerge", False):
+            # the planner merged fragments (ids 'first+N'): resolve them by re-running the
+            # deterministic merge instead of the reference's KeyError
+            ids = {f.fragment_id for f in fragments}
+            if any(m not in ids for g in plan.groups for lv in g.levels for m in lv.shared.members):
+                fragments = merge_fragments(fragments, self.cfg.merge_cfg, self.cost, self.scenario.models,
+                                            cap=self.cfg.realign_cfg.instance_cap,
+                                            max_share=self.cfg.realign_cfg.max_share)
+        self._epoch_kind = "deploy"
+        first = len(objs)
+        self._epoch_deploy = {"kind": "deploy", "plan": plan_to_dict(plan),
+                              "fragments": [frag_doc(f) for f in fragments], "first_stage": first}
 
         class Tracked(orig):
             def __init__(self, st):
@@ -172,7 +192,77 @@ def resnet18_case():
     run_case("resnet18_3cuts_realign", sc, cost, "realign", SimConfig(horizon_s=0.15))
 
 
+def vgg16_churn_case():
+    """BASELINE.json configs[3rd]: VGG-16 fragment groups under network-trace-driven partition-point
+    churn.  Four clients on a steppy bandwidth trace (fast -> slow -> fast, one step per epoch):
+    the reference's partition_client moves their cuts each epoch, the simulator re-plans
+    (simulator.py:297-349) and deploys a new plan while in-flight requests drain on the old
+    stages (drain-old / start-new).  Recorded per epoch: the deployed plan (or keep /
+    infeasible), the merged fragments, every stage's latency table in deployment order, and the
+    simulator's request records and dispatch log.  Drives test_serving_cpu (virtual clock, bit-
+    exact) and tests/test_replay_gpu.py (every batch executed on the B200)."""
+    from fragserve.workload import partition_client
+
+    from paper_2312_10636_b200.models import build_chain
+
+    chain = build_chain("vgg16")
+    doc = chain.model_spec_doc()
+    spec = ModelSpec(doc["model_id"], doc["input_bytes"],
+                     tuple(LayerSpec(l["compute_weight"], l["output_bytes"]) for l in doc["layers"]))
+    cost = SyntheticCostModel({spec.model_id: spec}, c0=0.5, c1=0.1, kappa=0.9, batch_max=8)
+    # handset: the conv blocks run at ~1 ms/GFLOP, the three FC layers (0.4 GB of weights) are
+    # memory-bound and slow on the device -> at low bandwidth the argmin cut is after the conv
+    # blocks (p = 5, 100 KB payload), at high bandwidth everything is offloaded (p = 0)
+    cum = [0.0]
+    for u, l in enumerate(spec.layers):
+        cum.append(cum[-1] + (1.0 * l.compute_weight if u < 5 else 30.0))
+    clients = []
+    for j in range(4):
+        dev = DeviceProfile(f"phone{j}", {spec.model_id: tuple(cum)})
+        hi, lo = 4000.0 + 500.0 * j, 60.0 + 10.0 * j
+        trace = BandwidthTrace((0.0, 0.1, 0.2), (hi, lo, hi))
+        clients.append(ClientSpec(f"v{j}", dev, spec, 40.0, 110.0, trace))
+        p_hi = partition_client(clients[-1], hi, cost).start_layer
+        p_lo = partition_client(clients[-1], lo, cost).start_layer
+        assert p_hi != p_lo, (j, p_hi, p_lo)
+    sc = Scenario(tuple(clients), 1, 0.1, {spec.model_id: spec})
+    cfg = SimConfig(horizon_s=0.3)
+    sim = RecordingSim(sc, cost, "realign", cfg)
+    sim.remerge = True
+    rep = sim.run()
+    lat = []
+    for ep in sim.epoch_log:
+        if ep["kind"] != "deploy":
+            continue
+        for g in ep["plan"]["groups"]:
+            for lv in g["levels"]:
+                for st in list(lv["align"]) + [lv["shared"]]:
+                    if st["instances"]:
+                        lat.append([0.0] + [cost.latency(st["model"], st["span"][0], st["span"][1], k, st["share"])
+                                            for k in range(1, st["batch"] + 1)])
+    assert len(lat) == len(sim.stage_objs), (len(lat), len(sim.stage_objs))
+    out = {
+        "name": "vgg16_churn_realign", "reference": "fragserve " + fragserve.__version__,
+        "epochs": sim.epoch_log,
+        "clients": [ClientView.from_reference(c).to_doc() for c in sorted(sc.clients, key=lambda c: c.client_id)],
+        "latency_by_stage": lat,
+        "horizon_s": cfg.horizon_s, "epoch_s": sc.epoch_s, "poisson": cfg.poisson, "seed": cfg.seed,
+        "expected": {
+            "requests": [[c, g, d, dl, st] for c, g, d, dl, st in rep.requests],
+            "dispatch": sim.dispatch,
+            "summary": {"generated": rep.generated, "completed": rep.completed, "dropped": rep.dropped,
+                        "in_flight": rep.in_flight, "p99": rep.latency_p99_ms},
+        },
+    }
+    (OUT.parent / "churn").mkdir(parents=True, exist_ok=True)
+    (OUT.parent / "churn" / "vgg16_churn_realign.json").write_text(json.dumps(out, separators=(",", ":")) + "\n")
+    kinds = [e["kind"] for e in sim.epoch_log]
+    print(f"vgg16_churn_realign: epochs={kinds} generated={rep.generated} completed={rep.completed} "
+          f"dropped={rep.dropped} batches={len(sim.dispatch)} stages={len(sim.stage_objs)}")
+
+
 def main():
+    vgg16_churn_case()
     resnet18_case()
     closed_form_cases()
     scen = REF / "scenarios"

@@ -89,3 +89,60 @@ def test_replay_realigned_group_matches_reference_and_oracle():
         done += 1
     assert done == exp["summary"]["completed"] and done > 50
     del keep
+
+
+def test_replay_vgg16_churn_plan_transitions():
+    """VGG-16 under partition-point churn (golden: tests/golden/churn/vgg16_churn_realign.json):
+    the reference re-plans every epoch (cuts 0 -> 5 -> 0); the executor switches routes at each
+    REPLAN, keeps the earlier deployments' instances alive for draining, and executes every batch.
+    Records / dispatch bit-exact; each request's logits vs the fp32 forward of its client's image,
+    whichever cut it entered at."""
+    from oracle.units import nchw_to_nhwc, run_span, units_for
+    from paper_2312_10636_b200.device import context
+    from paper_2312_10636_b200.engine import DeviceModel, StageInstance
+    from paper_2312_10636_b200.models import build_chain, torch_model
+    from paper_2312_10636_b200.plan import deploy_epochs
+    from paper_2312_10636_b200.serving import ClientView, serve
+
+    doc = json.loads((GOLDEN / "churn" / "vgg16_churn_realign.json").read_text())
+    epochs = deploy_epochs(doc["epochs"])
+    deps = [e for e in epochs if e is not None and not isinstance(e, str)]
+    stages = [s for d in deps for s in d.stages]
+    table = {id(s): doc["latency_by_stage"][i] for i, s in enumerate(stages)}
+    clients = [ClientView.from_doc(c) for c in doc["clients"]]
+    m = torch_model("vgg16")
+    chain = build_chain("vgg16", module=m)
+    dm = DeviceModel(chain, 0)
+    ctx = context(0)
+    units = units_for("vgg16", m)
+    instances = [[StageInstance(dm, s.start, s.end, s.batch, ctx.sm_budget(s.share)) for _ in range(s.instances)]
+                 for s in stages]
+    ingress, expected, keep = {}, {}, []
+    for ci, c in enumerate(sorted(clients, key=lambda c: c.client_id)):
+        x = torch.randn(1, 3, 224, 224, generator=torch.Generator().manual_seed(300 + ci))
+        expected[c.client_id] = run_span(units, 0, chain.n_units, x)[0]
+        for p in sorted({d.routes[c.client_id].point for d in deps if c.client_id in d.routes}):
+            act = nchw_to_nhwc(run_span(units, 0, p, x))[0].contiguous().cuda()
+            keep.append(act)
+            ingress[(c.client_id, p)] = (act.data_ptr(), act.numel() * 4, chain.ingress_channels(p))
+    rep = serve(None, clients, doc["horizon_s"], epoch_s=doc["epoch_s"], latency=lambda st, k: table[id(st)][k],
+                instances=instances, ctx=ctx, ingress=ingress, record_dispatch=True, max_inflight=512,
+                slot_bytes=1 << 23, return_outputs=True, epochs=epochs)
+    torch.cuda.synchronize()
+    exp = doc["expected"]
+    assert [list(r) for r in rep.requests] == exp["requests"]
+    assert rep.dispatch == [(t, s, k, tuple(q)) for t, s, k, q in exp["dispatch"]]
+    done = 0
+    for i, (cid, _g, _d, _dl, status) in enumerate(rep.requests):
+        if status != "completed":
+            continue
+        ref = expected[cid]
+        got = torch.from_numpy(rep.outputs[i].copy())
+        rel = ((got - ref).norm() / ref.norm()).item()
+        assert rel < 2e-2, (i, cid, rel)
+        top2 = ref.topk(2).values
+        if (top2[0] - top2[1]) > 0.02 * (ref.max() - ref.min()):
+            assert int(got.argmax()) == int(ref.argmax()), (i, cid)
+        done += 1
+    assert done == exp["summary"]["completed"]
+    del keep

@@ -76,3 +76,23 @@ def test_inflight_at_horizon_csv_row():
     assert rep.in_flight == 1
     row = rep.requests_csv().splitlines()[1]
     assert row.startswith("c0,0.000000,,,") and row.endswith("inflight")
+
+
+def test_churn_plan_transitions_match_reference():
+    """VGG-16 under partition-point churn (BASELINE configs: network-trace-driven churn): three
+    epochs, each deploying a new reference plan at its REPLAN (cuts 0 -> 5 -> 0); requests in flight
+    drain on the stages they were routed to.  Records and dispatch log bit-exact."""
+    from paper_2312_10636_b200.plan import deploy_epochs
+
+    doc = json.loads((GOLDEN / "churn" / "vgg16_churn_realign.json").read_text())
+    epochs = deploy_epochs(doc["epochs"])
+    assert sum(1 for e in epochs if e is not None and not isinstance(e, str)) == 3
+    stages = [s for e in epochs if e is not None and not isinstance(e, str) for s in e.stages]
+    table = {id(s): doc["latency_by_stage"][i] for i, s in enumerate(stages)}
+    clients = [ClientView.from_doc(c) for c in doc["clients"]]
+    rep = serve(None, clients, doc["horizon_s"], epoch_s=doc["epoch_s"], latency=lambda st, k: table[id(st)][k],
+                record_dispatch=True, epochs=epochs)
+    exp = doc["expected"]
+    assert [list(r) for r in rep.requests] == exp["requests"]
+    assert rep.dispatch == [(t, s, k, tuple(q)) for t, s, k, q in exp["dispatch"]]
+    assert {s for _t, s, _k, _q in rep.dispatch} == {0, 1, 2}  # every epoch's stage served batches
