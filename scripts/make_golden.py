@@ -192,6 +192,54 @@ def resnet18_case():
     run_case("resnet18_3cuts_realign", sc, cost, "realign", SimConfig(horizon_s=0.15))
 
 
+def realign_model_case(name, model, cuts, horizon_s, seed_rate=300.0, slo=100.0):
+    """One client per cut of `cuts` (each client's device cheap up to its cut, prohibitively slow
+    after it, so the reference's partition_client picks exactly that cut); the reference's
+    SyntheticCostModel over the unit chain's GFLOP weights; the first (c0, c1, kappa) whose
+    plan_realigned output re-aligns (>= 1 alignment stage) is recorded.  Covers BASELINE configs
+    beyond ResNet: Inception-v3 (concat gather across Mixed blocks) and BERT-base (encoder
+    fragments split at layer boundaries)."""
+    from fragserve.planners import plan_realigned
+    from fragserve.workload import generate_epoch, partition_client
+
+    from paper_2312_10636_b200.models import build_chain
+
+    chain = build_chain(model)
+    doc = chain.model_spec_doc()
+    spec = ModelSpec(doc["model_id"], doc["input_bytes"],
+                     tuple(LayerSpec(l["compute_weight"], l["output_bytes"]) for l in doc["layers"]))
+    n = spec.layer_count
+    for c0, c1, kappa, rate in ((2.0, 0.05, 0.9, seed_rate), (1.0, 0.05, 0.9, seed_rate), (4.0, 0.05, 0.5, seed_rate),
+                                (2.0, 0.2, 0.9, seed_rate), (2.0, 0.05, 0.9, 2 * seed_rate),
+                                (1.0, 0.05, 0.5, 2 * seed_rate), (0.5, 0.02, 0.9, seed_rate)):
+        cost = SyntheticCostModel({spec.model_id: spec}, c0=c0, c1=c1, kappa=kappa, batch_max=8)
+        clients = []
+        for j, p in enumerate(cuts):
+            cum = [0.0]
+            for u in range(n):
+                cum.append(cum[-1] + (0.2 if u < p else 500.0))
+            dev = DeviceProfile(f"dev{j}", {spec.model_id: tuple(cum)})
+            c = ClientSpec(f"c{j}", dev, spec, rate, slo, BandwidthTrace((0.0,), (4000.0 + 100.0 * j,)))
+            frag = partition_client(c, 4000.0 + 100.0 * j, cost)
+            if frag is None or frag.start_layer != p:
+                break
+            clients.append(c)
+        if len(clients) != len(cuts):
+            continue
+        try:
+            plan = plan_realigned(list(generate_epoch(clients, 0.0, cost).fragments), {spec.model_id: spec}, cost,
+                                  gpus=1, capacity=99)
+        except fragserve.InfeasibleError:
+            continue
+        if not any(not a.is_null for g in plan.groups for lv in g.levels for a in lv.align):
+            continue
+        sc = Scenario(tuple(clients), 1, 10.0, {spec.model_id: spec})
+        print(f"{name}: c0={c0} c1={c1} kappa={kappa} rate={rate}")
+        run_case(name, sc, cost, "realign", SimConfig(horizon_s=horizon_s))
+        return
+    raise SystemExit(f"{name}: no parameter set re-aligns")
+
+
 def vgg16_churn_case():
     """BASELINE.json configs[3rd]: VGG-16 fragment groups under network-trace-driven partition-point
     churn.  Four clients on a steppy bandwidth trace (fast -> slow -> fast, one step per epoch):
@@ -262,6 +310,8 @@ def vgg16_churn_case():
 
 
 def main():
+    realign_model_case("inception_v3_3cuts_realign", "inception_v3", (7, 10, 15), 0.1)
+    realign_model_case("bert_base_3cuts_realign", "bert_base", (3, 6, 9), 0.1)
     vgg16_churn_case()
     resnet18_case()
     closed_form_cases()

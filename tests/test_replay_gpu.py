@@ -26,7 +26,15 @@ from conftest import GOLDEN
 pytestmark = pytest.mark.gpu
 
 
-def _setup():
+CASES = {  # golden -> (model, client input shape): BASELINE configs[0], configs[3] (Inception, concat
+    # gather across Mixed blocks), configs[4] (BERT-base encoder fragments at layer boundaries)
+    "resnet18_3cuts_realign": ("resnet18", (3, 224, 224)),
+    "inception_v3_3cuts_realign": ("inception_v3", (3, 299, 299)),
+    "bert_base_3cuts_realign": ("bert_base", (128, 768)),
+}
+
+
+def _setup(case):
     from oracle.units import nchw_to_nhwc, run_span, units_for
     from paper_2312_10636_b200.device import context
     from paper_2312_10636_b200.engine import DeviceModel, StageInstance
@@ -34,44 +42,57 @@ def _setup():
     from paper_2312_10636_b200.plan import deploy
     from paper_2312_10636_b200.serving import ClientView
 
-    doc = json.loads((GOLDEN / "serving" / "resnet18_3cuts_realign.json").read_text())
+    name, shape = CASES[case]
+    doc = json.loads((GOLDEN / "serving" / f"{case}.json").read_text())
     dep = deploy(doc["plan"], doc["fragments"])
     clients = [ClientView.from_doc(c) for c in doc["clients"]]
-    m = torch_model("resnet18")
-    chain = build_chain("resnet18", module=m)
+    m = torch_model(name)
+    chain = build_chain(name, module=m)
     dm = DeviceModel(chain, 0)
     ctx = context(0)
-    units = units_for("resnet18", m)
+    units = units_for(name, m)
     instances = [[StageInstance(dm, s.start, s.end, s.batch, ctx.sm_budget(s.share)) for _ in range(s.instances)]
                  for s in dep.stages]
-    # one image per client; the client ran [0, p) in fp32 and ships the NHWC fp32 activation
-    ingress, expected, keep = {}, {}, []
+    # one input per client; the client ran [0, p) in fp32 and ships the (NHWC) fp32 activation
+    ingress, expected, keep, tol = {}, {}, [], {}
     for ci, c in enumerate(sorted(clients, key=lambda c: c.client_id)):
         route = dep.routes[c.client_id]
-        x = torch.randn(1, 3, 224, 224, generator=torch.Generator().manual_seed(100 + ci))
+        x = torch.randn(1, *shape, generator=torch.Generator().manual_seed(100 + ci))
         act = nchw_to_nhwc(run_span(units, 0, route.point, x))[0].contiguous().cuda()
         keep.append(act)
         ingress[c.client_id] = (act.data_ptr(), act.numel() * 4, chain.ingress_channels(route.point))
-        expected[c.client_id] = run_span(units, 0, chain.n_units, x)[0]
-    return doc, dep, clients, ctx, instances, ingress, expected, keep
+        expected[c.client_id] = run_span(units, 0, chain.n_units, x)[0].reshape(-1)
+        if name == "inception_v3":
+            # random-init Inception-v3 amplifies bf16 rounding ~20x (test_models_gpu.py): the bound
+            # is the framework's own bf16 error on the same suffix, from the same entry activation
+            import copy
+            mb = copy.deepcopy(m).to(torch.bfloat16)
+            with torch.no_grad():
+                fb = run_span(units_for(name, mb), route.point, chain.n_units,
+                              run_span(units, 0, route.point, x).to(torch.bfloat16)).float()[0].reshape(-1)
+            tol[c.client_id] = max(2e-2, 1.25 * ((fb - expected[c.client_id]).norm() /
+                                                 expected[c.client_id].norm()).item())
+    return doc, dep, clients, ctx, instances, ingress, expected, keep, tol
 
 
-def test_replay_realigned_group_matches_reference_and_oracle():
+@pytest.mark.parametrize("case", list(CASES))
+def test_replay_realigned_group_matches_reference_and_oracle(case):
     from paper_2312_10636_b200.serving import serve
 
-    doc, dep, clients, ctx, instances, ingress, expected, keep = _setup()
+    doc, dep, clients, ctx, instances, ingress, expected, keep, tol = _setup(case)
     lat = doc["latency"]
     rep = serve(dep, clients, doc["horizon_s"], epoch_s=doc["epoch_s"], latency=lambda st, k: lat[st.stage_id][k],
                 instances=instances, ctx=ctx, ingress=ingress, record_dispatch=True, max_inflight=1024,
-                slot_bytes=1 << 21, return_outputs=True)
+                slot_bytes=1 << 22, return_outputs=True)
     torch.cuda.synchronize()
     exp = doc["expected"]
     # plan, gather maps and batch composition: bit-exact with the reference simulator
     assert [list(r) for r in rep.requests] == exp["requests"]
     assert rep.dispatch == [(t, s, k, tuple(q)) for t, s, k, q in exp["dispatch"]]
-    # the plan really re-aligns: alignment batches ran and the shared stage mixed three entry points
-    kinds = {(s.start, s.end) for s in dep.stages}
-    assert (2, 6) in kinds and (4, 6) in kinds and (6, 10) in kinds
+    # the plan really re-aligns: alignment stages feed a shared suffix
+    n_end = max(x.end for x in dep.stages)
+    shared_starts = {s.start for s in dep.stages if s.end == n_end}
+    assert any(s.end < n_end and s.end in shared_starts for s in dep.stages)
     # numerics of every completed request
     out = rep.outputs
     done = 0
@@ -82,12 +103,13 @@ def test_replay_realigned_group_matches_reference_and_oracle():
         ref = expected[cid]
         got = torch.from_numpy(out[i].copy())
         rel = ((got - ref).norm() / ref.norm()).item()
-        assert rel < 2e-2, (i, cid, rel)
-        top2 = ref.topk(2).values
-        if (top2[0] - top2[1]) > 0.02 * (ref.max() - ref.min()):
-            assert int(got.argmax()) == int(ref.argmax()), (i, cid)
+        assert rel < tol.get(cid, 2e-2), (i, cid, rel, tol.get(cid))
+        if ref.numel() <= 1000:  # logits: identical top-1 when decisive
+            top2 = ref.topk(2).values
+            if (top2[0] - top2[1]) > 0.02 * (ref.max() - ref.min()):
+                assert int(got.argmax()) == int(ref.argmax()), (i, cid)
         done += 1
-    assert done == exp["summary"]["completed"] and done > 50
+    assert done == exp["summary"]["completed"] and done > 20
     del keep
 
 
