@@ -289,6 +289,7 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
       const int acc = t & 1;
       const uint32_t aph = (t >> 1) & 1;
       pipe_wait(&sp.tempty[acc], aph ^ 1, issuer);
+      if (issuer && a.trace && blockIdx.x == 0 && t < 4096) a.trace[8 * 8192 + t] = clock64();
       tc_fence_after();
       const uint32_t d = tmem_base + acc * acc_stride;
       for (int kb0 = 0; kb0 < a.num_kb; kb0 += KPS, ++it, st = (st + 1 == S_) ? 0 : st + 1, ph ^= (st == 0)) {
@@ -372,11 +373,13 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
       const int nb0 = n_blk * BN;
       const int ncols = min(BN, a.Cout - nb0);
       const int slot = t % nslot;
-      const float* bias = sp.sBias + nb0;
+      const uint32_t bias_s = smem_u32(sp.sBias + nb0);
       const uint8_t* res_base = sp.sRes + slot * res_slot_bytes;
       const int acc = t & 1;
       const uint32_t aph = (t >> 1) & 1;
       epi_wait(&sp.tfull[acc], aph);
+      const bool tr = a.trace && leader && blockIdx.x == 0 && t < 4096;
+      if (tr) a.trace[4 * 8192 + t * 4 + 0] = clock64();
       tc_fence_after();
       if (has_res) {
         epi_wait(&sp.rfull[slot], (t / nres) & 1);
@@ -398,7 +401,13 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
           const int n0 = nb0 + c;
           float f[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]) + bias[c + i];
+          for (int q4 = 0; q4 < 4; ++q4) {  // bias: 4 x ld.shared.v4 (a generic pointer made 16 LD.E)
+            const float4 bb = lds_f4(bias_s + static_cast<uint32_t>(c + 4 * q4) * 4u);
+            f[4 * q4 + 0] = __uint_as_float(v[4 * q4 + 0]) + bb.x;
+            f[4 * q4 + 1] = __uint_as_float(v[4 * q4 + 1]) + bb.y;
+            f[4 * q4 + 2] = __uint_as_float(v[4 * q4 + 2]) + bb.z;
+            f[4 * q4 + 3] = __uint_as_float(v[4 * q4 + 3]) + bb.w;
+          }
           if (has_res) {
             const uint8_t* rrow = res_base + (c >> 6) * kResGroupBytes + row * 128;
             const int j0 = (c & 63) >> 3;
@@ -454,15 +463,26 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
           }
         }
       };
-      for (int c = half * 16; c < ((a.dbg & 8) ? 0 : BN); c += 2 * cstep) {
-        uint32_t v0[16], v1[16];
-        const int c1 = c + cstep;
-        tmem_ld16(tbase + c, v0);
-        if (c1 < BN) tmem_ld16(tbase + c1, v1);
+      // this warp's 16-column chunks: c_j = half*16 + j*cstep.  Software-pipelined: the TMEM load
+      // of chunk j+1 is in flight while chunk j is converted and stored (tcgen05.wait::ld waits
+      // for all of the warp's loads, so the next load is issued before the math, waited after).
+      const int nch = (a.dbg & 8) ? 0 : (BN - half * 16 + cstep - 1) / cstep;
+      if (nch > 0) {
+        uint32_t va[16], vb[16];
+        tmem_ld16(tbase + half * 16, va);
         tmem_ld_wait();
-        emit(c, v0);
-        if (c1 < BN) emit(c1, v1);
+        for (int j = 0; j < nch; j += 2) {
+          const int ca = half * 16 + j * cstep, cb = ca + cstep;
+          if (j + 1 < nch) tmem_ld16(tbase + cb, vb);
+          emit(ca, va);
+          tmem_ld_wait();
+          if (j + 1 >= nch) break;
+          if (j + 2 < nch) tmem_ld16(tbase + cb + cstep, va);
+          emit(cb, vb);
+          tmem_ld_wait();
+        }
       }
+      if (tr) a.trace[4 * 8192 + t * 4 + 1] = clock64();
       tc_fence_before();
       mbar_arrive(&sp.tempty[acc]);
       if (ystore) {
@@ -476,6 +496,7 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
             bulk_wait_read<0>();  // the slot is refilled by the next residual load
             issue_res(t + nres);
           }
+          if (tr) a.trace[4 * 8192 + t * 4 + 2] = clock64();
         }
       } else if (has_res) {
         named_bar_sync(1, nepi);  // every epilogue thread is done with this residual slot

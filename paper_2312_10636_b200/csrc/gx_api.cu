@@ -119,7 +119,7 @@ bool encode_tmap_im2col_bf16(CUtensorMap* map, const void* base, int C, int W, i
 
 // ---------------------------------------------------------------- development trace buffer
 static unsigned long long* g_trace = nullptr;
-constexpr int kTraceEntries = 1 << 20;
+constexpr int kTraceEntries = 1 << 20;  // >= 8*8192 + 4096 (conv_tc layout)
 unsigned long long* debug_trace_buffer() {
   if (!g_trace) {
     cudaMalloc(&g_trace, kTraceEntries * sizeof(unsigned long long));
