@@ -350,7 +350,8 @@ def run_ours(args):
                              "host memory over PCIe (zero-copy), logits scattered to mapped host memory")
                     if args.e2e_ingress == "zero_copy" else
                     ("serve() with host ingress: each request's fp32 entry activation DMA-copied from pinned host "
-                     "memory into a device slot at arrival (copy engine), logits scattered to mapped host memory"),
+                     "memory into a device slot at arrival (copy engine, per-request event the batch waits on), "
+                     "logits scattered to mapped host memory"),
                     "h2d_bytes_per_step": int(stats[6].item() / K), "d2h_bytes_per_step": int(stats[7].item() / K)},
             "gpu_launches": int(stats[4].item()),
             "roofline": {"bound": "tensor",
@@ -478,8 +479,9 @@ def main():
     ap.add_argument("--clients", type=int, default=None, help="fleet size per GPU (default: largest feasible plan)")
     ap.add_argument("--max-inflight", type=int, default=8192)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-ingress", choices=("zero_copy", "dma"), default="zero_copy",
-                    help="e2e host ingress: gather reads pinned host memory (zero_copy) or a DMA copy at arrival")
+    ap.add_argument("--e2e-ingress", choices=("zero_copy", "dma"), default="dma",
+                    help="e2e host ingress: a copy-engine DMA of each request into a device slot at arrival "
+                         "(default), or the gather reading pinned host memory over PCIe (zero_copy)")
     ap.add_argument("--strict-shares", action="store_true",
                     help="SM budget = planned share exactly (default: work-conserving, share is a floor)")
     args = ap.parse_args()

@@ -235,7 +235,9 @@ typedef struct gx_serve_cfg {
   int32_t ingress_from_host; /* WALL: ingress lives in pinned host memory.  GX_INGRESS_ZERO_COPY:
                                  the stage's gather kernel reads it over PCIe directly (decode
                                  + cast fused into K1); GX_INGRESS_DMA: cudaMemcpyAsync into a
-                                 device slot at arrival; 0: ingress already in device memory  */
+                                 device slot at arrival on a copy-engine stream, the batch that
+                                 takes the request waits on that copy's event only;
+                                 0: ingress already in device memory                          */
   int32_t egress_to_host;    /* WALL: D2H copy of each request's output                     */
   int64_t slot_bytes;     /* per-request activation slot size on the device                 */
   int32_t max_inflight;   /* slot pool size                                                 */

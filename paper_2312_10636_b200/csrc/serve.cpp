@@ -60,6 +60,7 @@ struct Req {
   int cur_channels = 0;
   int slot = -1;
   int64_t result_idx = -1;  // row of `results` holding the request's output (final stage)
+  int h2d_ev = -1;          // GX_INGRESS_DMA: event of the arrival-time H2D copy into the slot
 };
 
 struct Batch {
@@ -141,6 +142,11 @@ struct gx_serve {
   std::vector<double> pool_last;  // wall ms of the lane's last dispatch
   cudaEvent_t ingress_ev = nullptr;
   bool ingress_pending = false;
+  // GX_INGRESS_DMA: copy-engine streams and a recycled event per in-flight arrival copy
+  std::vector<cudaStream_t> copy_streams;
+  std::vector<cudaEvent_t> h2d_events;
+  std::vector<int> free_h2d;
+  int64_t n_h2d = 0;
   double wall_ms = 0.0;
   int64_t n_batches = 0, n_kernels = 0;
   int64_t drops_no_slot = 0;
@@ -248,9 +254,20 @@ int gx_serve::arrive(int ri, double now) {
       free_slots.pop_back();
       void* dst = static_cast<uint8_t*>(slots) + static_cast<size_t>(r.slot) * cfg.slot_bytes;
       if (cfg.ingress_from_host == GX_INGRESS_DMA) {
-        cudaError_t e = cudaMemcpyAsync(dst, rt.ingress, rt.ingress_bytes, cudaMemcpyHostToDevice, ingress_stream);
-        if (e != cudaSuccess) return cuda_fail(e, "ingress H2D");
-        ingress_pending = true;
+        // the copy engine moves the request's activation into its slot as soon as it arrives
+        // (it waits in the stage queue anyway); the batch that takes it waits on this copy only
+        if (free_h2d.empty()) {
+          cudaEvent_t ev = nullptr;
+          GX_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+          h2d_events.push_back(ev);
+          free_h2d.push_back(static_cast<int>(h2d_events.size()) - 1);
+        }
+        const int ei = free_h2d.back();
+        free_h2d.pop_back();
+        cudaStream_t cs = copy_streams[n_h2d++ % copy_streams.size()];
+        GX_CUDA(cudaMemcpyAsync(dst, rt.ingress, rt.ingress_bytes, cudaMemcpyHostToDevice, cs));
+        GX_CUDA(cudaEventRecord(h2d_events[ei], cs));
+        r.h2d_ev = ei;
         r.cur = dst;
       }
     }
@@ -282,8 +299,18 @@ int gx_serve::dispatch_gpu(int si, int bi) {
   int32_t sdt[64];
   void* dst[64];
   int channels = 0;
+  // an idle lane if there is one, else the lane with the fewest / oldest batches in flight
+  int lane = 0;
+  for (int i = 1; i < static_cast<int>(pool.size()); ++i)
+    if (pool_n[i] < pool_n[lane] || (pool_n[i] == pool_n[lane] && pool_last[i] < pool_last[lane])) lane = i;
+  cudaStream_t sm = pool[lane];
   for (int i = 0; i < k; ++i) {
     Req& r = reqs[b.reqs[i]];
+    if (r.h2d_ev >= 0) {
+      GX_CUDA(cudaStreamWaitEvent(sm, h2d_events[r.h2d_ev], 0));
+      free_h2d.push_back(r.h2d_ev);
+      r.h2d_ev = -1;
+    }
     src[i] = r.cur;
     sdt[i] = r.cur_dtype;
     channels = std::max(channels, r.cur_channels);
@@ -299,15 +326,9 @@ int gx_serve::dispatch_gpu(int si, int bi) {
     GX_CUDA(cudaEventRecord(ingress_ev, ingress_stream));
     ingress_pending = false;
   }
-  // an idle lane if there is one, else the lane with the fewest / oldest batches in flight
-  int lane = 0;
-  for (int i = 1; i < static_cast<int>(pool.size()); ++i)
-    if (pool_n[i] < pool_n[lane] || (pool_n[i] == pool_n[lane] && pool_last[i] < pool_last[lane])) lane = i;
-  cudaStream_t sm = pool[lane];
   b.lane = lane;
   pool_n[lane] += 1;
   pool_last[lane] = b.t_disp;
-  GX_CUDA(cudaStreamWaitEvent(sm, ingress_ev, 0));
   int rc = gx::stage_run_on(g, sm, k, src, sdt, channels, dst, st.out_final ? GX_F32 : GX_BF16);
   if (rc != GX_OK) return rc;
   int kc = 0;
@@ -660,6 +681,11 @@ int gx_serve_create(gx_ctx* ctx, int n_stages, const gx_serve_stage* st, int n_r
     }
     s->pool_n.assign(s->pool.size(), 0);
     s->pool_last.assign(s->pool.size(), 0.0);
+    for (int i = 0; i < 4 && e == cudaSuccess && cfg->ingress_from_host == GX_INGRESS_DMA; ++i) {
+      cudaStream_t q = nullptr;
+      e = cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking);
+      if (e == cudaSuccess) s->copy_streams.push_back(q);
+    }
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ingress_ev, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventRecord(s->ingress_ev, s->ingress_stream);
     if (e != cudaSuccess) {
@@ -759,6 +785,8 @@ int gx_serve_destroy(gx_serve* s) {
         cudaFree(s->results);
     }
     if (s->ingress_ev) cudaEventDestroy(s->ingress_ev);
+    for (cudaEvent_t ev : s->h2d_events) cudaEventDestroy(ev);
+    for (cudaStream_t q : s->copy_streams) cudaStreamDestroy(q);
     if (s->ingress_stream) cudaStreamDestroy(s->ingress_stream);
     for (cudaStream_t q : s->pool) cudaStreamDestroy(q);
   }
