@@ -397,9 +397,12 @@ def _cpu_stage_latency(chain_name, spans_k, budget_s):
                 H, W, Cc, _ = chain.boundary_shape(a)
                 x = torch.randn(k, Cc, H, W).clamp_min(0)
             run_span(units, a, b, x)  # warm
-            t0 = time.perf_counter()
-            run_span(units, a, b, x)
-            out[(a, b, k)] = (time.perf_counter() - t0) * 1000.0
+            best = math.inf
+            for _ in range(2):  # best of two timed passes
+                t0 = time.perf_counter()
+                run_span(units, a, b, x)
+                best = min(best, (time.perf_counter() - t0) * 1000.0)
+            out[(a, b, k)] = best
     return out
 
 
@@ -438,7 +441,7 @@ def cpu_baseline(args, wl, dep, chain, budget_s: float = 20.0):
     recs, _ = simulate_fixed(dep, clients, horizon, 0.0, latency, on_batch=on_batch)
     met = sum(1 for _c, _g, d, dl, s in recs if s == "completed" and d <= dl + 1e-9)
     return {"value": round(met / horizon, 2), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-            "sample": f"fp32 CPU forward of {len(lat)} (span, k) points of this plan (one timed pass each, "
+            "sample": f"fp32 CPU forward of {len(lat)} (span, k) points of this plan (best of 2 timed passes, "
                       f"{time.time() - t0:.1f}s) driving the oracle event loop over a {horizon:.1f}s horizon"}
 
 
@@ -449,7 +452,9 @@ def run_reference(args):
     from paper_2312_10636_b200.models import build_chain
     from paper_2312_10636_b200.plan import deploy
 
-    wl = _workload(args.model, args.clients)
+    # the achievable-throughput rule steps the fleet down until p99 <= SLO; on the host CPU no fleet
+    # gets there, so the arm reports the smallest planned fleet (the most favourable to the CPU)
+    wl = _workload(args.model, args.clients) if args.clients is not None else _workloads(args.model)[0]
     dep = deploy(wl["plan"], wl["fragments"])
     chain = build_chain(args.model)
     vals = []
