@@ -49,14 +49,17 @@ def _peaks():
     return 1400.0, 1590.0, 6650.0, "fallback"
 
 
-def _workloads(name: str):
-    files = sorted(glob.glob(str(ROOT / "tests" / "golden" / "workload" / f"{name}_c*.json")),
-                   key=lambda f: int(f.rsplit("_c", 1)[1].split(".")[0]))
-    return [json.loads(Path(f).read_text()) for f in files]
+def _workloads(name: str, all_plans: bool = False):
+    """Planned fleets <name>_c<N>.json in ascending (clients, latency_scale) order; with all_plans
+    also the fleets planned against the load-calibrated table (<name>_s<F>_c<N>.json)."""
+    pats = [f"{name}_c[0-9]*.json"] + ([f"{name}_s*_c[0-9]*.json"] if all_plans else [])
+    files = [f for pat in pats for f in glob.glob(str(ROOT / "tests" / "golden" / "workload" / pat))]
+    docs = [json.loads(Path(f).read_text()) for f in files]
+    return sorted(docs, key=lambda d: (d["clients_n"], d.get("latency_scale", 1.0)))
 
 
 def _workload(name: str, clients: int | None):
-    files = sorted(glob.glob(str(ROOT / "tests" / "golden" / "workload" / f"{name}_c*.json")),
+    files = sorted(glob.glob(str(ROOT / "tests" / "golden" / "workload" / f"{name}_c[0-9]*.json")),
                    key=lambda f: int(f.rsplit("_c", 1)[1].split(".")[0]))
     if not files:
         raise SystemExit(f"no workload fixtures for {name}; run scripts/make_workload.py")
@@ -191,9 +194,12 @@ def run_ours(args):
             ok = bool(flag.item())
         return ok
 
-    workloads = _workloads(args.model)
+    # the achievable-throughput search runs over every planned fleet of the model: plans made
+    # against the measured table and against the load-calibrated table (make_workload.py --scale)
+    workloads = _workloads(args.plans or args.model, all_plans=args.plans is None)
+    key = lambda w: (w["clients_n"], w.get("latency_scale", 1.0))  # noqa: E731
     if args.clients is not None:
-        fleet = Fleet(_workload(args.model, args.clients))
+        fleet = Fleet(_workload(args.plans or args.model, args.clients))
     else:
         # achievable-throughput search: the largest planned fleet whose served
         # p99 stays within the SLO with < 1% drops, probed for 3 s each (p99 over arrivals after
@@ -204,7 +210,8 @@ def run_ours(args):
             rep = cand.serve(3.0)
             ok = p99_of(rep, 1000.0) <= wl["slo_ms"] and rep.dropped <= 0.01 * max(1, rep.generated)
             if rank == 0:
-                print(f"# probe clients={wl['clients_n']}: p99={p99_of(rep, 1000.0):.1f} ms "
+                print(f"# probe clients={wl['clients_n']} scale={wl.get('latency_scale', 1.0)}: "
+                      f"p99={p99_of(rep, 1000.0):.1f} ms "
                       f"met/s={rep.slo_met / 3.0:.0f} -> {'ok' if ok else 'over'}", file=sys.stderr, flush=True)
             if all_ok(ok):
                 fleet = cand
@@ -247,7 +254,7 @@ def run_ours(args):
         res = one_run(fleet, host=False)
         # the timed run is the verdict: if its p99 misses the SLO (or >1% drops), step down to the
         # next smaller planned fleet and measure again
-        smaller = [w for w in reversed(workloads) if w["clients_n"] < fleet.wl["clients_n"]]
+        smaller = [w for w in reversed(workloads) if key(w) < key(fleet.wl)]
         while args.clients is None and smaller and not all_ok(
                 res["p99"] <= fleet.wl["slo_ms"] and res["dropped"] <= 0.01 * max(1, res["generated"])):
             if rank == 0:
@@ -263,14 +270,15 @@ def run_ours(args):
     e2e_fleet = fleet
     res_e2e = one_run(fleet, host=True)
     if args.clients is None:
-        # PCIe zero-copy ingress makes the tail noisier than the resident run: a miss is retried
-        # once at the same fleet before stepping down
+        # host ingress makes the tail noisier than the resident run: a miss at the first fleet is
+        # retried once before stepping down
         retried = False
-        cands = [w for w in reversed(_workloads(args.model)) if w["clients_n"] < wl["clients_n"]]
+        cands = [w for w in reversed(workloads) if key(w) < key(wl)]
         while True:
             ok = all_ok(res_e2e["p99"] <= slo and res_e2e["dropped"] <= 0.01 * max(1, res_e2e["generated"]))
             if rank == 0:
-                print(f"# e2e clients={e2e_fleet.wl['clients_n']}: p99={res_e2e['p99']:.1f} ms -> "
+                print(f"# e2e clients={e2e_fleet.wl['clients_n']} scale={e2e_fleet.wl.get('latency_scale', 1.0)}: "
+                      f"p99={res_e2e['p99']:.1f} ms -> "
                       f"{'ok' if ok else 'over'}", file=sys.stderr, flush=True)
             if ok:
                 break
@@ -283,7 +291,6 @@ def run_ours(args):
             if e2e_fleet is not fleet:
                 del e2e_fleet
             e2e_fleet = Fleet(cands.pop(0))
-            retried = False
             res_e2e = one_run(e2e_fleet, host=True)
 
     # roofline of the dominant kernel, conv_tc_kernel (>=90% of GPU time in every launch list
@@ -337,7 +344,8 @@ def run_ours(args):
             "config": {"workload": f"{args.model} re-aligned fragment groups, {wl['clients_n']} clients x "
                                    f"{wl['rate_rps']:.0f} rps per GPU, 8 cut points, plan from the reference planner "
                                    f"on the measured B200 profile table, SM-share partitioning",
-                       "model": args.model, "clients_per_gpu": wl["clients_n"], "offered_rps_per_gpu":
+                       "model": args.model, "latency_scale": wl.get("latency_scale", 1.0),
+                       "clients_per_gpu": wl["clients_n"], "offered_rps_per_gpu":
                            wl["clients_n"] * wl["rate_rps"], "slo_ms": round(slo, 3), "window_s": window,
                        "stages": len(dep.stages), "instances": sum(s.instances for s in dep.stages),
                        "plan_resource": wl["plan"]["total_resource"], "parallelism": f"replica-per-gpu x{world}",
@@ -346,6 +354,7 @@ def run_ours(args):
             "dropped": int(stats[2].item()),
             "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "p99_ms": round(p99_e2e, 3),
                     "p99_ok": p99_e2e <= slo, "clients_per_gpu": e2e_fleet.wl["clients_n"],
+                    "latency_scale": e2e_fleet.wl.get("latency_scale", 1.0),
                     "path": ("serve() with host ingress: gather kernels read fp32 entry activations from pinned "
                              "host memory over PCIe (zero-copy), logits scattered to mapped host memory")
                     if args.e2e_ingress == "zero_copy" else
@@ -454,7 +463,7 @@ def run_reference(args):
 
     # the achievable-throughput rule steps the fleet down until p99 <= SLO; on the host CPU no fleet
     # gets there, so the arm reports the smallest planned fleet (the most favourable to the CPU)
-    wl = _workload(args.model, args.clients) if args.clients is not None else _workloads(args.model)[0]
+    wl = _workload(args.plans or args.model, args.clients) if args.clients is not None else _workloads(args.plans or args.model)[0]
     dep = deploy(wl["plan"], wl["fragments"])
     chain = build_chain(args.model)
     vals = []
@@ -481,6 +490,9 @@ def main():
     ap.add_argument("--window", type=float, default=1.0, help="seconds of arrivals per step")
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--model", default="resnet50")
+    ap.add_argument("--plans", default=None,
+                    help="workload fixture tag (default: the model; e.g. resnet50_s1.5 = plans made against the "
+                         "profile table scaled by the served/profiled latency ratio)")
     ap.add_argument("--clients", type=int, default=None, help="fleet size per GPU (default: largest feasible plan)")
     ap.add_argument("--max-inflight", type=int, default=8192)
     ap.add_argument("--no-cpu-baseline", action="store_true")
