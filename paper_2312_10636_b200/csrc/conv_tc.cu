@@ -16,6 +16,8 @@
 // epilogue of tile i overlaps the MMAs of tile i+1.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "gx_internal.h"
 #include "gx_ptx.cuh"
 
@@ -532,7 +534,10 @@ int conv_pick_stages(int BN, int num_kb, bool res, int Cout, int* nres_out, int 
     const size_t fixed = conv_smem_bytes(BN, 0, num_kb, nres, Cout, kps);
     int s = budget > fixed ? static_cast<int>((budget - fixed) / per_stage) : 0;
     if (s > 8) s = 8;
-    if (s >= 3 || nres <= 1) {
+    // short-K convs (the bottleneck expand 1x1s) are epilogue-bound: a second slot lets the next
+    // tile's residual load overlap this tile's epilogue, worth more than a deeper operand ring
+    const int kb_short = getenv("GX_RES2_KB") ? atoi(getenv("GX_RES2_KB")) : 0;  // measured neutral: off
+    if (s >= 3 || nres <= 1 || (s >= 2 && num_kb <= kb_short)) {
       best_s = s < 2 ? 2 : s;
       best_r = nres;
       break;
