@@ -72,7 +72,7 @@ __device__ __forceinline__ void pipe_wait(uint64_t* bar, uint32_t parity, bool i
 #endif
 }
 
-template <bool kTmaA, int KPS>
+template <bool kTmaA, int KPS, bool WST>
 __global__ void __launch_bounds__(kConvTcThreads, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap amap,
                    const __grid_constant__ CUtensorMap rmap, const __grid_constant__ CUtensorMap ymap,
@@ -343,7 +343,17 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
     const int row = q * 32 + lane;
     const int nepi = kTmaA ? 256 : 128;
     const int half = (kTmaA && warp < 4) ? 1 : 0;
-    const int cstep = kTmaA ? 32 : 16;
+    // column split between the two warps of a lane quarter: contiguous halves with per-warp stores
+    // (each warp owns whole 64-column groups and stores them itself), else interleaved 16-column
+    // chunks (measured 7% faster for the residual epilogue)
+    const bool halves = kTmaA && WST;
+    const int cbase = !kTmaA ? 0 : halves ? half * (BN / 2) : half * 16;
+    const int cstep = (!kTmaA || halves) ? 16 : 32;
+    const int cend = halves ? cbase + BN / 2 : BN;
+    // per-warp TMA stores (no residual): a warp overwrites only the smem rows/columns it stored
+    // itself, so no cross-warp barrier is needed around the output staging slot
+    constexpr bool wstore = WST;  // compile-time: the residual / shared-store paths keep their code
+    const bool wissuer = wstore && elect_one();
     const bool leader = warp == 6 && lane == 0;
     const int nres = a.nres;
     const int nslot = (has_res || ystore) ? nres : 1;
@@ -385,6 +395,15 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
       tc_fence_after();
       if (has_res) {
         epi_wait(&sp.rfull[slot], (t / nres) & 1);
+      } else if (wstore) {
+        // this warp's own previous store from this slot has finished reading it
+        if (wissuer) {
+          if (nres == 1)
+            bulk_wait_read<0>();
+          else
+            bulk_wait_read<1>();
+        }
+        __syncwarp();
       } else if (ystore) {
         // the TMA store that last used this slot (tile t - nres) has finished reading it
         if (leader) {
@@ -468,13 +487,13 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
       // this warp's 16-column chunks: c_j = half*16 + j*cstep.  Software-pipelined: the TMEM load
       // of chunk j+1 is in flight while chunk j is converted and stored (tcgen05.wait::ld waits
       // for all of the warp's loads, so the next load is issued before the math, waited after).
-      const int nch = (a.dbg & 8) ? 0 : (BN - half * 16 + cstep - 1) / cstep;
+      const int nch = (a.dbg & 8) ? 0 : (cend - cbase + cstep - 1) / cstep;
       if (nch > 0) {
         uint32_t va[16], vb[16];
-        tmem_ld16(tbase + half * 16, va);
+        tmem_ld16(tbase + cbase, va);
         tmem_ld_wait();
         for (int j = 0; j < nch; j += 2) {
-          const int ca = half * 16 + j * cstep, cb = ca + cstep;
+          const int ca = cbase + j * cstep, cb = ca + cstep;
           if (j + 1 < nch) tmem_ld16(tbase + cb, vb);
           emit(ca, va);
           tmem_ld_wait();
@@ -487,7 +506,16 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
       if (tr) a.trace[4 * 8192 + t * 4 + 1] = clock64();
       tc_fence_before();
       mbar_arrive(&sp.tempty[acc]);
-      if (ystore) {
+      if (wstore) {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (wissuer) {
+          for (int g = cbase / 64; g < cend / 64; ++g)
+            if (g * 64 < ncols)
+              tma_store_2d(YM, res_base + g * kResGroupBytes + q * 32 * 128, a.y_coff + nb0 + g * 64, m0 + q * 32);
+          bulk_commit();
+        }
+      } else if (ystore) {
         fence_proxy_async_smem();  // make the slot's generic-proxy writes visible to the TMA store
         named_bar_sync(1, nepi);
         if (leader) {
@@ -506,7 +534,11 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
       }
     }
   }
-  if (ystore && warp == 6 && lane == 0) bulk_wait<0>();  // output stores complete before exit
+  if (ystore && !WST && warp == 6 && lane == 0) bulk_wait<0>();  // output stores complete before exit
+  if (WST && ((warp >= 6 && warp <= 9) || (kTmaA && warp < 4))) {
+    if (elect_one()) bulk_wait<0>();
+    __syncwarp();
+  }
   // Let the next kernel in the stream start its prologue.
   pdl_launch_dependents();
   tc_fence_before();
@@ -551,11 +583,10 @@ cudaError_t launch_conv(const CUtensorMap& wmap, const CUtensorMap& amap, const 
                         const CUtensorMap& ymap, const ConvArgs& a, int grid, cudaStream_t s, bool pdl) {
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(conv_tc_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(conv_tc_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    cudaError_t e = cudaSuccess;
+    for (auto fn : {conv_tc_kernel<true, 1, false>, conv_tc_kernel<true, 2, false>, conv_tc_kernel<false, 1, false>,
+                    conv_tc_kernel<true, 1, true>, conv_tc_kernel<true, 2, true>})
+      if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     if (e != cudaSuccess) return e;
     configured = true;
   }
@@ -569,9 +600,12 @@ cudaError_t launch_conv(const CUtensorMap& wmap, const CUtensorMap& amap, const 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  if (a.tma_a && a.kps == 2) return cudaLaunchKernelEx(&cfg, conv_tc_kernel<true, 2>, wmap, amap, rmap, ymap, a);
-  if (a.tma_a) return cudaLaunchKernelEx(&cfg, conv_tc_kernel<true, 1>, wmap, amap, rmap, ymap, a);
-  return cudaLaunchKernelEx(&cfg, conv_tc_kernel<false, 1>, wmap, amap, rmap, ymap, a);
+  if (a.tma_a && a.wstore)
+    return a.kps == 2 ? cudaLaunchKernelEx(&cfg, conv_tc_kernel<true, 2, true>, wmap, amap, rmap, ymap, a)
+                      : cudaLaunchKernelEx(&cfg, conv_tc_kernel<true, 1, true>, wmap, amap, rmap, ymap, a);
+  if (a.tma_a && a.kps == 2) return cudaLaunchKernelEx(&cfg, conv_tc_kernel<true, 2, false>, wmap, amap, rmap, ymap, a);
+  if (a.tma_a) return cudaLaunchKernelEx(&cfg, conv_tc_kernel<true, 1, false>, wmap, amap, rmap, ymap, a);
+  return cudaLaunchKernelEx(&cfg, conv_tc_kernel<false, 1, false>, wmap, amap, rmap, ymap, a);
 }
 
 }  // namespace gx

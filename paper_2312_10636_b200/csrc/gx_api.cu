@@ -233,7 +233,9 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
   memset(&out->amap, 0, sizeof(out->amap));
   memset(&out->rmap, 0, sizeof(out->rmap));
   memset(&out->ymap, 0, sizeof(out->ymap));
-  if (a.ystore && !encode_tmap_2d_bf16(&out->ymap, a.y, to.C, a.M, static_cast<uint64_t>(to.C) * 2, 64, kBM))
+  a.wstore = a.ystore && !a.res && getenv("GX_NO_TMA_IM2COL") == nullptr && a.BN % 128 == 0 && getenv("GX_NO_WSTORE") == nullptr;
+  if (a.ystore && !encode_tmap_2d_bf16(&out->ymap, a.y, to.C, a.M, static_cast<uint64_t>(to.C) * 2, 64,
+                                       a.wstore ? 32 : kBM))
     return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for the conv output: " + g_last_encode);
   if (!encode_tmap_2d_bf16(&out->wmap, wbase + op.w_off, kpad, op.Cout, static_cast<uint64_t>(kpad) * 2, kBK, a.BN))
     return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for conv weights: " + g_last_encode);

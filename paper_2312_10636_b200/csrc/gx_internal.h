@@ -51,6 +51,7 @@ struct ConvArgs {
   int a2d;    // A via a plain 2D tiled map over [M, C] (1x1, stride 1, no padding)
   const CUtensorMap* gmaps;  // experiment: tensor maps read from global memory instead of params
   int ystore;  // bf16 output staged in the smem slots and written by TMA stores (ymap), else st.global
+  int wstore;  // ystore without residual: each epilogue warp TMA-stores its own 32-row box (ymap box 64x32)
   int dbg;  // GX_CONV_DBG timing attribution (results invalid): 1 skip A loads, 2 skip B loads,
             // 4 skip MMAs, 8 skip the epilogue's TMEM reads and stores
   int kps;  // k-blocks per pipeline stage (1 or 2; 2 only with TMA-built A)
