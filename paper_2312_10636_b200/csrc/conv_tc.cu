@@ -39,6 +39,7 @@ struct SmemPlan {
   uint64_t* tfull;
   uint64_t* tempty;
   uint64_t* rfull;  // [2] residual slot filled
+  uint64_t* rfw;    // [8 epilogue warps][2 slots] per-warp residual boxes filled (WST)
   uint64_t* bfull;  // bias vector staged
   uint32_t* tslot;
   int2* ktab;
@@ -103,7 +104,8 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
   sp.tempty = sp.tfull + 2;
   sp.rfull = sp.tempty + 2;
   sp.bfull = sp.rfull + 2;
-  sp.tslot = reinterpret_cast<uint32_t*>(sp.bfull + 1);
+  sp.rfw = sp.bfull + 1;
+  sp.tslot = reinterpret_cast<uint32_t*>(sp.rfw + 16);
   sp.ktab = reinterpret_cast<int2*>(sp.tslot + 4);
 
   const int tid = threadIdx.x;
@@ -141,6 +143,7 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
       }
       mbar_init(&sp.rfull[0], 1);
       mbar_init(&sp.rfull[1], 1);
+      for (int i = 0; i < 16; ++i) mbar_init(&sp.rfw[i], 1);
       mbar_init(sp.bfull, 1);
       fence_barrier_init();
     }
@@ -367,14 +370,31 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
         tma_load_2d(sp.sRes + slot * res_slot_bytes + g * kResGroupBytes, RM, &sp.rfull[slot],
                     (tile % a.n_tiles) * BN + g * 64, (tile / a.n_tiles) * kBM);
     };
+    // WST + residual: each epilogue warp TMA-loads its own 32-row x (BN/2)-column residual box
+    const int ew = warp >= 6 ? warp - 6 : 4 + warp;  // epilogue warp index 0..7
+    auto issue_res_w = [&](int t_idx) {
+      const int tile = blockIdx.x + t_idx * gridDim.x;
+      if (tile >= a.num_tiles) return;
+      const int slot = t_idx % nres;
+      uint64_t* bar = &sp.rfw[ew * 2 + slot];
+      mbar_arrive_expect_tx(bar, static_cast<uint32_t>((cend - cbase) / 64) * 32u * 128u);
+      for (int g = cbase / 64; g < cend / 64; ++g)
+        tma_load_2d(sp.sRes + slot * res_slot_bytes + g * kResGroupBytes + q * 32 * 128, RM, bar,
+                    (tile % a.n_tiles) * BN + g * 64, (tile / a.n_tiles) * kBM + q * 32);
+    };
     if (leader) {
       // the whole bias vector once per CTA; residual tiles run ahead by `nres` tiles
       mbar_arrive_expect_tx(sp.bfull, static_cast<uint32_t>(a.Cout) * 4u);
       bulk_load(sp.sBias, a.bias, static_cast<uint32_t>(a.Cout) * 4u, sp.bfull);
-      if (has_res) {
+      if (has_res && !WST) {
         tma_prefetch_desc(RM);
         for (int i = 0; i < nres; ++i) issue_res(i);
       }
+    }
+    if (WST && has_res) {
+      if (wissuer)
+        for (int i = 0; i < nres; ++i) issue_res_w(i);
+      __syncwarp();
     }
     epi_wait(sp.bfull, 0);
     int t = 0;
@@ -393,7 +413,9 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
       const bool tr = a.trace && leader && blockIdx.x == 0 && t < 4096;
       if (tr) a.trace[4 * 8192 + t * 4 + 0] = clock64();
       tc_fence_after();
-      if (has_res) {
+      if (WST && has_res) {
+        epi_wait(&sp.rfw[ew * 2 + slot], (t / nres) & 1);
+      } else if (has_res) {
         epi_wait(&sp.rfull[slot], (t / nres) & 1);
       } else if (wstore) {
         // this warp's own previous store from this slot has finished reading it
@@ -514,7 +536,12 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
             if (g * 64 < ncols)
               tma_store_2d(YM, res_base + g * kResGroupBytes + q * 32 * 128, a.y_coff + nb0 + g * 64, m0 + q * 32);
           bulk_commit();
+          if (has_res) {
+            bulk_wait_read<0>();  // this warp's region is refilled with its next residual box
+            issue_res_w(t + nres);
+          }
         }
+        __syncwarp();
       } else if (ystore) {
         fence_proxy_async_smem();  // make the slot's generic-proxy writes visible to the TMA store
         named_bar_sync(1, nepi);
@@ -552,7 +579,7 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
 
 size_t conv_smem_bytes(int BN, int stages, int num_kb, int nres, int Cout, int kps) {
   return 1024 + static_cast<size_t>(stages) * kps * (kATileBytes + BN * 128) +
-         static_cast<size_t>(nres) * res_groups(BN) * kResGroupBytes + bias_alloc(Cout) + (2 * stages + 9) * 8 + 16 +
+         static_cast<size_t>(nres) * res_groups(BN) * kResGroupBytes + bias_alloc(Cout) + (2 * stages + 25) * 8 + 16 +
          static_cast<size_t>(num_kb) * 8 * sizeof(int2);
 }
 

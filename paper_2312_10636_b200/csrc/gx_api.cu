@@ -157,7 +157,7 @@ static uint32_t tmem_cols_for(int bn) {
 }
 
 int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint8_t* wbase, int k, int sm_budget,
-              ConvLaunch* out, int bn_cap, const uint8_t* wsw) {
+              ConvLaunch* out, int bn_cap, const uint8_t* wsw, bool for_span) {
   const gx_tensor& ti = T[op.in];
   const gx_tensor& to = T[op.out];
   const int R = op.kind == GX_OP_LINEAR ? 1 : op.R;
@@ -233,7 +233,8 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
   memset(&out->amap, 0, sizeof(out->amap));
   memset(&out->rmap, 0, sizeof(out->rmap));
   memset(&out->ymap, 0, sizeof(out->ymap));
-  a.wstore = a.ystore && !a.res && getenv("GX_NO_TMA_IM2COL") == nullptr && a.BN % 128 == 0 && getenv("GX_NO_WSTORE") == nullptr;
+  a.wstore = !for_span && a.ystore && (!a.res || getenv("GX_NO_WRES") == nullptr) && getenv("GX_NO_TMA_IM2COL") == nullptr &&
+             a.BN % 128 == 0 && getenv("GX_NO_WSTORE") == nullptr;
   if (a.ystore && !encode_tmap_2d_bf16(&out->ymap, a.y, to.C, a.M, static_cast<uint64_t>(to.C) * 2, 64,
                                        a.wstore ? 32 : kBM))
     return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for the conv output: " + g_last_encode);
@@ -250,7 +251,8 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
                                                  (op.pw_hi >= 0 ? op.pw_hi : a.pw) - (a.S - 1),
                                                  (op.ph_hi >= 0 ? op.ph_hi : a.ph) - (a.R - 1), a.sw, a.sh, a.cpl))
     return fail(GX_ECUDA, "cuTensorMapEncodeIm2col failed for conv input");
-  if (a.res && !encode_tmap_2d_bf16(&out->rmap, a.res, a.res_ld, a.M, static_cast<uint64_t>(a.res_ld) * 2, 64, kBM))
+  if (a.res && !encode_tmap_2d_bf16(&out->rmap, a.res, a.res_ld, a.M, static_cast<uint64_t>(a.res_ld) * 2, 64,
+                                    a.wstore ? 32 : kBM))
     return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for the residual: " + g_last_encode);
   out->grid = std::min(a.num_tiles, std::max(1, sm_budget));
   a.gmaps = nullptr;

@@ -30,8 +30,10 @@ int elem_size(int dtype);
 int64_t tensor_elems(const gx_tensor& t);
 // wsw: the op's weights pre-tiled and pre-swizzled for bulk copies ([kb][Cout][64] bf16, 128B
 // swizzle), or null to load them with a tiled TMA from the [Cout][Kpad] blob.
+// for_span: plan for the persistent span kernel (span_kernel.cu), which loads 128-row residual
+// boxes and stores outputs itself: no per-warp epilogue I/O.
 int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint8_t* wbase, int k, int sm_budget,
-              ConvLaunch* out, int bn_cap = 256, const uint8_t* wsw = nullptr);
+              ConvLaunch* out, int bn_cap = 256, const uint8_t* wsw = nullptr, bool for_span = false);
 int launch_op(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint8_t* wbase, int k, int sm_budget,
               cudaStream_t s, bool pdl, const ConvLaunch* pre, int* kernels);
 unsigned long long* debug_trace_buffer();

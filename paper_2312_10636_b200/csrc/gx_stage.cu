@@ -157,7 +157,7 @@ int build_span_program(gx_stage* st, int k, gx_stage::PerK* out) {
       case GX_OP_CONV:
       case GX_OP_LINEAR: {
         ConvLaunch cl;
-        int rc = plan_conv(op, T, st->tptr.data(), wbase, k, st->sm_budget, &cl, 256);
+        int rc = plan_conv(op, T, st->tptr.data(), wbase, k, st->sm_budget, &cl, 256, nullptr, true);
         if (rc != GX_OK) return rc;
         const ConvArgs& a = cl.args;
         if (!a.tma_a) return fail(GX_EINVAL, "span kernel needs the TMA im2col path");
