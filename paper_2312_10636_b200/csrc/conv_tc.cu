@@ -611,8 +611,9 @@ cudaError_t launch_conv(const CUtensorMap& wmap, const CUtensorMap& amap, const 
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaSuccess;
-    for (auto fn : {conv_tc_kernel<true, 1, false>, conv_tc_kernel<true, 2, false>, conv_tc_kernel<false, 1, false>,
-                    conv_tc_kernel<true, 1, true>, conv_tc_kernel<true, 2, true>})
+    for (auto fn : {conv_tc_kernel<true, 1, false>, conv_tc_kernel<true, 2, false>, conv_tc_kernel<true, 3, false>,
+                    conv_tc_kernel<false, 1, false>, conv_tc_kernel<true, 1, true>, conv_tc_kernel<true, 2, true>,
+                    conv_tc_kernel<true, 3, true>})
       if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     if (e != cudaSuccess) return e;
     configured = true;
@@ -628,8 +629,10 @@ cudaError_t launch_conv(const CUtensorMap& wmap, const CUtensorMap& amap, const 
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
   if (a.tma_a && a.wstore)
-    return a.kps == 2 ? cudaLaunchKernelEx(&cfg, conv_tc_kernel<true, 2, true>, wmap, amap, rmap, ymap, a)
-                      : cudaLaunchKernelEx(&cfg, conv_tc_kernel<true, 1, true>, wmap, amap, rmap, ymap, a);
+    return a.kps == 3   ? cudaLaunchKernelEx(&cfg, conv_tc_kernel<true, 3, true>, wmap, amap, rmap, ymap, a)
+           : a.kps == 2 ? cudaLaunchKernelEx(&cfg, conv_tc_kernel<true, 2, true>, wmap, amap, rmap, ymap, a)
+                        : cudaLaunchKernelEx(&cfg, conv_tc_kernel<true, 1, true>, wmap, amap, rmap, ymap, a);
+  if (a.tma_a && a.kps == 3) return cudaLaunchKernelEx(&cfg, conv_tc_kernel<true, 3, false>, wmap, amap, rmap, ymap, a);
   if (a.tma_a && a.kps == 2) return cudaLaunchKernelEx(&cfg, conv_tc_kernel<true, 2, false>, wmap, amap, rmap, ymap, a);
   if (a.tma_a) return cudaLaunchKernelEx(&cfg, conv_tc_kernel<true, 1, false>, wmap, amap, rmap, ymap, a);
   return cudaLaunchKernelEx(&cfg, conv_tc_kernel<false, 1, false>, wmap, amap, rmap, ymap, a);

@@ -214,9 +214,11 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
     const bool tma = getenv("GX_NO_TMA_IM2COL") == nullptr;
     const char* e = getenv("GX_KPS");
     const int want = e ? atoi(e) : (a.BN <= 64 ? 2 : 1);
-    if (tma && want == 2 && a.num_kb >= 2) {
+    for (int kk = want; kk >= 2 && a.kps == 1; --kk) {
       int nres2 = 0;
-      if (conv_pick_stages(a.BN, a.num_kb, a.res != nullptr || a.ystore, a.Cout, &nres2, 2) >= 3) a.kps = 2;
+      if (tma && kk <= 3 && a.num_kb >= kk &&
+          conv_pick_stages(a.BN, a.num_kb, a.res != nullptr || a.ystore, a.Cout, &nres2, kk) >= 3)
+        a.kps = kk;
     }
   }
   a.stages = conv_pick_stages(a.BN, a.num_kb, a.res != nullptr || a.ystore, a.Cout, &a.nres, a.kps);
