@@ -1,0 +1,298 @@
+// K2 variant for 3x3 / stride-1 / pad-1 convolutions on wide images (ResNet layer1/layer2): the
+// A operand comes from ONE halo tile per 64-channel block instead of one im2col load per filter tap.
+//
+// An M tile covers BH whole output rows of one image laid out with a padded pitch Wp = W + 2:
+// virtual row u = i*Wp + j (i < BH output row, j < Wp; j >= W is a discarded column).  The halo
+// is the input rows h0-1 .. h0+BH, columns -1 .. W, fetched by one 4D tiled TMA with zero fill
+// for the padding, stored as [(BH+2)*Wp pixels][64 channels] with the 128-byte swizzle.  Tap
+// (r, s) of virtual row u reads halo pixel u + r*Wp + s, so the A operand of tap (r, s) is the
+// halo itself started (r*Wp + s) rows later: the nine MMAs of a channel block read one smem tile
+// at nine row offsets, and each input pixel crosses L2->SM
+// once per M tile instead of nine times.
+//
+// Roles (352 threads): warp 4 halo producer, warp 10 weight producer (bulk copies of the
+// pre-swizzled [kb][Cout][64] tiles, kb = tap*Cin/64 + cb), one elected lane of warp 5 issues the
+// MMAs, warps 0-3 and 6-9 run the epilogue (bias, ReLU, bf16, row-remapped stores).
+#include <cuda_bf16.h>
+
+#include "gx_internal.h"
+#include "gx_ptx.cuh"
+
+namespace gx {
+
+namespace {
+constexpr int kHaloRows = 256;                  // smem rows per halo buffer (>= 128 + 2*Wp + 2)
+constexpr int kHaloBytes = kHaloRows * 128;     // 32 KB
+
+struct HaloSmem {
+  uint8_t* halo;   // [2][kHaloBytes]
+  uint8_t* sB;     // [S][BN*128]
+  float* bias;
+  uint64_t *hfull, *hempty, *bfull, *bempty, *tfull, *tempty, *biasbar;
+  uint32_t* tslot;
+};
+
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+// K-major SW128 descriptor whose start may sit at any 128-byte row of a 1024-aligned atom: the
+// tensor core applies the 128-byte swizzle on absolute shared-memory address bits (as the TMA
+// wrote it), so the base-offset field stays 0 (measured: setting it to (addr >> 7) & 7 breaks
+// every tap but (0, 0); scripts/debug_halo.py).
+__device__ __forceinline__ uint64_t desc_sw128_row(uint32_t saddr) {
+  return ((static_cast<uint64_t>(saddr) >> 4) & 0x3FFFull) | (1ull << 16) | (64ull << 32) | (1ull << 46) |
+         (2ull << 61);
+}
+
+__global__ void __launch_bounds__(kConvTcThreads, 1)
+    conv_halo_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap hmap,
+                     const ConvArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int S_ = a.stages;
+  const int BN = a.BN;
+  const uint32_t b_bytes = static_cast<uint32_t>(BN) * 128u;
+  const int Wp = a.W + 2, BH = a.hBH, TPI = a.hTPI;
+  const int CB = a.Cin / 64;
+  const uint32_t hbytes = static_cast<uint32_t>(Wp * (BH + 2) * 128);
+  HaloSmem sp;
+  sp.halo = smem;
+  sp.sB = sp.halo + 2 * kHaloBytes;
+  sp.bias = reinterpret_cast<float*>(sp.sB + static_cast<size_t>(S_) * b_bytes);
+  sp.hfull = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sp.bias) + ((a.Cout * 4 + 1023) & ~1023));
+  sp.hempty = sp.hfull + 2;
+  sp.bfull = sp.hempty + 2;
+  sp.bempty = sp.bfull + S_;
+  sp.tfull = sp.bempty + S_;
+  sp.tempty = sp.tfull + 2;
+  sp.biasbar = sp.tempty + 2;
+  sp.tslot = reinterpret_cast<uint32_t*>(sp.biasbar + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 4) {
+    if (lane == 0) {
+      for (int i = 0; i < 2; ++i) {
+        mbar_init(&sp.hfull[i], 1);
+        mbar_init(&sp.hempty[i], 1);
+        mbar_init(&sp.tfull[i], 1);
+        mbar_init(&sp.tempty[i], 256);
+      }
+      for (int i = 0; i < S_; ++i) {
+        mbar_init(&sp.bfull[i], 1);
+        mbar_init(&sp.bempty[i], 1);
+      }
+      mbar_init(sp.biasbar, 1);
+      fence_barrier_init();
+    }
+    __syncwarp();
+    tmem_alloc(sp.tslot, a.tmem_cols);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *sp.tslot;
+  const uint32_t acc_stride = a.tmem_cols >> 1;
+  pdl_wait();
+
+  if (warp == 4) {
+    // ------------------------------------------------------------ halo producer
+    const bool issuer = elect_one();
+    if (issuer) tma_prefetch_desc(&hmap);
+    int hs = 0;
+    uint32_t hph = 0;
+    for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
+      const int m_blk = tile / a.n_tiles;
+      const int n = m_blk / TPI, h0 = (m_blk % TPI) * BH;
+      for (int cb = 0; cb < CB; ++cb) {
+        mbar_wait(&sp.hempty[hs], hph ^ 1);
+        if (issuer) {
+          mbar_arrive_expect_tx(&sp.hfull[hs], hbytes);
+          tma_load_4d(sp.halo + hs * kHaloBytes, &hmap, &sp.hfull[hs], cb * 64, -1, h0 - 1, n);
+        }
+        __syncwarp();
+        if (++hs == 2) {
+          hs = 0;
+          hph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 10) {
+    // ------------------------------------------------------------ weight producer
+    const bool issuer = elect_one();
+    if (issuer && !a.wsw) tma_prefetch_desc(&wmap);
+    int bs = 0;
+    uint32_t bph = 0;
+    for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
+      const int n_blk = tile % a.n_tiles;
+      for (int cb = 0; cb < CB; ++cb) {
+        for (int tap = 0; tap < 9; ++tap) {
+          const int kb = tap * CB + cb;
+          mbar_wait(&sp.bempty[bs], bph ^ 1);
+          if (issuer) {
+            uint8_t* dst = sp.sB + static_cast<size_t>(bs) * b_bytes;
+            mbar_arrive_expect_tx(&sp.bfull[bs], b_bytes);
+            if (a.wsw)
+              bulk_load(dst, a.wsw + (static_cast<size_t>(kb) * a.Cout + static_cast<size_t>(n_blk) * BN) * 128u,
+                        b_bytes, &sp.bfull[bs]);
+            else
+              tma_load_2d(dst, &wmap, &sp.bfull[bs], kb * kBK, n_blk * BN);
+          }
+          __syncwarp();
+          if (++bs == S_) {
+            bs = 0;
+            bph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 5) {
+    // ------------------------------------------------------------ MMA issuer
+    const bool issuer = elect_one();
+    int hs = 0, bs = 0, t = 0;
+    uint32_t hph = 0, bph = 0;
+    for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++t) {
+      const int acc = t & 1;
+      mbar_wait(&sp.tempty[acc], ((t >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem_base + acc * acc_stride;
+      for (int cb = 0; cb < CB; ++cb) {
+        mbar_wait(&sp.hfull[hs], hph);
+        tc_fence_after();
+        const uint32_t hbase = smem_u32(sp.halo + hs * kHaloBytes);
+        for (int tap = 0; tap < 9; ++tap) {
+          const int r = tap / 3, s = tap - r * 3;
+          mbar_wait(&sp.bfull[bs], bph);
+          tc_fence_after();
+          const uint64_t ad = desc_sw128_row(hbase + static_cast<uint32_t>(r * Wp + s) * 128u);
+          const uint64_t bd = umma_desc_sw128(sp.sB + static_cast<size_t>(bs) * b_bytes);
+          if (issuer) {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              umma_bf16(d, ad + 2 * kk, bd + 2 * kk, a.idesc, (cb | tap | kk) != 0);
+            umma_commit(&sp.bempty[bs]);
+          }
+          __syncwarp();
+          if (++bs == S_) {
+            bs = 0;
+            bph ^= 1;
+          }
+        }
+        if (issuer) umma_commit(&sp.hempty[hs]);
+        __syncwarp();
+        if (++hs == 2) {
+          hs = 0;
+          hph ^= 1;
+        }
+      }
+      if (issuer) umma_commit(&sp.tfull[acc]);
+      __syncwarp();
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (warps 0-3, 6-9)
+    const int q = warp & 3;
+    const int half = warp < 4 ? 1 : 0;
+    const int row = q * 32 + lane;  // virtual row u of the tile
+    const int i = row / Wp, j = row - (row / Wp) * Wp;
+    if (warp == 6 && lane == 0) {
+      mbar_arrive_expect_tx(sp.biasbar, static_cast<uint32_t>(a.Cout) * 4u);
+      bulk_load(sp.bias, a.bias, static_cast<uint32_t>(a.Cout) * 4u, sp.biasbar);
+    }
+    mbar_wait_sleepy(sp.biasbar, 0);
+    int t = 0;
+    for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++t) {
+      const int m_blk = tile / a.n_tiles, n_blk = tile % a.n_tiles;
+      const int n = m_blk / TPI, h = (m_blk % TPI) * BH + i;
+      const bool row_ok = i < BH && j < a.W && h < a.H;
+      const int nb0 = n_blk * BN;
+      const int ncols = min(BN, a.Cout - nb0);
+      const int acc = t & 1;
+      mbar_wait_sleepy(&sp.tfull[acc], (t >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + acc * acc_stride + (static_cast<uint32_t>(q * 32) << 16);
+      const uint32_t bias_s = smem_u32(sp.bias + nb0);
+      __nv_bfloat16* yrow = static_cast<__nv_bfloat16*>(a.y) +
+                            ((static_cast<size_t>(n) * a.H + h) * a.W + j) * a.y_ld + a.y_coff + nb0;
+      for (int c = half * 16; c < BN; c += 32) {
+        uint32_t v[16];
+        tmem_ld16(tbase + c, v);
+        tmem_ld_wait();
+        if (row_ok && c < ncols) {
+          float f[16];
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const float4 bb = lds_f4(bias_s + static_cast<uint32_t>(c + 4 * q4) * 4u);
+            f[4 * q4 + 0] = __uint_as_float(v[4 * q4 + 0]) + bb.x;
+            f[4 * q4 + 1] = __uint_as_float(v[4 * q4 + 1]) + bb.y;
+            f[4 * q4 + 2] = __uint_as_float(v[4 * q4 + 2]) + bb.z;
+            f[4 * q4 + 3] = __uint_as_float(v[4 * q4 + 3]) + bb.w;
+          }
+          if (a.act == GX_ACT_RELU) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) f[e] = fmaxf(f[e], 0.0f);
+          }
+          uint4* y4 = reinterpret_cast<uint4*>(yrow + c);
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            uint4 o;
+            o.x = pack_bf16x2(f[8 * e + 0], f[8 * e + 1]);
+            o.y = pack_bf16x2(f[8 * e + 2], f[8 * e + 3]);
+            o.z = pack_bf16x2(f[8 * e + 4], f[8 * e + 5]);
+            o.w = pack_bf16x2(f[8 * e + 6], f[8 * e + 7]);
+            y4[e] = o;
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&sp.tempty[acc]);
+    }
+  }
+  pdl_launch_dependents();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, a.tmem_cols);
+  }
+}
+}  // namespace
+
+size_t conv_halo_smem_bytes(int BN, int stages, int Cout) {
+  return 1024 + 2 * static_cast<size_t>(kHaloBytes) + static_cast<size_t>(stages) * BN * 128 +
+         ((static_cast<size_t>(Cout) * 4 + 1023) & ~size_t(1023)) + (2 * stages + 9) * 8 + 16;
+}
+
+int conv_halo_pick_stages(int BN, int Cout) {
+  const size_t budget = 220 * 1024;
+  const size_t fixed = conv_halo_smem_bytes(BN, 0, Cout);
+  int s = budget > fixed ? static_cast<int>((budget - fixed) / (static_cast<size_t>(BN) * 128 + 16)) : 0;
+  return s > 9 ? 9 : s;
+}
+
+cudaError_t launch_conv_halo(const CUtensorMap& wmap, const CUtensorMap& hmap, const ConvArgs& a, int grid,
+                             cudaStream_t s, bool pdl) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(conv_halo_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(kConvTcThreads, 1, 1);
+  cfg.dynamicSmemBytes = conv_halo_smem_bytes(a.BN, a.stages, a.Cout);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, conv_halo_kernel, wmap, hmap, a);
+}
+
+}  // namespace gx

@@ -128,6 +128,22 @@ unsigned long long* debug_trace_buffer() {
   return g_trace;
 }
 
+// NHWC input as a rank-4 (C, W, H, N) tiled map with a [64, box_w, box_h, 1] box (the halo of a
+// conv_halo_kernel M tile; negative / past-the-edge coordinates are zero-filled = padding).
+bool encode_tmap_halo_bf16(CUtensorMap* map, const void* base, int C, int W, int H, int N, int box_w, int box_h) {
+  PFN_encodeTiled_t fn = encode_fn();
+  if (fn == nullptr) return false;
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
+                        static_cast<cuuint64_t>(N)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(C) * 2, static_cast<cuuint64_t>(C) * 2 * W,
+                           static_cast<cuuint64_t>(C) * 2 * W * H};
+  cuuint32_t box[4] = {64, static_cast<cuuint32_t>(box_w), static_cast<cuuint32_t>(box_h), 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // ---------------------------------------------------------------- op planning
 int elem_size(int dtype) { return dtype == GX_F32 ? 4 : 2; }
 int64_t tensor_elems(const gx_tensor& t) { return static_cast<int64_t>(t.H) * t.W * t.C; }
@@ -187,6 +203,42 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
   a.M = k * a.Ho * a.Wo;
   a.Cout = op.Cout;
   a.m_tiles = (a.M + kBM - 1) / kBM;
+  // 3x3 / stride 1 / pad 1 on wide images: one halo tile per 64-channel block (conv_halo.cu)
+  const bool pad1 = a.ph == 1 && a.pw == 1 && (op.ph_hi < 0 || op.ph_hi == 1) && (op.pw_hi < 0 || op.pw_hi == 1);
+  if (!for_span && op.kind == GX_OP_CONV && R == 3 && S == 3 && a.sh == 1 && a.sw == 1 && pad1 && op.Cin % 64 == 0 &&
+      op.Cin == ti.C && a.Ho == ti.H && a.Wo == ti.W && ti.W >= 28 && ti.W + 2 <= 64 && op.in2 < 0 &&
+      to.dtype == GX_BF16 && getenv("GX_NO_HALO") == nullptr) {
+    const int Wp = ti.W + 2;
+    a.halo = 1;
+    a.hBH = std::min(ti.H, kBM / Wp);
+    a.hTPI = (ti.H + a.hBH - 1) / a.hBH;
+    a.m_tiles = k * a.hTPI;
+    a.BN = pick_bn(op.Cout, a.m_tiles, sm_budget, bn_cap);
+    a.n_tiles = (a.Cout + a.BN - 1) / a.BN;
+    a.num_tiles = a.m_tiles * a.n_tiles;
+    a.bias = reinterpret_cast<const float*>(wbase + op.b_off);
+    a.y = ptrs[op.out];
+    a.y_ld = to.C;
+    a.y_coff = op.out_coff;
+    a.act = op.act;
+    a.idesc = umma_idesc_bf16(kBM, a.BN);
+    a.stages = conv_halo_pick_stages(a.BN, a.Cout);
+    a.tmem_cols = tmem_cols_for(a.BN);
+    a.wsw = getenv("GX_NO_WBULK") ? nullptr : wsw;
+    a.dbg = getenv("GX_CONV_DBG") ? atoi(getenv("GX_CONV_DBG")) : 0;
+    a.tma_a = 1;
+    const int kpad = a.num_kb * kBK;
+    memset(&out->amap, 0, sizeof(out->amap));
+    memset(&out->rmap, 0, sizeof(out->rmap));
+    memset(&out->ymap, 0, sizeof(out->ymap));
+    if (!encode_tmap_2d_bf16(&out->wmap, wbase + op.w_off, kpad, op.Cout, static_cast<uint64_t>(kpad) * 2, kBK, a.BN))
+      return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for conv weights: " + g_last_encode);
+    if (!encode_tmap_halo_bf16(&out->amap, a.x, ti.C, ti.W, ti.H, k, Wp, a.hBH + 2))
+      return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for the conv halo");
+    if (a.stages < 2) return fail(GX_EINVAL, "halo conv: shared memory too small for the weight ring");
+    out->grid = std::min(a.num_tiles, std::max(1, sm_budget));
+    return GX_OK;
+  }
   a.BN = pick_bn(op.Cout, a.m_tiles, sm_budget, bn_cap);
   if (const char* e = getenv("GX_BN")) {  // tuning override (development)
     const int bn = atoi(e);
@@ -333,7 +385,10 @@ int launch_op(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
         if (rc != GX_OK) return rc;
         pre = &cl;
       }
-      GX_CUDA(launch_conv(pre->wmap, pre->amap, pre->rmap, pre->ymap, pre->args, pre->grid, s, pdl));
+      if (pre->args.halo)
+        GX_CUDA(launch_conv_halo(pre->wmap, pre->amap, pre->args, pre->grid, s, pdl));
+      else
+        GX_CUDA(launch_conv(pre->wmap, pre->amap, pre->rmap, pre->ymap, pre->args, pre->grid, s, pdl));
       break;
     }
     case GX_OP_MAXPOOL:

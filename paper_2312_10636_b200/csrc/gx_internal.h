@@ -57,6 +57,8 @@ struct ConvArgs {
   int kps;  // k-blocks per pipeline stage (1 or 2; 2 only with TMA-built A)
   unsigned long long* trace;  // dbg & 16: per-iteration clock64 stamps of CTA 0 (development)
   const uint8_t* wsw;  // B tiles by plain bulk copy from the pre-swizzled [kb][Cout][64] layout (or null)
+  int halo;            // 3x3/s1/p1 wide-image conv on conv_halo_kernel (amap = the 4D halo map)
+  int hBH, hTPI;       // halo: output rows per M tile, M tiles per image
 };
 constexpr int kConvThreads = 320;  // span kernel: 4 A-producer warps, TMA warp, MMA warp, 4 epilogue warps
 // conv_tc: warps 0-3 cp.async A producers (or epilogue when TMA builds A), 4 A/B TMA, 5 MMA,
@@ -70,6 +72,11 @@ int conv_pick_stages(int BN, int num_kb, bool res, int Cout, int* nres_out, int 
 // ymap: output [M][y_ld] (ystore).
 cudaError_t launch_conv(const CUtensorMap& wmap, const CUtensorMap& amap, const CUtensorMap& rmap,
                         const CUtensorMap& ymap, const ConvArgs& a, int grid, cudaStream_t s, bool pdl);
+size_t conv_halo_smem_bytes(int BN, int stages, int Cout);
+int conv_halo_pick_stages(int BN, int Cout);
+cudaError_t launch_conv_halo(const CUtensorMap& wmap, const CUtensorMap& hmap, const ConvArgs& a, int grid,
+                             cudaStream_t s, bool pdl);
+bool encode_tmap_halo_bf16(CUtensorMap* map, const void* base, int C, int W, int H, int N, int box_w, int box_h);
 bool encode_tmap_im2col_bf16(CUtensorMap* map, const void* base, int C, int W, int H, int N, int lower_w,
                              int lower_h, int upper_w, int upper_h, int stride_w, int stride_h, int cpl);
 

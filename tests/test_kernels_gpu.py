@@ -80,6 +80,11 @@ def _conv_case(k, H, W, Cin, Cout, R, S, stride, pad, residual, relu, cin_pad=No
         (2, 35, 35, 64, 96, 5, 5, 1, 2, False, True),         # 5x5
         (16, 7, 7, 512, 512, 3, 3, 1, 1, True, True),         # tail tile + residual
         (3, 14, 14, 1024, 2048, 1, 1, 2, 0, False, False),    # downsample into layer4
+        # halo path (conv_halo.cu): 3x3/s1/p1, Cin % 64 == 0, W >= 28
+        (1, 56, 56, 64, 64, 3, 3, 1, 1, False, True),         # layer1 3x3 at k=1 (BH=2)
+        (3, 28, 28, 128, 128, 3, 3, 1, 1, False, True),       # layer2 3x3 (BH=4)
+        (2, 35, 35, 64, 96, 3, 3, 1, 1, False, True),         # Inception 35x35 (BH=3, last tile short)
+        (2, 30, 30, 128, 192, 3, 3, 1, 1, False, False),      # W+2 = 32, BN not a power of two
     ],
 )
 def test_conv_matches_torch(k, H, W, Cin, Cout, R, S, stride, pad, residual, relu):
