@@ -1,7 +1,4 @@
-timeout 300 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-python scripts/bench_conv.py l1_3x3_64_k8,l1_3x3_k1 3
-GX_NO_HALO=1 python scripts/bench_conv.py l1_3x3_64_k8,l1_3x3_k1 3 | sed 's/^/nohalo /'
-for v in 0 1; do
-if [ $v = 1 ]; then export GX_NO_HALO=1; else unset GX_NO_HALO; fi
-timeout 300 python scripts/kernel_roofline.py --points 1:18:16:4,0:18:8:3,0:18:1:2,2:18:4:2 --out gpurun_out/kr_halo$v.csv 2>&1 | grep span | sed "s/^/nohalo=$v /" | cut -c1-110
-done
+for ns in 30 64 128; do for tc in resnet50_s1.5:1472 resnet50_s1.5:1536 resnet50_s1.5:1600; do
+tag=${tc%%:*}; c=${tc##*:}
+GX_SERVE_STREAMS=$ns timeout 300 python bench.py --plans $tag --clients $c --no-cpu-baseline --steps 3 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('streams=$ns $tag $c', d['value'], d['p99_ms'], 'e2e', d['e2e']['value'], d['e2e']['p99_ms'])"
+done; done
