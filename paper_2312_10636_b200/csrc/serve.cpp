@@ -150,7 +150,7 @@ struct gx_serve {
   double wall_ms = 0.0;
   int64_t n_batches = 0, n_kernels = 0;
   int64_t drops_no_slot = 0;
-  double host_dispatch_ms = 0.0, host_poll_ms = 0.0;  // diagnostics (GX_SERVE_DEBUG)
+  double host_dispatch_ms = 0.0, host_poll_ms = 0.0, host_copy_ms = 0.0;  // diagnostics (GX_SERVE_DEBUG)
   int64_t loop_iters = 0;
   size_t max_inflight_seen = 0;
   std::chrono::steady_clock::time_point t0;
@@ -262,6 +262,7 @@ int gx_serve::arrive(int ri, double now) {
           h2d_events.push_back(ev);
           free_h2d.push_back(static_cast<int>(h2d_events.size()) - 1);
         }
+        const double t_c = now_wall();
         const int ei = free_h2d.back();
         free_h2d.pop_back();
         cudaStream_t cs = copy_streams[n_h2d++ % copy_streams.size()];
@@ -269,6 +270,7 @@ int gx_serve::arrive(int ri, double now) {
         GX_CUDA(cudaEventRecord(h2d_events[ei], cs));
         r.h2d_ev = ei;
         r.cur = dst;
+        host_copy_ms += now_wall() - t_c;
       }
     }
   }
@@ -557,8 +559,8 @@ int gx_serve::run() {
   }
   wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   if (cfg.clock == GX_CLOCK_WALL && getenv("GX_SERVE_DEBUG")) {
-    fprintf(stderr, "[serve] wall=%.0fms batches=%lld host_dispatch=%.0fms (%.1fus/batch) loop_iters=%lld max_inflight=%zu\n",
-            wall_ms, static_cast<long long>(n_batches), host_dispatch_ms,
+    fprintf(stderr, "[serve] wall=%.0fms batches=%lld host_copy=%.0fms host_dispatch=%.0fms (%.1fus/batch) loop_iters=%lld max_inflight=%zu\n",
+            wall_ms, static_cast<long long>(n_batches), host_copy_ms, host_dispatch_ms,
             n_batches ? 1000.0 * host_dispatch_ms / n_batches : 0.0, static_cast<long long>(loop_iters),
             max_inflight_seen);
     for (size_t i = 0; i < stages.size(); ++i) {
