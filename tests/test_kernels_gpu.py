@@ -7,6 +7,7 @@ bit-exact.
 import pytest
 import torch
 import torch.nn.functional as F
+from paper_2312_10636_b200.errors import ValidationError
 
 pytestmark = pytest.mark.gpu
 
@@ -249,3 +250,42 @@ def test_attention_matches_torch(k, S, heads):
            torch.zeros(256, device="cuda"), k, 30)
     torch.cuda.synchronize()
     assert _rel(y.float().cpu(), ref) < 1.5e-2
+
+
+def test_gather_scatter_max_batch_ragged():
+    """The largest dispatched batch the ABI takes (64 rows), every row from its own buffer, fp32 and
+    bf16 sources interleaved at odd sizes: bit-exact."""
+    import ctypes as C
+    from paper_2312_10636_b200.device import context
+    ctx = context(0)
+    k, pix, Cc = 64, 7 * 7, 2048
+    srcs = [torch.randn(pix * Cc, device="cuda").to(torch.bfloat16 if i % 3 else torch.float32) for i in range(k)]
+    dts = [N.GX_F32 if t.dtype == torch.float32 else N.GX_BF16 for t in srcs]
+    dst = torch.empty(k, pix * Cc, dtype=torch.bfloat16, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    N.check(N.lib().gx_gather(ctx.handle, k, N.ptr_array([t.data_ptr() for t in srcs]), N.i32_array(dts), pix, Cc,
+                              Cc, C.c_void_p(dst.data_ptr()), 3, C.c_void_p(s)))
+    torch.cuda.synchronize()
+    for i in range(k):
+        assert torch.equal(dst[i], srcs[i].to(torch.bfloat16)), i
+    with pytest.raises(ValidationError):
+        N.check(N.lib().gx_gather(ctx.handle, 65, N.ptr_array([srcs[0].data_ptr()] * 65), N.i32_array(dts[:1] * 65),
+                                  pix, Cc, Cc, C.c_void_p(dst.data_ptr()), 3, C.c_void_p(s)))
+
+
+def test_stage_batch_sizes_share_one_instance():
+    """One stage instance serves k = 1 .. max_batch (a CUDA graph per k, one workspace): each batch
+    size gives the same per-request output, and k outside 1..max_batch is rejected."""
+    from paper_2312_10636_b200.engine import DeviceModel, StageInstance
+    from paper_2312_10636_b200.models import build_chain
+    chain = build_chain("resnet18")
+    dm = DeviceModel(chain, 0)
+    st = StageInstance(dm, 6, chain.n_units, max_batch=8, sm_budget=3)
+    x = [torch.rand(chain.boundary_elems(6), device="cuda") for _ in range(8)]
+    full = st.run(x)
+    for k in (1, 3, 8):
+        part = st.run(x[:k])
+        for i in range(k):
+            assert torch.equal(part[i], full[i]), (k, i)
+    with pytest.raises(ValidationError):
+        st.run(x + x[:1])

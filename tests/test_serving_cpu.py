@@ -96,3 +96,13 @@ def test_churn_plan_transitions_match_reference():
     assert [list(r) for r in rep.requests] == exp["requests"]
     assert rep.dispatch == [(t, s, k, tuple(q)) for t, s, k, q in exp["dispatch"]]
     assert {s for _t, s, _k, _q in rep.dispatch} == {0, 1, 2}  # every epoch's stage served batches
+
+
+def test_empty_fleet_and_zero_horizon():
+    """Edge cases of the event loop: no clients, and a horizon shorter than the first arrival."""
+    doc, dep, clients, latency = _load("closed_partial_batch")
+    rep = serve(dep, [], 1.0, latency=latency)
+    assert (rep.generated, rep.completed, rep.dropped) == (0, 0, 0)
+    assert rep.latency_p99_ms is None and rep.requests_csv().count("\n") == 1
+    rep = serve(dep, clients, 0.0, latency=latency)
+    assert rep.completed == 0
