@@ -300,8 +300,8 @@ def run_ours(args):
             e2e_fleet = Fleet(cands.pop(0))
             res_e2e = one_run(e2e_fleet, host=True)
 
-    # roofline of the dominant kernel, conv_tc_kernel (>=90% of GPU time in every launch list
-    # under profiles/): the busiest stage's span, each conv launched alone on the stage's stream
+    # roofline of the dominant kernel, the implicit-GEMM conv (conv_tc_kernel, plus conv_halo_kernel
+    # for wide 3x3 layers: >=90% of GPU time in every launch list under profiles/): the busiest stage's span, each conv launched alone on the stage's stream
     # and timed with CUDA events (gx_stage_profile_ops), algorithmic FLOPs = 2*M*N*K unpadded per
     # launch, peak = measured burst bf16 x (stage SM budget / SMs) since the kernel is timed alone.
     def stage_flops(i):
@@ -371,7 +371,8 @@ def run_ours(args):
                     "h2d_bytes_per_step": int(stats[6].item() / K), "d2h_bytes_per_step": int(stats[7].item() / K)},
             "gpu_launches": int(stats[4].item()),
             "roofline": {"bound": "tensor",
-                         "kernel": f"conv_tc_kernel x{len(convs)} launches of span [{st.start},{st.end}) k={st.batch} "
+                         "kernel": f"implicit-GEMM conv (conv_tc_kernel / conv_halo_kernel) x{len(convs)} launches of "
+                                   f"span [{st.start},{st.end}) k={st.batch} "
                                    f"on {inst.sm_budget} SMs (busiest stage, planned share {st.share}%)",
                          "achieved": round(achieved, 2), "peak": round(peak_scaled, 2), "unit": "TFLOP/s",
                          "frac": round(achieved / peak_scaled, 4), "traffic": traffic,

@@ -9,7 +9,7 @@ print(":".join(m.groups()))
 PY
 )
 IFS=: read A B K BUD <<< "$KEY"
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:conv_tc -c 60 -o /tmp/stage_conv python scripts/ncu_stage.py resnet50 $A $B $K $BUD > gpurun_out/ncu_stage.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:'conv_(tc|halo)_kernel' -c 60 -o /tmp/stage_conv python scripts/ncu_stage.py resnet50 $A $B $K $BUD > gpurun_out/ncu_stage.log 2>&1
 python scripts/ncu_conv_summary.py /tmp/stage_conv.ncu-rep resnet50:$A:$B:$K:$BUD
 cp profiles/ncu_conv_summary.json gpurun_out/
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches_serving.csv python bench.py --clients 256 --steps 1 --warmup 3 --window 0.25 --no-cpu-baseline > /dev/null 2>&1

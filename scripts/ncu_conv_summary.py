@@ -31,7 +31,8 @@ def val(r, name):
 
 launches = []
 for r in rows[2:]:
-    if "conv_tc_kernel" not in r[hdr.index("Kernel Name")]:
+    name = r[hdr.index("Kernel Name")]
+    if "conv_tc_kernel" not in name and "conv_halo_kernel" not in name:
         continue
     launches.append({
         "us": val(r, "gpu__time_duration.sum"),
