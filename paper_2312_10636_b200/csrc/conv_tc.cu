@@ -86,8 +86,10 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
   const CUtensorMap* YM = &ymap;
   const int S_ = a.stages;
   const int BN = a.BN;
-  const bool has_res = a.res != nullptr;
+  const bool has_res = a.res != nullptr && !a.res_mma;  // residual added in the epilogue
   const bool ystore = a.ystore != 0;
+  // k-blocks per tile: the conv's K, plus (res_mma) BN/64 residual x identity blocks
+  const int nkb_tile = a.num_kb + (a.res_mma ? BN / 64 : 0);
   const uint32_t b_bytes = static_cast<uint32_t>(BN) * 128u;
   SmemPlan sp;
   sp.sA = smem;
@@ -237,10 +239,10 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
       // packed weights are zero, so they contribute nothing.
       int c0 = 0, r = 0, s = 0;
       const uint8_t* wsrc = a.wsw ? a.wsw + static_cast<size_t>(n_blk) * BN * 128u : nullptr;
-      for (int kb0 = 0; kb0 < a.num_kb; kb0 += KPS, ++it) {
+      for (int kb0 = 0; kb0 < nkb_tile; kb0 += KPS, ++it) {
         pipe_wait(&sp.empty[st], ph ^ 1, issuer);
         if (issuer && warp == 4 && a.trace && blockIdx.x == 0 && it < 8192) a.trace[it * 4 + 0] = clock64();
-        const int nk = min(KPS, a.num_kb - kb0);
+        const int nk = min(KPS, nkb_tile - kb0);
         if (issuer) {
           if (tx)
             mbar_arrive_expect_tx(&sp.full[st], tx * nk);
@@ -251,7 +253,10 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
         const int kb = kb0 + j;
         uint8_t* const sa = sp.sA + st * sa_bytes + j * kATileBytes;
         uint8_t* const sb = sp.sB + static_cast<size_t>(st) * sb_bytes + j * b_bytes;
-        if (do_a) {
+        if (do_a && kb >= a.num_kb) {
+          // residual x identity block: A = residual columns [nb0 + 64*(kb - num_kb), +64)
+          if (issuer && !skipA) tma_load_2d(sa, RM, &sp.full[st], n_blk * BN + (kb - a.num_kb) * 64, m_blk * kBM);
+        } else if (do_a) {
           if (a.a2d) {
             // 1x1 / stride 1 / no padding: A is the plain [M, C] activation matrix
             if (issuer && !skipA) tma_load_2d(sa, AM, &sp.full[st], kb * kBK, m_blk * kBM);
@@ -272,8 +277,10 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
           }
         }
         if (do_b && !skipB && issuer) {
+          // identity blocks sit at kb = num_kb + column/64: this tile's are num_kb + nb0/64 + j
+          const int kbw = kb < a.num_kb ? kb : kb + n_blk * BN / 64;
           if (wsrc)  // pre-swizzled tile: one contiguous bulk copy (no tensor-map walk)
-            bulk_load(sb, wsrc + static_cast<size_t>(kb) * a.Cout * 128u, b_bytes, &sp.full[st]);
+            bulk_load(sb, wsrc + static_cast<size_t>(kbw) * a.Cout * 128u, b_bytes, &sp.full[st]);
           else
             tma_load_2d(sb, WM, &sp.full[st], kb * kBK, n_blk * BN);
         }
@@ -297,7 +304,7 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
       if (issuer && a.trace && blockIdx.x == 0 && t < 4096) a.trace[8 * 8192 + t] = clock64();
       tc_fence_after();
       const uint32_t d = tmem_base + acc * acc_stride;
-      for (int kb0 = 0; kb0 < a.num_kb; kb0 += KPS, ++it, st = (st + 1 == S_) ? 0 : st + 1, ph ^= (st == 0)) {
+      for (int kb0 = 0; kb0 < nkb_tile; kb0 += KPS, ++it, st = (st + 1 == S_) ? 0 : st + 1, ph ^= (st == 0)) {
         pipe_wait(&sp.full[st], ph, issuer);
         if (issuer && a.trace && blockIdx.x == 0 && it < 8192) a.trace[it * 4 + 1] = clock64();
         tc_fence_after();
@@ -306,7 +313,7 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
           __syncwarp();
           continue;
         }
-        const int nk = min(KPS, a.num_kb - kb0);
+        const int nk = min(KPS, nkb_tile - kb0);
         for (int jj = 0; jj < nk; ++jj) {
         const int kb = kb0 + jj;
         const uint32_t abase = smem_u32(sp.sA + st * sa_bytes + jj * kATileBytes);

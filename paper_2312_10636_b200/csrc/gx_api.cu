@@ -259,6 +259,12 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
   // never writes past its own channel slice of a concat tensor)
   a.ystore = !a.y_f32 && a.BN % 64 == 0 && a.Cout % 64 == 0 && to.C >= 64 && getenv("GX_NO_YSTORE") == nullptr &&
              getenv("GX_GMAPS") == nullptr;
+  // residual through the tensor core (identity k-blocks): needs the bulk-weight layout, the 2D A
+  // path and whole 64-column groups; the epilogue then runs residual-free
+  a.res_mma = !for_span && a.res && wsw && !getenv("GX_NO_WBULK") && res_through_mma(op) && a.BN % 64 == 0 &&
+              a.Cin == ti.C && getenv("GX_NO_TMA_IM2COL") == nullptr && getenv("GX_NO_A2D") == nullptr &&
+              getenv("GX_NO_RES_MMA") == nullptr;
+  const bool epi_res = a.res != nullptr && !a.res_mma;  // residual handled by the epilogue
   // two k-blocks per pipeline stage halve the barrier round trips per unit of K; worth it when the
   // per-k-block MMA time (2*BN cycles) is below the ~500-cycle stage round trip and >= 3 stages fit
   a.kps = 1;
@@ -266,14 +272,15 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
     const bool tma = getenv("GX_NO_TMA_IM2COL") == nullptr;
     const char* e = getenv("GX_KPS");
     const int want = e ? atoi(e) : (a.BN <= 64 ? 2 : 1);
-    for (int kk = want; kk >= 2 && a.kps == 1; --kk) {
+    for (int kk = want; kk >= 2 && a.kps == 1 && !a.res_mma; --kk) {
       int nres2 = 0;
       if (tma && kk <= 3 && a.num_kb >= kk &&
-          conv_pick_stages(a.BN, a.num_kb, a.res != nullptr || a.ystore, a.Cout, &nres2, kk) >= 3)
+          conv_pick_stages(a.BN, a.num_kb, epi_res || a.ystore, a.Cout, &nres2, kk) >= 3)
         a.kps = kk;
     }
   }
-  a.stages = conv_pick_stages(a.BN, a.num_kb, a.res != nullptr || a.ystore, a.Cout, &a.nres, a.kps);
+  a.stages = conv_pick_stages(a.BN, a.num_kb + (a.res_mma ? a.BN / 64 : 0), epi_res || a.ystore, a.Cout, &a.nres,
+                              a.kps);
   if (const char* e = getenv("GX_STAGES")) {
     const int st = atoi(e);
     if (st >= 1 && st <= a.stages) a.stages = st;
@@ -287,7 +294,7 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
   memset(&out->amap, 0, sizeof(out->amap));
   memset(&out->rmap, 0, sizeof(out->rmap));
   memset(&out->ymap, 0, sizeof(out->ymap));
-  a.wstore = !for_span && a.ystore && (!a.res || getenv("GX_NO_WRES") == nullptr) && getenv("GX_NO_TMA_IM2COL") == nullptr &&
+  a.wstore = !for_span && a.ystore && (!epi_res || getenv("GX_NO_WRES") == nullptr) && getenv("GX_NO_TMA_IM2COL") == nullptr &&
              a.BN % 128 == 0 && getenv("GX_NO_WSTORE") == nullptr;
   if (a.ystore && !encode_tmap_2d_bf16(&out->ymap, a.y, to.C, a.M, static_cast<uint64_t>(to.C) * 2, 64,
                                        a.wstore ? 32 : kBM))
@@ -306,7 +313,7 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
                                                  (op.ph_hi >= 0 ? op.ph_hi : a.ph) - (a.R - 1), a.sw, a.sh, a.cpl))
     return fail(GX_ECUDA, "cuTensorMapEncodeIm2col failed for conv input");
   if (a.res && !encode_tmap_2d_bf16(&out->rmap, a.res, a.res_ld, a.M, static_cast<uint64_t>(a.res_ld) * 2, 64,
-                                    a.wstore ? 32 : kBM))
+                                    (a.wstore && !a.res_mma) ? 32 : kBM))
     return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for the residual: " + g_last_encode);
   out->grid = std::min(a.num_tiles, std::max(1, sm_budget));
   a.gmaps = nullptr;

@@ -57,6 +57,8 @@ struct ConvArgs {
   int kps;  // k-blocks per pipeline stage (1 or 2; 2 only with TMA-built A)
   unsigned long long* trace;  // dbg & 16: per-iteration clock64 stamps of CTA 0 (development)
   const uint8_t* wsw;  // B tiles by plain bulk copy from the pre-swizzled [kb][Cout][64] layout (or null)
+  int res_mma;         // residual added by the MMA: BN/64 extra k-blocks per tile, A = residual tile
+                       // (rmap, box 64 x 128), B = identity blocks at kb = num_kb + col/64 (wsw)
   int halo;            // 3x3/s1/p1 wide-image conv on conv_halo_kernel (amap = the 4D halo map)
   int hBH, hTPI;       // halo: output rows per M tile, M tiles per image
 };

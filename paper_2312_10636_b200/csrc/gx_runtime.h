@@ -37,6 +37,13 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
 int launch_op(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint8_t* wbase, int k, int sm_budget,
               cudaStream_t s, bool pdl, const ConvLaunch* pre, int* kernels);
 unsigned long long* debug_trace_buffer();
+// 1x1 / stride-1 / unpadded convs with a residual: the residual is added by the tensor core through
+// identity k-blocks appended to the op's pre-swizzled weights (the epilogue then has no residual
+// traffic), when the op's planning confirms the 2D A path (plan_conv).
+inline bool res_through_mma(const gx_op& op) {
+  return op.kind == GX_OP_CONV && op.in2 >= 0 && op.R == 1 && op.S == 1 && op.sh == 1 && op.sw == 1 && op.ph == 0 &&
+         op.pw == 0 && op.Cout % 64 == 0 && op.Cin % 64 == 0;
+}
 void op_work(const gx_op& op, const gx_tensor* T, int k, double* flops, double* bytes);
 }  // namespace gx
 

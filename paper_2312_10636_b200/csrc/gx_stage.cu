@@ -265,6 +265,7 @@ int build_span_program(gx_stage* st, int k, gx_stage::PerK* out) {
 // shared memory exactly as a SWIZZLE_128B tensor-map load would (tiles start at multiples of 16
 // rows).  One extra k-block of slack lets a partial last N tile over-read harmlessly.
 cudaError_t build_bulk_weights(gx_model* m, const uint8_t* blob) {
+  // (res_through_mma: see gx_runtime.h)
   const int n = static_cast<int>(m->ops.size());
   m->wsw_off.assign(n, -1);
   size_t total = 0;
@@ -274,7 +275,7 @@ cudaError_t build_bulk_weights(gx_model* m, const uint8_t* blob) {
     const int R = op.kind == GX_OP_LINEAR ? 1 : op.R, S = op.kind == GX_OP_LINEAR ? 1 : op.S;
     const size_t kpad = (static_cast<size_t>(R) * S * op.Cin + 63) / 64 * 64;
     m->wsw_off[i] = static_cast<int64_t>(total);
-    total += kpad * op.Cout * 2;
+    total += (kpad + (res_through_mma(op) ? op.Cout : 0)) * op.Cout * 2;
   }
   if (total == 0) return cudaSuccess;
   total += 256 * 128;
@@ -292,6 +293,16 @@ cudaError_t build_bulk_weights(gx_model* m, const uint8_t* blob) {
         for (int j = 0; j < 8; ++j)
           std::memcpy(dst + ((kb * op.Cout + row) * 8 + (j ^ (row & 7))) * 16,
                       src + (static_cast<size_t>(row) * kpad + kb * 64 + j * 8) * 2, 16);
+    if (res_through_mma(op)) {
+      // identity k-blocks kb = nkb + c/64: B[row][c] = (row == c), so the residual tile fed as the
+      // A operand of those k-blocks is added by the tensor core in fp32
+      const uint16_t one = 0x3F80;  // bf16 1.0
+      for (int row = 0; row < op.Cout; ++row) {
+        const size_t kb = nkb + row / 64;
+        const int c = row % 64, j = c / 8, e = c % 8;
+        std::memcpy(dst + ((kb * op.Cout + row) * 8 + (j ^ (row & 7))) * 16 + e * 2, &one, 2);
+      }
+    }
   }
   cudaError_t e = cudaMalloc(&m->wsw, total);
   if (e == cudaSuccess) e = cudaMemcpy(m->wsw, h.data(), total, cudaMemcpyHostToDevice);

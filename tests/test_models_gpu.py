@@ -122,10 +122,12 @@ def test_inception_end_to_end_within_framework_bf16_error():
 def test_span_kernel_matches_per_op_path(budget, monkeypatch):
     """The single-launch persistent span kernel (GX_EXEC=span) and the per-op graph path run the
     same tiles in the same K order: identical outputs.  (The per-op path's halo kernel for wide
-    3x3 convs sums K in channel-block-major order; it is held to the torch reference by the
-    kernel and model tests, and switched off here so both sides use the tap-major order.)"""
+    3x3 convs sums K in channel-block-major order and its residual convs add the residual inside
+    the MMA; both are held to the torch reference by the kernel and model tests and switched off
+    here, so the two sides sum in the same order.)"""
     from paper_2312_10636_b200.engine import StageInstance
     monkeypatch.setenv("GX_NO_HALO", "1")
+    monkeypatch.setenv("GX_NO_RES_MMA", "1")
     m, chain, dm = _setup("resnet50")
     x = torch.randn(3, 3, 224, 224, generator=torch.Generator().manual_seed(5))
     inp = _inputs(x)
