@@ -261,7 +261,10 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
              getenv("GX_GMAPS") == nullptr;
   // residual through the tensor core (identity k-blocks): needs the bulk-weight layout, the 2D A
   // path and whole 64-column groups; the epilogue then runs residual-free
+  // only where the epilogue dominates (K <= 128: layer1/2 expands); for K >= 256 the extra BN/64
+  // identity k-blocks cost more MMA time than the epilogue add they remove (measured)
   a.res_mma = !for_span && a.res && wsw && !getenv("GX_NO_WBULK") && res_through_mma(op) && a.BN % 64 == 0 &&
+              a.num_kb <= 2 &&
               a.Cin == ti.C && getenv("GX_NO_TMA_IM2COL") == nullptr && getenv("GX_NO_A2D") == nullptr &&
               getenv("GX_NO_RES_MMA") == nullptr;
   const bool epi_res = a.res != nullptr && !a.res_mma;  // residual handled by the epilogue
