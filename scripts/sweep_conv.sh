@@ -1,4 +1,3 @@
-for ns in 30 64 128; do for tc in resnet50_s1.5:1472 resnet50_s1.5:1536 resnet50_s1.5:1600; do
-tag=${tc%%:*}; c=${tc##*:}
-GX_SERVE_STREAMS=$ns timeout 300 python bench.py --plans $tag --clients $c --no-cpu-baseline --steps 3 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('streams=$ns $tag $c', d['value'], d['p99_ms'], 'e2e', d['e2e']['value'], d['e2e']['p99_ms'])"
+for ncs in 4 1 16; do for c in 1152 1280; do
+GX_COPY_STREAMS=$ncs timeout 300 python bench.py --plans resnet50 --clients $c --no-cpu-baseline --steps 3 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('copy=$ncs $c', d['value'], d['p99_ms'], 'e2e', d['e2e']['value'], d['e2e']['p99_ms'])"
 done; done
