@@ -55,7 +55,7 @@ def _workloads(name: str, all_plans: bool = False):
     pats = [f"{name}_c[0-9]*.json"] + ([f"{name}_s*_c[0-9]*.json"] if all_plans else [])
     files = [f for pat in pats for f in glob.glob(str(ROOT / "tests" / "golden" / "workload" / pat))]
     docs = [json.loads(Path(f).read_text()) for f in files]
-    return sorted(docs, key=lambda d: (d["clients_n"], d.get("latency_scale", 1.0)))
+    return sorted(docs, key=lambda d: (d["clients_n"], d.get("latency_scale", 1.0), -d.get("merge_threshold", 0.2)))
 
 
 def _workload(name: str, clients: int | None):
@@ -195,9 +195,11 @@ def run_ours(args):
         return ok
 
     # the achievable-throughput search runs over every planned fleet of the model: plans made
-    # against the measured table and against the load-calibrated table (make_workload.py --scale)
+    # against the measured table and against the load-calibrated table (make_workload.py --scale),
+    # with the reference's default merge threshold and a lower one (--merge 0.05: fewer, larger
+    # merged fragments -> fewer stage instances competing for the 32 hardware queues)
     workloads = _workloads(args.plans or args.model, all_plans=args.plans is None)
-    key = lambda w: (w["clients_n"], w.get("latency_scale", 1.0))  # noqa: E731
+    key = lambda w: (w["clients_n"], w.get("latency_scale", 1.0), -w.get("merge_threshold", 0.2))  # noqa: E731
     if args.clients is not None:
         fleet = Fleet(_workload(args.plans or args.model, args.clients))
     else:
@@ -210,7 +212,8 @@ def run_ours(args):
             rep = cand.serve(3.0)
             ok = p99_of(rep, 1000.0) <= wl["slo_ms"] and rep.dropped <= 0.01 * max(1, rep.generated)
             if rank == 0:
-                print(f"# probe clients={wl['clients_n']} scale={wl.get('latency_scale', 1.0)}: "
+                print(f"# probe clients={wl['clients_n']} scale={wl.get('latency_scale', 1.0)} "
+                      f"merge={wl.get('merge_threshold', 0.2)}: "
                       f"p99={p99_of(rep, 1000.0):.1f} ms "
                       f"met/s={rep.slo_met / 3.0:.0f} -> {'ok' if ok else 'over'}", file=sys.stderr, flush=True)
             if all_ok(ok):
@@ -352,6 +355,7 @@ def run_ours(args):
                                    f"{wl['rate_rps']:.0f} rps per GPU, 8 cut points, plan from the reference planner "
                                    f"on the measured B200 profile table, SM-share partitioning",
                        "model": args.model, "latency_scale": wl.get("latency_scale", 1.0),
+                       "merge_threshold": wl.get("merge_threshold", 0.2),
                        "clients_per_gpu": wl["clients_n"], "offered_rps_per_gpu":
                            wl["clients_n"] * wl["rate_rps"], "slo_ms": round(slo, 3), "window_s": window,
                        "stages": len(dep.stages), "instances": sum(s.instances for s in dep.stages),
@@ -362,6 +366,7 @@ def run_ours(args):
             "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "p99_ms": round(p99_e2e, 3),
                     "p99_ok": p99_e2e <= slo, "clients_per_gpu": e2e_fleet.wl["clients_n"],
                     "latency_scale": e2e_fleet.wl.get("latency_scale", 1.0),
+                    "merge_threshold": e2e_fleet.wl.get("merge_threshold", 0.2),
                     "path": ("serve() with host ingress: gather kernels read fp32 entry activations from pinned "
                              "host memory over PCIe (zero-copy), logits scattered to mapped host memory")
                     if args.e2e_ingress == "zero_copy" else
