@@ -346,7 +346,14 @@ def run_ours(args):
     e2e_value = stats[3].item() / timed_s
     p99, p99_e2e = times[2].item(), times[3].item()
     if rank == 0:
-        cpu = cpu_baseline(args, wl, dep, chain) if not args.no_cpu_baseline else None
+        cpu = None
+        if not args.no_cpu_baseline:
+            # the CPU path's own achievable rate: the smallest planned fleet (no fleet meets the SLO
+            # on the host), plus the same CPU path on this run's plan for reference
+            wl0 = _workloads(args.plans or args.model)[0]
+            cpu = cpu_baseline(args, wl0, deploy(wl0["plan"], wl0["fragments"]), chain)
+            cpu["sample"] += f" ({wl0['clients_n']}-client fleet)"
+            cpu["value_on_bench_plan"] = cpu_baseline(args, wl, dep, chain, budget_s=10.0)["value"]
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": round(window * 1000.0, 3), "higher_is_better": True, "scaling": "weak",

@@ -497,7 +497,8 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
             float4* y4 = reinterpret_cast<float4*>(static_cast<float*>(a.y) + static_cast<size_t>(m) * a.y_ld +
                                                    a.y_coff + n0);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) y4[i] = make_float4(f[4 * i], f[4 * i + 1], f[4 * i + 2], f[4 * i + 3]);
+            for (int i = 0; i < 4; ++i)  // Cout % 4 tails (FC 1000)
+              if (c + 4 * i < ncols) y4[i] = make_float4(f[4 * i], f[4 * i + 1], f[4 * i + 2], f[4 * i + 3]);
           } else {
             uint4* y4 = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.y) + static_cast<size_t>(m) * a.y_ld +
                                                  a.y_coff + n0);
@@ -508,7 +509,7 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
               o.y = pack_bf16x2(f[8 * i + 2], f[8 * i + 3]);
               o.z = pack_bf16x2(f[8 * i + 4], f[8 * i + 5]);
               o.w = pack_bf16x2(f[8 * i + 6], f[8 * i + 7]);
-              y4[i] = o;
+              if (c + 8 * i < ncols) y4[i] = o;
             }
           }
         }

@@ -174,13 +174,19 @@ static uint32_t tmem_cols_for(int bn) {
 
 int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint8_t* wbase, int k, int sm_budget,
               ConvLaunch* out, int bn_cap, const uint8_t* wsw, bool for_span) {
-  const gx_tensor& ti = T[op.in];
-  const gx_tensor& to = T[op.out];
-  const int R = op.kind == GX_OP_LINEAR ? 1 : op.R;
-  const int S = op.kind == GX_OP_LINEAR ? 1 : op.S;
+  const bool fc = op.kind == GX_OP_FC;
+  if (fc && (for_span || !fc_on_tc(op) || op.Cin != tensor_elems(T[op.in])))
+    return fail(GX_EINVAL, "FC not eligible for the tensor-core path");
+  // an FC sees its flattened per-sample input as a 1x1 image with K channels (NHWC flatten order,
+  // which is how the weights are laid out) and writes a 1x1 output with Cout channels
+  const gx_tensor ti = fc ? gx_tensor{1, 1, op.Cin, T[op.in].dtype} : T[op.in];
+  const gx_tensor to = fc ? gx_tensor{1, 1, op.Cout, T[op.out].dtype} : T[op.out];
+  const bool gemm1x1 = op.kind != GX_OP_CONV;
+  const int R = gemm1x1 ? 1 : op.R;
+  const int S = gemm1x1 ? 1 : op.S;
   if (ti.dtype != GX_BF16) return fail(GX_EINVAL, "conv input must be bf16");
   if ((op.Cin & 7) || (ti.C & 7) || op.Cin > ti.C) return fail(GX_EINVAL, "conv Cin must be a multiple of 8");
-  if (op.Cout & 15) return fail(GX_EINVAL, "conv Cout must be a multiple of 16");
+  if (op.Cout & (fc ? 7 : 15)) return fail(GX_EINVAL, "conv Cout must be a multiple of 16");
   if ((to.C & 7) || (op.out_coff & 7)) return fail(GX_EINVAL, "conv output pitch/offset must be multiples of 8");
   ConvArgs& a = out->args;
   memset(&a, 0, sizeof(a));
@@ -194,10 +200,10 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
   a.Wo = to.W;
   a.R = R;
   a.S = S;
-  a.sh = op.kind == GX_OP_LINEAR ? 1 : op.sh;
-  a.sw = op.kind == GX_OP_LINEAR ? 1 : op.sw;
-  a.ph = op.kind == GX_OP_LINEAR ? 0 : op.ph;
-  a.pw = op.kind == GX_OP_LINEAR ? 0 : op.pw;
+  a.sh = gemm1x1 ? 1 : op.sh;
+  a.sw = gemm1x1 ? 1 : op.sw;
+  a.ph = gemm1x1 ? 0 : op.ph;
+  a.pw = gemm1x1 ? 0 : op.pw;
   a.K = R * S * op.Cin;
   a.num_kb = (a.K + kBK - 1) / kBK;
   a.M = k * a.Ho * a.Wo;
@@ -417,6 +423,16 @@ int launch_op(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
       break;
     }
     case GX_OP_FC: {
+      if (fc_on_tc(op)) {
+        ConvLaunch cl;
+        if (pre == nullptr) {
+          int rc = plan_conv(op, T, ptrs, wbase, k, sm_budget, &cl);
+          if (rc != GX_OK) return rc;
+          pre = &cl;
+        }
+        GX_CUDA(launch_conv(pre->wmap, pre->amap, pre->rmap, pre->ymap, pre->args, pre->grid, s, pdl));
+        break;
+      }
       const gx_tensor& ti = T[op.in];
       const gx_tensor& to = T[op.out];
       const int K = static_cast<int>(tensor_elems(ti));

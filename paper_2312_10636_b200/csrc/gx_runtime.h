@@ -44,6 +44,14 @@ inline bool res_through_mma(const gx_op& op) {
   return op.kind == GX_OP_CONV && op.in2 >= 0 && op.R == 1 && op.S == 1 && op.sh == 1 && op.sw == 1 && op.ph == 0 &&
          op.pw == 0 && op.Cout % 64 == 0 && op.Cin % 64 == 0;
 }
+// FC (GX_OP_FC) on the tcgen05 GEMM path: the flattened per-sample input is a [k, K] row-major A
+// operand (1x1 conv on a 1x1 image with Cin = K), the [Cout][K] weights the B operand.  Needs whole
+// 64-wide k-blocks and 8-aligned outputs; GX_FC_SIMT keeps the CUDA-core weight-streaming kernel.
+inline bool fc_on_tc(const gx_op& op) {
+  return op.kind == GX_OP_FC && op.Cin % 64 == 0 && op.Cout % 8 == 0 && op.b_off >= 0 && getenv("GX_FC_SIMT") == nullptr;
+}
+// ops executed by conv_tc_kernel / conv_halo_kernel (planned with plan_conv)
+inline bool is_gemm_op(const gx_op& op) { return op.kind == GX_OP_CONV || op.kind == GX_OP_LINEAR || fc_on_tc(op); }
 void op_work(const gx_op& op, const gx_tensor* T, int k, double* flops, double* bytes);
 }  // namespace gx
 

@@ -91,7 +91,7 @@ int capture_span(gx_stage* st, int k, gx_stage::PerK* out) {
   std::vector<ConvLaunch> plans(st->ops.size());
   for (size_t i = 0; i < st->ops.size(); ++i) {
     const gx_op& op = m->ops[st->ops[i]];
-    if (op.kind == GX_OP_CONV || op.kind == GX_OP_LINEAR) {
+    if (is_gemm_op(op)) {
       int rc = plan_conv(op, m->tensors.data(), st->tptr.data(), wbase, k, st->sm_budget, &plans[i], 256,
                          m->op_wsw(st->ops[i]));
       if (rc != GX_OK) return rc;
@@ -104,7 +104,7 @@ int capture_span(gx_stage* st, int k, gx_stage::PerK* out) {
   const bool use_pdl = getenv("GX_NO_PDL") == nullptr;
   for (size_t i = 0; i < st->ops.size() && rc == GX_OK; ++i) {
     const gx_op& op = m->ops[st->ops[i]];
-    const bool is_conv = op.kind == GX_OP_CONV || op.kind == GX_OP_LINEAR;
+    const bool is_conv = is_gemm_op(op);
     rc = launch_op(op, m->tensors.data(), st->tptr.data(), wbase, k, st->sm_budget, st->stream, use_pdl,
                    is_conv ? &plans[i] : nullptr, &kernels);
   }
@@ -271,8 +271,8 @@ cudaError_t build_bulk_weights(gx_model* m, const uint8_t* blob) {
   size_t total = 0;
   for (int i = 0; i < n; ++i) {
     const gx_op& op = m->ops[i];
-    if (op.kind != GX_OP_CONV && op.kind != GX_OP_LINEAR) continue;
-    const int R = op.kind == GX_OP_LINEAR ? 1 : op.R, S = op.kind == GX_OP_LINEAR ? 1 : op.S;
+    if (!is_gemm_op(op)) continue;
+    const int R = op.kind != GX_OP_CONV ? 1 : op.R, S = op.kind != GX_OP_CONV ? 1 : op.S;
     const size_t kpad = (static_cast<size_t>(R) * S * op.Cin + 63) / 64 * 64;
     m->wsw_off[i] = static_cast<int64_t>(total);
     total += (kpad + (res_through_mma(op) ? op.Cout : 0)) * op.Cout * 2;
@@ -283,7 +283,7 @@ cudaError_t build_bulk_weights(gx_model* m, const uint8_t* blob) {
   for (int i = 0; i < n; ++i) {
     if (m->wsw_off[i] < 0) continue;
     const gx_op& op = m->ops[i];
-    const int R = op.kind == GX_OP_LINEAR ? 1 : op.R, S = op.kind == GX_OP_LINEAR ? 1 : op.S;
+    const int R = op.kind != GX_OP_CONV ? 1 : op.R, S = op.kind != GX_OP_CONV ? 1 : op.S;
     const size_t kpad = (static_cast<size_t>(R) * S * op.Cin + 63) / 64 * 64;
     const size_t nkb = kpad / 64;
     const uint8_t* src = blob + op.w_off;  // [Cout][kpad] bf16
@@ -621,7 +621,7 @@ int gx_stage_profile_ops(gx_stage* st, int k, int iters, int cap, float* ms, dou
   for (size_t i = 0; i < st->ops.size(); ++i) {
     const gx_op& op = m->ops[st->ops[i]];
     ConvLaunch cl;
-    const bool is_conv = op.kind == GX_OP_CONV || op.kind == GX_OP_LINEAR;
+    const bool is_conv = is_gemm_op(op);
     if (is_conv) {
       if (int rc = plan_conv(op, T, st->tptr.data(), wbase, k, st->sm_budget, &cl, 256, m->op_wsw(st->ops[i])))
         return rc;

@@ -1,6 +1,6 @@
 # bench once, then an ncu --set full capture of the conv launches of the busiest stage it reports
 set -x
-timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench3.log 2> gpurun_out/bench3.err
+timeout 900 python bench.py ${BENCH_ARGS:-} > gpurun_out/bench3.log 2> gpurun_out/bench3.err
 KEY=$(python - <<'PY'
 import json,re
 d=json.loads(open("gpurun_out/bench3.log").read().strip().splitlines()[-1])

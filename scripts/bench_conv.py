@@ -21,6 +21,7 @@ SHAPES = {  # name: (k, H, W, Cin, Cout, R, S, stride, pad)
 
 def run(name, k, H, W, Cin, Cout, R, S, stride, pad, budget=0, iters=50):
     dev = "cuda"
+    res = name.endswith("_res")
     Ho = (H + 2 * pad - R) // stride + 1
     Wo = (W + 2 * pad - S) // stride + 1
     blob = WeightBlob()
@@ -29,16 +30,17 @@ def run(name, k, H, W, Cin, Cout, R, S, stride, pad, budget=0, iters=50):
     wdev = torch.from_numpy(blob.bytes()).to(dev)
     x = torch.randn(k, H, W, Cin, device=dev).to(torch.bfloat16)
     y = torch.empty(k, Ho, Wo, Cout, device=dev, dtype=torch.bfloat16)
-    op = N.make_op(N.GX_OP_CONV, 0, 1, act=N.GX_ACT_RELU, R=R, S=S, sh=stride, sw=stride, ph=pad, pw=pad, Cin=Cin,
-                   Cout=Cout, w_off=w_off, b_off=b_off)
-    descs = [tensor_desc(H, W, Cin), tensor_desc(Ho, Wo, Cout)]
+    op = N.make_op(N.GX_OP_CONV, 0, 1, in2=2 if res else -1, act=N.GX_ACT_RELU, R=R, S=S, sh=stride, sw=stride,
+                   ph=pad, pw=pad, Cin=Cin, Cout=Cout, w_off=w_off, b_off=b_off)
+    descs = [tensor_desc(H, W, Cin), tensor_desc(Ho, Wo, Cout), tensor_desc(Ho, Wo, Cout)]
+    tens = [x, y, torch.randn(k, Ho, Wo, Cout, device=dev).to(torch.bfloat16)]
     for _ in range(3):
-        run_op(op, [x, y], descs, wdev, k, budget)
+        run_op(op, tens, descs, wdev, k, budget)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     e0.record()
     for _ in range(iters):
-        run_op(op, [x, y], descs, wdev, k, budget)
+        run_op(op, tens, descs, wdev, k, budget)
     e1.record()
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1000 / iters
@@ -85,6 +87,9 @@ def run_graph(name, k, H, W, Cin, Cout, R, S, stride, pad, budget=0, iters=50):
 
 
 SHAPES["tiny"] = (1, 8, 8, 64, 64, 1, 1, 1, 0)
+SHAPES["l3_1x1_256_1024_k16_res"] = (16, 14, 14, 256, 1024, 1, 1, 1, 0)
+SHAPES["l3_1x1_256_1024_k16"] = (16, 14, 14, 256, 1024, 1, 1, 1, 0)
+SHAPES["l2_1x1_128_512_k16_res"] = (16, 28, 28, 128, 512, 1, 1, 1, 0)
 SHAPES["l1_1x1_64_256_k8"] = (8, 56, 56, 64, 256, 1, 1, 1, 0)
 SHAPES["l1_3x3_64_k8"] = (8, 56, 56, 64, 64, 3, 3, 1, 1)
 SHAPES["l3_3x3_256_k8"] = (8, 14, 14, 256, 256, 3, 3, 1, 1)

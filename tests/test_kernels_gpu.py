@@ -152,6 +152,41 @@ def test_gap_and_fc():
     assert _rel(logits.cpu(), ref) < 1e-3
 
 
+@pytest.mark.parametrize("path", ["tcgen05", "simt"])
+@pytest.mark.parametrize("k,H,W,Cc,O,out_f32,relu", [
+    (1, 1, 1, 2048, 1000, True, False),     # ResNet-50 head at batch 1 (Cout % 16 tail: 1000)
+    (16, 1, 1, 2048, 1000, True, False),
+    (3, 7, 7, 512, 4096, False, True),      # VGG-16 fc6: flattened 7x7x512 input, bf16 out + ReLU
+    (130, 1, 1, 512, 1000, True, False),    # two 128-row M tiles
+])
+def test_fc_paths(path, k, H, W, Cc, O, out_f32, relu, monkeypatch):
+    """FC on the tcgen05 GEMM path (conv_tc_kernel with the flattened [k, K] input as A) and on the
+    CUDA-core weight-streaming kernel (GX_FC_SIMT): same results vs an fp32 matmul of the bf16 data."""
+    if path == "simt":
+        monkeypatch.setenv("GX_FC_SIMT", "1")
+    g = torch.Generator().manual_seed(7)
+    K = H * W * Cc
+    x = torch.randn(k, H, W, Cc, generator=g).to(torch.bfloat16)
+    w = torch.randn(O, K, generator=g) / K ** 0.5
+    b = torch.randn(O, generator=g)
+    blob = WeightBlob()
+    w_off = blob.add_bf16(w)
+    b_off = blob.add_f32(b)
+    wdev = torch.from_numpy(blob.bytes()).cuda()
+    y = torch.full((k, O), float("nan"), dtype=torch.float32 if out_f32 else torch.bfloat16, device="cuda")
+    op = N.make_op(N.GX_OP_FC, 0, 1, Cin=K, Cout=O, w_off=w_off, b_off=b_off,
+                   act=N.GX_ACT_RELU if relu else N.GX_ACT_NONE)
+    run_op(op, [x.cuda(), y], [tensor_desc(H, W, Cc), tensor_desc(1, 1, O, N.GX_F32 if out_f32 else N.GX_BF16)],
+           wdev, k)
+    torch.cuda.synchronize()
+    ref = x.reshape(k, K).float() @ w.to(torch.bfloat16).float().t() + b
+    if relu:
+        ref = ref.clamp_min(0)
+    got = y.float().cpu()
+    assert not got.isnan().any()
+    assert _rel(got, ref) < (1e-3 if out_f32 else 1e-2)
+
+
 def test_gather_scatter_bit_exact():
     import ctypes as C
     from paper_2312_10636_b200.device import context
