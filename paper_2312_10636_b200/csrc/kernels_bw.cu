@@ -106,7 +106,27 @@ __global__ void scatter_kernel(const void* __restrict__ src, int src_f32, int k,
                                int dst_f32) {
   const int64_t vec_per_row = row_elems / 8;
   const int64_t total = vec_per_row * k;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (!src_f32 && !dst_f32) {
+    // bf16 rows -> bf16 slots: 4 independent 16-byte loads in flight per thread before any store
+    // (one per thread leaves too few bytes in flight to cover HBM latency at full occupancy)
+    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < total; i0 += 4 * stride) {
+      uint4 val[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (i0 + u * stride < total) val[u] = ldg_stream(reinterpret_cast<const uint4*>(src) + i0 + u * stride);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = i0 + u * stride;
+        if (i < total) {
+          const int r = static_cast<int>(i / vec_per_row);
+          reinterpret_cast<uint4*>(dst.p[r])[i - r * vec_per_row] = val[u];
+        }
+      }
+    }
+    return;
+  }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += stride) {
     const int r = static_cast<int>(i / vec_per_row);
     const int64_t v = i - r * vec_per_row;
     if (src_f32) {
@@ -135,42 +155,74 @@ __global__ void scatter_kernel(const void* __restrict__ src, int src_f32, int k,
 }
 
 // K4 pooling over NHWC, 8 channels per thread (C % 8 == 0).  mode 0 = max, 1 = average.
+// KR > 0: the window is KR x KR at compile time, so the taps unroll into independent (predicated)
+// 16-byte loads that are all in flight before the reduction; KR = 0 is the generic window.
+template <int KR>
 __global__ void pool_kernel(int mode, const __nv_bfloat16* __restrict__ x, int N, int H, int W, int C, int x_ld,
                             __nv_bfloat16* __restrict__ y, int Ho, int Wo, int y_ld, int y_coff, int R, int S,
                             int sh, int sw, int ph, int pw, int count_include_pad) {
   const int cv = C / 8;
   const int64_t total = static_cast<int64_t>(N) * Ho * Wo * cv;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c8 = static_cast<int>(i % cv);
-    int64_t p = i / cv;
-    const int wo = static_cast<int>(p % Wo);
+  // 32-bit index decomposition (the launcher guarantees total < 2^31): three 64-bit div/mod
+  // sequences per 16-byte output cost more issue slots than the nine loads
+  const int total32 = static_cast<int>(total);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total32; i += gridDim.x * blockDim.x) {
+    const int c8 = i % cv;
+    int p = i / cv;
+    const int wo = p % Wo;
     p /= Wo;
-    const int ho = static_cast<int>(p % Ho);
-    const int n = static_cast<int>(p / Ho);
+    const int ho = p % Ho;
+    const int n = p / Ho;
     float acc[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[j] = mode == 0 ? -INFINITY : 0.0f;
     int cnt = 0;
-    for (int r = 0; r < R; ++r) {
-      const int hi = ho * sh - ph + r;
-      if (hi < 0 || hi >= H) continue;
-      for (int s = 0; s < S; ++s) {
-        const int wi = wo * sw - pw + s;
-        if (wi < 0 || wi >= W) continue;
-        const uint4 v = __ldg(reinterpret_cast<const uint4*>(x + ((static_cast<int64_t>(n) * H + hi) * W + wi) * x_ld) + c8);
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    auto tap = [&](const uint4 v) {
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float2 f = unpack_bf16x2(w[j]);
-          if (mode == 0) {
-            acc[2 * j] = fmaxf(acc[2 * j], f.x);
-            acc[2 * j + 1] = fmaxf(acc[2 * j + 1], f.y);
-          } else {
-            acc[2 * j] += f.x;
-            acc[2 * j + 1] += f.y;
-          }
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = unpack_bf16x2(w[j]);
+        if (mode == 0) {
+          acc[2 * j] = fmaxf(acc[2 * j], f.x);
+          acc[2 * j + 1] = fmaxf(acc[2 * j + 1], f.y);
+        } else {
+          acc[2 * j] += f.x;
+          acc[2 * j + 1] += f.y;
         }
-        ++cnt;
+      }
+      ++cnt;
+    };
+    if constexpr (KR > 0) {
+      // all KR*KR taps are loaded first, from clamped in-bounds addresses, so they are independent
+      // loads in flight together (SASS: 9 LDG.128 before the first FMNMX); padding taps are then
+      // skipped in the reduction
+      uint4 v[KR * KR];
+#pragma unroll
+      for (int r = 0; r < KR; ++r)
+#pragma unroll
+        for (int s = 0; s < KR; ++s) {
+          const int hc = min(max(ho * sh - ph + r, 0), H - 1), wc = min(max(wo * sw - pw + s, 0), W - 1);
+          v[r * KR + s] =
+              __ldg(reinterpret_cast<const uint4*>(x + ((static_cast<int64_t>(n) * H + hc) * W + wc) * x_ld) + c8);
+        }
+#pragma unroll
+      for (int r = 0; r < KR; ++r) {
+        const int hi = ho * sh - ph + r;
+#pragma unroll
+        for (int s = 0; s < KR; ++s) {
+          const int wi = wo * sw - pw + s;
+          if (hi >= 0 && hi < H && wi >= 0 && wi < W) tap(v[r * KR + s]);
+        }
+      }
+    } else {
+      for (int r = 0; r < R; ++r) {
+        const int hi = ho * sh - ph + r;
+        if (hi < 0 || hi >= H) continue;
+        for (int s = 0; s < S; ++s) {
+          const int wi = wo * sw - pw + s;
+          if (wi < 0 || wi >= W) continue;
+          tap(__ldg(reinterpret_cast<const uint4*>(x + ((static_cast<int64_t>(n) * H + hi) * W + wi) * x_ld) + c8));
+        }
       }
     }
     if (mode == 1) {
@@ -194,33 +246,55 @@ __global__ void pool_kernel(int mode, const __nv_bfloat16* __restrict__ x, int N
   }
 }
 
-// Global average pool: [N, HW, C] -> [N, C]; one thread per 8 channels.
-__global__ void gap_kernel(const __nv_bfloat16* __restrict__ x, int N, int HW, int C, __nv_bfloat16* __restrict__ y) {
+// Global average pool: [N, HW, C] -> [N, C].  A block owns (sample, 256 channels): lane = 8
+// channels (a warp reads 512 contiguous bytes of one pixel), the 8 warps stride the HW pixels with
+// independent loads in flight, then the 8 partial sums are reduced through shared memory.  (The
+// former one-thread-per-8-channels kernel walked all HW pixels serially: 49 dependent loads.)
+constexpr int kGapWarps = 8;
+__global__ void __launch_bounds__(kGapWarps * 32) gap_kernel(const __nv_bfloat16* __restrict__ x, int N, int HW,
+                                                            int C, __nv_bfloat16* __restrict__ y) {
+  __shared__ float part[kGapWarps][32][9];  // +1 pad: lane-strided rows hit distinct banks
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int cv = C / 8;
-  const int64_t total = static_cast<int64_t>(N) * cv;
+  const int groups = (cv + 31) / 32;
   const float inv = 1.0f / HW;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int n = static_cast<int>(i / cv);
-    const int c8 = static_cast<int>(i % cv);
+  for (int64_t item = blockIdx.x; item < static_cast<int64_t>(N) * groups; item += gridDim.x) {
+    const int n = static_cast<int>(item / groups);
+    const int c8 = static_cast<int>(item % groups) * 32 + lane;
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    const uint4* base = reinterpret_cast<const uint4*>(x + static_cast<int64_t>(n) * HW * C) + c8;
-#pragma unroll 7
-    for (int p = 0; p < HW; ++p) {
-      const uint4 v = __ldg(base + static_cast<int64_t>(p) * cv);
-      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    if (c8 < cv) {
+      const uint4* base = reinterpret_cast<const uint4*>(x + static_cast<int64_t>(n) * HW * C) + c8;
+#pragma unroll 4
+      for (int p = warp; p < HW; p += kGapWarps) {
+        const uint4 v = ldg_stream(base + static_cast<int64_t>(p) * cv);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float2 f = unpack_bf16x2(w[j]);
-        acc[2 * j] += f.x;
-        acc[2 * j + 1] += f.y;
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = unpack_bf16x2(w[j]);
+          acc[2 * j] += f.x;
+          acc[2 * j + 1] += f.y;
+        }
       }
     }
-    uint4 o;
-    o.x = pack_bf16x2(acc[0] * inv, acc[1] * inv);
-    o.y = pack_bf16x2(acc[2] * inv, acc[3] * inv);
-    o.z = pack_bf16x2(acc[4] * inv, acc[5] * inv);
-    o.w = pack_bf16x2(acc[6] * inv, acc[7] * inv);
-    reinterpret_cast<uint4*>(y + static_cast<int64_t>(n) * C)[c8] = o;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) part[warp][lane][j] = acc[j];
+    __syncthreads();
+    if (warp == 0 && c8 < cv) {
+      float s[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        s[j] = 0.0f;
+#pragma unroll
+        for (int w = 0; w < kGapWarps; ++w) s[j] += part[w][lane][j];
+      }
+      uint4 o;
+      o.x = pack_bf16x2(s[0] * inv, s[1] * inv);
+      o.y = pack_bf16x2(s[2] * inv, s[3] * inv);
+      o.z = pack_bf16x2(s[4] * inv, s[5] * inv);
+      o.w = pack_bf16x2(s[6] * inv, s[7] * inv);
+      reinterpret_cast<uint4*>(y + static_cast<int64_t>(n) * C)[c8] = o;
+    }
+    __syncthreads();
   }
 }
 
@@ -361,12 +435,27 @@ __global__ void __launch_bounds__(256, 2) fc_kernel(const __nv_bfloat16* __restr
 __global__ void copy_channels_kernel(const __nv_bfloat16* __restrict__ x, int64_t pixels, int C, int x_ld,
                                      int x_coff, __nv_bfloat16* __restrict__ y, int y_ld, int y_coff) {
   const int cv = C / 8;
-  const int64_t total = pixels * cv;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t p = i / cv;
-    const int c8 = static_cast<int>(i - p * cv);
-    const uint4 v = __ldg(reinterpret_cast<const uint4*>(x + p * x_ld + x_coff) + c8);
-    reinterpret_cast<uint4*>(y + p * y_ld + y_coff)[c8] = v;
+  const int total = static_cast<int>(pixels * cv);  // < 2^31 (launcher)
+  const int stride = gridDim.x * blockDim.x;
+  // 4 independent 16-byte loads in flight per thread, then the 4 stores
+  for (int i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < total; i0 += 4 * stride) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * stride;
+      if (i < total) {
+        const int p = i / cv;
+        v[u] = ldg_stream(reinterpret_cast<const uint4*>(x + static_cast<int64_t>(p) * x_ld + x_coff) + (i - p * cv));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * stride;
+      if (i < total) {
+        const int p = i / cv;
+        reinterpret_cast<uint4*>(y + static_cast<int64_t>(p) * y_ld + y_coff)[i - p * cv] = v[u];
+      }
+    }
   }
 }
 
@@ -419,14 +508,20 @@ cudaError_t launch_pool(int mode, const __nv_bfloat16* x, int N, int H, int W, i
                         int count_include_pad, int grid, cudaStream_t s) {
   if (C & 7) return cudaErrorInvalidValue;
   const int64_t work = static_cast<int64_t>(N) * Ho * Wo * (C / 8);
-  pool_kernel<<<grid_for(work, 256, grid), 256, 0, s>>>(mode, x, N, H, W, C, x_ld, y, Ho, Wo, y_ld, y_coff, R, S, sh,
-                                                         sw, ph, pw, count_include_pad);
+  if (work >= (int64_t{1} << 31)) return cudaErrorInvalidValue;
+  if (R == 3 && S == 3)
+    pool_kernel<3><<<grid_for(work, 256, grid), 256, 0, s>>>(mode, x, N, H, W, C, x_ld, y, Ho, Wo, y_ld, y_coff, R, S,
+                                                             sh, sw, ph, pw, count_include_pad);
+  else
+    pool_kernel<0><<<grid_for(work, 256, grid), 256, 0, s>>>(mode, x, N, H, W, C, x_ld, y, Ho, Wo, y_ld, y_coff, R, S,
+                                                             sh, sw, ph, pw, count_include_pad);
   return cudaGetLastError();
 }
 
 cudaError_t launch_gap(const __nv_bfloat16* x, int N, int HW, int C, __nv_bfloat16* y, int grid, cudaStream_t s) {
   if (C & 7) return cudaErrorInvalidValue;
-  gap_kernel<<<grid_for(static_cast<int64_t>(N) * (C / 8), 32, grid), 32, 0, s>>>(x, N, HW, C, y);
+  gap_kernel<<<grid_for(static_cast<int64_t>(N) * ((C / 8 + 31) / 32), 1, grid), kGapWarps * 32, 0, s>>>(x, N, HW,
+                                                                                                       C, y);
   return cudaGetLastError();
 }
 
@@ -475,6 +570,7 @@ cudaError_t launch_fc(const __nv_bfloat16* x, int N, int K, const __nv_bfloat16*
 cudaError_t launch_copy_channels(const __nv_bfloat16* x, int64_t pixels, int C, int x_ld, int x_coff,
                                  __nv_bfloat16* y, int y_ld, int y_coff, int grid, cudaStream_t s) {
   if ((C | x_ld | x_coff | y_ld | y_coff) & 7) return cudaErrorInvalidValue;
+  if (pixels * (C / 8) >= (int64_t{1} << 31)) return cudaErrorInvalidValue;
   copy_channels_kernel<<<grid_for(pixels * (C / 8), 256, grid), 256, 0, s>>>(x, pixels, C, x_ld, x_coff, y, y_ld,
                                                                              y_coff);
   return cudaGetLastError();
