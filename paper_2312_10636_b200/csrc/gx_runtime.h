@@ -47,6 +47,10 @@ inline bool res_through_mma(const gx_op& op) {
 // FC (GX_OP_FC) on the tcgen05 GEMM path: the flattened per-sample input is a [k, K] row-major A
 // operand (1x1 conv on a 1x1 image with Cin = K), the [Cout][K] weights the B operand.  Needs whole
 // 64-wide k-blocks and 8-aligned outputs; GX_FC_SIMT keeps the CUDA-core weight-streaming kernel.
+// The choice must not depend on the batch or the SM budget: a request's bits may not depend on
+// which instance serves it (split-vs-whole bit-exactness, test_models_gpu.py), and the two paths
+// sum K in different orders.  (The CUDA-core kernel is faster only for batch-1 heads spread over
+// a whole GPU, which serving never runs.)
 inline bool fc_on_tc(const gx_op& op) {
   return op.kind == GX_OP_FC && op.Cin % 64 == 0 && op.Cout % 8 == 0 && op.b_off >= 0 && getenv("GX_FC_SIMT") == nullptr;
 }

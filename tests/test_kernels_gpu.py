@@ -177,7 +177,7 @@ def test_fc_paths(path, k, H, W, Cc, O, out_f32, relu, monkeypatch):
     op = N.make_op(N.GX_OP_FC, 0, 1, Cin=K, Cout=O, w_off=w_off, b_off=b_off,
                    act=N.GX_ACT_RELU if relu else N.GX_ACT_NONE)
     run_op(op, [x.cuda(), y], [tensor_desc(H, W, Cc), tensor_desc(1, 1, O, N.GX_F32 if out_f32 else N.GX_BF16)],
-           wdev, k)
+           wdev, k, sm_budget=4)
     torch.cuda.synchronize()
     ref = x.reshape(k, K).float() @ w.to(torch.bfloat16).float().t() + b
     if relu:
