@@ -246,6 +246,99 @@ __global__ void pool_kernel(int mode, const __nv_bfloat16* __restrict__ x, int N
   }
 }
 
+// 3x3 / stride-1 pooling (Inception's branch_pool avg pools, and max): a thread owns a vertical
+// strip of kPoolStrip outputs at one (column, 8 channels) and slides down it, combining each input
+// row's three taps once into a row value (max or sum) and each output from three row values:
+// 3*(T+2) loads for T outputs instead of 9*T, so the nine-fold tap reuse no longer has to come
+// from L1/L2 (the per-output kernel was L2->SM bound at 0.26 of HBM on 35x35x288).
+constexpr int kPoolStrip = 8;
+__global__ void pool3s1_kernel(int mode, const __nv_bfloat16* __restrict__ x, int N, int H, int W, int C, int x_ld,
+                               __nv_bfloat16* __restrict__ y, int Ho, int Wo, int y_ld, int y_coff, int ph, int pw,
+                               int count_include_pad) {
+  constexpr int T = kPoolStrip;
+  const int cv = C / 8;
+  const int strips = (Ho + T - 1) / T;
+  const int total = N * strips * Wo * cv;  // < 2^31 (launcher)
+  const float ident = mode == 0 ? -INFINITY : 0.0f;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int c8 = i % cv;
+    int p = i / cv;
+    const int wo = p % Wo;
+    p /= Wo;
+    const int st = p % strips;
+    const int n = p / strips;
+    const int ho0 = st * T;
+    const int w0 = wo - pw;
+    int ncols = 0;
+#pragma unroll
+    for (int s = 0; s < 3; ++s) ncols += (w0 + s >= 0 && w0 + s < W) ? 1 : 0;
+    float rv[T + 2][8];
+    bool rok[T + 2];
+#pragma unroll
+    for (int j = 0; j < T + 2; ++j) {
+      const int hi = ho0 - ph + j;
+      rok[j] = hi >= 0 && hi < H && ho0 + j - 2 < Ho;  // rows past the strip's last output unused
+      const int hc = min(max(hi, 0), H - 1);
+      uint4 v[3];
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        const int wc = min(max(w0 + s, 0), W - 1);
+        v[s] = __ldg(reinterpret_cast<const uint4*>(x + ((static_cast<int64_t>(n) * H + hc) * W + wc) * x_ld) + c8);
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) rv[j][e] = ident;
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        if (w0 + s < 0 || w0 + s >= W) continue;
+        const uint32_t w[4] = {v[s].x, v[s].y, v[s].z, v[s].w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 f = unpack_bf16x2(w[q]);
+          if (mode == 0) {
+            rv[j][2 * q] = fmaxf(rv[j][2 * q], f.x);
+            rv[j][2 * q + 1] = fmaxf(rv[j][2 * q + 1], f.y);
+          } else {
+            rv[j][2 * q] += f.x;
+            rv[j][2 * q + 1] += f.y;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const int ho = ho0 + t;
+      if (ho >= Ho) break;
+      float acc[8];
+      int nrows = 0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = ident;
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        if (!rok[t + r]) continue;
+        ++nrows;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] = mode == 0 ? fmaxf(acc[e], rv[t + r][e]) : acc[e] + rv[t + r][e];
+      }
+      if (mode == 1) {
+        int div = nrows * ncols;
+        if (count_include_pad) {
+          const int h0 = ho - ph, ww0 = wo - pw;
+          div = (min(h0 + 3, H + ph) - h0) * (min(ww0 + 3, W + pw) - ww0);
+        }
+        const float inv = 1.0f / static_cast<float>(div);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] *= inv;
+      }
+      uint4 o;
+      o.x = pack_bf16x2(acc[0], acc[1]);
+      o.y = pack_bf16x2(acc[2], acc[3]);
+      o.z = pack_bf16x2(acc[4], acc[5]);
+      o.w = pack_bf16x2(acc[6], acc[7]);
+      *reinterpret_cast<uint4*>(y + ((static_cast<int64_t>(n) * Ho + ho) * Wo + wo) * y_ld + y_coff + 8 * c8) = o;
+    }
+  }
+}
+
 // Global average pool: [N, HW, C] -> [N, C].  A block owns (sample, 256 channels): lane = 8
 // channels (a warp reads 512 contiguous bytes of one pixel), the 8 warps stride the HW pixels with
 // independent loads in flight, then the 8 partial sums are reduced through shared memory.  (The
@@ -509,7 +602,11 @@ cudaError_t launch_pool(int mode, const __nv_bfloat16* x, int N, int H, int W, i
   if (C & 7) return cudaErrorInvalidValue;
   const int64_t work = static_cast<int64_t>(N) * Ho * Wo * (C / 8);
   if (work >= (int64_t{1} << 31)) return cudaErrorInvalidValue;
-  if (R == 3 && S == 3)
+  if (R == 3 && S == 3 && sh == 1 && sw == 1 && ph <= 2 && pw <= 2 && getenv("GX_POOL_NOSTRIP") == nullptr) {
+    const int64_t strips = static_cast<int64_t>(N) * ((Ho + kPoolStrip - 1) / kPoolStrip) * Wo * (C / 8);
+    pool3s1_kernel<<<grid_for(strips, 256, grid), 256, 0, s>>>(mode, x, N, H, W, C, x_ld, y, Ho, Wo, y_ld, y_coff, ph,
+                                                               pw, count_include_pad);
+  } else if (R == 3 && S == 3)
     pool_kernel<3><<<grid_for(work, 256, grid), 256, 0, s>>>(mode, x, N, H, W, C, x_ld, y, Ho, Wo, y_ld, y_coff, R, S,
                                                              sh, sw, ph, pw, count_include_pad);
   else

@@ -110,7 +110,7 @@ def test_conv_large_m_persistent():
 
 
 @pytest.mark.parametrize("mode,R,stride,pad", [("max", 3, 2, 1), ("max", 2, 2, 0), ("avg", 3, 1, 1),
-                                                ("max", 3, 2, 0)])
+                                                ("max", 3, 2, 0), ("max", 3, 1, 1), ("avg", 3, 1, 0)])
 def test_pool(mode, R, stride, pad):
     g = torch.Generator().manual_seed(1)
     k, H, W, Cc = 3, 15, 15, 64
