@@ -268,13 +268,14 @@ def run_ours(args):
             res = one_run(fleet, host=False)
     wl, dep, clients, instances = fleet.wl, fleet.dep, fleet.clients, fleet.instances
     slo = wl["slo_ms"]
-    # e2e: the same achievable-throughput rule through the host path (ingress read from pinned host
-    # memory by the gather kernels, logits written to mapped host memory), from this fleet down
+    # e2e: the same achievable-throughput rule through the host path (each request's ingress
+    # DMA-copied from pinned host memory at arrival, or read in place by the gather with
+    # --e2e-ingress zero_copy; logits written to mapped host memory), from this fleet down
     e2e_fleet = fleet
     res_e2e = one_run(fleet, host=True)
     if args.clients is None:
-        # host ingress makes the tail noisier than the resident run: a miss at the first fleet is
-        # retried once before stepping down
+        # host ingress makes the tail noisier than the resident run: a near miss (p99 within 2x the
+        # SLO) is retried once before stepping down
         retried = False
         # fleets whose host->device demand exceeds ~85% of the measured PCIe Gen5 x16 rate (46 GB/s
         # for 1 MB copies, scripts/probe_h2d_streams.py) queue on the link without bound: skip them
@@ -292,7 +293,7 @@ def run_ours(args):
                       f"{'ok' if ok else 'over'}", file=sys.stderr, flush=True)
             if ok:
                 break
-            if not retried:
+            if not retried and res_e2e["p99"] <= 2.0 * slo:
                 retried = True
                 res_e2e = one_run(e2e_fleet, host=True)
                 continue
@@ -301,6 +302,7 @@ def run_ours(args):
             if e2e_fleet is not fleet:
                 del e2e_fleet
             e2e_fleet = Fleet(cands.pop(0))
+            retried = False
             res_e2e = one_run(e2e_fleet, host=True)
 
     # roofline of the dominant kernel, the implicit-GEMM conv (conv_tc_kernel, plus conv_halo_kernel
