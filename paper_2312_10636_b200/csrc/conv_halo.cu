@@ -25,7 +25,7 @@ constexpr int kHaloRows = 256;                  // smem rows per halo buffer (>=
 constexpr int kHaloBytes = kHaloRows * 128;     // 32 KB
 
 struct HaloSmem {
-  uint8_t* halo;   // [2][kHaloBytes]
+  uint8_t* halo;   // [NH][HB]: 2 x 32 KB (128-byte rows) or 4 x 16 KB (32-byte rows)
   uint8_t* sB;     // [S][BN*128]
   float* bias;
   uint64_t *hfull, *hempty, *bfull, *bempty, *tfull, *tempty, *biasbar;
@@ -50,6 +50,10 @@ __device__ __forceinline__ uint64_t desc_sw128_row(uint32_t saddr) {
          (2ull << 61);
 }
 
+// RB = bytes per halo pixel row: 128 (64-channel blocks, SWIZZLE_128B, 3x3 taps, four K=16 MMAs per
+// tap) or 32 (the 16-channel s2d stem, SWIZZLE_32B, 4x4 taps, one K=16 MMA per tap; the four taps
+// of filter row r are the four 32-byte K slices of weight k-block r)
+template <int RB>
 __global__ void __launch_bounds__(kConvTcThreads, 1)
     conv_halo_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap hmap,
                      const ConvArgs a) {
@@ -58,16 +62,21 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
   const int S_ = a.stages;
   const int BN = a.BN;
   const uint32_t b_bytes = static_cast<uint32_t>(BN) * 128u;
-  const int Wp = a.W + 2, BH = a.hBH, TPI = a.hTPI;
-  const int CB = a.Cin / 64;
-  const uint32_t hbytes = static_cast<uint32_t>(Wp * (BH + 2) * 128);
+  const int Wp = a.hWp, BH = a.hBH, TPI = a.hTPI;
+  const int CB = RB == 128 ? a.Cin / 64 : 1;
+  const int NKB = RB == 128 ? 9 : a.R;  // weight k-blocks per channel block
+  const uint32_t hbytes = static_cast<uint32_t>(Wp * (BH + a.R - 1) * RB);
+  // the stem's halo is ~15 KB and one tile's MMAs take ~0.3 us: four buffers keep enough TMA loads
+  // in flight to cover their latency
+  constexpr int NH = RB == 32 ? 4 : 2;
+  constexpr uint32_t HB = 2u * kHaloBytes / NH;
   HaloSmem sp;
   sp.halo = smem;
   sp.sB = sp.halo + 2 * kHaloBytes;
   sp.bias = reinterpret_cast<float*>(sp.sB + static_cast<size_t>(S_) * b_bytes);
   sp.hfull = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sp.bias) + ((a.Cout * 4 + 1023) & ~1023));
-  sp.hempty = sp.hfull + 2;
-  sp.bfull = sp.hempty + 2;
+  sp.hempty = sp.hfull + NH;
+  sp.bfull = sp.hempty + NH;
   sp.bempty = sp.bfull + S_;
   sp.tfull = sp.bempty + S_;
   sp.tempty = sp.tfull + 2;
@@ -77,9 +86,11 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 4) {
     if (lane == 0) {
-      for (int i = 0; i < 2; ++i) {
+      for (int i = 0; i < NH; ++i) {
         mbar_init(&sp.hfull[i], 1);
         mbar_init(&sp.hempty[i], 1);
+      }
+      for (int i = 0; i < 2; ++i) {
         mbar_init(&sp.tfull[i], 1);
         mbar_init(&sp.tempty[i], 256);
       }
@@ -113,10 +124,10 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
         mbar_wait(&sp.hempty[hs], hph ^ 1);
         if (issuer) {
           mbar_arrive_expect_tx(&sp.hfull[hs], hbytes);
-          tma_load_4d(sp.halo + hs * kHaloBytes, &hmap, &sp.hfull[hs], cb * 64, -1, h0 - 1, n);
+          tma_load_4d(sp.halo + hs * HB, &hmap, &sp.hfull[hs], cb * 64, -a.pw, h0 - a.ph, n);
         }
         __syncwarp();
-        if (++hs == 2) {
+        if (++hs == NH) {
           hs = 0;
           hph ^= 1;
         }
@@ -131,7 +142,7 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
     for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
       const int n_blk = tile % a.n_tiles;
       for (int cb = 0; cb < CB; ++cb) {
-        for (int tap = 0; tap < 9; ++tap) {
+        for (int tap = 0; tap < NKB; ++tap) {
           const int kb = tap * CB + cb;
           mbar_wait(&sp.bempty[bs], bph ^ 1);
           if (issuer) {
@@ -164,19 +175,29 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
       for (int cb = 0; cb < CB; ++cb) {
         mbar_wait(&sp.hfull[hs], hph);
         tc_fence_after();
-        const uint32_t hbase = smem_u32(sp.halo + hs * kHaloBytes);
-        for (int tap = 0; tap < 9; ++tap) {
-          const int r = tap / 3, s = tap - r * 3;
+        const uint32_t hbase = smem_u32(sp.halo + hs * HB);
+        for (int tap = 0; tap < NKB; ++tap) {
           mbar_wait(&sp.bfull[bs], bph);
           tc_fence_after();
-          const uint64_t ad = desc_sw128_row(hbase + static_cast<uint32_t>(r * Wp + s) * 128u);
           const uint64_t bd = umma_desc_sw128(sp.sB + static_cast<size_t>(bs) * b_bytes);
-          if (issuer) {
+          if (RB == 128) {
+            const int r = tap / 3, s = tap - r * 3;
+            const uint64_t ad = desc_sw128_row(hbase + static_cast<uint32_t>(r * Wp + s) * 128u);
+            if (issuer) {
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-              umma_bf16(d, ad + 2 * kk, bd + 2 * kk, a.idesc, (cb | tap | kk) != 0);
-            umma_commit(&sp.bempty[bs]);
+              for (int kk = 0; kk < 4; ++kk)
+                umma_bf16(d, ad + 2 * kk, bd + 2 * kk, a.idesc, (cb | tap | kk) != 0);
+            }
+          } else if (issuer) {
+            // k-block `tap` = filter row r; its K slice s (32 bytes) is tap (r, s), whose A operand
+            // is the halo started r*Wp + s pixel rows later (SWIZZLE_32B on absolute address bits,
+            // like the 128-byte case: base-offset field 0)
+#pragma unroll
+            for (int s = 0; s < 4; ++s)
+              umma_bf16(d, umma_desc_kmajor(hbase + static_cast<uint32_t>(tap * Wp + s) * 32u, 16, 0), bd + 2 * s,
+                        a.idesc, (tap | s) != 0);
           }
+          if (issuer) umma_commit(&sp.bempty[bs]);
           __syncwarp();
           if (++bs == S_) {
             bs = 0;
@@ -185,7 +206,7 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
         }
         if (issuer) umma_commit(&sp.hempty[hs]);
         __syncwarp();
-        if (++hs == 2) {
+        if (++hs == NH) {
           hs = 0;
           hph ^= 1;
         }
@@ -264,7 +285,7 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
 
 size_t conv_halo_smem_bytes(int BN, int stages, int Cout) {
   return 1024 + 2 * static_cast<size_t>(kHaloBytes) + static_cast<size_t>(stages) * BN * 128 +
-         ((static_cast<size_t>(Cout) * 4 + 1023) & ~size_t(1023)) + (2 * stages + 9) * 8 + 16;
+         ((static_cast<size_t>(Cout) * 4 + 1023) & ~size_t(1023)) + (2 * stages + 13) * 8 + 16;
 }
 
 int conv_halo_pick_stages(int BN, int Cout) {
@@ -278,7 +299,9 @@ cudaError_t launch_conv_halo(const CUtensorMap& wmap, const CUtensorMap& hmap, c
                              cudaStream_t s, bool pdl) {
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(conv_halo_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    cudaError_t e = cudaFuncSetAttribute(conv_halo_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(conv_halo_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     if (e != cudaSuccess) return e;
     configured = true;
   }
@@ -292,7 +315,8 @@ cudaError_t launch_conv_halo(const CUtensorMap& wmap, const CUtensorMap& hmap, c
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, conv_halo_kernel, wmap, hmap, a);
+  if (a.hRB == 32) return cudaLaunchKernelEx(&cfg, conv_halo_kernel<32>, wmap, hmap, a);
+  return cudaLaunchKernelEx(&cfg, conv_halo_kernel<128>, wmap, hmap, a);
 }
 
 }  // namespace gx

@@ -130,18 +130,20 @@ unsigned long long* debug_trace_buffer() {
 
 // NHWC input as a rank-4 (C, W, H, N) tiled map with a [64, box_w, box_h, 1] box (the halo of a
 // conv_halo_kernel M tile; negative / past-the-edge coordinates are zero-filled = padding).
-bool encode_tmap_halo_bf16(CUtensorMap* map, const void* base, int C, int W, int H, int N, int box_w, int box_h) {
+bool encode_tmap_halo_bf16(CUtensorMap* map, const void* base, int C, int W, int H, int N, int box_w, int box_h,
+                           int box_c) {
   PFN_encodeTiled_t fn = encode_fn();
   if (fn == nullptr) return false;
   cuuint64_t dims[4] = {static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
                         static_cast<cuuint64_t>(N)};
   cuuint64_t strides[3] = {static_cast<cuuint64_t>(C) * 2, static_cast<cuuint64_t>(C) * 2 * W,
                            static_cast<cuuint64_t>(C) * 2 * W * H};
-  cuuint32_t box[4] = {64, static_cast<cuuint32_t>(box_w), static_cast<cuuint32_t>(box_h), 1};
+  cuuint32_t box[4] = {static_cast<cuuint32_t>(box_c), static_cast<cuuint32_t>(box_w), static_cast<cuuint32_t>(box_h),
+                       1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+            CU_TENSOR_MAP_INTERLEAVE_NONE, box_c == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // ---------------------------------------------------------------- op planning
@@ -211,11 +213,17 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
   a.m_tiles = (a.M + kBM - 1) / kBM;
   // 3x3 / stride 1 / pad 1 on wide images: one halo tile per 64-channel block (conv_halo.cu)
   const bool pad1 = a.ph == 1 && a.pw == 1 && (op.ph_hi < 0 || op.ph_hi == 1) && (op.pw_hi < 0 || op.pw_hi == 1);
-  if (!for_span && op.kind == GX_OP_CONV && R == 3 && S == 3 && a.sh == 1 && a.sw == 1 && pad1 && op.Cin % 64 == 0 &&
-      op.Cin == ti.C && a.Ho == ti.H && a.Wo == ti.W && ti.W >= 28 && ti.W + 2 <= 64 && op.in2 < 0 &&
-      to.dtype == GX_BF16 && getenv("GX_NO_HALO") == nullptr) {
-    const int Wp = ti.W + 2;
+  const bool halo128 = R == 3 && S == 3 && pad1 && op.Cin % 64 == 0 && ti.W >= 28 && ti.W + 2 <= 64;
+  // the space-to-depth stem (4x4 / s1 / pad 2,2,1,1 over 16 channels): 32-byte halo rows, one K=16
+  // MMA per tap, 128 // (W + 3) output rows per tile
+  const bool halo32 = R == 4 && S == 4 && a.ph == 2 && a.pw == 2 && op.ph_hi == 1 && op.pw_hi == 1 && op.Cin == 16 &&
+                      ti.W + 3 <= kBM && getenv("GX_NO_HALO32") == nullptr;
+  if (!for_span && op.kind == GX_OP_CONV && (halo128 || halo32) && a.sh == 1 && a.sw == 1 && op.Cin == ti.C &&
+      a.Ho == ti.H && a.Wo == ti.W && op.in2 < 0 && to.dtype == GX_BF16 && getenv("GX_NO_HALO") == nullptr) {
+    const int Wp = ti.W + (halo32 ? 3 : 2);
     a.halo = 1;
+    a.hWp = Wp;
+    a.hRB = halo32 ? 32 : 128;
     a.hBH = std::min(ti.H, kBM / Wp);
     a.hTPI = (ti.H + a.hBH - 1) / a.hBH;
     a.m_tiles = k * a.hTPI;
@@ -239,7 +247,7 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
     memset(&out->ymap, 0, sizeof(out->ymap));
     if (!encode_tmap_2d_bf16(&out->wmap, wbase + op.w_off, kpad, op.Cout, static_cast<uint64_t>(kpad) * 2, kBK, a.BN))
       return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for conv weights: " + g_last_encode);
-    if (!encode_tmap_halo_bf16(&out->amap, a.x, ti.C, ti.W, ti.H, k, Wp, a.hBH + 2))
+    if (!encode_tmap_halo_bf16(&out->amap, a.x, ti.C, ti.W, ti.H, k, Wp, a.hBH + R - 1, halo32 ? 16 : 64))
       return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for the conv halo");
     if (a.stages < 2) return fail(GX_EINVAL, "halo conv: shared memory too small for the weight ring");
     out->grid = std::min(a.num_tiles, std::max(1, sm_budget));

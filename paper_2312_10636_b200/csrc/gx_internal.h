@@ -61,6 +61,7 @@ struct ConvArgs {
                        // (rmap, box 64 x 128), B = identity blocks at kb = num_kb + col/64 (wsw)
   int halo;            // 3x3/s1/p1 wide-image conv on conv_halo_kernel (amap = the 4D halo map)
   int hBH, hTPI;       // halo: output rows per M tile, M tiles per image
+  int hWp, hRB;        // halo: padded row pitch (W + left + right pad), bytes per halo pixel row (128 | 32)
 };
 constexpr int kConvThreads = 320;  // span kernel: 4 A-producer warps, TMA warp, MMA warp, 4 epilogue warps
 // conv_tc: warps 0-3 cp.async A producers (or epilogue when TMA builds A), 4 A/B TMA, 5 MMA,
@@ -78,7 +79,8 @@ size_t conv_halo_smem_bytes(int BN, int stages, int Cout);
 int conv_halo_pick_stages(int BN, int Cout);
 cudaError_t launch_conv_halo(const CUtensorMap& wmap, const CUtensorMap& hmap, const ConvArgs& a, int grid,
                              cudaStream_t s, bool pdl);
-bool encode_tmap_halo_bf16(CUtensorMap* map, const void* base, int C, int W, int H, int N, int box_w, int box_h);
+bool encode_tmap_halo_bf16(CUtensorMap* map, const void* base, int C, int W, int H, int N, int box_w, int box_h,
+                           int box_c = 64);
 bool encode_tmap_im2col_bf16(CUtensorMap* map, const void* base, int C, int W, int H, int N, int lower_w,
                              int lower_h, int upper_w, int upper_h, int stride_w, int stride_h, int cpl);
 

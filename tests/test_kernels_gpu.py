@@ -93,6 +93,34 @@ def test_conv_matches_torch(k, H, W, Cin, Cout, R, S, stride, pad, residual, rel
     assert _rel(got, ref) < 1.5e-2
 
 
+@pytest.mark.parametrize("k,H,Cout,path", [(2, 112, 64, "halo32"), (3, 56, 64, "halo32"), (1, 28, 32, "halo32"),
+                                            (2, 112, 64, "im2col")])
+def test_conv_s2d_stem(k, H, Cout, path, monkeypatch):
+    """The space-to-depth stem: 4x4 / stride 1 / pad (2, 2, 1, 1) over 16 channels, on the 32-byte
+    halo path (conv_halo_kernel<32>: one halo tile, sixteen K=16 MMAs at row offsets) and on the
+    im2col path (GX_NO_HALO32), vs torch on the same bf16 data."""
+    if path == "im2col":
+        monkeypatch.setenv("GX_NO_HALO32", "1")
+    g = torch.Generator().manual_seed(5)
+    x = torch.randn(k, H, H, 16, generator=g).to(torch.bfloat16)
+    w = torch.randn(Cout, 16, 4, 4, generator=g) / 16.0
+    b = torch.randn(Cout, generator=g) * 0.1
+    xp = F.pad(x.float().permute(0, 3, 1, 2), (2, 1, 2, 1))
+    ref = F.conv2d(xp, w.to(torch.bfloat16).float(), b).clamp_min(0).permute(0, 2, 3, 1)
+    blob = WeightBlob()
+    w_off = blob.add_bf16(pack_conv_weight(w, 16))
+    b_off = blob.add_f32(b)
+    wdev = torch.from_numpy(blob.bytes()).cuda()
+    y = torch.full((k, H, H, Cout), float("nan"), dtype=torch.bfloat16, device="cuda")
+    op = N.make_op(N.GX_OP_CONV, 0, 1, act=N.GX_ACT_RELU, R=4, S=4, sh=1, sw=1, ph=2, pw=2, ph_hi=1, pw_hi=1,
+                   Cin=16, Cout=Cout, w_off=w_off, b_off=b_off)
+    run_op(op, [x.cuda(), y], [tensor_desc(H, H, 16), tensor_desc(H, H, Cout)], wdev, k, 3)
+    torch.cuda.synchronize()
+    got = y.float().cpu()
+    assert torch.isfinite(got).all(), "conv left unwritten outputs"
+    assert _rel(got, ref) < 1.5e-2
+
+
 def test_conv_stem_channel_padded():
     # ResNet stem: 3-channel image zero-padded to 8 channels, 7x7 stride 2 pad 3
     got, ref = _conv_case(2, 64, 64, 3, 64, 7, 7, 2, 3, False, True, cin_pad=8)
