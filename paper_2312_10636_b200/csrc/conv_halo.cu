@@ -66,6 +66,9 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
   const int CB = RB == 128 ? a.Cin / 64 : 1;
   const int NKB = RB == 128 ? 9 : a.R;  // weight k-blocks per channel block
   const uint32_t hbytes = static_cast<uint32_t>(Wp * (BH + a.R - 1) * RB);
+  // stem (one N tile): its NKB weight k-blocks are loaded once into ring slots 0..NKB-1 and stay
+  // resident (every tile would otherwise re-load the same 32 KB, 60% of the kernel's TMA bytes)
+  const bool resident = RB == 32 && a.n_tiles == 1 && S_ >= NKB && CB == 1 && !(a.dbg & 32);  // GX_CONV_DBG=32: ring as before
   // the stem's halo is ~15 KB and one tile's MMAs take ~0.3 us: four buffers keep enough TMA loads
   // in flight to cover their latency
   constexpr int NH = RB == 32 ? 4 : 2;
@@ -139,7 +142,19 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
     if (issuer && !a.wsw) tma_prefetch_desc(&wmap);
     int bs = 0;
     uint32_t bph = 0;
-    for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
+    if (resident) {
+      if (issuer)
+        for (int kb = 0; kb < NKB; ++kb) {
+          uint8_t* dst = sp.sB + static_cast<size_t>(kb) * b_bytes;
+          mbar_arrive_expect_tx(&sp.bfull[kb], b_bytes);
+          if (a.wsw)
+            bulk_load(dst, a.wsw + static_cast<size_t>(kb) * a.Cout * 128u, b_bytes, &sp.bfull[kb]);
+          else
+            tma_load_2d(dst, &wmap, &sp.bfull[kb], kb * kBK, 0);
+        }
+      __syncwarp();
+    }
+    for (int tile = resident ? a.num_tiles : blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
       const int n_blk = tile % a.n_tiles;
       for (int cb = 0; cb < CB; ++cb) {
         for (int tap = 0; tap < NKB; ++tap) {
@@ -177,9 +192,11 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
         tc_fence_after();
         const uint32_t hbase = smem_u32(sp.halo + hs * HB);
         for (int tap = 0; tap < NKB; ++tap) {
-          mbar_wait(&sp.bfull[bs], bph);
+          const int slot = resident ? tap : bs;
+          // resident slots completed phase 0 once and are never re-armed: parity-0 waits pass
+          mbar_wait(&sp.bfull[slot], resident ? 0u : bph);
           tc_fence_after();
-          const uint64_t bd = umma_desc_sw128(sp.sB + static_cast<size_t>(bs) * b_bytes);
+          const uint64_t bd = umma_desc_sw128(sp.sB + static_cast<size_t>(slot) * b_bytes);
           if (RB == 128) {
             const int r = tap / 3, s = tap - r * 3;
             const uint64_t ad = desc_sw128_row(hbase + static_cast<uint32_t>(r * Wp + s) * 128u);
@@ -197,12 +214,14 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
               umma_bf16(d, umma_desc_kmajor(hbase + static_cast<uint32_t>(tap * Wp + s) * 32u, 16, 0), bd + 2 * s,
                         a.idesc, (tap | s) != 0);
           }
-          if (issuer) umma_commit(&sp.bempty[bs]);
-          __syncwarp();
-          if (++bs == S_) {
-            bs = 0;
-            bph ^= 1;
+          if (!resident) {
+            if (issuer) umma_commit(&sp.bempty[bs]);
+            if (++bs == S_) {
+              bs = 0;
+              bph ^= 1;
+            }
           }
+          __syncwarp();
         }
         if (issuer) umma_commit(&sp.hempty[hs]);
         __syncwarp();
