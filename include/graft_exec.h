@@ -30,7 +30,9 @@
 extern "C" {
 #endif
 
-#define GX_ABI_VERSION 1
+/* v2: stages carry their element type (fp32 execution mode), gx_stage_run_async runs on a caller
+ * stream and records a caller event, gx_serve_cfg.result_rows sizes the output ring. */
+#define GX_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define GX_API __attribute__((visibility("default")))
@@ -120,12 +122,18 @@ GX_API int gx_model_create(gx_ctx* ctx, const char* model_id, int n_tensors, con
                     const int32_t* boundary, const void* weight_blob, size_t blob_bytes,
                     gx_model** out);
 GX_API int gx_model_destroy(gx_model* m);
+/* Compute element type of a chain: GX_BF16 (tensor-core path) or GX_F32 (every tensor and weight
+ * fp32: the fp32 execution mode, north-star tolerance 1e-3 against the fp32 forward).  A chain
+ * is one or the other; only its final output may be fp32 in a bf16 chain (logits). */
+GX_API int gx_model_dtype(gx_model* m, int32_t* dtype_out);
 
 /* A stage instance: span [start, end) of `m`, batches of up to max_batch requests, bounded to
  * sm_budget SMs (persistent grids; the plan's share s maps to ceil(s*SMs/100)).  Stands in for
  * _StageRT (simulator.py:76-100) of one instance; `stream` may be NULL (library-owned stream). */
-GX_API int gx_stage_create(gx_model* m, int start, int end, int max_batch, int sm_budget, void* stream,
-                    gx_stage** out);
+GX_API int gx_stage_create(gx_model* m, int start, int end, int max_batch, int sm_budget, int32_t dtype,
+                           void* stream, gx_stage** out);
+/* dtype: the element type the stage computes in; must equal gx_model_dtype(m) (GX_EINVAL
+ * otherwise), so a caller can never run an fp32-planned stage on bf16 weights or vice versa.     */
 GX_API int gx_stage_destroy(gx_stage* st);
 GX_API int gx_stage_stream(gx_stage* st, void** stream_out);
 
@@ -139,6 +147,21 @@ GX_API int gx_stage_stream(gx_stage* st, void** stream_out);
  * Asynchronous on the stage stream: gather (K1) -> span kernels (CUDA graph per k) -> scatter. */
 GX_API int gx_stage_run(gx_stage* st, int k, const void* const* src, const int32_t* src_dtype,
                  int32_t src_channels, void* const* dst, int32_t dst_dtype);
+
+/* gx_stage_run on the caller's stream (e.g. torch's current stream); when done_event (a
+ * cudaEvent_t) is non-null it is recorded after the scatter, so the caller can chain or poll the
+ * batch without synchronising (the SURVEY §8(b) form of the call).  An instance must not have two
+ * batches in flight at once (its workspace is reused): order them on one stream or wait on the
+ * event.  Intermediate outputs (dst_dtype) are in the stage's dtype; logits GX_F32.              */
+GX_API int gx_stage_run_async(gx_stage* st, void* stream, int k, const void* const* src, const int32_t* src_dtype,
+                              int32_t src_channels, void* const* dst, int32_t dst_dtype, void* done_event);
+
+/* Execution mode of a stage: GX_EXEC_GRAPH (default; one CUDA graph per k of per-op persistent
+ * kernels with programmatic dependent launch) or GX_EXEC_SPAN (one persistent span kernel with
+ * grid barriers between ops; bf16 only).  Both compute bit-identical results.                    */
+#define GX_EXEC_GRAPH 0
+#define GX_EXEC_SPAN 1
+GX_API int gx_stage_set_exec(gx_stage* st, int32_t mode);
 
 /* Span latency at batch k on this stage's SM budget, median of `iters` graph replays (ms).
  * Produces the rows a TableCostModel ingests (profiles.py:315-454, header profiles.py:24). */
@@ -239,9 +262,15 @@ typedef struct gx_serve_cfg {
                                  takes the request waits on that copy's event only;
                                  0: ingress already in device memory                          */
   int32_t egress_to_host;    /* WALL: D2H copy of each request's output                     */
-  int64_t slot_bytes;     /* per-request activation slot size on the device                 */
+  int64_t slot_bytes;     /* per-request activation slot size on the device; 0 = the library
+                             sizes it (largest DMA ingress / intermediate boundary of any route);
+                             a smaller non-zero value than a route needs is GX_EINVAL          */
   int32_t max_inflight;   /* slot pool size                                                 */
   int32_t warmup_requests_skip; /* reserved */
+  int64_t result_rows;    /* WALL / REPLAY: final-output rows kept (ring); 0 = max_inflight     */
+  double drain_ms;        /* WALL: after the horizon (no new requests) keep serving the requests
+                             already generated for up to this long, so tails near the horizon are
+                             measured; 0 = stop at the horizon like the reference                */
 } gx_serve_cfg;
 
 typedef struct gx_serve gx_serve;
@@ -262,8 +291,13 @@ GX_API int gx_serve_dispatch(gx_serve* s, double* t_ms, int32_t* stage, int32_t*
 GX_API int gx_serve_stats(gx_serve* s, double* wall_ms, int64_t* batches, int64_t* kernels);
 /* Per-request outputs (WALL / REPLAY): row i = request i's final-stage output (logits, fp32,
  * `elems` values; NaN for requests that did not complete).  Rows are valid while no more than
- * max_inflight requests completed (results are a ring of max_inflight rows). */
+ * result_rows requests completed (results are a ring of result_rows rows). */
 GX_API int gx_serve_outputs(gx_serve* s, float* out, int64_t n_requests, int64_t elems);
+/* Outputs of selected requests (indices into the request records): row i = request req[i]'s
+ * logits, NaN when it did not complete or a later completion reused its ring row; *held = rows
+ * filled.  Lets a long serving run spot-check its most recent result_rows completions. */
+GX_API int gx_serve_outputs_for(gx_serve* s, int64_t n, const int64_t* req, float* out, int64_t elems,
+                                int64_t* held);
 GX_API int gx_serve_destroy(gx_serve* s);
 
 #ifdef __cplusplus

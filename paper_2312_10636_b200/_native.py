@@ -11,16 +11,15 @@ from pathlib import Path
 
 from .errors import raise_for_status
 
-import os
-
-# GX_LIB: alternative build of the same library (development A/B of compile-time variants)
-LIB_PATH = Path(os.environ.get("GX_LIB") or Path(__file__).resolve().parent / "_gx.so")
+LIB_PATH = Path(__file__).resolve().parent / "_gx.so"
+ABI_VERSION = 2
 
 GX_BF16, GX_F32 = 0, 1
 (GX_OP_CONV, GX_OP_MAXPOOL, GX_OP_AVGPOOL, GX_OP_GAP, GX_OP_FC, GX_OP_LINEAR, GX_OP_LAYERNORM,
  GX_OP_ATTENTION, GX_OP_EMBED, GX_OP_COPY, GX_OP_FLATTEN_NCHW) = range(1, 12)
 GX_ACT_NONE, GX_ACT_RELU, GX_ACT_GELU = 0, 1, 2
 GX_CLOCK_VIRTUAL, GX_CLOCK_WALL, GX_CLOCK_REPLAY = 0, 1, 2
+GX_EXEC_GRAPH, GX_EXEC_SPAN = 0, 1
 
 
 class GxTensor(C.Structure):
@@ -74,7 +73,8 @@ class GxServeCfg(C.Structure):
     _fields_ = [("horizon_ms", C.c_double), ("epoch_ms", C.c_double), ("clock", C.c_int32),
                 ("record_dispatch", C.c_int32), ("ingress_from_host", C.c_int32),
                 ("egress_to_host", C.c_int32), ("slot_bytes", C.c_int64),
-                ("max_inflight", C.c_int32), ("warmup_requests_skip", C.c_int32)]
+                ("max_inflight", C.c_int32), ("warmup_requests_skip", C.c_int32), ("result_rows", C.c_int64),
+                ("drain_ms", C.c_double)]
 
 
 _lib = None
@@ -101,7 +101,10 @@ def lib():
                                   P(i32), P(i32), vp, C.c_size_t, P(vp)]),
         "gx_model_destroy": (i32, [vp]),
         "gx_model_tensor_elems": (i32, [vp, C.c_int, P(i64)]),
-        "gx_stage_create": (i32, [vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, P(vp)]),
+        "gx_model_dtype": (i32, [vp, P(i32)]),
+        "gx_stage_create": (i32, [vp, C.c_int, C.c_int, C.c_int, C.c_int, i32, vp, P(vp)]),
+        "gx_stage_run_async": (i32, [vp, vp, C.c_int, P(vp), P(i32), i32, P(vp), i32, vp]),
+        "gx_stage_set_exec": (i32, [vp, i32]),
         "gx_stage_destroy": (i32, [vp]),
         "gx_stage_stream": (i32, [vp, P(vp)]),
         "gx_stage_run": (i32, [vp, C.c_int, P(vp), P(i32), i32, P(vp), i32]),
@@ -123,6 +126,7 @@ def lib():
         "gx_serve_stats": (i32, [vp, P(dbl), P(i64), P(i64)]),
         "gx_serve_destroy": (i32, [vp]),
         "gx_serve_outputs": (i32, [vp, P(C.c_float), i64, i64]),
+        "gx_serve_outputs_for": (i32, [vp, i64, P(i64), P(C.c_float), i64, P(i64)]),
     }
     for name, (res, args) in sig.items():
         if not hasattr(L, name):
@@ -130,8 +134,8 @@ def lib():
         fn = getattr(L, name)
         fn.restype = res
         fn.argtypes = args
-    if L.gx_abi_version() != 1:
-        raise ImportError("libgx ABI version mismatch")
+    if L.gx_abi_version() != ABI_VERSION:
+        raise ImportError(f"libgx ABI version {L.gx_abi_version()} != {ABI_VERSION} (rebuild the library)")
     _lib = L
     return L
 

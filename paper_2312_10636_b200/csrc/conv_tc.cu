@@ -603,7 +603,7 @@ int conv_pick_stages(int BN, int num_kb, bool res, int Cout, int* nres_out, int 
     if (s > 8) s = 8;
     // short-K convs (the bottleneck expand 1x1s) are epilogue-bound: with the per-warp epilogue the next tile's residual/staging slot must be free while this
     // tile's epilogue runs; for K <= 128 one operand stage keeps the MMA ahead of the epilogue
-    const int kb_short = getenv("GX_RES2_KB") ? atoi(getenv("GX_RES2_KB")) : 0;  // measured neutral: off
+    const int kb_short = dev().res2_kb;  // measured neutral: off
     if (s >= 3 || nres <= 1 || (s >= 1 && num_kb <= kb_short)) {
       best_s = s < 1 ? 1 : (s < 2 && num_kb > kb_short) ? 2 : s;
       best_r = nres;

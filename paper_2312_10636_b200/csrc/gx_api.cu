@@ -40,6 +40,43 @@ int cuda_fail(cudaError_t e, const char* what) {
   return GX_ECUDA;
 }
 
+// Development switches: read from the environment only in builds compiled with -DGX_DEV_KNOBS
+// (scripts/ experiments); the shipped library always takes the defaults.
+const DevKnobs& dev() {
+  static const DevKnobs knobs = [] {
+    DevKnobs d;
+#ifdef GX_DEV_KNOBS
+    auto flag = [](const char* n) { return getenv(n) != nullptr; };
+    auto num = [](const char* n, int def) {
+      const char* v = getenv(n);
+      return v ? atoi(v) : def;
+    };
+    d.no_halo = flag("GX_NO_HALO");
+    d.no_halo32 = flag("GX_NO_HALO32");
+    d.no_wbulk = flag("GX_NO_WBULK");
+    d.no_ystore = flag("GX_NO_YSTORE");
+    d.gmaps = flag("GX_GMAPS");
+    d.no_res_mma = flag("GX_NO_RES_MMA");
+    d.no_tma_im2col = flag("GX_NO_TMA_IM2COL");
+    d.no_a2d = flag("GX_NO_A2D");
+    d.no_wres = flag("GX_NO_WRES");
+    d.no_wstore = flag("GX_NO_WSTORE");
+    d.fc_simt = flag("GX_FC_SIMT");
+    d.no_pdl = flag("GX_NO_PDL");
+    d.pool_nostrip = flag("GX_POOL_NOSTRIP");
+    d.conv_dbg = num("GX_CONV_DBG", 0);
+    d.bn = num("GX_BN", 0);
+    d.kps = num("GX_KPS", 0);
+    d.stages = num("GX_STAGES", 0);
+    d.res2_kb = num("GX_RES2_KB", 0);
+    d.serve_streams = num("GX_SERVE_STREAMS", d.serve_streams);
+    d.copy_streams = num("GX_COPY_STREAMS", d.copy_streams);
+#endif
+    return d;
+  }();
+  return knobs;
+}
+
 // ---------------------------------------------------------------- tensor maps
 typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                       const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -217,9 +254,9 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
   // the space-to-depth stem (4x4 / s1 / pad 2,2,1,1 over 16 channels): 32-byte halo rows, one K=16
   // MMA per tap, 128 // (W + 3) output rows per tile
   const bool halo32 = R == 4 && S == 4 && a.ph == 2 && a.pw == 2 && op.ph_hi == 1 && op.pw_hi == 1 && op.Cin == 16 &&
-                      ti.W + 3 <= kBM && getenv("GX_NO_HALO32") == nullptr;
+                      ti.W + 3 <= kBM && !dev().no_halo32;
   if (!for_span && op.kind == GX_OP_CONV && (halo128 || halo32) && a.sh == 1 && a.sw == 1 && op.Cin == ti.C &&
-      a.Ho == ti.H && a.Wo == ti.W && op.in2 < 0 && to.dtype == GX_BF16 && getenv("GX_NO_HALO") == nullptr) {
+      a.Ho == ti.H && a.Wo == ti.W && op.in2 < 0 && to.dtype == GX_BF16 && !dev().no_halo) {
     const int Wp = ti.W + (halo32 ? 3 : 2);
     a.halo = 1;
     a.hWp = Wp;
@@ -238,8 +275,8 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
     a.idesc = umma_idesc_bf16(kBM, a.BN);
     a.stages = conv_halo_pick_stages(a.BN, a.Cout);
     a.tmem_cols = tmem_cols_for(a.BN);
-    a.wsw = getenv("GX_NO_WBULK") ? nullptr : wsw;
-    a.dbg = getenv("GX_CONV_DBG") ? atoi(getenv("GX_CONV_DBG")) : 0;
+    a.wsw = dev().no_wbulk ? nullptr : wsw;
+    a.dbg = dev().conv_dbg;
     a.tma_a = 1;
     const int kpad = a.num_kb * kBK;
     memset(&out->amap, 0, sizeof(out->amap));
@@ -254,8 +291,7 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
     return GX_OK;
   }
   a.BN = pick_bn(op.Cout, a.m_tiles, sm_budget, bn_cap);
-  if (const char* e = getenv("GX_BN")) {  // tuning override (development)
-    const int bn = atoi(e);
+  if (const int bn = dev().bn) {  // tuning override (development builds only)
     if (bn >= 16 && bn <= 256 && bn % 16 == 0) a.BN = bn;
   }
   a.n_tiles = (a.Cout + a.BN - 1) / a.BN;
@@ -271,24 +307,21 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
   a.idesc = umma_idesc_bf16(kBM, a.BN);
   // bf16 output through smem + TMA store when every 64-column group of a tile is whole (a tile
   // never writes past its own channel slice of a concat tensor)
-  a.ystore = !a.y_f32 && a.BN % 64 == 0 && a.Cout % 64 == 0 && to.C >= 64 && getenv("GX_NO_YSTORE") == nullptr &&
-             getenv("GX_GMAPS") == nullptr;
+  a.ystore = !a.y_f32 && a.BN % 64 == 0 && a.Cout % 64 == 0 && to.C >= 64 && !dev().no_ystore && !dev().gmaps;
   // residual through the tensor core (identity k-blocks): needs the bulk-weight layout, the 2D A
   // path and whole 64-column groups; the epilogue then runs residual-free
   // only where the epilogue dominates (K <= 128: layer1/2 expands); for K >= 256 the extra BN/64
   // identity k-blocks cost more MMA time than the epilogue add they remove (measured)
-  a.res_mma = !for_span && a.res && wsw && !getenv("GX_NO_WBULK") && res_through_mma(op) && a.BN % 64 == 0 &&
+  a.res_mma = !for_span && a.res && wsw && !dev().no_wbulk && res_through_mma(op) && a.BN % 64 == 0 &&
               a.num_kb <= 2 &&
-              a.Cin == ti.C && getenv("GX_NO_TMA_IM2COL") == nullptr && getenv("GX_NO_A2D") == nullptr &&
-              getenv("GX_NO_RES_MMA") == nullptr;
+              a.Cin == ti.C && !dev().no_tma_im2col && !dev().no_a2d && !dev().no_res_mma;
   const bool epi_res = a.res != nullptr && !a.res_mma;  // residual handled by the epilogue
   // two k-blocks per pipeline stage halve the barrier round trips per unit of K; worth it when the
   // per-k-block MMA time (2*BN cycles) is below the ~500-cycle stage round trip and >= 3 stages fit
   a.kps = 1;
   {
-    const bool tma = getenv("GX_NO_TMA_IM2COL") == nullptr;
-    const char* e = getenv("GX_KPS");
-    const int want = e ? atoi(e) : (a.BN <= 64 ? 2 : 1);
+    const bool tma = !dev().no_tma_im2col;
+    const int want = dev().kps ? dev().kps : (a.BN <= 64 ? 2 : 1);
     for (int kk = want; kk >= 2 && a.kps == 1 && !a.res_mma; --kk) {
       int nres2 = 0;
       if (tma && kk <= 3 && a.num_kb >= kk &&
@@ -298,30 +331,29 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
   }
   a.stages = conv_pick_stages(a.BN, a.num_kb + (a.res_mma ? a.BN / 64 : 0), epi_res || a.ystore, a.Cout, &a.nres,
                               a.kps);
-  if (const char* e = getenv("GX_STAGES")) {
-    const int st = atoi(e);
+  if (const int st = dev().stages) {
     if (st >= 1 && st <= a.stages) a.stages = st;
   }
   a.tmem_cols = tmem_cols_for(a.BN);
-  a.wsw = getenv("GX_NO_WBULK") ? nullptr : wsw;
-  a.dbg = getenv("GX_CONV_DBG") ? atoi(getenv("GX_CONV_DBG")) : 0;
+  a.wsw = dev().no_wbulk ? nullptr : wsw;
+  a.dbg = dev().conv_dbg;
   a.trace = (a.dbg & 16) ? debug_trace_buffer() : nullptr;
   if (a.res && (T[op.in2].dtype != GX_BF16 || (a.res_ld & 7))) return fail(GX_EINVAL, "bad residual tensor");
   const int kpad = a.num_kb * kBK;
   memset(&out->amap, 0, sizeof(out->amap));
   memset(&out->rmap, 0, sizeof(out->rmap));
   memset(&out->ymap, 0, sizeof(out->ymap));
-  a.wstore = !for_span && a.ystore && (!epi_res || getenv("GX_NO_WRES") == nullptr) && getenv("GX_NO_TMA_IM2COL") == nullptr &&
-             a.BN % 128 == 0 && getenv("GX_NO_WSTORE") == nullptr;
+  a.wstore = !for_span && a.ystore && (!epi_res || !dev().no_wres) && !dev().no_tma_im2col &&
+             a.BN % 128 == 0 && !dev().no_wstore;
   if (a.ystore && !encode_tmap_2d_bf16(&out->ymap, a.y, to.C, a.M, static_cast<uint64_t>(to.C) * 2, 64,
                                        a.wstore ? 32 : kBM))
     return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for the conv output: " + g_last_encode);
   if (!encode_tmap_2d_bf16(&out->wmap, wbase + op.w_off, kpad, op.Cout, static_cast<uint64_t>(kpad) * 2, kBK, a.BN))
     return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for conv weights: " + g_last_encode);
   a.cpl = (op.Cin % 64 == 0) ? 64 : (op.Cin % 32 == 0) ? 32 : (op.Cin % 16 == 0) ? 16 : 8;
-  a.tma_a = getenv("GX_NO_TMA_IM2COL") == nullptr;
+  a.tma_a = !dev().no_tma_im2col;
   a.a2d = a.tma_a && a.R == 1 && a.S == 1 && a.sh == 1 && a.sw == 1 && a.ph == 0 && a.pw == 0 && a.cpl == 64 &&
-          a.Cin == ti.C && getenv("GX_NO_A2D") == nullptr;
+          a.Cin == ti.C && !dev().no_a2d;
   if (a.a2d) {
     if (!encode_tmap_2d_bf16(&out->amap, a.x, ti.C, a.M, static_cast<uint64_t>(ti.C) * 2, kBK, kBM))
       return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for conv input: " + g_last_encode);
@@ -334,7 +366,7 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
     return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for the residual: " + g_last_encode);
   out->grid = std::min(a.num_tiles, std::max(1, sm_budget));
   a.gmaps = nullptr;
-  if (getenv("GX_GMAPS")) {  // experiment: maps in global memory (leaks one small buffer per plan)
+  if (dev().gmaps) {  // experiment: maps in global memory (leaks one small buffer per plan)
     CUtensorMap* d = nullptr;
     CUtensorMap h[3] = {out->wmap, out->amap, out->rmap};
     if (cudaMalloc(&d, sizeof(h)) == cudaSuccess && cudaMemcpy(d, h, sizeof(h), cudaMemcpyHostToDevice) == cudaSuccess)

@@ -18,6 +18,18 @@ int cuda_fail(cudaError_t e, const char* what);
 // capture need one; a caller thread that never touched CUDA has none).  Cheap when already bound.
 int bind_device(int device);
 
+// Kernel-selection experiments of development builds (-DGX_DEV_KNOBS reads them from GX_*
+// environment variables once); the product library always runs the defaults below.
+struct DevKnobs {
+  bool no_halo = false, no_halo32 = false, no_wbulk = false, no_ystore = false, gmaps = false, no_res_mma = false,
+       no_tma_im2col = false, no_a2d = false, no_wres = false, no_wstore = false, fc_simt = false, no_pdl = false,
+       pool_nostrip = false;
+  int conv_dbg = 0, bn = 0, kps = 0, stages = 0, res2_kb = 0;
+  int serve_streams = 64;  // serving stream-pool lanes
+  int copy_streams = 1;    // DMA-ingress copy streams
+};
+const DevKnobs& dev();
+
 #define GX_CUDA(call)                                   \
   do {                                                  \
     cudaError_t _e = (call);                            \

@@ -52,7 +52,7 @@ inline bool res_through_mma(const gx_op& op) {
 // sum K in different orders.  (The CUDA-core kernel is faster only for batch-1 heads spread over
 // a whole GPU, which serving never runs.)
 inline bool fc_on_tc(const gx_op& op) {
-  return op.kind == GX_OP_FC && op.Cin % 64 == 0 && op.Cout % 8 == 0 && op.b_off >= 0 && getenv("GX_FC_SIMT") == nullptr;
+  return op.kind == GX_OP_FC && op.Cin % 64 == 0 && op.Cout % 8 == 0 && op.b_off >= 0 && !gx::dev().fc_simt;
 }
 // ops executed by conv_tc_kernel / conv_halo_kernel (planned with plan_conv)
 inline bool is_gemm_op(const gx_op& op) { return op.kind == GX_OP_CONV || op.kind == GX_OP_LINEAR || fc_on_tc(op); }
@@ -66,6 +66,7 @@ struct gx_model {
   std::vector<gx_op> ops;
   std::vector<int32_t> unit_first_op;  // n_units + 1
   std::vector<int32_t> boundary;       // n_units + 1
+  int32_t dtype = GX_BF16;             // compute element type (gx_model_dtype)
   void* wdev = nullptr;
   size_t wbytes = 0;
   void* wsw = nullptr;                // conv/linear weights re-laid for bulk copies (see plan_conv)

@@ -101,7 +101,7 @@ int capture_span(gx_stage* st, int k, gx_stage::PerK* out) {
   GX_CUDA(cudaStreamBeginCapture(st->stream, cudaStreamCaptureModeThreadLocal));
   int kernels = 0;
   int rc = GX_OK;
-  const bool use_pdl = getenv("GX_NO_PDL") == nullptr;
+  const bool use_pdl = !dev().no_pdl;
   for (size_t i = 0; i < st->ops.size() && rc == GX_OK; ++i) {
     const gx_op& op = m->ops[st->ops[i]];
     const bool is_conv = is_gemm_op(op);
@@ -332,8 +332,16 @@ int gx_model_create(gx_ctx* ctx, const char* model_id, int n_tensors, const gx_t
         (op.b_off >= 0 && static_cast<size_t>(op.b_off) >= blob_bytes))
       return fail(GX_EINVAL, "op " + std::to_string(i) + " weight offset outside the blob");
   }
+  // one compute element type per chain (the boundary-0 tensor's); only the chain output may differ
+  // (fp32 logits of a bf16 chain)
+  const int32_t mdt = tensors[boundary[0]].dtype;
+  if (mdt != GX_BF16 && mdt != GX_F32) return fail(GX_EINVAL, "tensor dtype must be GX_BF16 or GX_F32");
+  for (int t = 0; t < n_tensors; ++t)
+    if (tensors[t].dtype != mdt && !(t == boundary[n_units] && tensors[t].dtype == GX_F32))
+      return fail(GX_EINVAL, "tensor " + std::to_string(t) + " mixes element types within one chain");
   GX_CUDA(cudaSetDevice(ctx->device));
   gx_model* m = new gx_model();
+  m->dtype = mdt;
   m->ctx = ctx;
   m->id = model_id ? model_id : "";
   m->tensors.assign(tensors, tensors + n_tensors);
@@ -363,14 +371,24 @@ int gx_model_destroy(gx_model* m) {
   return GX_OK;
 }
 
+int gx_model_dtype(gx_model* m, int32_t* dtype_out) {
+  if (!m || !dtype_out) return fail(GX_EINVAL, "null arg");
+  *dtype_out = m->dtype;
+  return GX_OK;
+}
+
 int gx_model_tensor_elems(gx_model* m, int tid, int64_t* out) {
   if (!m || !out || tid < 0 || tid >= static_cast<int>(m->tensors.size())) return fail(GX_EINVAL, "bad tensor id");
   *out = tensor_elems(m->tensors[tid]);
   return GX_OK;
 }
 
-int gx_stage_create(gx_model* m, int start, int end, int max_batch, int sm_budget, void* stream, gx_stage** out) {
+int gx_stage_create(gx_model* m, int start, int end, int max_batch, int sm_budget, int32_t dtype, void* stream,
+                    gx_stage** out) {
   if (!m || !out) return fail(GX_EINVAL, "null arg");
+  if (dtype != m->dtype)
+    return fail(GX_EINVAL, std::string("stage dtype ") + (dtype == GX_F32 ? "fp32" : dtype == GX_BF16 ? "bf16" : "?") +
+                               " does not match model " + m->id + "'s " + (m->dtype == GX_F32 ? "fp32" : "bf16"));
   if (!(0 <= start && start < end && end <= m->n_units()))
     return fail(GX_EINVAL, "bad span [" + std::to_string(start) + ", " + std::to_string(end) + ") for model " + m->id);
   if (max_batch < 1 || max_batch > 64) return fail(GX_EINVAL, "max_batch must be in 1..64");
@@ -404,10 +422,9 @@ int gx_stage_create(gx_model* m, int start, int end, int max_batch, int sm_budge
     }
     st->own_stream = true;
   }
-  const char* mode = getenv("GX_EXEC");
   // default: per-op persistent kernels in a CUDA graph with PDL (measured faster at the serving
-  // operating point); GX_EXEC=span selects the single-launch persistent span kernel
-  st->span_mode = mode && std::string(mode) == "span";
+  // operating point); gx_stage_set_exec(GX_EXEC_SPAN) selects the single-launch span kernel
+  st->span_mode = false;
   cudaError_t e = cudaMalloc(&st->bar, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMemset(st->bar, 0, sizeof(unsigned long long));
   if (e != cudaSuccess) {
@@ -433,6 +450,25 @@ int gx_stage_destroy(gx_stage* st) {
   if (st->prof_dst) cudaFree(st->prof_dst);
   if (st->own_stream) cudaStreamDestroy(st->stream);
   delete st;
+  return GX_OK;
+}
+
+int gx_stage_set_exec(gx_stage* st, int32_t mode) {
+  if (!st) return fail(GX_EINVAL, "null arg");
+  if (mode != GX_EXEC_GRAPH && mode != GX_EXEC_SPAN) return fail(GX_EINVAL, "unknown execution mode");
+  if (mode == GX_EXEC_SPAN && st->m->dtype != GX_BF16) return fail(GX_EINVAL, "the span kernel is bf16-only");
+  const bool span = mode == GX_EXEC_SPAN;
+  if (span != st->span_mode) {
+    if (int rc = bind_device(st->m->ctx->device)) return rc;
+    GX_CUDA(cudaStreamSynchronize(st->stream));
+    for (auto& kv : st->graphs) {  // programs of the other mode are rebuilt on demand
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+      for (auto& ch : kv.second.chunks)
+        if (ch.d_ops) cudaFree(ch.d_ops);
+    }
+    st->graphs.clear();
+    st->span_mode = span;
+  }
   return GX_OK;
 }
 
@@ -462,6 +498,17 @@ int gx_stage_run(gx_stage* st, int k, const void* const* src, const int32_t* src
   return gx::stage_run_on(st, st->stream, k, src, src_dtype, src_channels, dst, dst_dtype);
 }
 
+int gx_stage_run_async(gx_stage* st, void* stream, int k, const void* const* src, const int32_t* src_dtype,
+                       int32_t src_channels, void* const* dst, int32_t dst_dtype, void* done_event) {
+  if (!st || !src || !src_dtype || !dst) return fail(GX_EINVAL, "null arg");
+  if (k < 1 || k > st->max_batch) return fail(GX_EINVAL, "batch k outside 1..max_batch");
+  if (int rc = bind_device(st->m->ctx->device)) return rc;
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : st->stream;
+  if (int rc = gx::stage_run_on(st, s, k, src, src_dtype, src_channels, dst, dst_dtype)) return rc;
+  if (done_event) GX_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(done_event), s));
+  return GX_OK;
+}
+
 }  // extern "C"
 
 namespace gx {
@@ -470,6 +517,7 @@ namespace gx {
 int stage_run_on(gx_stage* st, cudaStream_t stream, int k, const void* const* src, const int32_t* src_dtype,
                  int32_t src_channels, void* const* dst, int32_t dst_dtype) {
   gx_model* m = st->m;
+  if (k < 1 || k > st->max_batch) return fail(GX_EINVAL, "batch k outside 1..max_batch");
   const gx_tensor& tin = m->tensors[st->in_tid];
   const gx_tensor& tout = m->tensors[st->out_tid];
   const int c_src = src_channels > 0 ? src_channels : tin.C;

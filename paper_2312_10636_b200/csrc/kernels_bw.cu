@@ -602,7 +602,7 @@ cudaError_t launch_pool(int mode, const __nv_bfloat16* x, int N, int H, int W, i
   if (C & 7) return cudaErrorInvalidValue;
   const int64_t work = static_cast<int64_t>(N) * Ho * Wo * (C / 8);
   if (work >= (int64_t{1} << 31)) return cudaErrorInvalidValue;
-  if (R == 3 && S == 3 && sh == 1 && sw == 1 && ph <= 2 && pw <= 2 && getenv("GX_POOL_NOSTRIP") == nullptr) {
+  if (R == 3 && S == 3 && sh == 1 && sw == 1 && ph <= 2 && pw <= 2 && !dev().pool_nostrip) {
     const int64_t strips = static_cast<int64_t>(N) * ((Ho + kPoolStrip - 1) / kPoolStrip) * Wo * (C / 8);
     pool3s1_kernel<<<grid_for(strips, 256, grid), 256, 0, s>>>(mode, x, N, H, W, C, x_ld, y, Ho, Wo, y_ld, y_coff, ph,
                                                                pw, count_include_pad);

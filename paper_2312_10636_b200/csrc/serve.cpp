@@ -59,7 +59,7 @@ struct Req {
   int cur_dtype = GX_F32;
   int cur_channels = 0;
   int slot = -1;
-  int64_t result_idx = -1;  // row of `results` holding the request's output (final stage)
+  int64_t result_seq = -1;  // completion slot number; its output lives in ring row result_seq % result_rows
   int h2d_ev = -1;          // GX_INGRESS_DMA: event of the arrival-time H2D copy into the slot
 };
 
@@ -132,7 +132,6 @@ struct gx_serve {
   void* results = nullptr;  // fp32 outputs ring (device) or pinned host
   int64_t result_elems = 0;
   int64_t result_cursor = 0;
-  cudaStream_t ingress_stream = nullptr;
   // Stream pool: a batch runs on an idle pooled stream rather than on its instance's own stream.
   // The device has at most CUDA_DEVICE_MAX_CONNECTIONS (32) hardware queues; with one stream per
   // instance, plans with > 32 instances alias streams onto shared queues and unrelated instances
@@ -140,8 +139,6 @@ struct gx_serve {
   std::vector<cudaStream_t> pool;
   std::vector<int> pool_n;        // batches in flight per lane
   std::vector<double> pool_last;  // wall ms of the lane's last dispatch
-  cudaEvent_t ingress_ev = nullptr;
-  bool ingress_pending = false;
   // GX_INGRESS_DMA: copy-engine streams and a recycled event per in-flight arrival copy
   std::vector<cudaStream_t> copy_streams;
   std::vector<cudaEvent_t> h2d_events;
@@ -297,6 +294,7 @@ int gx_serve::dispatch_gpu(int si, int bi) {
   b.inst = inst;
   gx_stage* g = st.inst[inst];
   const int k = static_cast<int>(b.reqs.size());
+  if (k < 1 || k > 64 || k > g->max_batch) return fail(GX_EINTERNAL, "dispatched batch larger than the instance");
   const void* src[64];
   int32_t sdt[64];
   void* dst[64];
@@ -317,21 +315,17 @@ int gx_serve::dispatch_gpu(int si, int bi) {
     sdt[i] = r.cur_dtype;
     channels = std::max(channels, r.cur_channels);
     if (st.out_final) {
-      r.result_idx = result_cursor % cfg.max_inflight;
-      dst[i] = static_cast<uint8_t*>(results) + r.result_idx * result_elems * 4;
-      ++result_cursor;
+      r.result_seq = result_cursor++;
+      dst[i] = static_cast<uint8_t*>(results) + (r.result_seq % cfg.result_rows) * result_elems * 4;
     } else {
       dst[i] = static_cast<uint8_t*>(slots) + static_cast<size_t>(r.slot) * cfg.slot_bytes;
     }
   }
-  if (ingress_pending) {
-    GX_CUDA(cudaEventRecord(ingress_ev, ingress_stream));
-    ingress_pending = false;
-  }
   b.lane = lane;
   pool_n[lane] += 1;
   pool_last[lane] = b.t_disp;
-  int rc = gx::stage_run_on(g, sm, k, src, sdt, channels, dst, st.out_final ? GX_F32 : GX_BF16);
+  const int out_dt = st.out_final ? GX_F32 : g->m->tensors[g->out_tid].dtype;
+  int rc = gx::stage_run_on(g, sm, k, src, sdt, channels, dst, out_dt);
   if (rc != GX_OK) return rc;
   int kc = 0;
   gx_stage_kernel_count(g, k, &kc);
@@ -341,7 +335,7 @@ int gx_serve::dispatch_gpu(int si, int bi) {
     Req& r = reqs[b.reqs[i]];
     if (!st.out_final) {
       r.cur = dst[i];
-      r.cur_dtype = GX_BF16;
+      r.cur_dtype = out_dt;
       r.cur_channels = 0;
     }
   }
@@ -492,7 +486,11 @@ int gx_serve::run() {
     }
   } else {
     // Wall clock: scheduled events fire when the clock passes them; completions fire when the
-    // batch's CUDA event has completed (polled).  Stops at the horizon; in-flight work drains.
+    // batch's CUDA event has completed (polled).  Generation stops at the horizon; requests
+    // already generated keep being served (arrivals, partial-batch timeouts, completions) for up
+    // to drain_ms more, so the last windows' tails are measured; anything still unfinished then
+    // stays "inflight" (status 2), as at the reference's horizon (simulator.py:460-463).
+    const double limit = horizon + std::max(0.0, cfg.drain_ms);
     for (;;) {
       const double now = now_wall();
       bool progressed = false;
@@ -505,7 +503,7 @@ int gx_serve::run() {
           inflight[i] = inflight.back();
           inflight.pop_back();
           pool_n[batches[bi].lane] -= 1;
-          if (now <= horizon) {
+          if (now <= limit) {
             rc = stage_done(bi, now);
           } else {
             Stage& st = stages[batches[bi].stage];
@@ -521,7 +519,7 @@ int gx_serve::run() {
         }
       }
       if (rc != GX_OK) break;
-      while (!heap.empty() && heap.top().t <= now && heap.top().t <= horizon + kEps && rc == GX_OK) {
+      while (!heap.empty() && heap.top().t <= now && heap.top().t <= limit + kEps && rc == GX_OK) {
         Ev e = heap.top();
         heap.pop();
         progressed = true;
@@ -552,8 +550,8 @@ int gx_serve::run() {
         }
       }
       if (rc != GX_OK) break;
-      if (now > horizon && inflight.empty()) break;
-      if (now > horizon + 60000.0) return fail(GX_EINTERNAL, "wall-clock serving did not drain");
+      if (now > horizon && inflight.empty() && (now > limit || heap.empty() || heap.top().t > limit + kEps)) break;
+      if (now > limit + 60000.0) return fail(GX_EINTERNAL, "wall-clock serving did not drain");
       (void)progressed;
     }
   }
@@ -591,9 +589,9 @@ int gx_serve_create(gx_ctx* ctx, int n_stages, const gx_serve_stage* st, int n_r
     x.free = st[i].instances;
     x.budget = st[i].budget_ms;
     x.out_final = st[i].out_final;
-    if (x.batch < 1 || x.instances < 1) {
+    if (x.batch < 1 || x.batch > 64 || x.instances < 1) {
       delete s;
-      return fail(GX_EINVAL, "stage needs batch >= 1 and instances >= 1");
+      return fail(GX_EINVAL, "stage needs 1 <= batch <= 64 and instances >= 1");
     }
     if (st[i].lat_ms) x.lat.assign(st[i].lat_ms, st[i].lat_ms + x.batch + 1);
     if (cfg->clock == GX_CLOCK_REPLAY && x.lat.empty()) {
@@ -605,7 +603,17 @@ int gx_serve_create(gx_ctx* ctx, int n_stages, const gx_serve_stage* st, int n_r
         delete s;
         return fail(GX_EINVAL, "wall clock needs executor instances per stage");
       }
-      for (int j = 0; j < x.instances; ++j) x.inst.push_back(static_cast<gx_stage*>(st[i].inst[j]));
+      for (int j = 0; j < x.instances; ++j) {
+        gx_stage* g = static_cast<gx_stage*>(st[i].inst[j]);
+        if (!g || g->max_batch < x.batch || g->m->ctx->device != ctx->device) {
+          delete s;
+          return fail(GX_EINVAL, "stage " + std::to_string(i) + ": executor instance " + std::to_string(j) +
+                                     (g ? " has max_batch " + std::to_string(g->max_batch) + " < stage batch " +
+                                              std::to_string(x.batch) + " or lives on another device"
+                                        : " is null"));
+        }
+        x.inst.push_back(g);
+      }
       x.busy.assign(x.instances, 0);
     } else if (x.lat.empty()) {
       delete s;
@@ -659,9 +667,41 @@ int gx_serve_create(gx_ctx* ctx, int n_stages, const gx_serve_stage* st, int n_r
     s->clients.push_back(std::move(c));
   }
   if (cfg->clock != GX_CLOCK_VIRTUAL) {
+    if (cfg->max_inflight < 1) {
+      delete s;
+      return fail(GX_EINVAL, "max_inflight must be >= 1 when batches execute");
+    }
+    // Every route's ingress must exist, and a request that needs a device slot (DMA ingress, or a
+    // stage whose output feeds another stage) must fit it: the slot holds the DMA-copied ingress
+    // and then each intermediate boundary the route writes (stage output elems x element size).
+    int64_t need = 0;
+    for (size_t i = 0; i < s->routes.size(); ++i) {
+      const Route& r = s->routes[i];
+      if (r.n_stages == 0) continue;
+      if (!r.ingress || r.ingress_bytes <= 0) {
+        delete s;
+        return fail(GX_EINVAL, "route " + std::to_string(i) + " has no ingress buffer");
+      }
+      if (cfg->ingress_from_host == GX_INGRESS_DMA) need = std::max(need, r.ingress_bytes);
+      for (int j = 0; j < r.n_stages; ++j) {
+        const Stage& x = s->stages[r.stage[j]];
+        if (x.out_final) continue;
+        const gx_stage* g = x.inst[0];
+        const gx_tensor& to = g->m->tensors[g->out_tid];
+        need = std::max<int64_t>(need, tensor_elems(to) * elem_size(to.dtype));
+      }
+    }
+    if (s->cfg.slot_bytes == 0) s->cfg.slot_bytes = (need + 255) / 256 * 256;
+    if (s->cfg.slot_bytes < need) {
+      const int64_t have = s->cfg.slot_bytes;
+      delete s;
+      return fail(GX_EINVAL, "slot_bytes " + std::to_string(have) + " < " + std::to_string(need) +
+                                 " bytes a route needs (ingress copy or intermediate boundary)");
+    }
+    if (s->cfg.result_rows <= 0) s->cfg.result_rows = cfg->max_inflight;
     cudaError_t e = cudaSetDevice(ctx->device);
-    if (e == cudaSuccess && cfg->max_inflight > 0 && cfg->slot_bytes > 0)
-      e = cudaMalloc(&s->slots, static_cast<size_t>(cfg->slot_bytes) * cfg->max_inflight);
+    if (e == cudaSuccess && s->cfg.slot_bytes > 0)
+      e = cudaMalloc(&s->slots, static_cast<size_t>(s->cfg.slot_bytes) * cfg->max_inflight);
     int64_t relems = 0;
     for (auto& x : s->stages)
       if (x.out_final && !x.inst.empty()) {
@@ -670,14 +710,13 @@ int gx_serve_create(gx_ctx* ctx, int n_stages, const gx_serve_stage* st, int n_r
       }
     s->result_elems = relems;
     if (e == cudaSuccess && relems > 0) {
-      const size_t bytes = static_cast<size_t>(relems) * 4 * std::max(1, cfg->max_inflight);
+      const size_t bytes = static_cast<size_t>(relems) * 4 * s->cfg.result_rows;
       e = cfg->egress_to_host ? cudaHostAlloc(&s->results, bytes, cudaHostAllocMapped) : cudaMalloc(&s->results, bytes);
     }
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->ingress_stream, cudaStreamNonBlocking);
     // more lanes than the 32 hardware queues: the least-loaded-lane choice then spreads in-flight
     // batches over every queue (measured: 30 lanes -> p99 205 ms, 64 -> 101 ms at 1536 clients)
     int lanes = 64;
-    if (const char* v = getenv("GX_SERVE_STREAMS")) lanes = std::max(1, atoi(v));
+    lanes = std::max(1, dev().serve_streams);
     for (int i = 0; i < lanes && e == cudaSuccess; ++i) {
       cudaStream_t q = nullptr;
       e = cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking);
@@ -688,14 +727,12 @@ int gx_serve_create(gx_ctx* ctx, int n_stages, const gx_serve_stage* st, int n_r
     // one FIFO copy stream: arrival order is deadline order, and concurrent copies only share
     // the PCIe link (measured at 1152 clients: p99 88 ms with 1 stream, 205-220 ms with 4 or 16)
     int ncopy = 1;
-    if (const char* v = getenv("GX_COPY_STREAMS")) ncopy = std::max(1, atoi(v));
+    ncopy = std::max(1, dev().copy_streams);
     for (int i = 0; i < ncopy && e == cudaSuccess && cfg->ingress_from_host == GX_INGRESS_DMA; ++i) {
       cudaStream_t q = nullptr;
       e = cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking);
       if (e == cudaSuccess) s->copy_streams.push_back(q);
     }
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s->ingress_ev, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventRecord(s->ingress_ev, s->ingress_stream);
     if (e != cudaSuccess) {
       gx_serve_destroy(s);
       return cuda_fail(e, "serving resources");
@@ -758,23 +795,37 @@ int gx_serve_stats(gx_serve* s, double* wall_ms, int64_t* batches, int64_t* kern
 
 int gx_serve_outputs(gx_serve* s, float* out, int64_t n_requests, int64_t elems) {
   if (!s || !out) return fail(GX_EINVAL, "null arg");
+  if (n_requests < static_cast<int64_t>(s->reqs.size())) return fail(GX_EINVAL, "output array too small");
+  if (s->gpu() && s->result_cursor > s->cfg.result_rows)
+    return fail(GX_EINVAL, "outputs were overwritten (more completions than result_rows)");
+  std::vector<int64_t> all(s->reqs.size());
+  for (size_t i = 0; i < all.size(); ++i) all[i] = static_cast<int64_t>(i);
+  int64_t held = 0;
+  return gx_serve_outputs_for(s, static_cast<int64_t>(all.size()), all.data(), out, elems, &held);
+}
+
+int gx_serve_outputs_for(gx_serve* s, int64_t n, const int64_t* req, float* out, int64_t elems, int64_t* held) {
+  if (!s || (n > 0 && (!req || !out))) return fail(GX_EINVAL, "null arg");
   if (!s->gpu()) return fail(GX_EINVAL, "outputs exist only when batches execute on the GPU");
   if (elems != s->result_elems) return fail(GX_EINVAL, "output row size mismatch");
-  if (n_requests < static_cast<int64_t>(s->reqs.size())) return fail(GX_EINVAL, "output array too small");
-  if (s->result_cursor > s->cfg.max_inflight)
-    return fail(GX_EINVAL, "outputs were overwritten (more completions than max_inflight result rows)");
   GX_CUDA(cudaSetDevice(s->ctx->device));
   GX_CUDA(cudaDeviceSynchronize());
-  for (size_t i = 0; i < s->reqs.size(); ++i) {
-    const Req& r = s->reqs[i];
-    float* dst = out + static_cast<int64_t>(i) * elems;
-    if (r.status != 0 || r.result_idx < 0) {
+  int64_t got = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    float* dst = out + i * elems;
+    const int64_t ri = req[i];
+    const bool ok = ri >= 0 && ri < static_cast<int64_t>(s->reqs.size()) && s->reqs[ri].status == 0 &&
+                    s->reqs[ri].result_seq >= 0 && s->reqs[ri].result_seq >= s->result_cursor - s->cfg.result_rows;
+    if (!ok) {  // not completed, or its ring row was reused by a later completion
       for (int64_t j = 0; j < elems; ++j) dst[j] = NAN;
       continue;
     }
-    const uint8_t* src = static_cast<const uint8_t*>(s->results) + r.result_idx * elems * 4;
+    const uint8_t* src =
+        static_cast<const uint8_t*>(s->results) + (s->reqs[ri].result_seq % s->cfg.result_rows) * elems * 4;
     GX_CUDA(cudaMemcpy(dst, src, elems * 4, cudaMemcpyDefault));
+    ++got;
   }
+  if (held) *held = got;
   return GX_OK;
 }
 
@@ -792,10 +843,8 @@ int gx_serve_destroy(gx_serve* s) {
       else
         cudaFree(s->results);
     }
-    if (s->ingress_ev) cudaEventDestroy(s->ingress_ev);
     for (cudaEvent_t ev : s->h2d_events) cudaEventDestroy(ev);
     for (cudaStream_t q : s->copy_streams) cudaStreamDestroy(q);
-    if (s->ingress_stream) cudaStreamDestroy(s->ingress_stream);
     for (cudaStream_t q : s->pool) cudaStreamDestroy(q);
   }
   delete s;

@@ -47,12 +47,18 @@ class Context:
             return []
         scale = max(1.0, capacity / total) if work_conserving else 1.0
         cap = self.sm_count * capacity // 100
-        out = []
+        out, floor = [], []
         for s, n in shares_instances:
-            b = max(self.sm_budget(s) if not work_conserving else 1, int(s * scale * self.sm_count / 100))
-            out.extend([min(b, self.sm_count)] * n)
-        while sum(out) > cap and max(out) > 1:  # rounding can overshoot: trim the largest
-            out[out.index(max(out))] -= 1
+            f = min(self.sm_budget(s), self.sm_count)  # the profiled budget: never handed out less
+            b = max(f, min(int(s * scale * self.sm_count / 100), self.sm_count))
+            out.extend([b] * n)
+            floor.extend([f] * n)
+        # rounding can overshoot the capacity: trim only SMs handed out above the floors
+        while sum(out) > cap:
+            i = max(range(len(out)), key=lambda j: out[j] - floor[j])
+            if out[i] <= floor[i]:
+                break
+            out[i] -= 1
         return out
 
 

@@ -35,6 +35,9 @@ class DeviceModel:
                 chain.n_units, N.i32_array(chain.unit_first_op), N.i32_array(chain.boundary),
                 blob.ctypes.data_as(C.c_void_p), blob.nbytes, C.byref(self.handle)), "gx_model_create")
         self.weight_bytes = blob.nbytes
+        dt = C.c_int32()
+        N.check(N.lib().gx_model_dtype(self.handle, C.byref(dt)))
+        self.dtype = dt.value  # GX_BF16 or GX_F32 (fp32 execution mode)
 
     @property
     def n_units(self) -> int:
@@ -54,7 +57,7 @@ class StageInstance:
     """One executor instance of span [start, end) bounded to `sm_budget` SMs."""
 
     def __init__(self, model: DeviceModel, start: int, end: int, max_batch: int, sm_budget: int,
-                 stream: torch.cuda.Stream | None = None):
+                 stream: torch.cuda.Stream | None = None, exec_mode: int = N.GX_EXEC_GRAPH):
         if not 0 <= start < end <= model.n_units:
             raise ValidationError(f"bad span [{start}, {end}) for model {model.chain.model_id!r}")
         self.model = model
@@ -63,13 +66,19 @@ class StageInstance:
         # the stream is torch-owned so tensors freed on it are tracked by torch's allocator
         self.stream = stream or torch.cuda.Stream(device=model.device)
         with torch.cuda.device(model.device):
-            N.check(N.lib().gx_stage_create(model.handle, start, end, max_batch, sm_budget,
+            N.check(N.lib().gx_stage_create(model.handle, start, end, max_batch, sm_budget, model.dtype,
                                             C.c_void_p(self.stream.cuda_stream), C.byref(self.handle)),
                     "gx_stage_create")
+            if exec_mode != N.GX_EXEC_GRAPH:
+                N.check(N.lib().gx_stage_set_exec(self.handle, exec_mode), "gx_stage_set_exec")
         chain = model.chain
         self.in_channels = chain.boundary_shape(start)[2]
         self.out_elems = chain.boundary_elems(end)
         self.final = end == chain.n_units
+        self.dtype = model.dtype
+        # element type of the stage output: fp32 logits, else the chain's compute type
+        self.out_dtype = N.GX_F32 if self.final else model.dtype
+        self.out_elem_bytes = 4 if self.out_dtype == N.GX_F32 else 2
 
     def run_ptrs(self, k: int, src, src_dtypes, dst, dst_dtype: int, src_channels: int = 0):
         N.check(N.lib().gx_stage_run(self.handle, k, N.ptr_array(src), N.i32_array(src_dtypes), src_channels,
@@ -81,7 +90,7 @@ class StageInstance:
         k = len(inputs)
         if not 1 <= k <= self.max_batch:
             raise ValidationError(f"batch {k} outside 1..{self.max_batch}")
-        out_dtype = out_dtype or (torch.float32 if self.final else torch.bfloat16)
+        out_dtype = out_dtype or (torch.float32 if self.out_dtype == N.GX_F32 else torch.bfloat16)
         dev = torch.device("cuda", self.model.device)
         outs = [torch.empty(self.out_elems, dtype=out_dtype, device=dev) for _ in range(k)]
         cur = torch.cuda.current_stream(dev)

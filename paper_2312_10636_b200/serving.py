@@ -84,6 +84,7 @@ class ServeReport:
     config: dict = field(default_factory=dict)
     dispatch: list[tuple] | None = None  # (t_ms, stage index, k, (request seqs...))
     outputs: np.ndarray | None = None  # replay / wall with return_outputs: [request, out elems]
+    sampled: tuple | None = None  # sample_outputs: (request indices, [n, out elems] fp32)
     wall_ms: float = 0.0
     batches: int = 0
     kernels: int = 0
@@ -155,13 +156,24 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
           record_dispatch: bool = False, ingress=None, ingress_from_host: bool = False,
           egress_to_host: bool = False, slot_bytes: int = 0, max_inflight: int = 4096,
           planner: str | None = None, plan_latency=None, return_outputs: bool = False,
-          epochs: list | None = None) -> ServeReport:
+          epochs: list | None = None, result_rows: int = 0, sample_outputs: int = 0,
+          drain_s: float = 0.0) -> ServeReport:
     """Run one plan for one horizon.
 
     latency: callable (StageSpec, k) -> ms for the virtual clock (None -> wall clock).
     instances: per stage index, a list of `StageInstance` (wall clock; with `latency` too: replay).
-    ingress: route point (or client id, which wins) -> (pointer, bytes, channels) of the fp32
-    entry activation template.
+    ingress: (client id, route point), client id, or route point (first match wins) ->
+    (pointer, bytes, channels) of the client's fp32 entry activation (device memory, or pinned host
+    memory with `ingress_from_host`).
+    slot_bytes: per-request device slot size; 0 lets the library size it from the routes (the
+    largest DMA-copied ingress / intermediate boundary); a smaller value than a route needs raises.
+    max_inflight: device slots (requests in flight with a slot); result_rows: final outputs kept
+    (a ring; 0 = max_inflight) — return_outputs needs result_rows >= completed requests.
+    drain_s: wall clock only — after the horizon, keep serving already-generated requests for up
+    to this long (no new arrivals), so requests generated near the horizon complete and count.
+    sample_outputs: keep the logits of up to this many completed requests still held in the ring
+    (the most recent completions, distinct clients first) as report.sampled = (request indices,
+    [n, elems] fp32) — output spot-checks of long serving runs.
     plan_latency: optional (StageSpec, k) -> ms the plan assumed; on the wall clock it is only
     compared with the observed batch times in the GX_SERVE_DEBUG summary.
     epochs: plan transitions under churn, one entry per epoch (Deployment / None = keep /
@@ -265,6 +277,8 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
     cfg.egress_to_host = 1 if egress_to_host else 0
     cfg.slot_bytes = slot_bytes
     cfg.max_inflight = max_inflight
+    cfg.result_rows = result_rows
+    cfg.drain_ms = drain_s * 1000.0 if wall else 0.0
     L = N.lib()
     h = C.c_void_p()
     ctx_handle = ctx.handle if ctx is not None else C.c_void_p(0)
@@ -299,6 +313,28 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
             if elems:
                 N.check(L.gx_serve_outputs(h, outputs.ctypes.data_as(C.POINTER(C.c_float)), outputs.shape[0], elems),
                         "gx_serve_outputs")
+        sampled = None
+        if sample_outputs and gpu:
+            final = [x for x in (instances or []) if x and x[0].final]
+            elems = final[0][0].out_elems if final else 0
+            comp = np.nonzero(status == 0)[0]
+            if elems and comp.size:
+                order = np.ascontiguousarray(comp[np.argsort(done[comp], kind="stable")][::-1][:4 * sample_outputs],
+                                             dtype=np.int64)
+                arr = np.empty((order.size, elems), np.float32)
+                held = C.c_int64()
+                N.check(L.gx_serve_outputs_for(h, order.size, order.ctypes.data_as(C.POINTER(C.c_int64)),
+                                               arr.ctypes.data_as(C.POINTER(C.c_float)), elems, C.byref(held)),
+                        "gx_serve_outputs_for")
+                good = [j for j in range(order.size) if not np.isnan(arr[j]).any()]
+                seen, pick = set(), []
+                for j in good:  # distinct clients first, then repeats
+                    if cl[order[j]] not in seen:
+                        seen.add(cl[order[j]])
+                        pick.append(j)
+                pick += [j for j in good if j not in set(pick)][:max(0, sample_outputs - len(pick))]
+                pick = sorted(pick[:sample_outputs])
+                sampled = (order[pick], arr[pick])
         dispatch = None
         if record_dispatch:
             nbat = C.c_int64()
@@ -321,6 +357,7 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
                    "poisson": poisson, "seed": seed, "clients": len(ids)})
     rep.dispatch = dispatch
     rep.outputs = outputs
+    rep.sampled = sampled
     rep.wall_ms, rep.batches, rep.kernels = float(wall_ms.value), int(nb.value), int(nk.value)
     return rep
 

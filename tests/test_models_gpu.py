@@ -10,6 +10,7 @@ import torch
 pytestmark = pytest.mark.gpu
 
 from oracle.units import nchw_to_nhwc, run_span, units_for
+from paper_2312_10636_b200 import _native as N
 from paper_2312_10636_b200.models import build_chain, torch_model
 
 RES = {"resnet18": 224, "resnet50": 224, "vgg16": 224, "inception_v3": 299}
@@ -119,25 +120,25 @@ def test_inception_end_to_end_within_framework_bf16_error():
 
 
 @pytest.mark.parametrize("budget", [4, 148])
-def test_span_kernel_matches_per_op_path(budget, monkeypatch):
-    """The single-launch persistent span kernel (GX_EXEC=span) and the per-op graph path run the
-    same tiles in the same K order: identical outputs.  (The per-op path's halo kernel for wide
-    3x3 convs sums K in channel-block-major order and its residual convs add the residual inside
-    the MMA; both are held to the torch reference by the kernel and model tests and switched off
-    here, so the two sides sum in the same order.)"""
+def test_span_kernel_matches_per_op_path(budget):
+    """The single-launch persistent span kernel (gx_stage_set_exec(GX_EXEC_SPAN)) and the per-op
+    graph path compute the same span.  The per-op path sums the wide 3x3 convs in halo order and
+    adds the expand convs' residual inside the MMA, so the two agree to bf16 rounding, and both
+    agree with the fp32 oracle."""
     from paper_2312_10636_b200.engine import StageInstance
-    monkeypatch.setenv("GX_NO_HALO", "1")
-    monkeypatch.setenv("GX_NO_RES_MMA", "1")
     m, chain, dm = _setup("resnet50")
     x = torch.randn(3, 3, 224, 224, generator=torch.Generator().manual_seed(5))
     inp = _inputs(x)
-    monkeypatch.setenv("GX_EXEC", "graph")
     ref = StageInstance(dm, 0, chain.n_units, max_batch=4, sm_budget=budget).run(inp, src_channels=3)
-    monkeypatch.setenv("GX_EXEC", "span")
-    got = StageInstance(dm, 0, chain.n_units, max_batch=4, sm_budget=budget).run(inp, src_channels=3)
-    for a, b in zip(got, ref):
+    got = StageInstance(dm, 0, chain.n_units, max_batch=4, sm_budget=budget,
+                        exec_mode=N.GX_EXEC_SPAN).run(inp, src_channels=3)
+    oracle = run_span(units_for("resnet50", m), 0, chain.n_units, x)
+    for i, (a, b) in enumerate(zip(got, ref)):
         rel = ((a - b).norm() / b.norm()).item()
-        assert rel < 1e-3, rel
+        assert rel < 1e-2, rel
+        for t in (a, b):
+            o = oracle[i].reshape(-1)
+            assert ((t.cpu() - o).norm() / o.norm()).item() < 2e-2
 
 
 def test_bert_full_span_matches_fp32_oracle():
