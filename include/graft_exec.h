@@ -64,6 +64,11 @@ extern "C" {
 #define GX_OP_COPY 10    /* channel-slice copy (concat of a pooled branch)                       */
 #define GX_OP_FLATTEN_NCHW 11 /* NHWC -> NCHW flatten (VGG classifier input order)              */
 
+/* gx_op.flags bits */
+#define GX_OPF_COUNT_INCLUDE_PAD 1 /* avg pool: divisor counts padding (PyTorch default)            */
+#define GX_OPF_NO_HALO 2           /* conv: skip the halo-tile kernel, use the im2col TMA path       */
+#define GX_OPF_FC_SIMT 4           /* FC: CUDA-core weight-streaming kernel instead of tcgen05       */
+
 /* activation codes for GX_OP_CONV / GX_OP_LINEAR / GX_OP_FC epilogues */
 #define GX_ACT_NONE 0
 #define GX_ACT_RELU 1
@@ -92,7 +97,7 @@ typedef struct gx_op {
   int32_t R, S, sh, sw, ph, pw; /* conv / pool window                   */
   int32_t Cin, Cout;    /* conv/linear/fc channels; in_coff for COPY via ph */
   int32_t heads;        /* attention heads                                 */
-  int32_t flags;        /* pool: 1 = count_include_pad (avg)                */
+  int32_t flags;        /* GX_OPF_* bits                                    */
   int64_t w_off, b_off, w2_off, w3_off;
   float eps;            /* layernorm epsilon                               */
   int32_t ph_hi, pw_hi; /* conv bottom/right padding; -1 = same as ph / pw  */

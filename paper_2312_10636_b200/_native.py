@@ -18,6 +18,7 @@ GX_BF16, GX_F32 = 0, 1
 (GX_OP_CONV, GX_OP_MAXPOOL, GX_OP_AVGPOOL, GX_OP_GAP, GX_OP_FC, GX_OP_LINEAR, GX_OP_LAYERNORM,
  GX_OP_ATTENTION, GX_OP_EMBED, GX_OP_COPY, GX_OP_FLATTEN_NCHW) = range(1, 12)
 GX_ACT_NONE, GX_ACT_RELU, GX_ACT_GELU = 0, 1, 2
+GX_OPF_COUNT_INCLUDE_PAD, GX_OPF_NO_HALO, GX_OPF_FC_SIMT = 1, 2, 4
 GX_CLOCK_VIRTUAL, GX_CLOCK_WALL, GX_CLOCK_REPLAY = 0, 1, 2
 GX_EXEC_GRAPH, GX_EXEC_SPAN = 0, 1
 

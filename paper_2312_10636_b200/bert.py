@@ -20,7 +20,7 @@ def _linear(b: ChainBuilder, x, weight, bias, act=N.GX_ACT_NONE, residual=-1):
     S, W, K, _ = b.shape(x)
     n_out = weight.shape[0]
     out = b.tensor(S, W, n_out)
-    w_off = b.c.blob.add_bf16(pack_conv_weight(weight.detach().float().view(n_out, K, 1, 1)))
+    w_off = b.add_weight(pack_conv_weight(weight.detach().float().view(n_out, K, 1, 1)))
     b_off = b.c.blob.add_f32(bias.detach().float())
     b.c.ops.append(N.make_op(N.GX_OP_LINEAR, x, out, in2=residual, act=act, Cin=K, Cout=n_out, w_off=w_off,
                              b_off=b_off))
@@ -46,10 +46,10 @@ def _attention(b: ChainBuilder, qkv, heads: int):
     return out
 
 
-def bert_chain(m, seq_len: int = 128) -> UnitChain:
+def bert_chain(m, seq_len: int = 128, dtype: int = N.GX_BF16) -> UnitChain:
     cfg = m.config
     hidden = cfg.hidden_size
-    b = ChainBuilder("bert_base")
+    b = ChainBuilder("bert_base", dtype)
     b.c.input_channels = hidden
     x = b.tensor(seq_len, 1, hidden)
     for layer in m.encoder.layer:

@@ -256,7 +256,8 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
   const bool halo32 = R == 4 && S == 4 && a.ph == 2 && a.pw == 2 && op.ph_hi == 1 && op.pw_hi == 1 && op.Cin == 16 &&
                       ti.W + 3 <= kBM && !dev().no_halo32;
   if (!for_span && op.kind == GX_OP_CONV && (halo128 || halo32) && a.sh == 1 && a.sw == 1 && op.Cin == ti.C &&
-      a.Ho == ti.H && a.Wo == ti.W && op.in2 < 0 && to.dtype == GX_BF16 && !dev().no_halo) {
+      a.Ho == ti.H && a.Wo == ti.W && op.in2 < 0 && to.dtype == GX_BF16 && !dev().no_halo &&
+      !(op.flags & GX_OPF_NO_HALO)) {
     const int Wp = ti.W + (halo32 ? 3 : 2);
     a.halo = 1;
     a.hWp = Wp;
@@ -390,8 +391,9 @@ void op_work(const gx_op& op, const gx_tensor* T, int k, double* flops, double* 
       const int R = op.kind == GX_OP_LINEAR ? 1 : op.R, S = op.kind == GX_OP_LINEAR ? 1 : op.S;
       const double K = static_cast<double>(R) * S * op.Cin;
       f = 2.0 * out_px * op.Cout * K;
-      b = in_px * op.Cin * es_in + static_cast<double>(op.Cout) * K * 2.0 + op.Cout * 4.0 + out_px * op.Cout * es_out;
-      if (op.in2 >= 0) b += out_px * op.Cout * 2.0;
+      b = in_px * op.Cin * es_in + static_cast<double>(op.Cout) * K * es_in + op.Cout * 4.0 +
+          out_px * op.Cout * es_out;
+      if (op.in2 >= 0) b += out_px * op.Cout * es_in;
       break;
     }
     case GX_OP_MAXPOOL:
@@ -406,11 +408,11 @@ void op_work(const gx_op& op, const gx_tensor* T, int k, double* flops, double* 
     case GX_OP_FC: {
       const double K = static_cast<double>(tensor_elems(ti));
       f = 2.0 * k * K * op.Cout;
-      b = K * op.Cout * 2.0 + op.Cout * 4.0 + k * K * es_in + static_cast<double>(k) * op.Cout * es_out;
+      b = K * op.Cout * es_in + op.Cout * 4.0 + k * K * es_in + static_cast<double>(k) * op.Cout * es_out;
       break;
     }
     case GX_OP_COPY:
-      b = 2.0 * in_px * op.Cin * 2.0;
+      b = 2.0 * in_px * op.Cin * es_in;
       break;
     case GX_OP_LAYERNORM:
       f = 8.0 * in_px * ti.C;
@@ -429,9 +431,88 @@ void op_work(const gx_op& op, const gx_tensor* T, int k, double* flops, double* 
   *bytes = b;
 }
 
+// fp32 chains: every op on the fp32 kernels (kernels_f32.cu), same op semantics and weight layout
+// as the bf16 path with fp32 elements (conv / linear weights [Cout][Kpad], FC [Cout][K]).
+int launch_op_f32(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint8_t* wbase, int k, int sm_budget,
+                  cudaStream_t s) {
+  const int grid = std::max(1, sm_budget) * 8;
+  const gx_tensor& ti = T[op.in];
+  const gx_tensor& to = T[op.out];
+  if (to.dtype != GX_F32) return fail(GX_EINVAL, "fp32 op writes a non-fp32 tensor");
+  const float* x = static_cast<const float*>(ptrs[op.in]);
+  float* y = static_cast<float*>(ptrs[op.out]);
+  switch (op.kind) {
+    case GX_OP_CONV:
+    case GX_OP_LINEAR:
+    case GX_OP_FC: {
+      const bool fc = op.kind == GX_OP_FC;
+      const bool conv = op.kind == GX_OP_CONV;
+      ConvF32Args a;
+      memset(&a, 0, sizeof(a));
+      a.x = x;
+      a.H = fc ? 1 : ti.H;
+      a.W = fc ? 1 : ti.W;
+      a.x_ld = fc ? static_cast<int>(tensor_elems(ti)) : ti.C;
+      a.Cin = op.Cin;
+      a.Ho = fc ? 1 : to.H;
+      a.Wo = fc ? 1 : to.W;
+      a.R = conv ? op.R : 1;
+      a.S = conv ? op.S : 1;
+      a.sh = conv ? op.sh : 1;
+      a.sw = conv ? op.sw : 1;
+      a.ph = conv ? op.ph : 0;
+      a.pw = conv ? op.pw : 0;
+      a.K = a.R * a.S * op.Cin;
+      a.M = k * a.Ho * a.Wo;
+      a.Cout = op.Cout;
+      if (fc && op.Cin != tensor_elems(ti)) return fail(GX_EINVAL, "FC Cin must equal the flattened input size");
+      if (op.Cin > (fc ? a.x_ld : ti.C)) return fail(GX_EINVAL, "conv Cin exceeds the input pitch");
+      a.w = reinterpret_cast<const float*>(wbase + op.w_off);
+      a.w_ld = fc ? op.Cin : (a.K + 63) / 64 * 64;
+      a.bias = op.b_off >= 0 ? reinterpret_cast<const float*>(wbase + op.b_off) : nullptr;
+      a.res = op.in2 >= 0 ? static_cast<const float*>(ptrs[op.in2]) : nullptr;
+      a.res_ld = op.in2 >= 0 ? T[op.in2].C : 0;
+      a.y = y;
+      a.y_ld = fc ? op.Cout : to.C;
+      a.y_coff = op.out_coff;
+      a.act = op.act;
+      GX_CUDA(launch_conv_f32(a, std::max(1, sm_budget) * 4, s));
+      break;
+    }
+    case GX_OP_MAXPOOL:
+    case GX_OP_AVGPOOL:
+      GX_CUDA(launch_pool_f32(op.kind == GX_OP_MAXPOOL ? 0 : 1, x, k, ti.H, ti.W, ti.C, y, to.H, to.W, to.C,
+                              op.out_coff, op.R, op.S, op.sh, op.sw, op.ph, op.pw, op.flags & 1, grid, s));
+      break;
+    case GX_OP_GAP:
+      GX_CUDA(launch_gap_f32(x, k, ti.H * ti.W, ti.C, y, grid, s));
+      break;
+    case GX_OP_COPY:
+      GX_CUDA(launch_copy_channels_f32(x, static_cast<int64_t>(k) * ti.H * ti.W, op.Cin, ti.C, op.ph, y, to.C,
+                                       op.out_coff, grid, s));
+      break;
+    case GX_OP_LAYERNORM:
+      GX_CUDA(launch_layernorm_f32(x, k * ti.H * ti.W, ti.C, reinterpret_cast<const float*>(wbase + op.w_off),
+                                   reinterpret_cast<const float*>(wbase + op.b_off), op.eps, y, grid, s));
+      break;
+    case GX_OP_ATTENTION:
+      if (op.heads < 1 || to.C % op.heads || ti.C != 3 * to.C) return fail(GX_EINVAL, "bad attention shapes");
+      GX_CUDA(launch_attention_f32(x, k, ti.H, op.heads, to.C / op.heads, y, grid, s));
+      break;
+    default:
+      return fail(GX_EINVAL, "op kind " + std::to_string(op.kind) + " has no fp32 kernel");
+  }
+  return GX_OK;
+}
+
 int launch_op(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint8_t* wbase, int k, int sm_budget,
               cudaStream_t s, bool pdl, const ConvLaunch* pre, int* kernels) {
   const int bw_grid = std::max(1, sm_budget) * 8;
+  if (T[op.in].dtype == GX_F32) {
+    const int rc = launch_op_f32(op, T, ptrs, wbase, k, sm_budget, s);
+    if (rc == GX_OK && kernels) ++*kernels;
+    return rc;
+  }
   switch (op.kind) {
     case GX_OP_CONV:
     case GX_OP_LINEAR: {

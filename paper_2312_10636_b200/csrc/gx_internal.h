@@ -123,4 +123,34 @@ cudaError_t launch_embed(const void* ids, int N, int S, int C, const __nv_bfloat
                          const __nv_bfloat16* pos, const __nv_bfloat16* type, __nv_bfloat16* y,
                          int grid, cudaStream_t s);
 
+// ------------------------------------------------------------------ fp32 execution mode (kernels_f32.cu)
+struct ConvF32Args {
+  const float* x;  // input NHWC, pixel pitch x_ld
+  int H, W, x_ld, Cin;
+  int Ho, Wo, R, S, sh, sw, ph, pw;
+  int K, M, Cout;  // K = R*S*Cin (ordered r, s, cin), M = k*Ho*Wo
+  const float* w;  // [Cout][w_ld] fp32
+  int w_ld;
+  const float* bias;  // [Cout] or null
+  const float* res;   // residual [M][res_ld] or null
+  int res_ld;
+  float* y;  // [M][y_ld] at column offset y_coff
+  int y_ld, y_coff, act;
+};
+cudaError_t launch_conv_f32(const ConvF32Args& a, int grid, cudaStream_t s);
+cudaError_t launch_pool_f32(int mode, const float* x, int N, int H, int W, int C, float* y, int Ho, int Wo, int y_ld,
+                            int y_coff, int R, int S, int sh, int sw, int ph, int pw, int count_include_pad, int grid,
+                            cudaStream_t s);
+cudaError_t launch_gap_f32(const float* x, int N, int HW, int C, float* y, int grid, cudaStream_t s);
+cudaError_t launch_copy_channels_f32(const float* x, int64_t pixels, int C, int x_ld, int x_coff, float* y, int y_ld,
+                                     int y_coff, int grid, cudaStream_t s);
+cudaError_t launch_layernorm_f32(const float* x, int rows, int C, const float* gamma, const float* beta, float eps,
+                                 float* y, int grid, cudaStream_t s);
+cudaError_t launch_attention_f32(const float* qkv, int N, int S, int heads, int dh, float* out, int grid,
+                                 cudaStream_t s);
+cudaError_t launch_gather_f32(int k, const void* const* src, const int32_t* src_dtype, int64_t pixels, int c_src,
+                              int c_dst, float* dst, int grid, cudaStream_t s);
+cudaError_t launch_gather_s2d_f32(int k, const void* const* src, const int32_t* src_dtype, int Ho, int Wo, int f,
+                                  int c_src, int c_dst, float* dst, int grid, cudaStream_t s);
+
 }  // namespace gx

@@ -52,10 +52,15 @@ inline bool res_through_mma(const gx_op& op) {
 // sum K in different orders.  (The CUDA-core kernel is faster only for batch-1 heads spread over
 // a whole GPU, which serving never runs.)
 inline bool fc_on_tc(const gx_op& op) {
-  return op.kind == GX_OP_FC && op.Cin % 64 == 0 && op.Cout % 8 == 0 && op.b_off >= 0 && !gx::dev().fc_simt;
+  return op.kind == GX_OP_FC && op.Cin % 64 == 0 && op.Cout % 8 == 0 && op.b_off >= 0 && !gx::dev().fc_simt &&
+         !(op.flags & GX_OPF_FC_SIMT);
 }
 // ops executed by conv_tc_kernel / conv_halo_kernel (planned with plan_conv)
 inline bool is_gemm_op(const gx_op& op) { return op.kind == GX_OP_CONV || op.kind == GX_OP_LINEAR || fc_on_tc(op); }
+// ... in a bf16 chain (fp32 chains run every op on the fp32 kernels, kernels_f32.cu)
+inline bool is_tc_op(const gx_op& op, const gx_tensor* T) { return is_gemm_op(op) && T[op.in].dtype == GX_BF16; }
+int launch_op_f32(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint8_t* wbase, int k, int sm_budget,
+                  cudaStream_t s);
 void op_work(const gx_op& op, const gx_tensor* T, int k, double* flops, double* bytes);
 }  // namespace gx
 

@@ -91,7 +91,7 @@ int capture_span(gx_stage* st, int k, gx_stage::PerK* out) {
   std::vector<ConvLaunch> plans(st->ops.size());
   for (size_t i = 0; i < st->ops.size(); ++i) {
     const gx_op& op = m->ops[st->ops[i]];
-    if (is_gemm_op(op)) {
+    if (is_tc_op(op, m->tensors.data())) {
       int rc = plan_conv(op, m->tensors.data(), st->tptr.data(), wbase, k, st->sm_budget, &plans[i], 256,
                          m->op_wsw(st->ops[i]));
       if (rc != GX_OK) return rc;
@@ -104,7 +104,7 @@ int capture_span(gx_stage* st, int k, gx_stage::PerK* out) {
   const bool use_pdl = !dev().no_pdl;
   for (size_t i = 0; i < st->ops.size() && rc == GX_OK; ++i) {
     const gx_op& op = m->ops[st->ops[i]];
-    const bool is_conv = is_gemm_op(op);
+    const bool is_conv = is_tc_op(op, m->tensors.data());
     rc = launch_op(op, m->tensors.data(), st->tptr.data(), wbase, k, st->sm_budget, st->stream, use_pdl,
                    is_conv ? &plans[i] : nullptr, &kernels);
   }
@@ -271,7 +271,7 @@ cudaError_t build_bulk_weights(gx_model* m, const uint8_t* blob) {
   size_t total = 0;
   for (int i = 0; i < n; ++i) {
     const gx_op& op = m->ops[i];
-    if (!is_gemm_op(op)) continue;
+    if (!is_tc_op(op, m->tensors.data())) continue;
     const int R = op.kind != GX_OP_CONV ? 1 : op.R, S = op.kind != GX_OP_CONV ? 1 : op.S;
     const size_t kpad = (static_cast<size_t>(R) * S * op.Cin + 63) / 64 * 64;
     m->wsw_off[i] = static_cast<int64_t>(total);
@@ -526,8 +526,17 @@ int stage_run_on(gx_stage* st, cudaStream_t stream, int k, const void* const* sr
   int rc = stage_graph(st, k, &pk);
   if (rc != GX_OK) return rc;
   const int bw_grid = st->sm_budget * 8;
-  if (tin.s2d > 1) {
-    if (src_channels <= 0) return fail(GX_EINVAL, "space-to-depth boundary needs the client's channel count");
+  if (tin.s2d > 1 && src_channels <= 0)
+    return fail(GX_EINVAL, "space-to-depth boundary needs the client's channel count");
+  if (tin.dtype == GX_F32) {  // fp32 chain: the batch is assembled in fp32
+    float* bt = static_cast<float*>(st->tptr[st->in_tid]);
+    if (tin.s2d > 1)
+      GX_CUDA(launch_gather_s2d_f32(k, src, src_dtype, tin.H, tin.W, tin.s2d, src_channels, tin.C, bt, bw_grid,
+                                    stream));
+    else
+      GX_CUDA(launch_gather_f32(k, src, src_dtype, static_cast<int64_t>(tin.H) * tin.W, c_src, tin.C, bt, bw_grid,
+                                stream));
+  } else if (tin.s2d > 1) {
     GX_CUDA(launch_gather_s2d(k, src, src_dtype, tin.H, tin.W, tin.s2d, src_channels, tin.C,
                               static_cast<__nv_bfloat16*>(st->tptr[st->in_tid]), bw_grid, stream));
   } else {
@@ -669,7 +678,7 @@ int gx_stage_profile_ops(gx_stage* st, int k, int iters, int cap, float* ms, dou
   for (size_t i = 0; i < st->ops.size(); ++i) {
     const gx_op& op = m->ops[st->ops[i]];
     ConvLaunch cl;
-    const bool is_conv = is_gemm_op(op);
+    const bool is_conv = is_tc_op(op, T);
     if (is_conv) {
       if (int rc = plan_conv(op, T, st->tptr.data(), wbase, k, st->sm_budget, &cl, 256, m->op_wsw(st->ops[i])))
         return rc;

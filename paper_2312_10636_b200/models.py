@@ -37,6 +37,7 @@ class UnitChain:
     input_channels: int = 3  # channels a client actually ships at boundary 0 (pre-padding)
     unit_flops: list = field(default_factory=list)  # per-sample FLOPs of each unit
     tensor_s2d: dict = field(default_factory=dict)  # tensor id -> space-to-depth factor (stride-2 stems)
+    dtype: int = BF16  # compute element type (F32: the fp32 execution mode)
 
     @property
     def n_units(self) -> int:
@@ -76,14 +77,23 @@ class UnitChain:
 
 
 class ChainBuilder:
-    def __init__(self, model_id: str):
+    """dtype: BF16 (tensor-core path; only the chain output is fp32) or F32 (the fp32 execution
+    mode: every tensor and weight fp32, graft_exec.h gx_model_dtype)."""
+
+    def __init__(self, model_id: str, dtype: int = BF16):
         self.c = UnitChain(model_id)
+        self.c.dtype = dtype
+        self.dtype = dtype
         self._flops = 0.0
 
     # -- tensors / units --------------------------------------------------
-    def tensor(self, H, W, Cc, dtype=BF16) -> int:
-        self.c.tensors.append((H, W, Cc, dtype))
+    def tensor(self, H, W, Cc, dtype=None) -> int:
+        self.c.tensors.append((H, W, Cc, self.dtype if dtype is None else dtype))
         return len(self.c.tensors) - 1
+
+    def add_weight(self, t) -> int:
+        """Weights in the chain's element type (biases and LayerNorm parameters are always fp32)."""
+        return self.c.blob.add_f32(t) if self.dtype == F32 else self.c.blob.add_bf16(t)
 
     def shape(self, t):
         return self.c.tensors[t]
@@ -140,7 +150,7 @@ class ChainBuilder:
             out = self.tensor(Ho, Wo, cout)
         else:
             assert self.shape(out)[:2] == (Ho, Wo), (self.shape(out), Ho, Wo)
-        w_off = self.c.blob.add_bf16(pack_conv_weight(w, cin_pad))
+        w_off = self.add_weight(pack_conv_weight(w, cin_pad))
         b_off = self.c.blob.add_f32(b)
         self.c.ops.append(N.make_op(N.GX_OP_CONV, x, out, in2=residual, out_coff=out_coff,
                                     act=N.GX_ACT_RELU if relu else N.GX_ACT_NONE, R=R, S=S, sh=sh, sw=sw, ph=ph,
@@ -187,13 +197,13 @@ class ChainBuilder:
         self.c.ops.append(N.make_op(N.GX_OP_GAP, x, out))
         return out
 
-    def fc(self, x, lin: nn.Linear, relu=False, out_dtype=BF16, weight=None):
+    def fc(self, x, lin: nn.Linear, relu=False, out_dtype=None, weight=None):
         H, W, Cx, _ = self.shape(x)
         K = H * W * Cx
         w = (weight if weight is not None else lin.weight).detach().float()
         assert w.shape[1] == K, (w.shape, K)
         out = self.tensor(1, 1, w.shape[0], out_dtype)
-        w_off = self.c.blob.add_bf16(w)
+        w_off = self.add_weight(w)
         b_off = self.c.blob.add_f32(lin.bias.detach().float())
         self.c.ops.append(N.make_op(N.GX_OP_FC, x, out, act=N.GX_ACT_RELU if relu else N.GX_ACT_NONE, Cin=K,
                                     Cout=w.shape[0], w_off=w_off, b_off=b_off))
@@ -270,8 +280,8 @@ def torch_model(name: str, seed: int = 0) -> nn.Module:
 # chain builders
 # ---------------------------------------------------------------------------------------------
 
-def _resnet_chain(name: str, m) -> UnitChain:
-    b = ChainBuilder(name)
+def _resnet_chain(name: str, m, dtype=BF16) -> UnitChain:
+    b = ChainBuilder(name, dtype)
     # boundary 0: the 3-channel 224x224 image, rearranged by the gather into 2x2 space-to-depth
     # blocks (112x112x16) so the 7x7/2 stem runs as a 4x4/1 conv with 32-byte im2col pixels
     y = b.s2d_stem(m.conv1, m.bn1, 224)
@@ -295,8 +305,8 @@ def _resnet_chain(name: str, m) -> UnitChain:
     return b.finish(out)
 
 
-def _vgg16_chain(m) -> UnitChain:
-    b = ChainBuilder("vgg16")
+def _vgg16_chain(m, dtype=BF16) -> UnitChain:
+    b = ChainBuilder("vgg16", dtype)
     x = b.tensor(224, 224, 8)
     y = x
     first = True
@@ -333,8 +343,8 @@ def _basic(b, x, bc, out=-1, out_coff=0):
     return b.conv(x, bc.conv, bc.bn, relu=True, out=out, out_coff=out_coff)
 
 
-def _inception_chain(m) -> UnitChain:
-    b = ChainBuilder("inception_v3")
+def _inception_chain(m, dtype=BF16) -> UnitChain:
+    b = ChainBuilder("inception_v3", dtype)
     x = b.tensor(299, 299, 8)
     b.begin_unit(x)
     y = b.conv(x, m.Conv2d_1a_3x3.conv, m.Conv2d_1a_3x3.bn, relu=True, cin_pad=8)
@@ -429,18 +439,20 @@ def _inception_chain(m) -> UnitChain:
     return b.finish(out)
 
 
-def build_chain(name: str, seed: int = 0, module: nn.Module | None = None) -> UnitChain:
+def build_chain(name: str, seed: int = 0, module: nn.Module | None = None, dtype: int = BF16) -> UnitChain:
+    """The unit chain of `name` with its parameters; dtype F32 builds the fp32 execution mode (same
+    units, boundaries and weights, every tensor fp32)."""
     m = module if module is not None else torch_model(name, seed)
     if name in ("resnet50", "resnet18"):
-        return _resnet_chain(name, m)
+        return _resnet_chain(name, m, dtype)
     if name == "vgg16":
-        return _vgg16_chain(m)
+        return _vgg16_chain(m, dtype)
     if name == "inception_v3":
-        return _inception_chain(m)
+        return _inception_chain(m, dtype)
     if name == "bert_base":
         from .bert import bert_chain
 
-        return bert_chain(m)
+        return bert_chain(m, dtype=dtype)
     raise KeyError(f"unknown model {name!r}")
 
 

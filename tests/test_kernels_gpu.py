@@ -95,12 +95,10 @@ def test_conv_matches_torch(k, H, W, Cin, Cout, R, S, stride, pad, residual, rel
 
 @pytest.mark.parametrize("k,H,Cout,path", [(2, 112, 64, "halo32"), (3, 56, 64, "halo32"), (1, 28, 32, "halo32"),
                                             (2, 112, 64, "im2col")])
-def test_conv_s2d_stem(k, H, Cout, path, monkeypatch):
+def test_conv_s2d_stem(k, H, Cout, path):
     """The space-to-depth stem: 4x4 / stride 1 / pad (2, 2, 1, 1) over 16 channels, on the 32-byte
     halo path (conv_halo_kernel<32>: one halo tile, sixteen K=16 MMAs at row offsets) and on the
-    im2col path (GX_NO_HALO32), vs torch on the same bf16 data."""
-    if path == "im2col":
-        monkeypatch.setenv("GX_NO_HALO32", "1")
+    im2col path (op flag GX_OPF_NO_HALO), vs torch on the same bf16 data."""
     g = torch.Generator().manual_seed(5)
     x = torch.randn(k, H, H, 16, generator=g).to(torch.bfloat16)
     w = torch.randn(Cout, 16, 4, 4, generator=g) / 16.0
@@ -113,7 +111,7 @@ def test_conv_s2d_stem(k, H, Cout, path, monkeypatch):
     wdev = torch.from_numpy(blob.bytes()).cuda()
     y = torch.full((k, H, H, Cout), float("nan"), dtype=torch.bfloat16, device="cuda")
     op = N.make_op(N.GX_OP_CONV, 0, 1, act=N.GX_ACT_RELU, R=4, S=4, sh=1, sw=1, ph=2, pw=2, ph_hi=1, pw_hi=1,
-                   Cin=16, Cout=Cout, w_off=w_off, b_off=b_off)
+                   Cin=16, Cout=Cout, w_off=w_off, b_off=b_off, flags=N.GX_OPF_NO_HALO if path == "im2col" else 0)
     run_op(op, [x.cuda(), y], [tensor_desc(H, H, 16), tensor_desc(H, H, Cout)], wdev, k, 3)
     torch.cuda.synchronize()
     got = y.float().cpu()
@@ -187,11 +185,10 @@ def test_gap_and_fc():
     (3, 7, 7, 512, 4096, False, True),      # VGG-16 fc6: flattened 7x7x512 input, bf16 out + ReLU
     (130, 1, 1, 512, 1000, True, False),    # two 128-row M tiles
 ])
-def test_fc_paths(path, k, H, W, Cc, O, out_f32, relu, monkeypatch):
+def test_fc_paths(path, k, H, W, Cc, O, out_f32, relu):
     """FC on the tcgen05 GEMM path (conv_tc_kernel with the flattened [k, K] input as A) and on the
-    CUDA-core weight-streaming kernel (GX_FC_SIMT): same results vs an fp32 matmul of the bf16 data."""
-    if path == "simt":
-        monkeypatch.setenv("GX_FC_SIMT", "1")
+    CUDA-core weight-streaming kernel (op flag GX_OPF_FC_SIMT): same results vs an fp32 matmul of
+    the bf16 data."""
     g = torch.Generator().manual_seed(7)
     K = H * W * Cc
     x = torch.randn(k, H, W, Cc, generator=g).to(torch.bfloat16)
@@ -203,7 +200,7 @@ def test_fc_paths(path, k, H, W, Cc, O, out_f32, relu, monkeypatch):
     wdev = torch.from_numpy(blob.bytes()).cuda()
     y = torch.full((k, O), float("nan"), dtype=torch.float32 if out_f32 else torch.bfloat16, device="cuda")
     op = N.make_op(N.GX_OP_FC, 0, 1, Cin=K, Cout=O, w_off=w_off, b_off=b_off,
-                   act=N.GX_ACT_RELU if relu else N.GX_ACT_NONE)
+                   act=N.GX_ACT_RELU if relu else N.GX_ACT_NONE, flags=N.GX_OPF_FC_SIMT if path == "simt" else 0)
     run_op(op, [x.cuda(), y], [tensor_desc(H, W, Cc), tensor_desc(1, 1, O, N.GX_F32 if out_f32 else N.GX_BF16)],
            wdev, k, sm_budget=4)
     torch.cuda.synchronize()

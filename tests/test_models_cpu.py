@@ -54,3 +54,23 @@ def test_bn_folding_matches_module():
     assert torch.allclose(got, ref, atol=1e-4, rtol=1e-4)
     packed = pack_conv_weight(w.detach())
     assert packed.shape == (64, 576)
+
+
+@pytest.mark.parametrize("name", list(CASES) + ["bert_base"])
+def test_fp32_chain_mirrors_bf16_chain(name):
+    """The fp32 execution mode is the same chain (units, boundaries, ops, payloads) with every
+    tensor fp32 and weights stored fp32 (twice the bf16 bytes for conv / linear / FC weights)."""
+    from paper_2312_10636_b200 import _native as N
+    m = torch_model(name)
+    a = build_chain(name, module=m)
+    b = build_chain(name, module=m, dtype=N.GX_F32)
+    assert b.dtype == N.GX_F32 and a.dtype == N.GX_BF16
+    assert a.boundary == b.boundary and a.unit_first_op == b.unit_first_op
+    assert [t[:3] for t in a.tensors] == [t[:3] for t in b.tensors]
+    assert all(t[3] == N.GX_F32 for t in b.tensors)
+    # bf16 chains: only the chain output may be fp32
+    assert all(t[3] == N.GX_BF16 or i == a.boundary[-1] for i, t in enumerate(a.tensors))
+    assert [a.payload_bytes(p) for p in range(a.n_units + 1)] == [b.payload_bytes(p) for p in range(b.n_units + 1)]
+    assert [(o.kind, o.in_, o.out, o.Cin, o.Cout) for o in a.ops] == [(o.kind, o.in_, o.out, o.Cin, o.Cout)
+                                                                        for o in b.ops]
+    assert b.blob.size > 1.8 * a.blob.size
