@@ -205,6 +205,13 @@ GX_API int gx_gather(gx_ctx* ctx, int k, const void* const* src, const int32_t* 
               int64_t pixels, int32_t c_src, int32_t c_dst, void* dst, int sm_budget, void* stream);
 GX_API int gx_scatter(gx_ctx* ctx, int k, const void* src, int32_t src_dtype, int64_t row_elems,
                void* const* dst, int32_t dst_dtype, int sm_budget, void* stream);
+/* K1 gather in its general form: into a batch of element type dst_dtype (GX_BF16, or GX_F32 for
+ * fp32 chains), with the space-to-depth rearrangement when f > 1 (client image [Ho*f, Wo*f, c_src]
+ * -> [Ho, Wo, c_dst], channel (dy*f + dx)*c_src + c; zero above f*f*c_src); f = 1 is the plain
+ * channel-padded gather of Ho*Wo pixels. */
+GX_API int gx_gather_ex(gx_ctx* ctx, int k, const void* const* src, const int32_t* src_dtype, int32_t Ho,
+                        int32_t Wo, int32_t f, int32_t c_src, int32_t c_dst, void* dst, int32_t dst_dtype,
+                        int sm_budget, void* stream);
 
 /* ----------------------------------------------------------------------------------------
  * Native serving runtime: the event loop of _Sim.run (simulator.py:430-463) with the batching
@@ -221,9 +228,13 @@ typedef struct gx_serve_stage {
   int32_t batch, instances;
   double budget_ms;
   const double* lat_ms; /* [batch+1] virtual latency per k (index 0 unused)                  */
-  gx_stage* const* inst; /* [instances] executor instances (WALL clock only)                */
+  gx_stage* const* inst; /* [instances] executor instances (WALL / REPLAY clocks); each lives on
+                            its own device: a plan placed across GPUs (placement.py:24-70) runs
+                            instance i of the stage on placement[stage][i]                        */
   int32_t in_boundary_elems_is_input; /* reserved */
   int32_t out_final;    /* 1: the stage output is the chain output (logits)                 */
+  const int32_t* inst_gpu; /* [instances] GPU of each instance for the VIRTUAL clock's routing
+                              (NULL: all on one GPU); the GPU clocks use each instance's device */
 } gx_serve_stage;
 
 typedef struct gx_serve_route { /* _Route (simulator.py:103-107) + the arrival terms of _gen_request */
@@ -293,6 +304,11 @@ GX_API int gx_serve_requests(gx_serve* s, int32_t* client, double* gen_ms, doubl
 /* Dispatch log: per dispatched batch (t_ms, stage index, k) and the k request seqs. */
 GX_API int gx_serve_count_dispatch(gx_serve* s, int64_t* n_batches, int64_t* n_items);
 GX_API int gx_serve_dispatch(gx_serve* s, double* t_ms, int32_t* stage, int32_t* k, int64_t* seqs);
+/* Where each dispatched batch ran (same order as gx_serve_dispatch): instance index within its
+ * stage and that instance's GPU.  Among free instances a batch goes to one on the GPU holding most
+ * of its requests' current activations (ties: lowest index) — the same-GPU preference for the
+ * align -> shared hand-off that co-located placement sets up (placement.py:58-59). */
+GX_API int gx_serve_dispatch_placement(gx_serve* s, int32_t* inst, int32_t* gpu);
 GX_API int gx_serve_stats(gx_serve* s, double* wall_ms, int64_t* batches, int64_t* kernels);
 /* Per-request outputs (WALL / REPLAY): row i = request i's final-stage output (logits, fp32,
  * `elems` values; NaN for requests that did not complete).  Rows are valid while no more than

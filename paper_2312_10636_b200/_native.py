@@ -54,7 +54,8 @@ def make_op(kind, in_, out, in2=-1, out_coff=0, act=GX_ACT_NONE, R=1, S=1, sh=1,
 class GxServeStage(C.Structure):
     _fields_ = [("batch", C.c_int32), ("instances", C.c_int32), ("budget_ms", C.c_double),
                 ("lat_ms", C.POINTER(C.c_double)), ("inst", C.POINTER(C.c_void_p)),
-                ("in_boundary_elems_is_input", C.c_int32), ("out_final", C.c_int32)]
+                ("in_boundary_elems_is_input", C.c_int32), ("out_final", C.c_int32),
+                ("inst_gpu", C.POINTER(C.c_int32))]
 
 
 class GxServeRoute(C.Structure):
@@ -117,6 +118,7 @@ def lib():
         "gx_run_op": (i32, [vp, P(GxOp), P(GxTensor), P(vp), vp, C.c_int, C.c_int, vp]),
         "gx_gather": (i32, [vp, C.c_int, P(vp), P(i32), i64, i32, i32, vp, C.c_int, vp]),
         "gx_scatter": (i32, [vp, C.c_int, vp, i32, i64, P(vp), i32, C.c_int, vp]),
+        "gx_gather_ex": (i32, [vp, C.c_int, P(vp), P(i32), i32, i32, i32, i32, i32, vp, i32, C.c_int, vp]),
         "gx_serve_create": (i32, [vp, C.c_int, P(GxServeStage), C.c_int, P(GxServeRoute), C.c_int,
                                   P(GxServeClient), P(GxServeCfg), P(vp)]),
         "gx_serve_run": (i32, [vp]),
@@ -125,6 +127,7 @@ def lib():
         "gx_serve_count_dispatch": (i32, [vp, P(i64), P(i64)]),
         "gx_serve_dispatch": (i32, [vp, P(dbl), P(i32), P(i32), P(i64)]),
         "gx_serve_stats": (i32, [vp, P(dbl), P(i64), P(i64)]),
+        "gx_serve_dispatch_placement": (i32, [vp, P(i32), P(i32)]),
         "gx_serve_destroy": (i32, [vp]),
         "gx_serve_outputs": (i32, [vp, P(C.c_float), i64, i64]),
         "gx_serve_outputs_for": (i32, [vp, i64, P(i64), P(C.c_float), i64, P(i64)]),

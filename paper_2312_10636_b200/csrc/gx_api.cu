@@ -674,6 +674,31 @@ int gx_gather(gx_ctx* ctx, int k, const void* const* src, const int32_t* src_dty
   return GX_OK;
 }
 
+int gx_gather_ex(gx_ctx* ctx, int k, const void* const* src, const int32_t* src_dtype, int32_t Ho, int32_t Wo,
+                 int32_t f, int32_t c_src, int32_t c_dst, void* dst, int32_t dst_dtype, int sm_budget, void* stream) {
+  if (!ctx || !src || !src_dtype || !dst) return fail(GX_EINVAL, "null arg");
+  if (k < 1 || k > 64) return fail(GX_EINVAL, "gather batch must be in 1..64");
+  if (f < 1 || Ho < 1 || Wo < 1 || c_src < 1 || c_dst < 1 || f * f * c_src > c_dst)
+    return fail(GX_EINVAL, "bad gather shape");
+  if (int rc = bind_device(ctx->device)) return rc;
+  if (sm_budget <= 0 || sm_budget > ctx->sm_count) sm_budget = ctx->sm_count;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int grid = sm_budget * 8;
+  if (dst_dtype == GX_F32) {
+    if (f > 1)
+      GX_CUDA(launch_gather_s2d_f32(k, src, src_dtype, Ho, Wo, f, c_src, c_dst, static_cast<float*>(dst), grid, s));
+    else
+      GX_CUDA(launch_gather_f32(k, src, src_dtype, static_cast<int64_t>(Ho) * Wo, c_src, c_dst,
+                                static_cast<float*>(dst), grid, s));
+  } else if (f > 1) {
+    GX_CUDA(launch_gather_s2d(k, src, src_dtype, Ho, Wo, f, c_src, c_dst, static_cast<__nv_bfloat16*>(dst), grid, s));
+  } else {
+    GX_CUDA(launch_gather(k, src, src_dtype, static_cast<int64_t>(Ho) * Wo, c_src, c_dst,
+                          static_cast<__nv_bfloat16*>(dst), grid, s));
+  }
+  return GX_OK;
+}
+
 int gx_scatter(gx_ctx* ctx, int k, const void* src, int32_t src_dtype, int64_t row_elems, void* const* dst,
                int32_t dst_dtype, int sm_budget, void* stream) {
   if (!ctx) return fail(GX_EINVAL, "null ctx");

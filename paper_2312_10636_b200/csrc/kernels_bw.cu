@@ -65,6 +65,48 @@ __global__ void gather_s2d_kernel(RowPtrs src, int k, int Ho, int Wo, int f, int
   }
 }
 
+// The stem's case (2x2 blocks of a 3-channel image into 16 channels, 12 used): a thread owns one
+// output pixel, reads its two 6-value input row segments as 8-byte vectors (the pixel pair starts
+// at an even column: 24-byte aligned) and writes the 32-byte output pixel as two 16-byte stores.
+// (The per-element kernel above did a 64-bit div/mod chain and a 2-byte store per element.)
+__global__ void gather_s2d_rgb2_kernel(RowPtrs src, int k, int Ho, int Wo, __nv_bfloat16* __restrict__ dst) {
+  const int per_row = Ho * Wo;
+  const int total = per_row * k;  // < 2^31: k <= 64 rows of <= 112x112 pixels
+  const int Wi = Wo * 2;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int r = i / per_row;
+    const int px = i - r * per_row;
+    const int ho = px / Wo, wo = px - (px / Wo) * Wo;
+    float v[12];  // channel (dy*2 + dx)*3 + c
+#pragma unroll
+    for (int dy = 0; dy < 2; ++dy) {
+      const int64_t e0 = (static_cast<int64_t>(2 * ho + dy) * Wi + 2 * wo) * 3;  // 6 values: (dx, c)
+      if (src.dt[r] == GX_F32) {
+        const float2* p = reinterpret_cast<const float2*>(static_cast<const float*>(src.p[r]) + e0);
+        const float2 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
+        v[dy * 6 + 0] = a.x, v[dy * 6 + 1] = a.y, v[dy * 6 + 2] = b.x;
+        v[dy * 6 + 3] = b.y, v[dy * 6 + 4] = c.x, v[dy * 6 + 5] = c.y;
+      } else {
+        const __nv_bfloat16* p = static_cast<const __nv_bfloat16*>(src.p[r]) + e0;
+#pragma unroll
+        for (int j = 0; j < 6; ++j) v[dy * 6 + j] = __bfloat162float(p[j]);
+      }
+    }
+    uint4 o0, o1;
+    o0.x = pack_bf16x2(v[0], v[1]);
+    o0.y = pack_bf16x2(v[2], v[3]);
+    o0.z = pack_bf16x2(v[4], v[5]);
+    o0.w = pack_bf16x2(v[6], v[7]);
+    o1.x = pack_bf16x2(v[8], v[9]);
+    o1.y = pack_bf16x2(v[10], v[11]);
+    o1.z = 0u;
+    o1.w = 0u;
+    uint4* d = reinterpret_cast<uint4*>(dst + static_cast<int64_t>(i) * 16);
+    d[0] = o0;
+    d[1] = o1;
+  }
+}
+
 __global__ void gather_kernel(RowPtrs src, int k, int64_t pixels, int c_src, int c_dst,
                               __nv_bfloat16* __restrict__ dst) {
   if (c_src == c_dst && (c_dst & 7) == 0) {
@@ -580,6 +622,11 @@ cudaError_t launch_gather_s2d(int k, const void* const* src, const int32_t* src_
   for (int i = 0; i < k; ++i) {
     rp.p[i] = src[i];
     rp.dt[i] = src_dtype[i];
+  }
+  if (f == 2 && c_src == 3 && c_dst == 16 && (Wo & 1) == 0) {  // the ResNet stems: one thread per output pixel
+    const int64_t work = static_cast<int64_t>(Ho) * Wo * k;
+    gather_s2d_rgb2_kernel<<<grid_for(work, 256, grid), 256, 0, s>>>(rp, k, Ho, Wo, dst);
+    return cudaGetLastError();
   }
   const int64_t work = static_cast<int64_t>(Ho) * Wo * c_dst * k;
   gather_s2d_kernel<<<grid_for(work, 256, grid), 256, 0, s>>>(rp, k, Ho, Wo, f, c_src, c_dst, dst);

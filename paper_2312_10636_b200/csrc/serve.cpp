@@ -1,15 +1,24 @@
 // Native serving runtime: the discrete-event loop of fragserve's _Sim (simulator.py:430-463) with
 // its batching (_service / _enqueue / _stage_done, simulator.py:387-426) and admission control
-// (_arrive, simulator.py:377-385), for one deployed plan over one horizon.
+// (_arrive, simulator.py:377-385), for one deployed plan (or a sequence of per-epoch plans) over
+// one horizon.
 //
 // GX_CLOCK_VIRTUAL replays the reference exactly: the same event heap keyed (t, rank, seq), the same
 // push order (so request seqs match _Request.seq), the same float arithmetic; a batch completes at
 // dispatch time + the stage's latency table entry for k.  GX_CLOCK_WALL runs the same state machine
 // against the wall clock: every dispatched batch executes on the GPU (gx_stage_run on a free
-// instance's stream) and completes when its CUDA event fires.  GX_CLOCK_REPLAY keeps the virtual
-// clock (so dispatch order and batch composition are the reference's, bit for bit) and also
-// executes every dispatched batch on the GPU, synchronously, with the real per-request
-// activations flowing align -> shared through the ragged gather: the numerics-parity mode.
+// instance, on a pooled stream of that instance's device) and completes when its CUDA event fires.
+// GX_CLOCK_REPLAY keeps the virtual clock (so dispatch order and batch composition are the
+// reference's, bit for bit) and also executes every dispatched batch on the GPU, synchronously,
+// with the real per-request activations flowing align -> shared through the ragged gather: the
+// numerics-parity mode.
+//
+// Placement (multi-GPU, placement.py:24-70): a stage's instances may live on different GPUs of
+// the box.  Each stage keeps ONE global FIFO (simulator.py:91); a dispatched batch goes to a free
+// instance, preferring the GPU that holds most of the batch's current activations.  A request's
+// activation lives in a device slot on the GPU of the instance that produced it; a batch on another
+// GPU gathers it over NVLink through peer access (no copy, no collective).  Per GPU: a stream pool,
+// a slot pool, copy streams for DMA ingress and a recycled event pool.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -19,6 +28,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <map>
 #include <queue>
 #include <string>
 #include <vector>
@@ -54,22 +64,25 @@ struct Req {
   double stage_enq = 0.0;
   int status = 2;  // 0 completed, 1 dropped, 2 inflight
   double done = NAN;
-  // WALL: where the request's current activation lives
+  int loc = -1;  // device-table index of the GPU holding the current activation (routing)
+  // GPU clocks: where the request's current activation lives
   const void* cur = nullptr;
   int cur_dtype = GX_F32;
   int cur_channels = 0;
-  int slot = -1;
+  int slot = -1, slot_dev = -1;  // device slot holding the activation (DMA ingress / stage outputs)
+  int old_slot = -1, old_dev = -1;  // slot the running batch reads; freed when the batch completes
   int64_t result_seq = -1;  // completion slot number; its output lives in ring row result_seq % result_rows
-  int h2d_ev = -1;          // GX_INGRESS_DMA: event of the arrival-time H2D copy into the slot
+  int h2d_ev = -1, h2d_dev = -1;  // GX_INGRESS_DMA: event of the arrival-time H2D copy into the slot
 };
 
 struct Batch {
   int stage;
-  int inst;
+  int inst = -1;
+  int dev = -1;  // device-table index the batch runs on
   std::vector<int> reqs;
-  cudaEvent_t ev = nullptr;
-  double t_disp = 0.0;  // wall ms at dispatch (diagnostics)
-  int lane = -1;        // stream-pool lane the batch runs on
+  int ev = -1;           // completion event (pool of `dev`)
+  double t_disp = 0.0;   // wall ms at dispatch (diagnostics)
+  int lane = -1;         // stream-pool lane the batch runs on
 };
 
 struct Stage {
@@ -79,6 +92,7 @@ struct Stage {
   std::deque<int> queue;
   int64_t armed_seq = -1;
   std::vector<gx_stage*> inst;
+  std::vector<int> inst_dev;  // device-table index per instance
   std::vector<char> busy;
   int out_final = 0;
   // wall-clock diagnostics (GX_SERVE_DEBUG): observed dispatch->completion time per batch
@@ -105,6 +119,25 @@ struct Route {
   int64_t ingress_bytes;
   int ingress_dtype;
   int ingress_channels;
+  int home = 0;  // device-table index of the first stage's instance 0 (DMA ingress slots live there)
+};
+
+// Per-GPU serving resources.  Stream pool: a batch runs on an idle pooled stream rather than on
+// its instance's own stream.  A device has at most CUDA_DEVICE_MAX_CONNECTIONS (32) hardware
+// queues; with one stream per instance, plans with > 32 instances alias streams onto shared queues
+// and unrelated instances serialise.  Pooling keeps every in-flight batch on its own queue while
+// <= pool size.
+struct DevRes {
+  int device = 0;
+  std::vector<cudaStream_t> pool;
+  std::vector<int> pool_n;        // batches in flight per lane
+  std::vector<double> pool_last;  // wall ms of the lane's last dispatch
+  std::vector<cudaStream_t> copy_streams;
+  int64_t n_copies = 0;
+  void* slots = nullptr;
+  std::vector<int> free_slots;
+  std::vector<cudaEvent_t> events;  // recycled: batch completions and H2D copies on this device
+  std::vector<int> free_events;
 };
 
 }  // namespace
@@ -121,33 +154,23 @@ struct gx_serve {
   int cur_epoch = 0;  // advanced by REPLAN events (simulator.py:457-458 -> _plan_epoch)
   // dispatch log
   std::vector<double> d_t;
-  std::vector<int32_t> d_stage, d_k;
+  std::vector<int32_t> d_stage, d_k, d_inst, d_gpu;
   std::vector<int64_t> d_seqs;
-  // WALL resources
+  // devices: table index -> GPU ordinal (index 0 = the context's device)
+  std::vector<int> gpus;
+  std::vector<DevRes> devs;
+  int cur_device = -1;
+  // batches
   std::vector<Batch> batches;
   std::vector<int> free_batches;
   std::vector<int> inflight;  // batch ids in flight (WALL)
-  void* slots = nullptr;
-  std::vector<int> free_slots;
-  void* results = nullptr;  // fp32 outputs ring (device) or pinned host
+  void* results = nullptr;  // fp32 outputs ring (context device) or mapped pinned host
   int64_t result_elems = 0;
   int64_t result_cursor = 0;
-  // Stream pool: a batch runs on an idle pooled stream rather than on its instance's own stream.
-  // The device has at most CUDA_DEVICE_MAX_CONNECTIONS (32) hardware queues; with one stream per
-  // instance, plans with > 32 instances alias streams onto shared queues and unrelated instances
-  // serialise.  Pooling keeps every in-flight batch on its own queue while <= pool size.
-  std::vector<cudaStream_t> pool;
-  std::vector<int> pool_n;        // batches in flight per lane
-  std::vector<double> pool_last;  // wall ms of the lane's last dispatch
-  // GX_INGRESS_DMA: copy-engine streams and a recycled event per in-flight arrival copy
-  std::vector<cudaStream_t> copy_streams;
-  std::vector<cudaEvent_t> h2d_events;
-  std::vector<int> free_h2d;
-  int64_t n_h2d = 0;
   double wall_ms = 0.0;
   int64_t n_batches = 0, n_kernels = 0;
-  int64_t drops_no_slot = 0;
-  double host_dispatch_ms = 0.0, host_poll_ms = 0.0, host_copy_ms = 0.0;  // diagnostics (GX_SERVE_DEBUG)
+  int64_t drops_no_slot = 0, remote_gathers = 0;
+  double host_dispatch_ms = 0.0, host_copy_ms = 0.0;  // diagnostics (GX_SERVE_DEBUG)
   int64_t loop_iters = 0;
   size_t max_inflight_seen = 0;
   std::chrono::steady_clock::time_point t0;
@@ -174,6 +197,39 @@ struct gx_serve {
     }
     return now + 1000.0 / c.rate;
   }
+  int dev_index(int gpu_ordinal) {
+    for (size_t i = 0; i < gpus.size(); ++i)
+      if (gpus[i] == gpu_ordinal) return static_cast<int>(i);
+    gpus.push_back(gpu_ordinal);
+    return static_cast<int>(gpus.size()) - 1;
+  }
+  int set_device(int d) {
+    if (cur_device != gpus[d]) {
+      GX_CUDA(cudaSetDevice(gpus[d]));
+      cur_device = gpus[d];
+    }
+    return GX_OK;
+  }
+  uint8_t* slot_ptr(int d, int slot) const {
+    return static_cast<uint8_t*>(devs[d].slots) + static_cast<size_t>(slot) * cfg.slot_bytes;
+  }
+  void free_slot(int d, int& slot) {
+    if (slot >= 0) devs[d].free_slots.push_back(slot);
+    slot = -1;
+  }
+  int take_event(int d, int* out) {
+    DevRes& r = devs[d];
+    if (r.free_events.empty()) {
+      if (int rc = set_device(d)) return rc;
+      cudaEvent_t ev = nullptr;
+      GX_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      r.events.push_back(ev);
+      r.free_events.push_back(static_cast<int>(r.events.size()) - 1);
+    }
+    *out = r.free_events.back();
+    r.free_events.pop_back();
+    return GX_OK;
+  }
 
   int gen_request(int cid, double now);
   int arrive(int ri, double now);
@@ -181,6 +237,7 @@ struct gx_serve {
   int service(int si, double now);
   int stage_done(int bi, double now);
   int complete(int ri, double now);
+  int pick_instance(Stage& st, const Batch& b) const;
   int dispatch_gpu(int si, int bi);
   int run();
 };
@@ -189,10 +246,8 @@ int gx_serve::complete(int ri, double now) {
   Req& r = reqs[ri];
   r.status = 0;
   r.done = now;
-  if (r.slot >= 0) {
-    free_slots.push_back(r.slot);
-    r.slot = -1;
-  }
+  if (r.slot >= 0) free_slot(r.slot_dev, r.slot);
+  if (r.old_slot >= 0) free_slot(r.old_dev, r.old_slot);
   return GX_OK;
 }
 
@@ -233,6 +288,7 @@ int gx_serve::arrive(int ri, double now) {
   }
   const Route& rt = routes[r.route];
   if (rt.n_stages == 0) return complete(ri, now);
+  r.loc = rt.home;
   if (gpu()) {
     r.cur = rt.ingress;
     r.cur_dtype = rt.ingress_dtype;
@@ -242,30 +298,28 @@ int gx_serve::arrive(int ri, double now) {
     const bool needs_slot = cfg.ingress_from_host == GX_INGRESS_DMA || rt.n_stages > 1 ||
                             !stages[rt.stage[0]].out_final;
     if (needs_slot) {
-      if (free_slots.empty()) {  // out of device slots: counts as an admission drop
+      DevRes& home = devs[rt.home];
+      if (home.free_slots.empty()) {  // out of device slots: counts as an admission drop
         r.status = 1;
         ++drops_no_slot;
         return GX_OK;
       }
-      r.slot = free_slots.back();
-      free_slots.pop_back();
-      void* dst = static_cast<uint8_t*>(slots) + static_cast<size_t>(r.slot) * cfg.slot_bytes;
+      r.slot = home.free_slots.back();
+      r.slot_dev = rt.home;
+      home.free_slots.pop_back();
       if (cfg.ingress_from_host == GX_INGRESS_DMA) {
         // the copy engine moves the request's activation into its slot as soon as it arrives
         // (it waits in the stage queue anyway); the batch that takes it waits on this copy only
-        if (free_h2d.empty()) {
-          cudaEvent_t ev = nullptr;
-          GX_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-          h2d_events.push_back(ev);
-          free_h2d.push_back(static_cast<int>(h2d_events.size()) - 1);
-        }
         const double t_c = now_wall();
-        const int ei = free_h2d.back();
-        free_h2d.pop_back();
-        cudaStream_t cs = copy_streams[n_h2d++ % copy_streams.size()];
+        if (int rc = set_device(rt.home)) return rc;
+        int ei = -1;
+        if (int rc = take_event(rt.home, &ei)) return rc;
+        cudaStream_t cs = home.copy_streams[home.n_copies++ % home.copy_streams.size()];
+        void* dst = slot_ptr(rt.home, r.slot);
         GX_CUDA(cudaMemcpyAsync(dst, rt.ingress, rt.ingress_bytes, cudaMemcpyHostToDevice, cs));
-        GX_CUDA(cudaEventRecord(h2d_events[ei], cs));
+        GX_CUDA(cudaEventRecord(home.events[ei], cs));
         r.h2d_ev = ei;
+        r.h2d_dev = rt.home;
         r.cur = dst;
         host_copy_ms += now_wall() - t_c;
       }
@@ -280,57 +334,80 @@ int gx_serve::enqueue(int si, int ri, double now) {
   return service(si, now);
 }
 
+// A free instance on the GPU that holds most of the batch's activations; ties -> lowest index.
+int gx_serve::pick_instance(Stage& st, const Batch& b) const {
+  int best = -1, best_score = -1;
+  for (int i = 0; i < static_cast<int>(st.busy.size()); ++i) {
+    if (st.busy[i]) continue;
+    int score = 0;
+    for (int ri : b.reqs) score += reqs[ri].loc == st.inst_dev[i];
+    if (score > best_score) {
+      best = i;
+      best_score = score;
+    }
+  }
+  return best;
+}
+
 int gx_serve::dispatch_gpu(int si, int bi) {
   Stage& st = stages[si];
   Batch& b = batches[bi];
-  int inst = -1;
-  for (int i = 0; i < static_cast<int>(st.busy.size()); ++i)
-    if (!st.busy[i]) {
-      inst = i;
-      break;
-    }
-  if (inst < 0) return fail(GX_EINTERNAL, "no free instance although free > 0");
-  st.busy[inst] = 1;
-  b.inst = inst;
-  gx_stage* g = st.inst[inst];
+  gx_stage* g = st.inst[b.inst];
+  const int d = b.dev;
+  DevRes& dr = devs[d];
   const int k = static_cast<int>(b.reqs.size());
   if (k < 1 || k > 64 || k > g->max_batch) return fail(GX_EINTERNAL, "dispatched batch larger than the instance");
+  if (int rc = set_device(d)) return rc;
   const void* src[64];
   int32_t sdt[64];
   void* dst[64];
   int channels = 0;
   // an idle lane if there is one, else the lane with the fewest / oldest batches in flight
   int lane = 0;
-  for (int i = 1; i < static_cast<int>(pool.size()); ++i)
-    if (pool_n[i] < pool_n[lane] || (pool_n[i] == pool_n[lane] && pool_last[i] < pool_last[lane])) lane = i;
-  cudaStream_t sm = pool[lane];
+  for (int i = 1; i < static_cast<int>(dr.pool.size()); ++i)
+    if (dr.pool_n[i] < dr.pool_n[lane] || (dr.pool_n[i] == dr.pool_n[lane] && dr.pool_last[i] < dr.pool_last[lane]))
+      lane = i;
+  cudaStream_t sm = dr.pool[lane];
   for (int i = 0; i < k; ++i) {
     Req& r = reqs[b.reqs[i]];
-    if (r.h2d_ev >= 0) {
-      GX_CUDA(cudaStreamWaitEvent(sm, h2d_events[r.h2d_ev], 0));
-      free_h2d.push_back(r.h2d_ev);
+    if (r.h2d_ev >= 0) {  // (cross-device event waits are allowed)
+      GX_CUDA(cudaStreamWaitEvent(sm, devs[r.h2d_dev].events[r.h2d_ev], 0));
+      devs[r.h2d_dev].free_events.push_back(r.h2d_ev);
       r.h2d_ev = -1;
     }
     src[i] = r.cur;
     sdt[i] = r.cur_dtype;
     channels = std::max(channels, r.cur_channels);
+    if (r.loc != d && r.slot >= 0) ++remote_gathers;
     if (st.out_final) {
       r.result_seq = result_cursor++;
       dst[i] = static_cast<uint8_t*>(results) + (r.result_seq % cfg.result_rows) * result_elems * 4;
     } else {
-      dst[i] = static_cast<uint8_t*>(slots) + static_cast<size_t>(r.slot) * cfg.slot_bytes;
+      // the output goes to a slot on this GPU: the request's own if it is here, else a fresh one
+      // (the old one is read by this batch's gather and freed when the batch completes); with no
+      // free slot here, the scatter writes the request's existing slot over NVLink
+      if (r.slot_dev != d && !dr.free_slots.empty()) {
+        r.old_slot = r.slot;
+        r.old_dev = r.slot_dev;
+        r.slot = dr.free_slots.back();
+        r.slot_dev = d;
+        dr.free_slots.pop_back();
+      }
+      if (r.slot < 0) return fail(GX_EINTERNAL, "request without an output slot");
+      dst[i] = slot_ptr(r.slot_dev, r.slot);
     }
   }
   b.lane = lane;
-  pool_n[lane] += 1;
-  pool_last[lane] = b.t_disp;
+  dr.pool_n[lane] += 1;
+  dr.pool_last[lane] = b.t_disp;
   const int out_dt = st.out_final ? GX_F32 : g->m->tensors[g->out_tid].dtype;
   int rc = gx::stage_run_on(g, sm, k, src, sdt, channels, dst, out_dt);
   if (rc != GX_OK) return rc;
   int kc = 0;
   gx_stage_kernel_count(g, k, &kc);
   n_kernels += kc;
-  GX_CUDA(cudaEventRecord(b.ev, sm));
+  if (int e = take_event(d, &b.ev)) return e;
+  GX_CUDA(cudaEventRecord(dr.events[b.ev], sm));
   for (int i = 0; i < k; ++i) {
     Req& r = reqs[b.reqs[i]];
     if (!st.out_final) {
@@ -362,7 +439,6 @@ int gx_serve::service(int si, double now) {
     } else {
       batches.emplace_back();
       bi = static_cast<int>(batches.size()) - 1;
-      if (gpu()) GX_CUDA(cudaEventCreateWithFlags(&batches[bi].ev, cudaEventDisableTiming));
     }
     Batch& b = batches[bi];
     b.stage = si;
@@ -373,10 +449,16 @@ int gx_serve::service(int si, double now) {
     }
     st.free -= 1;
     ++n_batches;
+    b.inst = pick_instance(st, b);
+    if (b.inst < 0) return fail(GX_EINTERNAL, "no free instance although free > 0");
+    st.busy[b.inst] = 1;
+    b.dev = st.inst_dev[b.inst];
     if (cfg.record_dispatch) {
       d_t.push_back(now);
       d_stage.push_back(si);
       d_k.push_back(k);
+      d_inst.push_back(b.inst);
+      d_gpu.push_back(gpus[b.dev]);
       for (int ri : b.reqs) d_seqs.push_back(reqs[ri].seq);
     }
     if (cfg.clock == GX_CLOCK_VIRTUAL) {
@@ -386,9 +468,11 @@ int gx_serve::service(int si, double now) {
       // this batch's outputs); completion stays on the virtual clock
       int rc = dispatch_gpu(si, bi);
       if (rc != GX_OK) return rc;
-      GX_CUDA(cudaStreamSynchronize(pool[b.lane]));
+      GX_CUDA(cudaStreamSynchronize(devs[b.dev].pool[b.lane]));
       inflight.pop_back();
-      pool_n[b.lane] -= 1;
+      devs[b.dev].pool_n[b.lane] -= 1;
+      devs[b.dev].free_events.push_back(b.ev);
+      b.ev = -1;
       push(now + st.lat[k], R_DONE, bi);
     } else {
       const double t_a = now_wall();
@@ -414,7 +498,7 @@ int gx_serve::stage_done(int bi, double now) {
   Batch& b = batches[bi];
   Stage& st = stages[b.stage];
   st.free += 1;
-  if (gpu()) st.busy[b.inst] = 0;
+  st.busy[b.inst] = 0;
   if (cfg.clock == GX_CLOCK_WALL) {
     st.obs_ms += now - b.t_disp;
     if (b.reqs.size() < st.lat.size()) st.plan_ms += st.lat[b.reqs.size()];
@@ -423,9 +507,12 @@ int gx_serve::stage_done(int bi, double now) {
   }
   std::vector<int> reqs_copy = b.reqs;
   const int si = b.stage;
+  const int dev = b.dev;
   free_batches.push_back(bi);
   for (int ri : reqs_copy) {
     Req& r = reqs[ri];
+    if (!st.out_final) r.loc = dev;  // its output now lives on the GPU that ran the batch
+    if (r.old_slot >= 0) free_slot(r.old_dev, r.old_slot);
     r.stage_idx += 1;
     const Route& rt = routes[r.route];
     if (r.stage_idx < rt.n_stages) {
@@ -493,24 +580,26 @@ int gx_serve::run() {
     const double limit = horizon + std::max(0.0, cfg.drain_ms);
     for (;;) {
       const double now = now_wall();
-      bool progressed = false;
       ++loop_iters;
       max_inflight_seen = std::max(max_inflight_seen, inflight.size());
       for (size_t i = 0; i < inflight.size();) {
         const int bi = inflight[i];
-        cudaError_t q = cudaEventQuery(batches[bi].ev);
+        Batch& b = batches[bi];
+        DevRes& dr = devs[b.dev];
+        cudaError_t q = cudaEventQuery(dr.events[b.ev]);
         if (q == cudaSuccess) {
           inflight[i] = inflight.back();
           inflight.pop_back();
-          pool_n[batches[bi].lane] -= 1;
+          dr.pool_n[b.lane] -= 1;
+          dr.free_events.push_back(b.ev);
+          b.ev = -1;
           if (now <= limit) {
             rc = stage_done(bi, now);
           } else {
-            Stage& st = stages[batches[bi].stage];
+            Stage& st = stages[b.stage];
             st.free += 1;
-            st.busy[batches[bi].inst] = 0;
+            st.busy[b.inst] = 0;
           }
-          progressed = true;
           if (rc != GX_OK) break;
         } else if (q == cudaErrorNotReady) {
           ++i;
@@ -522,7 +611,6 @@ int gx_serve::run() {
       while (!heap.empty() && heap.top().t <= now && heap.top().t <= limit + kEps && rc == GX_OK) {
         Ev e = heap.top();
         heap.pop();
-        progressed = true;
         // events fire at their scheduled time (the clock has passed it); state uses that time
         switch (e.rank) {
           case R_REPLAN:
@@ -552,15 +640,16 @@ int gx_serve::run() {
       if (rc != GX_OK) break;
       if (now > horizon && inflight.empty() && (now > limit || heap.empty() || heap.top().t > limit + kEps)) break;
       if (now > limit + 60000.0) return fail(GX_EINTERNAL, "wall-clock serving did not drain");
-      (void)progressed;
     }
   }
   wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-  if (cfg.clock == GX_CLOCK_WALL && getenv("GX_SERVE_DEBUG")) {
-    fprintf(stderr, "[serve] wall=%.0fms batches=%lld host_copy=%.0fms host_dispatch=%.0fms (%.1fus/batch) loop_iters=%lld max_inflight=%zu\n",
+  if (cfg.clock == GX_CLOCK_WALL && getenv("GX_SERVE_DEBUG")) {  // diagnostics only: prints, changes nothing
+    fprintf(stderr,
+            "[serve] wall=%.0fms batches=%lld host_copy=%.0fms host_dispatch=%.0fms (%.1fus/batch) loop_iters=%lld "
+            "max_inflight=%zu gpus=%zu remote_gathers=%lld\n",
             wall_ms, static_cast<long long>(n_batches), host_copy_ms, host_dispatch_ms,
             n_batches ? 1000.0 * host_dispatch_ms / n_batches : 0.0, static_cast<long long>(loop_iters),
-            max_inflight_seen);
+            max_inflight_seen, gpus.size(), static_cast<long long>(remote_gathers));
     for (size_t i = 0; i < stages.size(); ++i) {
       const Stage& st = stages[i];
       if (!st.obs_n) continue;
@@ -573,6 +662,79 @@ int gx_serve::run() {
   return rc;
 }
 
+namespace {
+// GPU-clock resources: per device a stream pool, copy streams, a slot pool; peer access between
+// every pair of devices the plan spans (batches gather activations produced on another GPU).
+int create_gpu_resources(gx_serve* s) {
+  const gx_serve_cfg& cfg = s->cfg;
+  for (size_t a = 0; a < s->gpus.size(); ++a)
+    for (size_t b = 0; b < s->gpus.size(); ++b) {
+      if (a == b) continue;
+      int can = 0;
+      GX_CUDA(cudaDeviceCanAccessPeer(&can, s->gpus[a], s->gpus[b]));
+      if (!can)
+        return fail(GX_EINFEASIBLE, "GPU " + std::to_string(s->gpus[a]) + " cannot access GPU " +
+                                        std::to_string(s->gpus[b]) + " (peer access needed across the placement)");
+      GX_CUDA(cudaSetDevice(s->gpus[a]));
+      const cudaError_t e = cudaDeviceEnablePeerAccess(s->gpus[b], 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled)
+        cudaGetLastError();
+      else if (e != cudaSuccess)
+        return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+    }
+  s->devs.resize(s->gpus.size());
+  for (size_t d = 0; d < s->gpus.size(); ++d) {
+    DevRes& r = s->devs[d];
+    r.device = s->gpus[d];
+    GX_CUDA(cudaSetDevice(r.device));
+    if (cfg.slot_bytes > 0) GX_CUDA(cudaMalloc(&r.slots, static_cast<size_t>(cfg.slot_bytes) * cfg.max_inflight));
+    for (int i = cfg.max_inflight - 1; i >= 0; --i) r.free_slots.push_back(i);
+    // more lanes than the 32 hardware queues: the least-loaded-lane choice then spreads in-flight
+    // batches over every queue (measured: 30 lanes -> p99 205 ms, 64 -> 101 ms at 1536 clients)
+    const int lanes = std::max(1, dev().serve_streams);
+    for (int i = 0; i < lanes; ++i) {
+      cudaStream_t q = nullptr;
+      GX_CUDA(cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking));
+      r.pool.push_back(q);
+    }
+    r.pool_n.assign(r.pool.size(), 0);
+    r.pool_last.assign(r.pool.size(), 0.0);
+    // one FIFO copy stream: arrival order is deadline order, and concurrent copies only share
+    // the PCIe link (measured at 1152 clients: p99 88 ms with 1 stream, 205-220 ms with 4 or 16)
+    const int ncopy = cfg.ingress_from_host == GX_INGRESS_DMA ? std::max(1, dev().copy_streams) : 0;
+    for (int i = 0; i < ncopy; ++i) {
+      cudaStream_t q = nullptr;
+      GX_CUDA(cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking));
+      r.copy_streams.push_back(q);
+    }
+  }
+  int64_t relems = 0;
+  for (auto& x : s->stages)
+    if (x.out_final && !x.inst.empty()) {
+      const gx_stage* g = x.inst[0];
+      relems = std::max<int64_t>(relems, tensor_elems(g->m->tensors[g->out_tid]));
+    }
+  s->result_elems = relems;
+  GX_CUDA(cudaSetDevice(s->gpus[0]));
+  s->cur_device = s->gpus[0];
+  if (relems > 0) {
+    const size_t bytes = static_cast<size_t>(relems) * 4 * cfg.result_rows;
+    if (cfg.egress_to_host)
+      GX_CUDA(cudaHostAlloc(&s->results, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+    else
+      GX_CUDA(cudaMalloc(&s->results, bytes));
+  }
+  return GX_OK;
+}
+
+int device_of_pointer(const void* p, int fallback) {
+  cudaPointerAttributes at;
+  if (p && cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeDevice) return at.device;
+  cudaGetLastError();
+  return fallback;
+}
+}  // namespace
+
 extern "C" {
 
 int gx_serve_create(gx_ctx* ctx, int n_stages, const gx_serve_stage* st, int n_routes, const gx_serve_route* rt,
@@ -582,6 +744,8 @@ int gx_serve_create(gx_ctx* ctx, int n_stages, const gx_serve_stage* st, int n_r
   gx_serve* s = new gx_serve();
   s->ctx = ctx;
   s->cfg = *cfg;
+  const bool gpu_clock = cfg->clock != GX_CLOCK_VIRTUAL;
+  s->gpus.push_back(gpu_clock ? ctx->device : 0);
   for (int i = 0; i < n_stages; ++i) {
     Stage x;
     x.batch = st[i].batch;
@@ -598,26 +762,30 @@ int gx_serve_create(gx_ctx* ctx, int n_stages, const gx_serve_stage* st, int n_r
       delete s;
       return fail(GX_EINVAL, "replay clock needs a latency table per stage");
     }
-    if (cfg->clock != GX_CLOCK_VIRTUAL) {
+    x.busy.assign(x.instances, 0);
+    if (gpu_clock) {
       if (!st[i].inst) {
         delete s;
         return fail(GX_EINVAL, "wall clock needs executor instances per stage");
       }
       for (int j = 0; j < x.instances; ++j) {
         gx_stage* g = static_cast<gx_stage*>(st[i].inst[j]);
-        if (!g || g->max_batch < x.batch || g->m->ctx->device != ctx->device) {
+        if (!g || g->max_batch < x.batch) {
           delete s;
           return fail(GX_EINVAL, "stage " + std::to_string(i) + ": executor instance " + std::to_string(j) +
                                      (g ? " has max_batch " + std::to_string(g->max_batch) + " < stage batch " +
-                                              std::to_string(x.batch) + " or lives on another device"
+                                              std::to_string(x.batch)
                                         : " is null"));
         }
         x.inst.push_back(g);
+        x.inst_dev.push_back(s->dev_index(g->m->ctx->device));
       }
-      x.busy.assign(x.instances, 0);
-    } else if (x.lat.empty()) {
-      delete s;
-      return fail(GX_EINVAL, "virtual clock needs a latency table per stage");
+    } else {
+      if (x.lat.empty()) {
+        delete s;
+        return fail(GX_EINVAL, "virtual clock needs a latency table per stage");
+      }
+      for (int j = 0; j < x.instances; ++j) x.inst_dev.push_back(s->dev_index(st[i].inst_gpu ? st[i].inst_gpu[j] : 0));
     }
     s->stages.push_back(std::move(x));
   }
@@ -638,6 +806,13 @@ int gx_serve_create(gx_ctx* ctx, int n_stages, const gx_serve_stage* st, int n_r
         delete s;
         return fail(GX_EINVAL, "route references a bad stage");
       }
+    if (r.n_stages > 0) {
+      // where the request's activation is when it arrives: DMA ingress lands on the first stage's
+      // instance-0 GPU; device-resident ingress lives where it was allocated
+      r.home = s->stages[r.stage[0]].inst_dev[0];
+      if (gpu_clock && cfg->ingress_from_host != GX_INGRESS_DMA && r.ingress)
+        r.home = s->dev_index(device_of_pointer(r.ingress, s->gpus[r.home]));
+    }
     s->routes.push_back(r);
   }
   for (int i = 0; i < n_clients; ++i) {
@@ -666,7 +841,7 @@ int gx_serve_create(gx_ctx* ctx, int n_stages, const gx_serve_stage* st, int n_r
     }
     s->clients.push_back(std::move(c));
   }
-  if (cfg->clock != GX_CLOCK_VIRTUAL) {
+  if (gpu_clock) {
     if (cfg->max_inflight < 1) {
       delete s;
       return fail(GX_EINVAL, "max_inflight must be >= 1 when batches execute");
@@ -699,45 +874,10 @@ int gx_serve_create(gx_ctx* ctx, int n_stages, const gx_serve_stage* st, int n_r
                                  " bytes a route needs (ingress copy or intermediate boundary)");
     }
     if (s->cfg.result_rows <= 0) s->cfg.result_rows = cfg->max_inflight;
-    cudaError_t e = cudaSetDevice(ctx->device);
-    if (e == cudaSuccess && s->cfg.slot_bytes > 0)
-      e = cudaMalloc(&s->slots, static_cast<size_t>(s->cfg.slot_bytes) * cfg->max_inflight);
-    int64_t relems = 0;
-    for (auto& x : s->stages)
-      if (x.out_final && !x.inst.empty()) {
-        const gx_stage* g = x.inst[0];
-        relems = std::max<int64_t>(relems, tensor_elems(g->m->tensors[g->out_tid]));
-      }
-    s->result_elems = relems;
-    if (e == cudaSuccess && relems > 0) {
-      const size_t bytes = static_cast<size_t>(relems) * 4 * s->cfg.result_rows;
-      e = cfg->egress_to_host ? cudaHostAlloc(&s->results, bytes, cudaHostAllocMapped) : cudaMalloc(&s->results, bytes);
-    }
-    // more lanes than the 32 hardware queues: the least-loaded-lane choice then spreads in-flight
-    // batches over every queue (measured: 30 lanes -> p99 205 ms, 64 -> 101 ms at 1536 clients)
-    int lanes = 64;
-    lanes = std::max(1, dev().serve_streams);
-    for (int i = 0; i < lanes && e == cudaSuccess; ++i) {
-      cudaStream_t q = nullptr;
-      e = cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking);
-      if (e == cudaSuccess) s->pool.push_back(q);
-    }
-    s->pool_n.assign(s->pool.size(), 0);
-    s->pool_last.assign(s->pool.size(), 0.0);
-    // one FIFO copy stream: arrival order is deadline order, and concurrent copies only share
-    // the PCIe link (measured at 1152 clients: p99 88 ms with 1 stream, 205-220 ms with 4 or 16)
-    int ncopy = 1;
-    ncopy = std::max(1, dev().copy_streams);
-    for (int i = 0; i < ncopy && e == cudaSuccess && cfg->ingress_from_host == GX_INGRESS_DMA; ++i) {
-      cudaStream_t q = nullptr;
-      e = cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking);
-      if (e == cudaSuccess) s->copy_streams.push_back(q);
-    }
-    if (e != cudaSuccess) {
+    if (int rc = create_gpu_resources(s)) {
       gx_serve_destroy(s);
-      return cuda_fail(e, "serving resources");
+      return rc;
     }
-    for (int i = cfg->max_inflight - 1; i >= 0; --i) s->free_slots.push_back(i);
   }
   *out = s;
   return GX_OK;
@@ -745,7 +885,10 @@ int gx_serve_create(gx_ctx* ctx, int n_stages, const gx_serve_stage* st, int n_r
 
 int gx_serve_run(gx_serve* s) {
   if (!s) return fail(GX_EINVAL, "null arg");
-  if (s->gpu()) GX_CUDA(cudaSetDevice(s->ctx->device));
+  if (s->gpu()) {
+    GX_CUDA(cudaSetDevice(s->gpus[0]));
+    s->cur_device = s->gpus[0];
+  }
   return s->run();
 }
 
@@ -785,6 +928,13 @@ int gx_serve_dispatch(gx_serve* s, double* t_ms, int32_t* stage, int32_t* k, int
   return GX_OK;
 }
 
+int gx_serve_dispatch_placement(gx_serve* s, int32_t* inst, int32_t* gpu) {
+  if (!s) return fail(GX_EINVAL, "null arg");
+  if (inst) std::copy(s->d_inst.begin(), s->d_inst.end(), inst);
+  if (gpu) std::copy(s->d_gpu.begin(), s->d_gpu.end(), gpu);
+  return GX_OK;
+}
+
 int gx_serve_stats(gx_serve* s, double* wall_ms, int64_t* batches, int64_t* kernels) {
   if (!s) return fail(GX_EINVAL, "null arg");
   if (wall_ms) *wall_ms = s->wall_ms;
@@ -808,8 +958,12 @@ int gx_serve_outputs_for(gx_serve* s, int64_t n, const int64_t* req, float* out,
   if (!s || (n > 0 && (!req || !out))) return fail(GX_EINVAL, "null arg");
   if (!s->gpu()) return fail(GX_EINVAL, "outputs exist only when batches execute on the GPU");
   if (elems != s->result_elems) return fail(GX_EINVAL, "output row size mismatch");
-  GX_CUDA(cudaSetDevice(s->ctx->device));
-  GX_CUDA(cudaDeviceSynchronize());
+  for (int g : s->gpus) {
+    GX_CUDA(cudaSetDevice(g));
+    GX_CUDA(cudaDeviceSynchronize());
+  }
+  GX_CUDA(cudaSetDevice(s->gpus[0]));
+  s->cur_device = s->gpus[0];
   int64_t got = 0;
   for (int64_t i = 0; i < n; ++i) {
     float* dst = out + i * elems;
@@ -832,20 +986,21 @@ int gx_serve_outputs_for(gx_serve* s, int64_t n, const int64_t* req, float* out,
 int gx_serve_destroy(gx_serve* s) {
   if (!s) return GX_OK;
   if (s->gpu()) {
-    cudaSetDevice(s->ctx->device);
-    cudaDeviceSynchronize();
-    for (auto& b : s->batches)
-      if (b.ev) cudaEventDestroy(b.ev);
-    if (s->slots) cudaFree(s->slots);
+    for (DevRes& r : s->devs) {
+      cudaSetDevice(r.device);
+      cudaDeviceSynchronize();
+      for (cudaEvent_t ev : r.events) cudaEventDestroy(ev);
+      for (cudaStream_t q : r.copy_streams) cudaStreamDestroy(q);
+      for (cudaStream_t q : r.pool) cudaStreamDestroy(q);
+      if (r.slots) cudaFree(r.slots);
+    }
+    if (!s->gpus.empty()) cudaSetDevice(s->gpus[0]);
     if (s->results) {
       if (s->cfg.egress_to_host)
         cudaFreeHost(s->results);
       else
         cudaFree(s->results);
     }
-    for (cudaEvent_t ev : s->h2d_events) cudaEventDestroy(ev);
-    for (cudaStream_t q : s->copy_streams) cudaStreamDestroy(q);
-    for (cudaStream_t q : s->pool) cudaStreamDestroy(q);
   }
   delete s;
   return GX_OK;

@@ -53,6 +53,32 @@ class DeviceModel:
             self.handle = None
 
 
+def placed_instances(dep, models: dict, work_conserving: bool = True) -> list:
+    """Executor instances of a deployment placed across the GPUs of one box: instance i of stage s
+    runs on GPU s.gpus[i] (the plan's placement, placement.py:24-70; None = GPU 0).  `models` maps
+    a plan GPU index to the DeviceModel resident on it.  SM budgets are assigned per GPU from the
+    shares of the instances placed on that GPU (Context.sm_budgets)."""
+    per_gpu = {}
+    for si, s in enumerate(dep.stages):
+        for i, g in enumerate(s.gpus if s.gpus is not None else (0,) * s.instances):
+            per_gpu.setdefault(g, []).append((si, i, s.share))
+    budget = {}
+    for g, lst in per_gpu.items():
+        if g not in models:
+            raise ValidationError(f"plan places instances on GPU {g} but no model is resident there")
+        bs = models[g].ctx.sm_budgets([(share, 1) for _si, _i, share in lst], work_conserving=work_conserving)
+        for (si, i, _share), b in zip(lst, bs):
+            budget[(si, i)] = (g, b)
+    out = []
+    for si, s in enumerate(dep.stages):
+        row = []
+        for i in range(s.instances):
+            g, b = budget[(si, i)]
+            row.append(StageInstance(models[g], s.start, s.end, s.batch, b))
+        out.append(row)
+    return out
+
+
 class StageInstance:
     """One executor instance of span [start, end) bounded to `sm_budget` SMs."""
 

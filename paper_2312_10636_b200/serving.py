@@ -83,6 +83,7 @@ class ServeReport:
     requests: list[tuple]
     config: dict = field(default_factory=dict)
     dispatch: list[tuple] | None = None  # (t_ms, stage index, k, (request seqs...))
+    placement: list[tuple] | None = None  # per dispatched batch: (instance index, GPU)
     outputs: np.ndarray | None = None  # replay / wall with return_outputs: [request, out elems]
     sampled: tuple | None = None  # sample_outputs: (request indices, [n, out elems] fp32)
     wall_ms: float = 0.0
@@ -217,6 +218,11 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
         if lat_fn is not None:
             lat = (C.c_double * (s.batch + 1))(0.0, *[float(lat_fn(s, k)) for k in range(1, s.batch + 1)])
             st_arr[i].lat_ms = keep(lat)
+        if s.gpus is not None:  # placement (placement.py:24-70): GPU of each instance
+            if len(s.gpus) != s.instances:
+                raise ValidationError(f"stage {s.stage_id}: placement lists {len(s.gpus)} GPUs for {s.instances} "
+                                      f"instances")
+            st_arr[i].inst_gpu = keep((C.c_int32 * s.instances)(*s.gpus))
         if gpu:
             insts = instances[i]
             if len(insts) != s.instances:
@@ -335,7 +341,7 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
                 pick += [j for j in good if j not in set(pick)][:max(0, sample_outputs - len(pick))]
                 pick = sorted(pick[:sample_outputs])
                 sampled = (order[pick], arr[pick])
-        dispatch = None
+        dispatch = placement = None
         if record_dispatch:
             nbat = C.c_int64()
             nit = C.c_int64()
@@ -350,12 +356,17 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
             for i in range(nbat.value):
                 dispatch.append((float(t[i]), int(si[i]), int(kk[i]), tuple(int(x) for x in sq[off:off + kk[i]])))
                 off += kk[i]
+            pi = np.zeros(nbat.value, np.int32)
+            pg = np.zeros(nbat.value, np.int32)
+            N.check(L.gx_serve_dispatch_placement(h, P(pi, C.c_int32), P(pg, C.c_int32)))
+            placement = [(int(a), int(b)) for a, b in zip(pi, pg)]
     finally:
         L.gx_serve_destroy(h)
     rep = _report(planner or deps[0].planner, horizon_s, ids, cl, gen, done, dl, status,
                   {"clock": "wall" if wall else "replay" if replay else "virtual", "horizon_s": horizon_s,
                    "poisson": poisson, "seed": seed, "clients": len(ids)})
     rep.dispatch = dispatch
+    rep.placement = placement
     rep.outputs = outputs
     rep.sampled = sampled
     rep.wall_ms, rep.batches, rep.kernels = float(wall_ms.value), int(nb.value), int(nk.value)

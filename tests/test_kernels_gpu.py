@@ -349,3 +349,34 @@ def test_stage_batch_sizes_share_one_instance():
             assert torch.equal(part[i], full[i]), (k, i)
     with pytest.raises(ValidationError):
         st.run(x + x[:1])
+
+
+@pytest.mark.parametrize("f,c_src,c_dst,H,dst_f32", [(2, 3, 16, 112, False), (2, 3, 16, 112, True),
+                                                    (2, 3, 16, 56, False), (1, 3, 8, 37, False),
+                                                    (1, 3, 8, 37, True), (2, 2, 12, 20, False)])
+def test_gather_ex_space_to_depth_bit_exact(f, c_src, c_dst, H, dst_f32):
+    """K1 gather into the stem's space-to-depth boundary (the vectorised one-pixel-per-thread path
+    for 2x2 RGB blocks, the generic per-element path otherwise) and the plain channel-padded gather,
+    into bf16 and into fp32 batches, for ragged fp32 / bf16 sources: bit-exact with torch's own
+    rearrangement and cast."""
+    import ctypes as C
+    from paper_2312_10636_b200.device import context
+    ctx = context(0)
+    k = 5
+    g = torch.Generator().manual_seed(9)
+    imgs = [torch.randn(H * f, H * f, c_src, generator=g) for _ in range(k)]
+    srcs = [im.cuda() if i % 2 == 0 else im.to(torch.bfloat16).cuda() for i, im in enumerate(imgs)]
+    refs = []
+    for im, s in zip(imgs, srcs):
+        v = s.float().cpu()
+        v = v.view(H, f, H, f, c_src).permute(0, 2, 1, 3, 4).reshape(H, H, f * f * c_src)
+        refs.append(F.pad(v, (0, c_dst - f * f * c_src)))
+    ref = torch.stack(refs)
+    dt = torch.float32 if dst_f32 else torch.bfloat16
+    out = torch.full((k, H, H, c_dst), float("nan"), dtype=dt, device="cuda")
+    N.check(N.lib().gx_gather_ex(ctx.handle, k, N.ptr_array([s.data_ptr() for s in srcs]),
+                                 N.i32_array([N.GX_F32 if s.dtype == torch.float32 else N.GX_BF16 for s in srcs]),
+                                 H, H, f, c_src, c_dst, C.c_void_p(out.data_ptr()), N.GX_F32 if dst_f32 else N.GX_BF16,
+                                 3, C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    assert torch.equal(out.cpu(), ref.to(dt))
