@@ -67,7 +67,9 @@ def _workloads(name: str, all_plans: bool = False):
     pats = [f"{name}_c[0-9]*.json"] + ([f"{name}_s*_c[0-9]*.json"] if all_plans else [])
     files = [f for pat in pats for f in glob.glob(str(ROOT / "tests" / "golden" / "workload" / pat))]
     docs = [json.loads(Path(f).read_text()) for f in files]
-    return sorted(docs, key=_fkey)
+    # plans for an N-GPU box (<tag>_g<N>_c*) belong to --placement plan only
+    gpus = int(name.rsplit("_g", 1)[1]) if "_g" in name else 1
+    return sorted((d for d in docs if d.get("gpus", 1) == gpus), key=_fkey)
 
 
 def _workload(name: str, clients: int | None):
