@@ -66,9 +66,11 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
   const int CB = RB == 128 ? a.Cin / 64 : 1;
   const int NKB = RB == 128 ? 9 : a.R;  // weight k-blocks per channel block
   const uint32_t hbytes = static_cast<uint32_t>(Wp * (BH + a.R - 1) * RB);
-  // stem (one N tile): its NKB weight k-blocks are loaded once into ring slots 0..NKB-1 and stay
-  // resident (every tile would otherwise re-load the same 32 KB, 60% of the kernel's TMA bytes)
-  const bool resident = RB == 32 && a.n_tiles == 1 && S_ >= NKB && CB == 1 && !(a.dbg & 32);  // GX_CONV_DBG=32: ring as before
+  // one N tile and one channel block (the stem; layer1's 56x56x64 3x3): the NKB weight k-blocks
+  // are loaded once into ring slots 0..NKB-1 and stay resident.  Every tile would otherwise
+  // re-load the same weights: 32 KB per stem tile (60% of its TMA bytes), 72 KB per layer1 tile
+  // (2.4x its halo bytes) through a few-SM budget's L2 feed.
+  const bool resident = a.n_tiles == 1 && S_ >= NKB && CB == 1 && !(a.dbg & 32);  // GX_CONV_DBG=32: ring as before
   // the stem's halo is ~15 KB and one tile's MMAs take ~0.3 us: four buffers keep enough TMA loads
   // in flight to cover their latency
   constexpr int NH = RB == 32 ? 4 : 2;

@@ -41,9 +41,16 @@ struct SmemPlan {
   uint64_t* rfull;  // [2] residual slot filled
   uint64_t* rfw;    // [8 epilogue warps][2 slots] per-warp residual boxes filled (WST)
   uint64_t* bfull;  // bias vector staged
+  uint64_t* bresbar;  // resident weights (and identity block) landed
+  uint8_t* sBres;     // bres: [num_kb][BN*128] resident weight k-blocks of the CTA's N tile
+  uint8_t* sIdent;    // bres + res_mma: one 64x64 identity block (swizzled, 8 KB)
   uint32_t* tslot;
   int2* ktab;
 };
+
+__host__ __device__ inline uint32_t bres_alloc(int bres, int num_kb, int BN, int res_mma) {
+  return bres ? static_cast<uint32_t>(num_kb) * BN * 128u + (res_mma ? 8192u : 0u) : 0u;
+}
 
 __host__ __device__ inline int res_groups(int BN) { return (BN + 63) / 64; }
 __host__ __device__ inline uint32_t bias_alloc(int Cout) { return (static_cast<uint32_t>(Cout) * 4u + 1023u) & ~1023u; }
@@ -94,9 +101,12 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
   SmemPlan sp;
   sp.sA = smem;
   // KPS: k-blocks per pipeline stage (TMA mode): one barrier round trip per KPS*64 of K
-  const uint32_t sa_bytes = KPS * kATileBytes, sb_bytes = KPS * b_bytes;
+  const bool bres = a.bres != 0;
+  const uint32_t sa_bytes = KPS * kATileBytes, sb_bytes = bres ? 0u : KPS * b_bytes;
   sp.sB = sp.sA + static_cast<size_t>(S_) * sa_bytes;
-  sp.sRes = sp.sB + static_cast<size_t>(S_) * sb_bytes;
+  sp.sBres = sp.sB + static_cast<size_t>(S_) * sb_bytes;
+  sp.sIdent = sp.sBres + static_cast<size_t>(a.num_kb) * b_bytes;
+  sp.sRes = sp.sBres + bres_alloc(a.bres, a.num_kb, BN, a.res_mma);
   // slots: the residual tile (TMA-loaded) and/or the staged output tile (TMA-stored), in place
   const uint32_t res_slot_bytes = (has_res || ystore) ? res_groups(BN) * kResGroupBytes : 0u;
   sp.sBias = reinterpret_cast<float*>(sp.sRes + a.nres * res_slot_bytes);
@@ -107,7 +117,8 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
   sp.rfull = sp.tempty + 2;
   sp.bfull = sp.rfull + 2;
   sp.rfw = sp.bfull + 1;
-  sp.tslot = reinterpret_cast<uint32_t*>(sp.rfw + 16);
+  sp.bresbar = sp.rfw + 16;
+  sp.tslot = reinterpret_cast<uint32_t*>(sp.bresbar + 1);
   sp.ktab = reinterpret_cast<int2*>(sp.tslot + 4);
 
   const int tid = threadIdx.x;
@@ -147,6 +158,7 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
       mbar_init(&sp.rfull[1], 1);
       for (int i = 0; i < 16; ++i) mbar_init(&sp.rfw[i], 1);
       mbar_init(sp.bfull, 1);
+      mbar_init(sp.bresbar, 1);
       fence_barrier_init();
     }
     __syncwarp();
@@ -216,7 +228,19 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
       if (do_b && !a.wsw) tma_prefetch_desc(WM);
       if (do_a) tma_prefetch_desc(AM);
     }
-    const uint32_t tx = (do_a && !skipA ? kATileBytes : 0u) + (do_b && !skipB ? b_bytes : 0u);
+    const bool loadB = do_b && !skipB && !bres;  // bres: the weights were loaded once, below
+    const uint32_t tx = (do_a && !skipA ? kATileBytes : 0u) + (loadB ? b_bytes : 0u);
+    if (do_b && bres && issuer) {
+      // every tile of this CTA has the same N tile (planned so): its num_kb weight k-blocks, and
+      // with res_mma the 64x64 identity block (rows 0..63 of identity k-block num_kb), once
+      const int n_fix = blockIdx.x % a.n_tiles;
+      mbar_arrive_expect_tx(sp.bresbar, bres_alloc(1, a.num_kb, BN, a.res_mma));
+      for (int kb = 0; kb < a.num_kb; ++kb)
+        bulk_load(sp.sBres + static_cast<size_t>(kb) * b_bytes,
+                  a.wsw + (static_cast<size_t>(kb) * a.Cout + static_cast<size_t>(n_fix) * BN) * 128u, b_bytes,
+                  sp.bresbar);
+      if (a.res_mma) bulk_load(sp.sIdent, a.wsw + static_cast<size_t>(a.num_kb) * a.Cout * 128u, 8192u, sp.bresbar);
+    }
     const int cpl = a.cpl;
     const int nl = kBK / cpl;
     const uint32_t region = static_cast<uint32_t>(kBM * cpl * 2);
@@ -276,7 +300,7 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
             }
           }
         }
-        if (do_b && !skipB && issuer) {
+        if (loadB && issuer) {
           // identity blocks sit at kb = num_kb + column/64: this tile's are num_kb + nb0/64 + j
           const int kbw = kb < a.num_kb ? kb : kb + n_blk * BN / 64;
           if (wsrc)  // pre-swizzled tile: one contiguous bulk copy (no tensor-map walk)
@@ -297,6 +321,10 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
     const bool issuer = elect_one();
     int it = 0, t = 0, st = 0;
     uint32_t ph = 0;
+    if (bres) {  // resident weights (completed phase 0 once, never re-armed)
+      pipe_wait(sp.bresbar, 0, issuer);
+      tc_fence_after();
+    }
     for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++t) {
       const int acc = t & 1;
       const uint32_t aph = (t >> 1) & 1;
@@ -317,8 +345,20 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
         for (int jj = 0; jj < nk; ++jj) {
         const int kb = kb0 + jj;
         const uint32_t abase = smem_u32(sp.sA + st * sa_bytes + jj * kATileBytes);
-        const uint64_t bd = umma_desc_sw128(sp.sB + static_cast<size_t>(st) * sb_bytes + jj * b_bytes);
-        if (!kTmaA || a.cpl == 64) {
+        const uint64_t bd = bres ? umma_desc_sw128(sp.sBres + static_cast<size_t>(min(kb, a.num_kb - 1)) * b_bytes)
+                                 : umma_desc_sw128(sp.sB + static_cast<size_t>(st) * sb_bytes + jj * b_bytes);
+        if (bres && kb >= a.num_kb) {
+          // residual columns [64j, 64j+64) x identity: four M=128 N=64 K=16 MMAs into that 64-column
+          // slice of the accumulator (a quarter of the work of a full-width identity k-block, and
+          // no identity weights streamed per tile)
+          const uint32_t dj = d + 64u * static_cast<uint32_t>(kb - a.num_kb);
+          const uint64_t ad = umma_desc_kmajor(abase, 64, 0);
+          const uint64_t idd = umma_desc_sw128(sp.sIdent);
+          if (issuer) {
+#pragma unroll
+            for (int kk = 0; kk < kBK / 16; ++kk) umma_bf16(dj, ad + 2 * kk, idd + 2 * kk, a.idesc64, 1);
+          }
+        } else if (!kTmaA || a.cpl == 64) {
           const uint64_t ad = umma_desc_kmajor(abase, 64, 0);
           if (issuer) {
 #pragma unroll
@@ -585,20 +625,20 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
 }
 }  // namespace
 
-size_t conv_smem_bytes(int BN, int stages, int num_kb, int nres, int Cout, int kps) {
-  return 1024 + static_cast<size_t>(stages) * kps * (kATileBytes + BN * 128) +
-         static_cast<size_t>(nres) * res_groups(BN) * kResGroupBytes + bias_alloc(Cout) + (2 * stages + 25) * 8 + 16 +
+size_t conv_smem_bytes(int BN, int stages, int num_kb, int nres, int Cout, int kps, size_t bres_bytes) {
+  return 1024 + static_cast<size_t>(stages) * kps * (kATileBytes + (bres_bytes ? 0 : BN * 128)) + bres_bytes +
+         static_cast<size_t>(nres) * res_groups(BN) * kResGroupBytes + bias_alloc(Cout) + (2 * stages + 26) * 8 + 16 +
          static_cast<size_t>(num_kb) * 8 * sizeof(int2);
 }
 
 // Pipeline depth and residual slots that fit in ~220 KB: prefer >= 3 stages with a double-
 // buffered residual, else a single residual slot.
-int conv_pick_stages(int BN, int num_kb, bool res, int Cout, int* nres_out, int kps) {
+int conv_pick_stages(int BN, int num_kb, bool res, int Cout, int* nres_out, int kps, size_t bres_bytes) {
   const size_t budget = 220 * 1024;
-  const size_t per_stage = static_cast<size_t>(kps) * (kATileBytes + BN * 128) + 16;
+  const size_t per_stage = static_cast<size_t>(kps) * (kATileBytes + (bres_bytes ? 0 : BN * 128)) + 16;
   int best_s = 2, best_r = res ? 1 : 0;
   for (int nres = res ? 2 : 0; nres >= (res ? 1 : 0); --nres) {
-    const size_t fixed = conv_smem_bytes(BN, 0, num_kb, nres, Cout, kps);
+    const size_t fixed = conv_smem_bytes(BN, 0, num_kb, nres, Cout, kps, bres_bytes);
     int s = budget > fixed ? static_cast<int>((budget - fixed) / per_stage) : 0;
     if (s > 8) s = 8;
     // short-K convs (the bottleneck expand 1x1s) are epilogue-bound: with the per-warp epilogue the next tile's residual/staging slot must be free while this
@@ -629,7 +669,8 @@ cudaError_t launch_conv(const CUtensorMap& wmap, const CUtensorMap& amap, const 
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);
   cfg.blockDim = dim3(kConvTcThreads, 1, 1);
-  cfg.dynamicSmemBytes = conv_smem_bytes(a.BN, a.stages, a.num_kb, a.nres, a.Cout, a.kps);
+  cfg.dynamicSmemBytes =
+      conv_smem_bytes(a.BN, a.stages, a.num_kb, a.nres, a.Cout, a.kps, bres_alloc(a.bres, a.num_kb, a.BN, a.res_mma));
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

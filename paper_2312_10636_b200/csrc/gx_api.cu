@@ -64,6 +64,7 @@ const DevKnobs& dev() {
     d.fc_simt = flag("GX_FC_SIMT");
     d.no_pdl = flag("GX_NO_PDL");
     d.pool_nostrip = flag("GX_POOL_NOSTRIP");
+    d.no_bres = flag("GX_NO_BRES");
     d.conv_dbg = num("GX_CONV_DBG", 0);
     d.bn = num("GX_BN", 0);
     d.kps = num("GX_KPS", 0);
@@ -317,6 +318,19 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
               a.num_kb <= 2 &&
               a.Cin == ti.C && !dev().no_tma_im2col && !dev().no_a2d && !dev().no_res_mma;
   const bool epi_res = a.res != nullptr && !a.res_mma;  // residual handled by the epilogue
+  // Resident weights: when every tile a CTA runs shares one N tile and its weight k-blocks fit,
+  // they are bulk-loaded once per CTA instead of once per tile.  At BN=256 the per-tile weight
+  // stream is twice the A operand's bytes, through an L2 feed of ~86 B/clk per SM on the serving
+  // budgets (the layer1/2 1x1 convs); with res_mma the BN/64 full-width identity k-blocks per tile
+  // (128 KB at BN=256) become N=64 MMAs against one resident 8 KB identity block.
+  {
+    const int grid = std::min(a.num_tiles, std::max(1, sm_budget));
+    const size_t bytes = static_cast<size_t>(a.num_kb) * a.BN * 128 + (a.res_mma ? 8192 : 0);
+    a.bres = !for_span && wsw && !dev().no_wbulk && !dev().no_tma_im2col && !dev().no_bres &&
+             (a.n_tiles == 1 || grid % a.n_tiles == 0 || grid >= a.num_tiles) && bytes <= 72 * 1024;
+    a.idesc64 = umma_idesc_bf16(kBM, 64);
+  }
+  const size_t bres_bytes = a.bres ? static_cast<size_t>(a.num_kb) * a.BN * 128 + (a.res_mma ? 8192 : 0) : 0;
   // two k-blocks per pipeline stage halve the barrier round trips per unit of K; worth it when the
   // per-k-block MMA time (2*BN cycles) is below the ~500-cycle stage round trip and >= 3 stages fit
   a.kps = 1;
@@ -326,12 +340,12 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
     for (int kk = want; kk >= 2 && a.kps == 1 && !a.res_mma; --kk) {
       int nres2 = 0;
       if (tma && kk <= 3 && a.num_kb >= kk &&
-          conv_pick_stages(a.BN, a.num_kb, epi_res || a.ystore, a.Cout, &nres2, kk) >= 3)
+          conv_pick_stages(a.BN, a.num_kb, epi_res || a.ystore, a.Cout, &nres2, kk, bres_bytes) >= 3)
         a.kps = kk;
     }
   }
   a.stages = conv_pick_stages(a.BN, a.num_kb + (a.res_mma ? a.BN / 64 : 0), epi_res || a.ystore, a.Cout, &a.nres,
-                              a.kps);
+                              a.kps, bres_bytes);
   if (const int st = dev().stages) {
     if (st >= 1 && st <= a.stages) a.stages = st;
   }

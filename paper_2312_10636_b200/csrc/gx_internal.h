@@ -23,7 +23,7 @@ int bind_device(int device);
 struct DevKnobs {
   bool no_halo = false, no_halo32 = false, no_wbulk = false, no_ystore = false, gmaps = false, no_res_mma = false,
        no_tma_im2col = false, no_a2d = false, no_wres = false, no_wstore = false, fc_simt = false, no_pdl = false,
-       pool_nostrip = false;
+       pool_nostrip = false, no_bres = false;
   int conv_dbg = 0, bn = 0, kps = 0, stages = 0, res2_kb = 0;
   int serve_streams = 64;  // serving stream-pool lanes
   int copy_streams = 1;    // DMA-ingress copy streams
@@ -74,6 +74,10 @@ struct ConvArgs {
   int halo;            // 3x3/s1/p1 wide-image conv on conv_halo_kernel (amap = the 4D halo map)
   int hBH, hTPI;       // halo: output rows per M tile, M tiles per image
   int hWp, hRB;        // halo: padded row pitch (W + left + right pad), bytes per halo pixel row (128 | 32)
+  int bres;            // B resident: the CTA's num_kb weight k-blocks (its N tile is fixed) are bulk-loaded
+                       // once and stay in smem; with res_mma the residual is added by N=64 MMAs into
+                       // the accumulator's 64-column slices against one resident 64x64 identity block
+  uint32_t idesc64;    // instruction descriptor of those M=128, N=64 MMAs
 };
 constexpr int kConvThreads = 320;  // span kernel: 4 A-producer warps, TMA warp, MMA warp, 4 epilogue warps
 // conv_tc: warps 0-3 cp.async A producers (or epilogue when TMA builds A), 4 A/B TMA, 5 MMA,
@@ -81,8 +85,9 @@ constexpr int kConvThreads = 320;  // span kernel: 4 A-producer warps, TMA warp,
 constexpr int kConvTcThreads = 352;
 constexpr int kBM = 128;
 constexpr int kBK = 64;
-size_t conv_smem_bytes(int BN, int stages, int num_kb, int nres, int Cout, int kps = 1);
-int conv_pick_stages(int BN, int num_kb, bool res, int Cout, int* nres_out, int kps = 1);
+// bres_bytes: resident weight (+ identity) bytes; stages then hold only the A operand
+size_t conv_smem_bytes(int BN, int stages, int num_kb, int nres, int Cout, int kps = 1, size_t bres_bytes = 0);
+int conv_pick_stages(int BN, int num_kb, bool res, int Cout, int* nres_out, int kps = 1, size_t bres_bytes = 0);
 // wmap: weights [Cout][Kpad]; amap: im2col map of the input (tma_a); rmap: residual [M][res_ld];
 // ymap: output [M][y_ld] (ystore).
 cudaError_t launch_conv(const CUtensorMap& wmap, const CUtensorMap& amap, const CUtensorMap& rmap,
