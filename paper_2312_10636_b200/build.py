@@ -24,6 +24,10 @@ NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
     "--expt-relaxed-constexpr", "-Xptxas", "-v,-warn-spills", "-DNDEBUG",
 ]
+# GX_BUILD_DEV=1: a development build whose kernel-selection switches read GX_* environment
+# variables (scripts/ A/B experiments on a scratch copy); never the shipped library
+if os.environ.get("GX_BUILD_DEV") == "1":
+    NVCC_FLAGS.append("-DGX_DEV_KNOBS")
 
 
 def nvcc() -> str:

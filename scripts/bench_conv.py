@@ -97,6 +97,12 @@ SHAPES["l3_1x1_1024_256_k8"] = (8, 14, 14, 1024, 256, 1, 1, 1, 0)
 SHAPES["l4_3x3_512_k8"] = (8, 7, 7, 512, 512, 3, 3, 1, 1)
 
 SHAPES["l1_3x3_k1"] = (1, 56, 56, 64, 64, 3, 3, 1, 1)
+SHAPES["l1_1x1_64_256_k16_res"] = (16, 56, 56, 64, 256, 1, 1, 1, 0)
+SHAPES["l1_1x1_64_256_k16"] = (16, 56, 56, 64, 256, 1, 1, 1, 0)
+SHAPES["l1_1x1_256_64_k16"] = (16, 56, 56, 256, 64, 1, 1, 1, 0)
+SHAPES["l1_1x1_64_64_k16"] = (16, 56, 56, 64, 64, 1, 1, 1, 0)
+SHAPES["l1_3x3_64_k16"] = (16, 56, 56, 64, 64, 3, 3, 1, 1)
+SHAPES["l2_3x3_128_k16"] = (16, 28, 28, 128, 128, 3, 3, 1, 1)
 SHAPES["l3_3x3_k1"] = (1, 14, 14, 256, 256, 3, 3, 1, 1)
 SHAPES["l1_1x1_576_k1"] = (1, 56, 56, 576, 64, 1, 1, 1, 0)
 
