@@ -41,6 +41,25 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "SLO-met requests/sec (p99<=SLO) for re-aligned ResNet-50 groups"
+# --config: the BASELINE.json configs served on the same path (model, fixture tag, metric, workload)
+CONFIGS = {
+    "resnet50": ("resnet50", None, METRIC,
+                 "resnet50 re-aligned fragment groups, {n} clients x {rps} rps per GPU, 8 cut points, plan from the "
+                 "reference planner on the measured B200 profile table, SM-share partitioning"),
+    "vgg16_churn": ("vgg16", "vgg16_churn_s2", "SLO-met requests/sec (p99<=SLO) for VGG-16 fragment groups under "
+                    "partition-point churn",
+                    "vgg16 fragment groups under network-trace-driven partition-point churn: {n} clients x {rps} rps "
+                    "per GPU on a fast/slow bandwidth trace (half out of phase), re-partitioned and re-planned by "
+                    "the reference every 2-s epoch, plan transitions served on the wall clock"),
+    "inception_v3": ("inception_v3", "inception_v3_s2_m0", "SLO-met requests/sec (p99<=SLO) for re-aligned "
+                     "Inception-v3 groups",
+                     "inception_v3 multi-branch re-aligned fragment groups (ragged gather across concat "
+                     "boundaries), {n} clients x {rps} rps per GPU, 8 cut points at the Mixed blocks"),
+    "bert_base": ("bert_base", "bert_base_s2_m0", "SLO-met requests/sec (p99<=SLO) for re-aligned BERT-base "
+                  "encoder groups, seq 128",
+                  "bert_base encoder fragments split at layer boundaries (cuts 0/3/6/9), seq 128, {n} clients x "
+                  "{rps} rps per GPU, shared-suffix GEMM batching"),
+}
 UNIT = "req/s"
 PCIE_GBS = 46.0  # measured H2D for 1 MB pinned copies on these hosts (scripts/probe_h2d_streams.py)
 
@@ -84,14 +103,25 @@ def _workload(name: str, clients: int | None):
     return json.loads(Path(files[-1]).read_text())
 
 
+def _plans(wl) -> list:
+    return [e["plan"] for e in wl["epochs"] if e["kind"] == "deploy"] if "epochs" in wl else [wl["plan"]]
+
+
 def _align_stages(wl) -> int:
-    return sum(1 for g in wl["plan"]["groups"] for lv in g["levels"] for a in lv["align"] if a["span"][0] != a["span"][1])
+    """Alignment stages of the plan (of the largest epoch plan for a churn fleet)."""
+    return max(sum(1 for g in pl["groups"] for lv in g["levels"] for a in lv["align"] if a["span"][0] != a["span"][1])
+               for pl in _plans(wl))
+
+
+def _plan_resource(wl) -> int:
+    return max(pl["total_resource"] for pl in _plans(wl))
 
 
 def _h2d_gbs(w) -> float:
     by_id = {c["client_id"]: c for c in w["clients"]}
-    return sum(by_id[cid]["rate_rps"] * by_id[cid]["payload_bytes"][f["start_layer"]]
-               for f in w["fragments"] for cid in f["clients"]) / 1e9
+    frs = [e["fragments"] for e in w["epochs"] if e["kind"] == "deploy"] if "epochs" in w else [w["fragments"]]
+    return max(sum(by_id[cid]["rate_rps"] * by_id[cid]["payload_bytes"][f["start_layer"]]
+                   for f in fr for cid in f["clients"]) for fr in frs) / 1e9
 
 
 def _p99(lats):
@@ -171,7 +201,7 @@ def run_ours(args):
     from paper_2312_10636_b200.device import context
     from paper_2312_10636_b200.engine import DeviceModel, StageInstance
     from paper_2312_10636_b200.models import build_chain
-    from paper_2312_10636_b200.plan import deploy
+    from paper_2312_10636_b200.plan import deploy, deploy_epochs
     from paper_2312_10636_b200.serving import ClientView, serve
 
     world, rank, local = _dist()
@@ -184,54 +214,94 @@ def run_ours(args):
 
     class Fleet:
         """One planned fleet made executable on this GPU: stage instances plus every client's own
-        fp32 entry activation (one seeded tensor per client, post-ReLU at inner boundaries)."""
+        fp32 entry activation (one seeded tensor per (client, cut point), post-ReLU at inner
+        boundaries).  A churn fleet (BASELINE configs[2]) carries one deployment per epoch, put in
+        place at that epoch's REPLAN (simulator.py:297-349); stages of every deployment stay alive
+        so requests drain on the stages they were routed to."""
 
         def __init__(self, wl, strict: bool = False):
             self.wl = wl
-            self.dep = deploy(wl["plan"], wl["fragments"])
+            if "epochs" in wl:
+                self.epochs = deploy_epochs(wl["epochs"])
+                self.deps = [d for d in self.epochs if d is not None and not isinstance(d, str)]
+            else:
+                self.epochs = None
+                self.deps = [deploy(wl["plan"], wl["fragments"])]
+            self.dep = self.deps[0]
+            self.stages = [s for d in self.deps for s in d.stages]
             self.clients = [ClientView.from_doc(c) for c in wl["clients"]]
-            budgets = ctx.sm_budgets([(s.share, s.instances) for s in self.dep.stages], work_conserving=not strict)
-            it = iter(budgets)
-            self.instances = [[StageInstance(dm, s.start, s.end, s.batch, next(it)) for _ in range(s.instances)]
-                              for s in self.dep.stages]
-            ids = sorted(c.client_id for c in self.clients if c.client_id in self.dep.routes)
-            sizes = [chain.ingress_elems(self.dep.routes[cid].point) for cid in ids]
+            self.instances = []
+            for d in self.deps:  # each deployment gets its planned shares on the whole GPU
+                it = iter(ctx.sm_budgets([(s.share, s.instances) for s in d.stages], work_conserving=not strict))
+                self.instances += [[StageInstance(dm, s.start, s.end, s.batch, next(it)) for _ in range(s.instances)]
+                                   for s in d.stages]
+            keys = sorted({(cid, r.point) for d in self.deps for cid, r in d.routes.items()})
+            sizes = [chain.ingress_elems(p) for _cid, p in keys]
+            pads = [-(-n // 16) * 16 for n in sizes]  # every client slice 64-byte aligned (16-byte vectors)
             g = torch.Generator(device="cuda").manual_seed(1234 + rank)
-            self.act = torch.randn(sum(sizes), device="cuda", generator=g)  # one slab, a slice per client
+            self.act = torch.randn(sum(pads), device="cuda", generator=g)  # one slab, a slice per client
             self.dev_in, self.slices, off = {}, {}, 0
-            for cid, n in zip(ids, sizes):
-                p = self.dep.routes[cid].point
-                if p > 0:
+            for key, n, npad in zip(keys, sizes, pads):
+                p = key[1]
+                if chain.boundary_shape(p)[3] == N.GX_I32:  # BERT boundary 0: token ids (int32 bits)
+                    self.act[off:off + n].view(torch.int32).random_(0, 30522, generator=g)
+                elif p > 0 and chain.relu_boundary(p):
                     self.act[off:off + n].clamp_(min=0)
-                self.slices[cid] = (off, n, p)
-                self.dev_in[cid] = (self.act.data_ptr() + off * 4, n * 4, chain.ingress_channels(p))
-                off += n
+                self.slices[key] = (off, n, p)
+                self.dev_in[key] = (self.act.data_ptr() + off * 4, n * 4, chain.ingress_channels(p))
+                off += npad
             self.host = None
             self.host_in = None
-            for s, insts in zip(self.dep.stages, self.instances):  # capture every (instance, k) graph
+            for s, insts in zip(self.stages, self.instances):  # capture every (instance, k) graph
                 for inst in insts:
                     for k in range(1, s.batch + 1):
                         inst.kernel_count(k)
             torch.cuda.synchronize()
+
+        def point_of(self, cid, gen_ms):
+            """The cut point a request generated at gen_ms was routed at (routes are chosen at
+            generation, simulator.py:353-366); None if ambiguous (generated at a REPLAN instant)."""
+            if self.epochs is None:
+                return self.dep.routes[cid].point
+            ep = self.wl["epoch_s"] * 1000.0
+            e = min(int(gen_ms // ep), len(self.epochs) - 1)
+            if abs(gen_ms - round(gen_ms / ep) * ep) < 1e-6:
+                return None
+            di = -1
+            for j in range(e + 1):
+                d = self.epochs[j]
+                if isinstance(d, str):
+                    di = -1
+                elif d is not None:
+                    di = sum(1 for x in self.epochs[:j] if x is not None and not isinstance(x, str))
+            r = self.deps[di].routes.get(cid) if di >= 0 else None
+            return r.point if r is not None else None
 
         def pin(self):
             if self.host is None:
                 self.host = torch.empty(self.act.numel(), dtype=torch.float32, pin_memory=True)
                 self.host.copy_(self.act.cpu())
                 base = self.host.data_ptr()
-                self.host_in = {cid: (base + off * 4, n * 4, self.dev_in[cid][2])
-                                for cid, (off, n, _p) in self.slices.items()}
+                self.host_in = {key: (base + off * 4, n * 4, self.dev_in[key][2])
+                                for key, (off, n, _p) in self.slices.items()}
             return self.host_in
 
-        def activation(self, cid):
-            off, n, p = self.slices[cid]
-            return self.act[off:off + n].cpu(), p
+        def activation(self, cid, p):
+            off, n, _p = self.slices[(cid, p)]
+            return self.act[off:off + n].cpu()
 
         def serve(self, horizon, host=False, drain=0.0, sample=0):
-            return serve(self.dep, self.clients, horizon, ctx=ctx, instances=self.instances,
+            extra = {} if self.epochs is None else {"epochs": self.epochs, "epoch_s": self.wl["epoch_s"]}
+            return serve(self.dep, self.clients, horizon, ctx=ctx, instances=self.instances, **extra,
                          ingress=self.pin() if host else self.dev_in,
                          ingress_from_host=(args.e2e_ingress if host else False), egress_to_host=host,
-                         max_inflight=args.max_inflight, drain_s=drain, sample_outputs=sample)
+                         max_inflight=self.max_inflight(), drain_s=drain, sample_outputs=sample)
+
+        def max_inflight(self):
+            """Device slots: at least --max-inflight, and 1.5x the requests an SLO's worth of
+            arrivals keeps in flight (a request finding no free slot is an admission drop)."""
+            rps = sum(c.rate_rps for c in self.clients)
+            return max(args.max_inflight, int(math.ceil(1.5 * rps * self.wl["slo_ms"] / 1000.0)))
 
     def all_ok(ok: bool) -> bool:
         if world > 1:
@@ -271,7 +341,8 @@ def run_ours(args):
         return {"met": met, "generated": len(timed), "dropped": dropped, "p99": _p99(lats),
                 "unfinished": sum(1 for r in timed if r[4] == "inflight"), "wall_ms": rep.wall_ms,
                 "device_ms": e0.elapsed_time(e1), "kernels": rep.kernels, "batches": rep.batches, "rep": rep,
-                "h2d": sum(ing[r[0]][1] for r in timed if r[4] != "dropped" and r[0] in ing) if host else 0,
+                "h2d": sum(ing[(c, fleet.point_of(c, g))][1] for c, g, _d, _dl, s in timed
+                           if s != "dropped" and (c, fleet.point_of(c, g)) in ing) if host else 0,
                 "d2h": sum(1 for r in timed if r[4] == "completed") * chain.boundary_elems(chain.n_units) * 4
                 if host else 0}
 
@@ -321,7 +392,7 @@ def run_ours(args):
         else:
             fleet = search(all_wl)
             fleet, res, _ = timed_search(fleet, all_wl, sample=sample)
-    wl, dep, instances = fleet.wl, fleet.dep, fleet.instances
+    wl, stages, instances = fleet.wl, fleet.stages, fleet.instances
     slo = wl["slo_ms"]
     log(f"# value: clients={wl['clients_n']} met/s={res['met'] / (K * window):.0f} p99={res['p99']:.1f} ms")
 
@@ -365,11 +436,11 @@ def run_ours(args):
     # (gx_stage_profile_ops), algorithmic FLOPs = 2*M*N*K unpadded per launch, peak = measured burst
     # bf16 x (stage SM budget / SMs) since the kernel is timed alone.
     def stage_flops(i):
-        s = dep.stages[i]
+        s = stages[i]
         return s.instances * s.batch * sum(chain.unit_flops[s.start:s.end])
 
-    busiest = max(range(len(dep.stages)), key=stage_flops)
-    st = dep.stages[busiest]
+    busiest = max(range(len(stages)), key=stage_flops)
+    st = stages[busiest]
     inst = instances[busiest][0]
     span_ms = inst.profile(st.batch, 20)
     ops = inst.profile_ops(st.batch, 10)
@@ -412,20 +483,18 @@ def run_ours(args):
             # timed run vs the fp32 CPU forward of their clients' activations
             cpu["output_check"] = output_check(args.model, res["rep"], fleet)
         line = {
-            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
-            "ms_per_step": round(window * 1000.0, 3), "higher_is_better": True, "scaling": "weak",
+            "metric": args.metric, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": W, "ms_per_step": round(window * 1000.0, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded random-init weights, a distinct seeded "
                                                           "fp32 activation per client)",
-            "config": {"workload": f"{args.model} re-aligned fragment groups, {wl['clients_n']} clients x "
-                                   f"{wl['rate_rps']:.0f} rps per GPU, 8 cut points, plan from the reference planner "
-                                   f"on the measured B200 profile table, SM-share partitioning",
+            "config": {"workload": args.workload.format(n=wl["clients_n"], rps=f"{wl['rate_rps']:.0f}"),
                        "model": args.model, "latency_scale": wl.get("latency_scale", 1.0),
                        "merge_threshold": wl.get("merge_threshold", 0.2), "align_stages": _align_stages(wl),
                        "clients_per_gpu": wl["clients_n"], "offered_rps_per_gpu":
                            wl["clients_n"] * wl["rate_rps"], "slo_ms": round(slo, 3), "window_s": window,
-                       "drain_s": args.drain, "stages": len(dep.stages),
-                       "instances": sum(s.instances for s in dep.stages),
-                       "plan_resource": wl["plan"]["total_resource"], "parallelism": f"replica-per-gpu x{world}",
+                       "drain_s": args.drain, "stages": len(stages),
+                       "instances": sum(s.instances for s in stages),
+                       "plan_resource": _plan_resource(wl), "parallelism": f"replica-per-gpu x{world}",
                        "sm_budgets": "work-conserving (planned share is a floor)",
                        "l2": "per-client activations in HBM (2+ GB > L2), weights L2-resident per stage"},
             "p99_ms": round(p99, 3), "p99_ok": p99 <= slo, "generated": int(stats[1].item()),
@@ -549,7 +618,7 @@ def run_placed(args):
         n_inst = collections_counter(s for g in chosen["plan"]["groups"] for lv in g["levels"]
                                      for st in [lv["shared"], *lv["align"]] for s in (st["gpu"] or []))
         value = res["met"] / (K * window)
-        line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+        line = {"metric": args.metric, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
                 "ms_per_step": window * 1000.0, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "bf16", "data": "synthetic (seeded random-init weights, a distinct activation per client)",
                 "config": {"workload": f"{args.model} re-aligned fragment groups, ONE {chosen['clients_n']}-client "
@@ -584,7 +653,7 @@ def output_check(model, rep, fleet, tol=2e-2):
     from paper_2312_10636_b200.models import build_chain, torch_model
 
     if rep.sampled is None or len(rep.sampled[0]) == 0:
-        return {"checked": 0}
+        return {"checked": 0, "sampled": 0}
     t0 = time.time()
     torch.set_num_threads(os.cpu_count() or 1)
     m = torch_model(model)
@@ -592,22 +661,26 @@ def output_check(model, rep, fleet, tol=2e-2):
     ch = build_chain(model, module=m)
     idx, outs = rep.sampled
     cids = [rep.requests[i][0] for i in idx]
+    points = [fleet.point_of(rep.requests[i][0], rep.requests[i][1]) for i in idx]
     by_point = {}
-    for j, cid in enumerate(cids):
-        by_point.setdefault(fleet.dep.routes[cid].point, []).append(j)
+    for j, (cid, p) in enumerate(zip(cids, points)):
+        if p is not None:
+            by_point.setdefault(p, []).append(j)
+    classifier = model != "bert_base"  # BERT's final output is the hidden state: no top-1
     rels, agree, decisive = [], 0, 0
     for p, js in by_point.items():
         for b0 in range(0, len(js), 16):
             part = js[b0:b0 + 16]
             xs = []
             for j in part:
-                a, _ = fleet.activation(cids[j])
-                if p == 0:
-                    H, W, _C, _ = ch.boundary_shape(0)
+                a = fleet.activation(cids[j], p)
+                H, W, Cc, _ = ch.boundary_shape(p)
+                if not classifier:
+                    xs.append(a.view(torch.int32).view(1, H) if p == 0 else a.view(1, H, Cc))
+                elif p == 0:
                     f = ch.tensor_s2d.get(ch.boundary[0], 1)
                     xs.append(a.view(1, H * f, W * f, ch.input_channels))
                 else:
-                    H, W, Cc, _ = ch.boundary_shape(p)
                     xs.append(a.view(1, H, W, Cc))
             ref = run_span(units, p, ch.n_units, nhwc_to_nchw(torch.cat(xs)))
             for r, j in zip(ref, part):
@@ -615,9 +688,11 @@ def output_check(model, rep, fleet, tol=2e-2):
                 r = r.reshape(-1)
                 rels.append(((got - r).norm() / r.norm()).item())
                 top2 = r.topk(2).values
-                if (top2[0] - top2[1]) > 0.02 * (r.max() - r.min()):
+                if classifier and (top2[0] - top2[1]) > 0.02 * (r.max() - r.min()):
                     decisive += 1
                     agree += int(int(got.argmax()) == int(r.argmax()))
+    if not rels:
+        return {"checked": 0, "sampled": len(idx), "unresolved_points": sum(1 for p in points if p is None)}
     return {"checked": len(rels), "distinct_clients": len(set(cids)), "cut_points": sorted(by_point),
             "max_rel_l2": round(max(rels), 6), "median_rel_l2": round(sorted(rels)[len(rels) // 2], 6),
             "top1_decisive": decisive, "top1_agree": agree, "tolerance": tol,
@@ -645,6 +720,9 @@ def reference_cpu_path(wl, repeats=3):
     where = _ref_import()
     if where is None:
         return {"unavailable": "reference not installed (baseline/_ref) and source tree absent"}
+    if "epochs" in wl:
+        return {"unavailable": "churn fleets are re-planned per epoch by the reference's own loop "
+                               "(scripts/make_config_fleets.py); timed on the static fleets only"}
     import logging
 
     import fragserve
@@ -719,7 +797,7 @@ def reference_cpu_path(wl, repeats=3):
             "note": "the reference executes no DNN: simulate() prices each batch with the cost table"}
 
 
-def cpu_serving_rate(model, budget_s=40.0, horizon_s=3.0):
+def cpu_serving_rate(model, budget_s=40.0, horizon_s=3.0, tag=None):
     """The CPU restatement of the execution step as a steady-state rate: the
     reference's batching (oracle event loop, pinned bit-exact to the reference) with every
     dispatched batch executed for real — fp32 torch forward of the span on all host cores, one
@@ -738,8 +816,9 @@ def cpu_serving_rate(model, budget_s=40.0, horizon_s=3.0):
     m = torch_model(model)
     units = units_for(model, m)
     chain = build_chain(model, module=m)
-    wl = _workloads(model)[0]
-    dep = deploy(wl["plan"], wl["fragments"])
+    wl = (_workloads(tag) if tag else _workloads(model) or _workloads(model, all_plans=True))[0]
+    first = next(e for e in wl["epochs"] if e["kind"] == "deploy") if "epochs" in wl else wl
+    dep = deploy(first["plan"], first["fragments"])
     # clients in descending id order: the cut mix cycles from the cheapest suffix (cut 17) down to
     # the full model (cut 0), so every prefix is the most favourable fleet of its size for the CPU
     allc = sorted((ClientView.from_doc(c) for c in wl["clients"]), key=lambda c: c.client_id, reverse=True)
@@ -748,7 +827,9 @@ def cpu_serving_rate(model, budget_s=40.0, horizon_s=3.0):
     def x_for(a, k):
         if (a, k) not in inputs:
             H, W, Cc, _ = chain.boundary_shape(a)
-            if a == 0:
+            if model == "bert_base":
+                inputs[(a, k)] = torch.randint(0, 30522, (k, H)) if a == 0 else torch.randn(k, H, Cc)
+            elif a == 0:
                 f = chain.tensor_s2d.get(chain.boundary[0], 1)
                 inputs[(a, k)] = torch.randn(k, chain.input_channels, H * f, W * f)
             else:
@@ -791,7 +872,7 @@ def cpu_serving_rate(model, budget_s=40.0, horizon_s=3.0):
     return {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
             "host": _lscpu(),
             "sample": (f"{best['clients'] if best else 0} clients of the {wl['clients_n']}-client fleet "
-                       f"(its cut cycle {wl['cuts']} from the cheapest cut down, 30 rps each), {horizon_s:.0f} s of arrivals per size, every "
+                       f"(its cut cycle {wl.get('cuts', 'of epoch 0')} from the cheapest cut down, {wl['rate_rps']:.0f} rps each), {horizon_s:.0f} s of arrivals per size, every "
                        f"dispatched batch run as fp32 torch on {os.cpu_count()} threads (no interpolation)"),
             "search": tried,
             "cpu_exec_img_per_s": round(exec_imgs / exec_s, 2) if exec_s else None,
@@ -801,7 +882,7 @@ def cpu_serving_rate(model, budget_s=40.0, horizon_s=3.0):
 def cpu_paths(args, budget_s=40.0):
     """Both CPU legs: the steady-state CPU serving rate (the baseline value) and the reference's
     own planner / simulator timings on the headline fleet."""
-    out = cpu_serving_rate(args.model, budget_s=budget_s)
+    out = cpu_serving_rate(args.model, budget_s=budget_s, tag=args.plans)
     head = [w for w in _workloads(args.plans or args.model, all_plans=True)]
     try:
         out["reference_path"] = reference_cpu_path(head[-1] if head else _workloads(args.model)[-1])
@@ -818,7 +899,7 @@ def run_reference(args):
     vals = []
     cpu = None
     for _ in range(max(1, args.steps)):
-        cpu = cpu_serving_rate(args.model, budget_s=max(20.0, 150.0 / max(1, args.steps)))
+        cpu = cpu_serving_rate(args.model, budget_s=max(20.0, 150.0 / max(1, args.steps)), tag=args.plans)
         vals.append(cpu["value"])
     value = sum(vals) / len(vals)
     head = _workloads(args.plans or args.model, all_plans=True)
@@ -826,7 +907,7 @@ def run_reference(args):
         cpu["reference_path"] = reference_cpu_path(head[-1])
     except Exception as e:  # noqa: BLE001
         cpu["reference_path"] = {"error": f"{type(e).__name__}: {e}"}
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+    line = {"impl": "reference", "metric": args.metric, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": args.window * 1000.0, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{args.model} re-aligned fragment groups (the workload's cut mix), CPU path",
@@ -844,7 +925,10 @@ def main():
     ap.add_argument("--window", type=float, default=1.0, help="seconds of arrivals per step")
     ap.add_argument("--drain", type=float, default=0.5, help="seconds served after the last window (no new arrivals)")
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--model", default="resnet50")
+    ap.add_argument("--config", choices=tuple(CONFIGS), default="resnet50",
+                    help="BASELINE.json config: resnet50 (configs[1], the headline), vgg16_churn (configs[2]), "
+                         "inception_v3 (configs[3]), bert_base (configs[4])")
+    ap.add_argument("--model", default=None, help="override the config's model")
     ap.add_argument("--plans", default=None,
                     help="workload fixture tag (default: the model; e.g. resnet50_s1.5 = plans made against the "
                          "profile table scaled by the served/profiled latency ratio)")
@@ -860,6 +944,9 @@ def main():
                     help="N > 1: an independent fleet per GPU (default), or one fleet planned and placed across "
                          "the N GPUs (run_placed)")
     args = ap.parse_args()
+    model, tag, args.metric, args.workload = CONFIGS[args.config]
+    args.model = args.model or model
+    args.plans = args.plans or tag
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":

@@ -31,8 +31,10 @@ extern "C" {
 #endif
 
 /* v2: stages carry their element type (fp32 execution mode), gx_stage_run_async runs on a caller
- * stream and records a caller event, gx_serve_cfg.result_rows sizes the output ring. */
-#define GX_ABI_VERSION 2
+ * stream and records a caller event, gx_serve_cfg.result_rows sizes the output ring.
+ * v3: on-device top-1 (K9: gx_stage_run_top1, gx_serve_cfg.top1, gx_serve_top1_for); GX_I32 token
+ *     ids and the GX_OP_EMBED op (K8: BERT fragments entering at boundary 0). */
+#define GX_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define GX_API __attribute__((visibility("default")))
@@ -50,6 +52,7 @@ extern "C" {
 /* element types */
 #define GX_BF16 0
 #define GX_F32 1
+#define GX_I32 2 /* token ids (the input of a K8 embedding; BERT boundary 0) */
 
 /* op kinds of a unit chain (one ModelSpec layer = one unit = a run of ops) */
 #define GX_OP_CONV 1     /* implicit-GEMM conv, NHWC, folded BN bias, opt. residual add + ReLU  */
@@ -77,7 +80,7 @@ extern "C" {
 /* Per-sample tensor shape. Conv nets: NHWC (H, W, C). Sequences: (S, 1, hidden). */
 typedef struct gx_tensor {
   int32_t H, W, C;
-  int32_t dtype; /* GX_BF16 or GX_F32 */
+  int32_t dtype; /* GX_BF16 or GX_F32 (GX_I32: token ids, the input of an EMBED op) */
   int32_t s2d;   /* >1: this (boundary) tensor is the space-to-depth(s2d) form of an [H*s2d, W*s2d, c]
                     client image; the gather performs the rearrangement (stride-2 stems)          */
 } gx_tensor;
@@ -88,7 +91,9 @@ typedef struct gx_tensor {
  *   FC            : bf16 [N][K]
  *   bias          : fp32 [Cout]
  *   LAYERNORM     : fp32 gamma[C], beta[C] (w_off = gamma, b_off = beta)
- *   EMBED         : bf16 word[V][C], pos[P][C], type[2][C] at w_off, w2_off, w3_off */
+ *   EMBED         : (K8) in = GX_I32 token ids [S,1,1], out = [S,1,C] in the chain's type;
+ *                   word[V][C], pos[P][C], type[2][C] in the chain's type at w_off, w2_off, w3_off,
+ *                   LayerNorm fp32 gamma[C], beta[C] at b_off, b_off + 4C; Cin = V, R = P, eps */
 typedef struct gx_op {
   int32_t kind;
   int32_t in, in2, out; /* in2: residual (CONV/LINEAR), mask/aux otherwise */
@@ -160,6 +165,13 @@ GX_API int gx_stage_run(gx_stage* st, int k, const void* const* src, const int32
  * event.  Intermediate outputs (dst_dtype) are in the stage's dtype; logits GX_F32.              */
 GX_API int gx_stage_run_async(gx_stage* st, void* stream, int k, const void* const* src, const int32_t* src_dtype,
                               int32_t src_channels, void* const* dst, int32_t dst_dtype, void* done_event);
+
+/* gx_stage_run_async for a stage ending at the chain output of a classifier, with K9 fused into
+ * the scatter: top1[i] (device or mapped host int32) receives the argmax of request i's logits
+ * (first maximal index, torch.argmax's rule); dst may be NULL (top-1 only, no logits written)
+ * or hold per-request fp32 logit rows as in gx_stage_run.  GX_EINVAL for a non-fp32 output.      */
+GX_API int gx_stage_run_top1(gx_stage* st, void* stream, int k, const void* const* src, const int32_t* src_dtype,
+                             int32_t src_channels, void* const* dst, int32_t* const* top1, void* done_event);
 
 /* Execution mode of a stage: GX_EXEC_GRAPH (default; one CUDA graph per k of per-op persistent
  * kernels with programmatic dependent launch) or GX_EXEC_SPAN (one persistent span kernel with
@@ -287,7 +299,12 @@ typedef struct gx_serve_cfg {
   double drain_ms;        /* WALL: after the horizon (no new requests) keep serving the requests
                              already generated for up to this long, so tails near the horizon are
                              measured; 0 = stop at the horizon like the reference                */
+  int32_t top1;           /* GX_TOP1_*: the final stage's scatter also writes each request's
+                             argmax (classifier chains; K9), into a ring like the logits          */
+  int32_t reserved2;
 } gx_serve_cfg;
+
+enum { GX_TOP1_NONE = 0, GX_TOP1_WITH_LOGITS = 1, GX_TOP1_ONLY = 2 /* no logits kept: egress is 4 B/request */ };
 
 typedef struct gx_serve gx_serve;
 
@@ -319,6 +336,10 @@ GX_API int gx_serve_outputs(gx_serve* s, float* out, int64_t n_requests, int64_t
  * filled.  Lets a long serving run spot-check its most recent result_rows completions. */
 GX_API int gx_serve_outputs_for(gx_serve* s, int64_t n, const int64_t* req, float* out, int64_t elems,
                                 int64_t* held);
+/* Top-1 class of selected requests (K9, GX_TOP1_* serving): out[i] = argmax of request req[i]'s
+ * logits (first maximal index, torch.argmax's rule), -1 when it did not complete or its ring row
+ * was reused; *held = entries filled. */
+GX_API int gx_serve_top1_for(gx_serve* s, int64_t n, const int64_t* req, int32_t* out, int64_t* held);
 GX_API int gx_serve_destroy(gx_serve* s);
 
 #ifdef __cplusplus

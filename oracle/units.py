@@ -43,14 +43,22 @@ def inception_units(m) -> list:
 
 def bert_units(m) -> list:
     """Unit u = encoder layer u on [k, S, hidden] (transformers BertLayer, no attention mask:
-    the reference's profiled BERT runs full 128-token sequences)."""
+    the reference's profiled BERT runs full 128-token sequences); unit 0 starts
+    from the token ids [k, S] through BertEmbeddings (token types 0, positions 0..S-1)."""
     out = []
-    for layer in m.encoder.layer:
-        def f(x, layer=layer):
+    for i, layer in enumerate(m.encoder.layer):
+        def f(x, layer=layer, first=i == 0):
+            if first:
+                x = m.embeddings(input_ids=x.long())
             r = layer(x)
             return r[0] if isinstance(r, tuple) else r
         out.append(f)
     return out
+
+
+def bert_token_ids(n: int, seed: int, vocab: int = 30522, seq: int = 128) -> torch.Tensor:
+    """A BERT client's input at boundary 0: token ids randint(0, 30522, (n, 128)) (SURVEY §8 inputs)."""
+    return torch.randint(0, vocab, (n, seq), generator=torch.Generator().manual_seed(seed), dtype=torch.int32)
 
 
 def units_for(name: str, m) -> list:

@@ -12,15 +12,16 @@ from pathlib import Path
 from .errors import raise_for_status
 
 LIB_PATH = Path(__file__).resolve().parent / "_gx.so"
-ABI_VERSION = 2
+ABI_VERSION = 3
 
-GX_BF16, GX_F32 = 0, 1
+GX_BF16, GX_F32, GX_I32 = 0, 1, 2
 (GX_OP_CONV, GX_OP_MAXPOOL, GX_OP_AVGPOOL, GX_OP_GAP, GX_OP_FC, GX_OP_LINEAR, GX_OP_LAYERNORM,
  GX_OP_ATTENTION, GX_OP_EMBED, GX_OP_COPY, GX_OP_FLATTEN_NCHW) = range(1, 12)
 GX_ACT_NONE, GX_ACT_RELU, GX_ACT_GELU = 0, 1, 2
 GX_OPF_COUNT_INCLUDE_PAD, GX_OPF_NO_HALO, GX_OPF_FC_SIMT = 1, 2, 4
 GX_CLOCK_VIRTUAL, GX_CLOCK_WALL, GX_CLOCK_REPLAY = 0, 1, 2
 GX_EXEC_GRAPH, GX_EXEC_SPAN = 0, 1
+GX_TOP1_NONE, GX_TOP1_WITH_LOGITS, GX_TOP1_ONLY = 0, 1, 2
 
 
 class GxTensor(C.Structure):
@@ -76,7 +77,7 @@ class GxServeCfg(C.Structure):
                 ("record_dispatch", C.c_int32), ("ingress_from_host", C.c_int32),
                 ("egress_to_host", C.c_int32), ("slot_bytes", C.c_int64),
                 ("max_inflight", C.c_int32), ("warmup_requests_skip", C.c_int32), ("result_rows", C.c_int64),
-                ("drain_ms", C.c_double)]
+                ("drain_ms", C.c_double), ("top1", C.c_int32), ("reserved2", C.c_int32)]
 
 
 _lib = None
@@ -106,6 +107,7 @@ def lib():
         "gx_model_dtype": (i32, [vp, P(i32)]),
         "gx_stage_create": (i32, [vp, C.c_int, C.c_int, C.c_int, C.c_int, i32, vp, P(vp)]),
         "gx_stage_run_async": (i32, [vp, vp, C.c_int, P(vp), P(i32), i32, P(vp), i32, vp]),
+        "gx_stage_run_top1": (i32, [vp, vp, C.c_int, P(vp), P(i32), i32, P(vp), P(vp), vp]),
         "gx_stage_set_exec": (i32, [vp, i32]),
         "gx_stage_destroy": (i32, [vp]),
         "gx_stage_stream": (i32, [vp, P(vp)]),
@@ -131,6 +133,7 @@ def lib():
         "gx_serve_destroy": (i32, [vp]),
         "gx_serve_outputs": (i32, [vp, P(C.c_float), i64, i64]),
         "gx_serve_outputs_for": (i32, [vp, i64, P(i64), P(C.c_float), i64, P(i64)]),
+        "gx_serve_top1_for": (i32, [vp, i64, P(i64), P(i32), P(i64)]),
     }
     for name, (res, args) in sig.items():
         if not hasattr(L, name):

@@ -185,7 +185,7 @@ bool encode_tmap_halo_bf16(CUtensorMap* map, const void* base, int C, int W, int
 }
 
 // ---------------------------------------------------------------- op planning
-int elem_size(int dtype) { return dtype == GX_F32 ? 4 : 2; }
+int elem_size(int dtype) { return dtype == GX_BF16 ? 2 : 4; }  // GX_F32, GX_I32: 4 bytes
 int64_t tensor_elems(const gx_tensor& t) { return static_cast<int64_t>(t.H) * t.W * t.C; }
 
 static int pick_bn(int Cout, int m_tiles, int sm_budget, int cap) {
@@ -432,6 +432,10 @@ void op_work(const gx_op& op, const gx_tensor* T, int k, double* flops, double* 
       f = 8.0 * in_px * ti.C;
       b = in_px * ti.C * (es_in + es_out) + ti.C * 8.0;
       break;
+    case GX_OP_EMBED:  // ids in; three table rows per token; LayerNorm (~8 flops per element)
+      f = 10.0 * out_px * to.C;
+      b = in_px * 4.0 + out_px * to.C * (3.0 * es_out + es_out) + to.C * 8.0;
+      break;
     case GX_OP_ATTENTION: {
       const double S = ti.H, D = to.C;  // D = heads * head_dim
       f = 4.0 * k * S * S * D;
@@ -522,6 +526,19 @@ int launch_op_f32(const gx_op& op, const gx_tensor* T, void* const* ptrs, const 
 int launch_op(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint8_t* wbase, int k, int sm_budget,
               cudaStream_t s, bool pdl, const ConvLaunch* pre, int* kernels) {
   const int bw_grid = std::max(1, sm_budget) * 8;
+  if (op.kind == GX_OP_EMBED) {
+    // K8: token ids (int32 [S]) -> LayerNorm(word[id] + pos[s] + type[0]) in the chain's type
+    const gx_tensor& ti = T[op.in];
+    const gx_tensor& to = T[op.out];
+    if (ti.dtype != GX_I32 || ti.C != 1 || ti.W != 1 || to.H != ti.H || to.W != 1 || ti.H > op.R)
+      return fail(GX_EINVAL, "embed: int32 ids [S,1,1] -> [S,1,C] with S <= max positions");
+    GX_CUDA(launch_embed(static_cast<const int32_t*>(ptrs[op.in]), k * ti.H, ti.H, to.C, wbase + op.w_off, op.Cin,
+                         wbase + op.w2_off, wbase + op.w3_off, reinterpret_cast<const float*>(wbase + op.b_off),
+                         reinterpret_cast<const float*>(wbase + op.b_off) + to.C, op.eps, ptrs[op.out],
+                         to.dtype == GX_F32, bw_grid, s));
+    if (kernels) ++*kernels;
+    return GX_OK;
+  }
   if (T[op.in].dtype == GX_F32) {
     const int rc = launch_op_f32(op, T, ptrs, wbase, k, sm_budget, s);
     if (rc == GX_OK && kernels) ++*kernels;

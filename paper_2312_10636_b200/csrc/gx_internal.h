@@ -108,6 +108,12 @@ cudaError_t launch_gather_s2d(int k, const void* const* src, const int32_t* src_
                               int c_src, int c_dst, __nv_bfloat16* dst, int grid, cudaStream_t s);
 cudaError_t launch_scatter(int k, const void* src, int src_dtype, int64_t row_elems, void* const* dst,
                            int dst_dtype, int grid, cudaStream_t s);
+cudaError_t launch_gather_words(int k, const void* const* src, int64_t words, uint32_t* dst, int grid,
+                                cudaStream_t s);
+// K1 scatter of fp32 chain outputs fused with K9 top-1 (argmax, first maximal index) per row;
+// dst may be null (or hold null rows): top-1 only
+cudaError_t launch_scatter_top1(int k, const float* src, int64_t row_elems, void* const* dst, int32_t* const* top1,
+                                cudaStream_t s);
 cudaError_t launch_pool(int mode, const __nv_bfloat16* x, int N, int H, int W, int C, int x_ld,
                         __nv_bfloat16* y, int Ho, int Wo, int y_ld, int y_coff, int R, int S, int sh,
                         int sw, int ph, int pw, int count_include_pad, int grid, cudaStream_t s);
@@ -119,14 +125,16 @@ cudaError_t launch_copy_channels(const __nv_bfloat16* x, int64_t pixels, int C, 
                                  __nv_bfloat16* y, int y_ld, int y_coff, int grid, cudaStream_t s);
 cudaError_t launch_flatten_nchw(const __nv_bfloat16* x, int N, int HW, int C, __nv_bfloat16* y, int grid,
                                 cudaStream_t s);
+// K8 BERT embeddings + LayerNorm: ids int32 [rows], token s = row % S; tables in bf16 (f32 = 0)
+// or fp32 (f32 = 1), output in the same type
+cudaError_t launch_embed(const int32_t* ids, int rows, int S, int C, const void* word, int V, const void* pos,
+                         const void* type0, const float* gamma, const float* beta, float eps, void* y, int f32,
+                         int grid, cudaStream_t s);
 cudaError_t launch_layernorm(const __nv_bfloat16* x, const __nv_bfloat16* res, int rows, int C,
                              const float* gamma, const float* beta, float eps, __nv_bfloat16* y, int grid,
                              cudaStream_t s);
 cudaError_t launch_attention(const __nv_bfloat16* qkv, int N, int S, int heads, int dh,
                              __nv_bfloat16* out, int grid, cudaStream_t s);
-cudaError_t launch_embed(const void* ids, int N, int S, int C, const __nv_bfloat16* word,
-                         const __nv_bfloat16* pos, const __nv_bfloat16* type, __nv_bfloat16* y,
-                         int grid, cudaStream_t s);
 
 // ------------------------------------------------------------------ fp32 execution mode (kernels_f32.cu)
 struct ConvF32Args {

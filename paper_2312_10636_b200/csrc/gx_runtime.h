@@ -116,6 +116,8 @@ struct gx_stage {
 
 namespace gx {
 // gx_stage_run on an explicit stream (gx_stage.cu); used by the serving loop's stream pool.
+// top1 (optional): per-row int32 destinations of the output's argmax (K9, fp32 chain outputs
+// only); dst may then be null (top-1 only, no logits written).
 int stage_run_on(gx_stage* st, cudaStream_t stream, int k, const void* const* src, const int32_t* src_dtype,
-                 int32_t src_channels, void* const* dst, int32_t dst_dtype);
+                 int32_t src_channels, void* const* dst, int32_t dst_dtype, int32_t* const* top1 = nullptr);
 }  // namespace gx

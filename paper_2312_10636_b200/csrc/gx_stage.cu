@@ -334,11 +334,29 @@ int gx_model_create(gx_ctx* ctx, const char* model_id, int n_tensors, const gx_t
   }
   // one compute element type per chain (the boundary-0 tensor's); only the chain output may differ
   // (fp32 logits of a bf16 chain)
-  const int32_t mdt = tensors[boundary[0]].dtype;
+  // (fp32 logits of a bf16 chain) and the int32 token ids a K8 embedding reads
+  std::vector<char> ids_tensor(n_tensors, 0);
+  int32_t mdt = -1;
+  for (int i = 0; i < n_ops; ++i)
+    if (ops[i].kind == GX_OP_EMBED) {
+      ids_tensor[ops[i].in] = 1;
+      if (ops[i].in == boundary[0]) mdt = tensors[ops[i].out].dtype;
+      if ((ops[i].w2_off >= 0 && static_cast<size_t>(ops[i].w2_off) >= blob_bytes) ||
+          (ops[i].w3_off >= 0 && static_cast<size_t>(ops[i].w3_off) >= blob_bytes) || ops[i].w_off < 0 ||
+          ops[i].w2_off < 0 || ops[i].w3_off < 0 || ops[i].b_off < 0 || ops[i].Cin < 1 || ops[i].R < 1)
+        return fail(GX_EINVAL, "op " + std::to_string(i) + ": embed needs word/pos/type tables, LayerNorm "
+                               "parameters, the vocabulary size (Cin) and max positions (R)");
+    }
+  if (mdt < 0) mdt = tensors[boundary[0]].dtype;
   if (mdt != GX_BF16 && mdt != GX_F32) return fail(GX_EINVAL, "tensor dtype must be GX_BF16 or GX_F32");
-  for (int t = 0; t < n_tensors; ++t)
+  for (int t = 0; t < n_tensors; ++t) {
+    if (ids_tensor[t]) {
+      if (tensors[t].dtype != GX_I32) return fail(GX_EINVAL, "embed input must be GX_I32 token ids");
+      continue;
+    }
     if (tensors[t].dtype != mdt && !(t == boundary[n_units] && tensors[t].dtype == GX_F32))
       return fail(GX_EINVAL, "tensor " + std::to_string(t) + " mixes element types within one chain");
+  }
   GX_CUDA(cudaSetDevice(ctx->device));
   gx_model* m = new gx_model();
   m->dtype = mdt;
@@ -509,26 +527,50 @@ int gx_stage_run_async(gx_stage* st, void* stream, int k, const void* const* src
   return GX_OK;
 }
 
+int gx_stage_run_top1(gx_stage* st, void* stream, int k, const void* const* src, const int32_t* src_dtype,
+                      int32_t src_channels, void* const* dst, int32_t* const* top1, void* done_event) {
+  if (!st || !src || !src_dtype || !top1) return fail(GX_EINVAL, "null arg");
+  if (k < 1 || k > st->max_batch) return fail(GX_EINVAL, "batch k outside 1..max_batch");
+  if (int rc = bind_device(st->m->ctx->device)) return rc;
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : st->stream;
+  if (int rc = gx::stage_run_on(st, s, k, src, src_dtype, src_channels, dst, GX_F32, top1)) return rc;
+  if (done_event) GX_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(done_event), s));
+  return GX_OK;
+}
+
 }  // extern "C"
 
 namespace gx {
 // The body of gx_stage_run on an explicit stream: the serving loop runs batches of any instance on
 // a pooled stream (an instance never has two batches in flight, so its workspace is never shared).
 int stage_run_on(gx_stage* st, cudaStream_t stream, int k, const void* const* src, const int32_t* src_dtype,
-                 int32_t src_channels, void* const* dst, int32_t dst_dtype) {
+                 int32_t src_channels, void* const* dst, int32_t dst_dtype, int32_t* const* top1) {
   gx_model* m = st->m;
   if (k < 1 || k > st->max_batch) return fail(GX_EINVAL, "batch k outside 1..max_batch");
   const gx_tensor& tin = m->tensors[st->in_tid];
   const gx_tensor& tout = m->tensors[st->out_tid];
   const int c_src = src_channels > 0 ? src_channels : tin.C;
   if (c_src > tin.C) return fail(GX_EINVAL, "source has more channels than the boundary tensor");
+  if (top1 && (tout.dtype != GX_F32 || (dst && dst_dtype != GX_F32)))
+    return fail(GX_EINVAL, "top-1 needs the fp32 chain output (logits)");
+  for (int i = 0; i < k; ++i) {
+    const void* d = dst ? dst[i] : nullptr;
+    if (!src[i] || (!d && !top1) || ((reinterpret_cast<uintptr_t>(src[i]) | reinterpret_cast<uintptr_t>(d)) & 15u))
+      return fail(GX_EINVAL, "batch row " + std::to_string(i) + ": null or not 16-byte aligned source/destination");
+    if (top1 && !top1[i]) return fail(GX_EINVAL, "batch row " + std::to_string(i) + ": null top-1 destination");
+  }
   gx_stage::PerK* pk = nullptr;
   int rc = stage_graph(st, k, &pk);
   if (rc != GX_OK) return rc;
   const int bw_grid = st->sm_budget * 8;
   if (tin.s2d > 1 && src_channels <= 0)
     return fail(GX_EINVAL, "space-to-depth boundary needs the client's channel count");
-  if (tin.dtype == GX_F32) {  // fp32 chain: the batch is assembled in fp32
+  if (tin.dtype == GX_I32) {  // token ids (K8 embedding input): a plain 4-byte word gather
+    for (int i = 0; i < k; ++i)
+      if (src_dtype[i] != GX_I32) return fail(GX_EINVAL, "a token-id boundary takes GX_I32 sources");
+    GX_CUDA(launch_gather_words(k, src, tensor_elems(tin), static_cast<uint32_t*>(st->tptr[st->in_tid]), bw_grid,
+                                stream));
+  } else if (tin.dtype == GX_F32) {  // fp32 chain: the batch is assembled in fp32
     float* bt = static_cast<float*>(st->tptr[st->in_tid]);
     if (tin.s2d > 1)
       GX_CUDA(launch_gather_s2d_f32(k, src, src_dtype, tin.H, tin.W, tin.s2d, src_channels, tin.C, bt, bw_grid,
@@ -557,8 +599,12 @@ int stage_run_on(gx_stage* st, cudaStream_t stream, int k, const void* const* sr
   } else {
     GX_CUDA(cudaGraphLaunch(pk->exec, stream));
   }
-  GX_CUDA(launch_scatter(k, st->tptr[st->out_tid], tout.dtype, tensor_elems(tout), dst, dst_dtype, bw_grid,
-                         stream));
+  if (top1)
+    GX_CUDA(launch_scatter_top1(k, static_cast<const float*>(st->tptr[st->out_tid]), tensor_elems(tout), dst, top1,
+                                stream));
+  else
+    GX_CUDA(launch_scatter(k, st->tptr[st->out_tid], tout.dtype, tensor_elems(tout), dst, dst_dtype, bw_grid,
+                           stream));
   return GX_OK;
 }
 }  // namespace gx
@@ -621,7 +667,7 @@ int gx_stage_profile(gx_stage* st, int k, int iters, float* ms_out) {
     GX_CUDA(cudaMalloc(&st->prof_dst, out_bytes * st->max_batch));
   }
   std::vector<const void*> src(k);
-  std::vector<int32_t> dt(k, GX_F32);
+  std::vector<int32_t> dt(k, tin.dtype == GX_I32 ? GX_I32 : GX_F32);
   std::vector<void*> dst(k);
   for (int i = 0; i < k; ++i) {
     src[i] = static_cast<uint8_t*>(st->prof_src) + i * in_bytes;

@@ -66,6 +66,93 @@ __global__ void layernorm_kernel(const __nv_bfloat16* __restrict__ x, int rows, 
   }
 }
 
+// K8: BERT embeddings for fragments entering at boundary 0 (BertEmbeddings: word[id] + pos[s] +
+// type[0], then LayerNorm).  One warp per token row; the row's C values stay in registers between
+// the mean, variance and normalise passes (C % 256 == 0, C <= 1024; 8 elements per lane-vector).
+// Tables are in the chain's element type T (bf16 or fp32), sums and LayerNorm in fp32.  Token ids
+// outside [0, V) are clamped (torch raises; the executor never reads outside the table).
+__device__ __forceinline__ void load8(const __nv_bfloat16* p, float* v) {
+  const uint4 q = __ldg(reinterpret_cast<const uint4*>(p));
+  const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 f = unpack_bf16x2(w[j]);
+    v[2 * j] = f.x;
+    v[2 * j + 1] = f.y;
+  }
+}
+__device__ __forceinline__ void load8(const float* p, float* v) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(p)), b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+  v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w, v[4] = b.x, v[5] = b.y, v[6] = b.z, v[7] = b.w;
+}
+__device__ __forceinline__ void store8(__nv_bfloat16* p, const float* o) {
+  uint4 q;
+  q.x = pack_bf16x2(o[0], o[1]);
+  q.y = pack_bf16x2(o[2], o[3]);
+  q.z = pack_bf16x2(o[4], o[5]);
+  q.w = pack_bf16x2(o[6], o[7]);
+  *reinterpret_cast<uint4*>(p) = q;
+}
+__device__ __forceinline__ void store8(float* p, const float* o) {
+  reinterpret_cast<float4*>(p)[0] = make_float4(o[0], o[1], o[2], o[3]);
+  reinterpret_cast<float4*>(p)[1] = make_float4(o[4], o[5], o[6], o[7]);
+}
+
+template <typename T, int VPL>
+__global__ void embed_ln_kernel(const int32_t* __restrict__ ids, int rows, int S, int C, const T* __restrict__ word,
+                                int V, const T* __restrict__ pos, const T* __restrict__ type0,
+                                const float* __restrict__ g, const float* __restrict__ b, float eps,
+                                T* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
+    const int id = min(max(__ldg(ids + r), 0), V - 1);
+    const int sp = r % S;
+    const T* wr = word + static_cast<int64_t>(id) * C;
+    const T* pr = pos + static_cast<int64_t>(sp) * C;
+    float v[VPL * 8];
+    float s = 0.0f;
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const int c0 = (lane + 32 * i) * 8;
+      float a[8], p8[8], t8[8];
+      load8(wr + c0, a);
+      load8(pr + c0, p8);
+      load8(type0 + c0, t8);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        v[8 * i + j] = a[j] + t8[j] + p8[j];  // torch: (inputs_embeds + token_type) + position
+        s += v[8 * i + j];
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    const float mean = s / C;
+    float ss = 0.0f;
+#pragma unroll
+    for (int i = 0; i < VPL * 8; ++i) {
+      const float d = v[i] - mean;
+      ss += d * d;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+    const float inv = rsqrtf(ss / C + eps);
+    T* yr = y + static_cast<int64_t>(r) * C;
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const int c0 = (lane + 32 * i) * 8;
+      const float4 g0 = __ldg(reinterpret_cast<const float4*>(g + c0)), g1 = __ldg(reinterpret_cast<const float4*>(g + c0 + 4));
+      const float4 b0 = __ldg(reinterpret_cast<const float4*>(b + c0)), b1 = __ldg(reinterpret_cast<const float4*>(b + c0 + 4));
+      const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+      const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+      float o[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = (v[8 * i + j] - mean) * inv * gg[j] + bb[j];
+      store8(yr + c0, o);
+    }
+  }
+}
+
 __device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
       "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
@@ -207,6 +294,35 @@ __global__ void __launch_bounds__(128) attention_kernel(const __nv_bfloat16* __r
 }
 
 }  // namespace
+
+template <typename T>
+static cudaError_t launch_embed_t(const int32_t* ids, int rows, int S, int C, const T* word, int V, const T* pos,
+                                  const T* type0, const float* gamma, const float* beta, float eps, T* y, int grid,
+                                  cudaStream_t s) {
+  if (C % 256 != 0 || C > 1024 || V < 1 || S < 1) return cudaErrorInvalidValue;
+  const int wpb = 8;
+  int blocks = (rows + wpb - 1) / wpb;
+  if (blocks > grid) blocks = grid;
+  if (blocks < 1) blocks = 1;
+  switch (C / 256) {
+    case 1: embed_ln_kernel<T, 1><<<blocks, 32 * wpb, 0, s>>>(ids, rows, S, C, word, V, pos, type0, gamma, beta, eps, y); break;
+    case 2: embed_ln_kernel<T, 2><<<blocks, 32 * wpb, 0, s>>>(ids, rows, S, C, word, V, pos, type0, gamma, beta, eps, y); break;
+    case 3: embed_ln_kernel<T, 3><<<blocks, 32 * wpb, 0, s>>>(ids, rows, S, C, word, V, pos, type0, gamma, beta, eps, y); break;
+    default: embed_ln_kernel<T, 4><<<blocks, 32 * wpb, 0, s>>>(ids, rows, S, C, word, V, pos, type0, gamma, beta, eps, y); break;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_embed(const int32_t* ids, int rows, int S, int C, const void* word, int V, const void* pos,
+                         const void* type0, const float* gamma, const float* beta, float eps, void* y, int f32,
+                         int grid, cudaStream_t s) {
+  if (f32)
+    return launch_embed_t<float>(ids, rows, S, C, static_cast<const float*>(word), V, static_cast<const float*>(pos),
+                                 static_cast<const float*>(type0), gamma, beta, eps, static_cast<float*>(y), grid, s);
+  return launch_embed_t<__nv_bfloat16>(ids, rows, S, C, static_cast<const __nv_bfloat16*>(word), V,
+                                       static_cast<const __nv_bfloat16*>(pos), static_cast<const __nv_bfloat16*>(type0),
+                                       gamma, beta, eps, static_cast<__nv_bfloat16*>(y), grid, s);
+}
 
 cudaError_t launch_layernorm(const __nv_bfloat16* x, const __nv_bfloat16* res, int rows, int C, const float* gamma,
                              const float* beta, float eps, __nv_bfloat16* y, int grid, cudaStream_t s) {

@@ -143,6 +143,16 @@ __global__ void gather_kernel(RowPtrs src, int k, int64_t pixels, int c_src, int
   }
 }
 
+// K1 gather of 4-byte words (token ids at a K8 embedding boundary): k rows of `words` each.
+__global__ void gather_words_kernel(RowPtrs src, int k, int64_t words, uint32_t* __restrict__ dst) {
+  const int64_t total = words * k;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(i / words);
+    dst[i] = __ldg(static_cast<const uint32_t*>(src.p[r]) + (i - r * words));
+  }
+}
+
 // K1 scatter: batch rows -> per-request destinations (bf16 activations or fp32 logits).
 __global__ void scatter_kernel(const void* __restrict__ src, int src_f32, int k, int64_t row_elems, RowDst dst,
                                int dst_f32) {
@@ -193,6 +203,69 @@ __global__ void scatter_kernel(const void* __restrict__ src, int src_f32, int k,
     } else {
       reinterpret_cast<uint4*>(dst.p[r])[v] = val;
     }
+  }
+}
+
+// K1 scatter of the chain output fused with K9 (head / top-1): one block per request row of fp32
+// logits; the row is copied to dst[r] (when non-null) while the block reduces (value, index) to the
+// first maximal index (torch.argmax's tie rule), written to top1[r].
+struct RowTop1 {
+  int32_t* p[kMaxRows];
+};
+__global__ void __launch_bounds__(256) scatter_top1_kernel(const float* __restrict__ src, int64_t row_elems,
+                                                           RowDst dst, RowTop1 top1) {
+  __shared__ float sv[8];
+  __shared__ int si[8];
+  const int r = blockIdx.x;
+  const float* row = src + static_cast<int64_t>(r) * row_elems;
+  float* out = static_cast<float*>(dst.p[r]);
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  const int64_t nv = row_elems / 4;
+  for (int64_t v = threadIdx.x; v < nv; v += blockDim.x) {
+    const float4 x = __ldg(reinterpret_cast<const float4*>(row) + v);
+    if (out) reinterpret_cast<float4*>(out)[v] = x;
+    const float e[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int idx = static_cast<int>(4 * v + j);
+      if (e[j] > best || (e[j] == best && idx < bi)) {
+        best = e[j];
+        bi = idx;
+      }
+    }
+  }
+  for (int64_t i = nv * 4 + threadIdx.x; i < row_elems; i += blockDim.x) {  // row_elems % 4 tail
+    const float e = row[i];
+    if (out) out[i] = e;
+    if (e > best || (e == best && static_cast<int>(i) < bi)) {
+      best = e;
+      bi = static_cast<int>(i);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) {
+      best = ov;
+      bi = oi;
+    }
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    sv[warp] = best;
+    si[warp] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
+      if (sv[w] > best || (sv[w] == best && si[w] < bi)) {
+        best = sv[w];
+        bi = si[w];
+      }
+    // a row of NaNs (no value compares greater than -inf) reports index 0
+    *top1.p[r] = bi == 0x7fffffff ? 0 : bi;
   }
 }
 
@@ -633,6 +706,15 @@ cudaError_t launch_gather_s2d(int k, const void* const* src, const int32_t* src_
   return cudaGetLastError();
 }
 
+cudaError_t launch_gather_words(int k, const void* const* src, int64_t words, uint32_t* dst, int grid,
+                                cudaStream_t s) {
+  if (k > kMaxRows) return cudaErrorInvalidValue;
+  RowPtrs rp;
+  for (int i = 0; i < k; ++i) rp.p[i] = src[i];
+  gather_words_kernel<<<grid_for(words * k, 256, grid), 256, 0, s>>>(rp, k, words, dst);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_scatter(int k, const void* src, int src_dtype, int64_t row_elems, void* const* dst,
                            int dst_dtype, int grid, cudaStream_t s) {
   if (k > kMaxRows || (row_elems & 7)) return cudaErrorInvalidValue;
@@ -640,6 +722,20 @@ cudaError_t launch_scatter(int k, const void* src, int src_dtype, int64_t row_el
   for (int i = 0; i < k; ++i) rd.p[i] = dst[i];
   scatter_kernel<<<grid_for(row_elems / 8 * k, 256, grid), 256, 0, s>>>(src, src_dtype == GX_F32, k, row_elems, rd,
                                                                      dst_dtype == GX_F32);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter_top1(int k, const float* src, int64_t row_elems, void* const* dst, int32_t* const* top1,
+                                cudaStream_t s) {
+  if (k > kMaxRows || (row_elems & 3) || (reinterpret_cast<uintptr_t>(src) & 15)) return cudaErrorInvalidValue;
+  RowDst rd;
+  RowTop1 rt;
+  for (int i = 0; i < k; ++i) {
+    rd.p[i] = dst ? dst[i] : nullptr;
+    rt.p[i] = top1[i];
+    if (!rt.p[i]) return cudaErrorInvalidValue;
+  }
+  scatter_top1_kernel<<<k, 256, 0, s>>>(src, row_elems, rd, rt);
   return cudaGetLastError();
 }
 

@@ -165,6 +165,7 @@ struct gx_serve {
   std::vector<int> free_batches;
   std::vector<int> inflight;  // batch ids in flight (WALL)
   void* results = nullptr;  // fp32 outputs ring (context device) or mapped pinned host
+  int32_t* top1s = nullptr;  // GX_TOP1_*: int32 argmax ring, same rows and memory kind as `results`
   int64_t result_elems = 0;
   int64_t result_cursor = 0;
   double wall_ms = 0.0;
@@ -361,6 +362,7 @@ int gx_serve::dispatch_gpu(int si, int bi) {
   const void* src[64];
   int32_t sdt[64];
   void* dst[64];
+  int32_t* t1[64];
   int channels = 0;
   // an idle lane if there is one, else the lane with the fewest / oldest batches in flight
   int lane = 0;
@@ -381,7 +383,9 @@ int gx_serve::dispatch_gpu(int si, int bi) {
     if (r.loc != d && r.slot >= 0) ++remote_gathers;
     if (st.out_final) {
       r.result_seq = result_cursor++;
-      dst[i] = static_cast<uint8_t*>(results) + (r.result_seq % cfg.result_rows) * result_elems * 4;
+      const int64_t row = r.result_seq % cfg.result_rows;
+      dst[i] = results ? static_cast<uint8_t*>(results) + row * result_elems * 4 : nullptr;
+      t1[i] = top1s ? top1s + row : nullptr;
     } else {
       // the output goes to a slot on this GPU: the request's own if it is here, else a fresh one
       // (the old one is read by this batch's gather and freed when the batch completes); with no
@@ -401,7 +405,9 @@ int gx_serve::dispatch_gpu(int si, int bi) {
   dr.pool_n[lane] += 1;
   dr.pool_last[lane] = b.t_disp;
   const int out_dt = st.out_final ? GX_F32 : g->m->tensors[g->out_tid].dtype;
-  int rc = gx::stage_run_on(g, sm, k, src, sdt, channels, dst, out_dt);
+  const bool with_top1 = st.out_final && top1s;
+  int rc = gx::stage_run_on(g, sm, k, src, sdt, channels, (st.out_final && !results) ? nullptr : dst, out_dt,
+                            with_top1 ? t1 : nullptr);
   if (rc != GX_OK) return rc;
   int kc = 0;
   gx_stage_kernel_count(g, k, &kc);
@@ -717,12 +723,21 @@ int create_gpu_resources(gx_serve* s) {
   s->result_elems = relems;
   GX_CUDA(cudaSetDevice(s->gpus[0]));
   s->cur_device = s->gpus[0];
-  if (relems > 0) {
+  if (relems > 0 && cfg.top1 != GX_TOP1_ONLY) {
     const size_t bytes = static_cast<size_t>(relems) * 4 * cfg.result_rows;
     if (cfg.egress_to_host)
       GX_CUDA(cudaHostAlloc(&s->results, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
     else
       GX_CUDA(cudaMalloc(&s->results, bytes));
+  }
+  if (relems > 0 && cfg.top1 != GX_TOP1_NONE) {
+    void* p = nullptr;
+    const size_t bytes = static_cast<size_t>(cfg.result_rows) * 4;
+    if (cfg.egress_to_host)
+      GX_CUDA(cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+    else
+      GX_CUDA(cudaMalloc(&p, bytes));
+    s->top1s = static_cast<int32_t*>(p);
   }
   return GX_OK;
 }
@@ -806,6 +821,11 @@ int gx_serve_create(gx_ctx* ctx, int n_stages, const gx_serve_stage* st, int n_r
         delete s;
         return fail(GX_EINVAL, "route references a bad stage");
       }
+    if (r.ingress && (reinterpret_cast<uintptr_t>(r.ingress) & 15u)) {
+      // the gather and the DMA copy move 16-byte vectors: every ingress row starts 16-byte aligned
+      delete s;
+      return fail(GX_EINVAL, "route ingress pointer is not 16-byte aligned");
+    }
     if (r.n_stages > 0) {
       // where the request's activation is when it arrives: DMA ingress lands on the first stage's
       // instance-0 GPU; device-resident ingress lives where it was allocated
@@ -874,6 +894,16 @@ int gx_serve_create(gx_ctx* ctx, int n_stages, const gx_serve_stage* st, int n_r
                                  " bytes a route needs (ingress copy or intermediate boundary)");
     }
     if (s->cfg.result_rows <= 0) s->cfg.result_rows = cfg->max_inflight;
+    if (cfg->top1 < GX_TOP1_NONE || cfg->top1 > GX_TOP1_ONLY) {
+      delete s;
+      return fail(GX_EINVAL, "top1 must be GX_TOP1_NONE, GX_TOP1_WITH_LOGITS or GX_TOP1_ONLY");
+    }
+    if (cfg->top1 != GX_TOP1_NONE)
+      for (const Stage& x : s->stages)
+        if (x.out_final && !x.inst.empty() && x.inst[0]->m->tensors[x.inst[0]->out_tid].dtype != GX_F32) {
+          delete s;
+          return fail(GX_EINVAL, "top-1 needs a classifier chain (fp32 logits as the chain output)");
+        }
     if (int rc = create_gpu_resources(s)) {
       gx_serve_destroy(s);
       return rc;
@@ -954,9 +984,34 @@ int gx_serve_outputs(gx_serve* s, float* out, int64_t n_requests, int64_t elems)
   return gx_serve_outputs_for(s, static_cast<int64_t>(all.size()), all.data(), out, elems, &held);
 }
 
+int gx_serve_top1_for(gx_serve* s, int64_t n, const int64_t* req, int32_t* out, int64_t* held) {
+  if (!s || (n > 0 && (!req || !out))) return fail(GX_EINVAL, "null arg");
+  if (!s->gpu()) return fail(GX_EINVAL, "outputs exist only when batches execute on the GPU");
+  if (!s->top1s) return fail(GX_EINVAL, "serving ran without top-1 (gx_serve_cfg.top1 = GX_TOP1_NONE)");
+  for (int g : s->gpus) {
+    GX_CUDA(cudaSetDevice(g));
+    GX_CUDA(cudaDeviceSynchronize());
+  }
+  GX_CUDA(cudaSetDevice(s->gpus[0]));
+  s->cur_device = s->gpus[0];
+  std::vector<int32_t> ring(static_cast<size_t>(s->cfg.result_rows));
+  GX_CUDA(cudaMemcpy(ring.data(), s->top1s, ring.size() * 4, cudaMemcpyDefault));
+  int64_t got = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t ri = req[i];
+    const bool ok = ri >= 0 && ri < static_cast<int64_t>(s->reqs.size()) && s->reqs[ri].status == 0 &&
+                    s->reqs[ri].result_seq >= 0 && s->reqs[ri].result_seq >= s->result_cursor - s->cfg.result_rows;
+    out[i] = ok ? ring[s->reqs[ri].result_seq % s->cfg.result_rows] : -1;
+    got += ok;
+  }
+  if (held) *held = got;
+  return GX_OK;
+}
+
 int gx_serve_outputs_for(gx_serve* s, int64_t n, const int64_t* req, float* out, int64_t elems, int64_t* held) {
   if (!s || (n > 0 && (!req || !out))) return fail(GX_EINVAL, "null arg");
   if (!s->gpu()) return fail(GX_EINVAL, "outputs exist only when batches execute on the GPU");
+  if (!s->results) return fail(GX_EINVAL, "serving kept no logits (gx_serve_cfg.top1 = GX_TOP1_ONLY)");
   if (elems != s->result_elems) return fail(GX_EINVAL, "output row size mismatch");
   for (int g : s->gpus) {
     GX_CUDA(cudaSetDevice(g));
@@ -995,11 +1050,12 @@ int gx_serve_destroy(gx_serve* s) {
       if (r.slots) cudaFree(r.slots);
     }
     if (!s->gpus.empty()) cudaSetDevice(s->gpus[0]);
-    if (s->results) {
+    for (void* p : {s->results, static_cast<void*>(s->top1s)}) {
+      if (!p) continue;
       if (s->cfg.egress_to_host)
-        cudaFreeHost(s->results);
+        cudaFreeHost(p);
       else
-        cudaFree(s->results);
+        cudaFree(p);
     }
   }
   delete s;

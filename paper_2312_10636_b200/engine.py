@@ -53,6 +53,12 @@ class DeviceModel:
             self.handle = None
 
 
+def _gx_dtype(t: torch.Tensor) -> int:
+    """Element type of a request's entry tensor: fp32 client ingress, bf16 from an alignment
+    stage, int32 token ids (BERT boundary 0)."""
+    return {torch.float32: N.GX_F32, torch.bfloat16: N.GX_BF16, torch.int32: N.GX_I32}[t.dtype]
+
+
 def placed_instances(dep, models: dict, work_conserving: bool = True) -> list:
     """Executor instances of a deployment placed across the GPUs of one box: instance i of stage s
     runs on GPU s.gpus[i] (the plan's placement, placement.py:24-70; None = GPU 0).  `models` maps
@@ -121,12 +127,32 @@ class StageInstance:
         outs = [torch.empty(self.out_elems, dtype=out_dtype, device=dev) for _ in range(k)]
         cur = torch.cuda.current_stream(dev)
         self.stream.wait_stream(cur)
-        self.run_ptrs(k, [t.data_ptr() for t in inputs],
-                      [N.GX_F32 if t.dtype == torch.float32 else N.GX_BF16 for t in inputs],
+        self.run_ptrs(k, [t.data_ptr() for t in inputs], [_gx_dtype(t) for t in inputs],
                       [o.data_ptr() for o in outs], N.GX_F32 if out_dtype == torch.float32 else N.GX_BF16,
                       src_channels)
         cur.wait_stream(self.stream)
         return outs
+
+    def run_top1(self, inputs: list[torch.Tensor], logits: bool = True, src_channels: int = 0):
+        """Execute one batch of a classifier's final stage with the top-1 (K9) fused into the
+        scatter: returns (per-request fp32 logits or None, int32 [k] argmax on the device)."""
+        k = len(inputs)
+        if not self.final:
+            raise ValidationError("top-1 is computed by the stage that ends at the chain output")
+        if not 1 <= k <= self.max_batch:
+            raise ValidationError(f"batch {k} outside 1..{self.max_batch}")
+        dev = torch.device("cuda", self.model.device)
+        outs = [torch.empty(self.out_elems, dtype=torch.float32, device=dev) for _ in range(k)] if logits else None
+        top1 = torch.full((k,), -1, dtype=torch.int32, device=dev)
+        cur = torch.cuda.current_stream(dev)
+        self.stream.wait_stream(cur)
+        N.check(N.lib().gx_stage_run_top1(self.handle, None, k, N.ptr_array([t.data_ptr() for t in inputs]),
+                                          N.i32_array([_gx_dtype(t) for t in inputs]), src_channels,
+                                          N.ptr_array([o.data_ptr() for o in outs]) if logits else None,
+                                          N.ptr_array([top1.data_ptr() + 4 * i for i in range(k)]), None),
+                "gx_stage_run_top1")
+        cur.wait_stream(self.stream)
+        return outs, top1
 
     def profile(self, k: int, iters: int = 20) -> float:
         ms = C.c_float()

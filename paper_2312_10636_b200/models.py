@@ -61,6 +61,11 @@ class UnitChain:
         f = self.tensor_s2d.get(self.boundary[p], 1)
         return H * f * W * f * self.ingress_channels(p)
 
+    def relu_boundary(self, p: int) -> bool:
+        """Whether activations at inner boundary p are non-negative (CNN boundaries follow a ReLU /
+        pool of ReLU outputs; BERT's hidden state is a LayerNorm output)."""
+        return p > 0 and self.model_id != "bert_base"
+
     def payload_bytes(self, p: int) -> int:
         """fp32 wire bytes at boundary p (what ModelSpec.output_bytes records)."""
         return self.ingress_elems(p) * 4

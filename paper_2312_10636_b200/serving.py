@@ -158,7 +158,7 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
           egress_to_host: bool = False, slot_bytes: int = 0, max_inflight: int = 4096,
           planner: str | None = None, plan_latency=None, return_outputs: bool = False,
           epochs: list | None = None, result_rows: int = 0, sample_outputs: int = 0,
-          drain_s: float = 0.0) -> ServeReport:
+          drain_s: float = 0.0, top1: int = 0) -> ServeReport:
     """Run one plan for one horizon.
 
     latency: callable (StageSpec, k) -> ms for the virtual clock (None -> wall clock).
@@ -175,6 +175,8 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
     sample_outputs: keep the logits of up to this many completed requests still held in the ring
     (the most recent completions, distinct clients first) as report.sampled = (request indices,
     [n, elems] fp32) — output spot-checks of long serving runs.
+    top1: GX_TOP1_* (0 none, 1 logits + top-1, 2 top-1 only): the final stage's scatter also writes
+    each request's argmax (K9, classifier chains); report.top1 = int32 per request (-1: none).
     plan_latency: optional (StageSpec, k) -> ms the plan assumed; on the wall clock it is only
     compared with the observed batch times in the GX_SERVE_DEBUG summary.
     epochs: plan transitions under churn, one entry per epoch (Deployment / None = keep /
@@ -246,7 +248,11 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
             rt.worst_rem_ms = r.worst_rem_ms
             rt.mobile_ms = c.mobile_ms[r.point]
             rt.payload_bytes = c.payload_bytes[r.point]
-            rt.ingress_dtype = N.GX_F32
+            rt.ingress_dtype = N.GX_F32  # the client wire format (fp32), token ids at a BERT boundary 0
+            if gpu and r.stages:
+                ch = instances[offset[di] + r.stages[0]][0].model.chain
+                if ch.boundary_shape(r.point)[3] == N.GX_I32:
+                    rt.ingress_dtype = N.GX_I32
             if ingress is not None:
                 key = (cid, r.point) if (cid, r.point) in ingress else cid if cid in ingress else r.point
                 ptr, nbytes, channels = ingress[key]
@@ -285,6 +291,7 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
     cfg.max_inflight = max_inflight
     cfg.result_rows = result_rows
     cfg.drain_ms = drain_s * 1000.0 if wall else 0.0
+    cfg.top1 = int(top1)
     L = N.lib()
     h = C.c_void_p()
     ctx_handle = ctx.handle if ctx is not None else C.c_void_p(0)
@@ -311,8 +318,15 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
         nb = C.c_int64()
         nk = C.c_int64()
         N.check(L.gx_serve_stats(h, C.byref(wall_ms), C.byref(nb), C.byref(nk)))
+        top1_out = None
+        if top1 and gpu:
+            top1_out = np.full(n, -1, np.int32)
+            held = C.c_int64()
+            allreq = np.arange(n, dtype=np.int64)
+            N.check(L.gx_serve_top1_for(h, n, allreq.ctypes.data_as(C.POINTER(C.c_int64)), P(top1_out, C.c_int32),
+                                        C.byref(held)), "gx_serve_top1_for")
         outputs = None
-        if return_outputs and gpu:
+        if return_outputs and gpu and top1 != N.GX_TOP1_ONLY:
             final = [x for x in (instances or []) if x and x[0].final]
             elems = final[0][0].out_elems if final else 0
             outputs = np.zeros((max(1, n), max(1, elems)), np.float32)
@@ -320,7 +334,7 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
                 N.check(L.gx_serve_outputs(h, outputs.ctypes.data_as(C.POINTER(C.c_float)), outputs.shape[0], elems),
                         "gx_serve_outputs")
         sampled = None
-        if sample_outputs and gpu:
+        if sample_outputs and gpu and top1 != N.GX_TOP1_ONLY:
             final = [x for x in (instances or []) if x and x[0].final]
             elems = final[0][0].out_elems if final else 0
             comp = np.nonzero(status == 0)[0]
@@ -369,6 +383,7 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
     rep.placement = placement
     rep.outputs = outputs
     rep.sampled = sampled
+    rep.top1 = top1_out
     rep.wall_ms, rep.batches, rep.kernels = float(wall_ms.value), int(nb.value), int(nk.value)
     return rep
 

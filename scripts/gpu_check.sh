@@ -1,0 +1,17 @@
+# One GPU pass: the -m gpu suite, smoke, the bench line of each BASELINE config, and an ncu --set full
+# capture of the headline's busiest-stage conv launches (profiles/ncu_conv_summary.json).
+# Usage (GPU box): TAG=c4 bash scripts/gpu_check.sh
+TAG=${TAG:-run}
+O=gpurun_out
+timeout 1500 python -m pytest tests -m gpu -x -q > $O/${TAG}_gputest.log 2>&1; echo "pytest rc=$?" >> $O/${TAG}_gputest.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/${TAG}_smoke.log 2>&1
+for c in ${CONFIGS:-bert_base inception_v3 vgg16_churn}; do
+  timeout 900 python bench.py --config $c --no-variants > $O/${TAG}_bench_$c.log 2>&1; echo "rc=$?" >> $O/${TAG}_bench_$c.log
+done
+if [ -n "$NCU" ]; then
+  IFS=: read A B K BUD <<< "$NCU"
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:'conv_(tc|halo)_kernel' -c 60 \
+    -o $O/${TAG}_stage_conv python scripts/ncu_stage.py resnet50 $A $B $K $BUD > $O/${TAG}_ncu_stage.log 2>&1
+  python scripts/ncu_conv_summary.py $O/${TAG}_stage_conv.ncu-rep resnet50:$A:$B:$K:$BUD >> $O/${TAG}_ncu_stage.log 2>&1
+  cp profiles/ncu_conv_summary.json $O/${TAG}_ncu_conv_summary.json
+fi

@@ -20,7 +20,7 @@ def test_library_exports_every_declared_symbol():
     lib = C.CDLL(str(N.LIB_PATH))
     missing = [n for n in names if not hasattr(lib, n)]
     assert not missing, missing
-    assert N.lib().gx_abi_version() == N.ABI_VERSION == 2
+    assert N.lib().gx_abi_version() == N.ABI_VERSION == 3
 
 
 def test_struct_layouts_match_c(tmp_path):

@@ -153,7 +153,8 @@ def _inputs(name, n, seed):
     from oracle.units import nchw_to_nhwc
     g = torch.Generator().manual_seed(seed)
     if name == "bert_base":
-        x = torch.randn(n, 128, 768, generator=g)
+        from oracle.units import bert_token_ids
+        x = bert_token_ids(n, seed)
         return x, [x[i].contiguous().cuda() for i in range(n)]
     x = torch.randn(n, 3, RES[name], RES[name], generator=g)
     return x, [nchw_to_nhwc(x[i:i + 1])[0].contiguous().cuda() for i in range(n)]
@@ -226,7 +227,7 @@ def test_replay_realigned_group_f32(case):
     """The reference's re-aligned plan and dispatch (tests/golden/serving), every batch executed in
     fp32: records / dispatch bit-exact with the reference, every completed request's output within
     1e-3 of the fp32 CPU forward of its client's input and the same top-1."""
-    from oracle.units import nchw_to_nhwc, run_span, units_for
+    from oracle.units import bert_token_ids, nchw_to_nhwc, run_span, units_for
     from paper_2312_10636_b200.device import context
     from paper_2312_10636_b200.engine import StageInstance
     from paper_2312_10636_b200.plan import deploy
@@ -244,7 +245,8 @@ def test_replay_realigned_group_f32(case):
     ingress, expected, keep = {}, {}, []
     for ci, c in enumerate(sorted(clients, key=lambda c: c.client_id)):
         p = dep.routes[c.client_id].point
-        x = torch.randn(1, *shape, generator=torch.Generator().manual_seed(100 + ci))
+        x = (bert_token_ids(1, 100 + ci) if name == "bert_base"
+             else torch.randn(1, *shape, generator=torch.Generator().manual_seed(100 + ci)))
         act = nchw_to_nhwc(run_span(units, 0, p, x))[0].contiguous().cuda()
         keep.append(act)
         ingress[c.client_id] = (act.data_ptr(), act.numel() * 4, chain.ingress_channels(p))

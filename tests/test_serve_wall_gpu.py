@@ -147,3 +147,57 @@ def test_wall_clock_serving_outputs_match_oracle(ingress):
         else:
             first[c] = i
     del keep
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_wall_clock_serving_top1_on_device(mode):
+    """K9: the final stage's scatter writes each request's argmax (first maximal index) next to the
+    logits (mode 1: equal to argmax of the logits the ring holds) or instead of them (mode 2:
+    4 bytes of egress per request, the same classes)."""
+    from paper_2312_10636_b200.serving import serve
+
+    dep, clients, ctx, instances, dev_in, host_in, expected, keep = _setup()
+    rep = serve(dep, clients, 0.3, ctx=ctx, instances=instances, ingress=host_in, ingress_from_host="dma",
+                egress_to_host=True, max_inflight=4096, result_rows=16384, return_outputs=True, drain_s=0.5,
+                top1=mode)
+    ok = np.array([r[4] == "completed" for r in rep.requests])
+    assert ok.sum() > 500 and rep.top1 is not None
+    assert (rep.top1[~ok] == -1).all() and (rep.top1[ok] >= 0).all() and (rep.top1[ok] < 1000).all()
+    ids = [r[0] for r in rep.requests]
+    ref = torch.stack([expected[ids[i]] for i in np.nonzero(ok)[0]])
+    top2 = ref.topk(2, dim=1).values
+    decisive = ((top2[:, 0] - top2[:, 1]) > 0.02 * (ref.max(1).values - ref.min(1).values)).numpy()
+    assert (rep.top1[ok][decisive] == ref.argmax(1).numpy()[decisive]).all()
+    if mode == 1:
+        out = torch.from_numpy(rep.outputs[ok])
+        assert (out.argmax(1).numpy() == rep.top1[ok]).all()
+    else:
+        assert rep.outputs is None
+    del keep
+
+
+def test_stage_top1_entry_matches_logits_argmax():
+    """gx_stage_run_top1 on a final stage: top-1 equals torch.argmax of the logits the same call
+    writes, the logits are bit-identical to gx_stage_run's, and logits=None still yields the
+    classes; a non-final stage is rejected."""
+    from paper_2312_10636_b200.device import context
+    from paper_2312_10636_b200.engine import DeviceModel, StageInstance
+    from paper_2312_10636_b200.errors import ValidationError
+    from paper_2312_10636_b200.models import build_chain
+
+    chain = build_chain("resnet18")
+    dm = DeviceModel(chain, 0)
+    st = StageInstance(dm, 6, chain.n_units, max_batch=8, sm_budget=8)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    xs = [torch.randn(chain.boundary_elems(6), device="cuda", generator=g).clamp_min(0) for _ in range(7)]
+    logits = st.run(xs)
+    outs, top1 = st.run_top1(xs)
+    _, top1_only = st.run_top1(xs, logits=False)
+    torch.cuda.synchronize()
+    L = torch.stack(logits)
+    assert torch.equal(torch.stack(outs), L)
+    assert torch.equal(top1.long().cpu(), L.argmax(1).cpu())
+    assert torch.equal(top1_only, top1)
+    with pytest.raises(ValidationError):
+        StageInstance(dm, 2, 6, max_batch=2, sm_budget=4).run_top1(xs[:1])
+    del context
