@@ -260,13 +260,12 @@ def run_ours(args):
 
         def point_of(self, cid, gen_ms):
             """The cut point a request generated at gen_ms was routed at (routes are chosen at
-            generation, simulator.py:353-366); None if ambiguous (generated at a REPLAN instant)."""
+            generation, simulator.py:353-366; a REPLAN at the same instant fires first, rank 0 <
+            _R_GEN, simulator.py:40), None if it had no route."""
             if self.epochs is None:
                 return self.dep.routes[cid].point
             ep = self.wl["epoch_s"] * 1000.0
             e = min(int(gen_ms // ep), len(self.epochs) - 1)
-            if abs(gen_ms - round(gen_ms / ep) * ep) < 1e-6:
-                return None
             di = -1
             for j in range(e + 1):
                 d = self.epochs[j]
@@ -668,6 +667,7 @@ def output_check(model, rep, fleet, tol=2e-2):
             by_point.setdefault(p, []).append(j)
     classifier = model != "bert_base"  # BERT's final output is the hidden state: no top-1
     rels, agree, decisive = [], 0, 0
+    units_bf16, relaxed, passed = None, [], []
     for p, js in by_point.items():
         for b0 in range(0, len(js), 16):
             part = js[b0:b0 + 16]
@@ -682,21 +682,40 @@ def output_check(model, rep, fleet, tol=2e-2):
                     xs.append(a.view(1, H * f, W * f, ch.input_channels))
                 else:
                     xs.append(a.view(1, H, W, Cc))
-            ref = run_span(units, p, ch.n_units, nhwc_to_nchw(torch.cat(xs)))
-            for r, j in zip(ref, part):
+            xin = nhwc_to_nchw(torch.cat(xs))
+            ref = run_span(units, p, ch.n_units, xin)
+            for jj, (r, j) in enumerate(zip(ref, part)):
                 got = torch.from_numpy(outs[j])
                 r = r.reshape(-1)
-                rels.append(((got - r).norm() / r.norm()).item())
+                rel = ((got - r).norm() / r.norm()).item()
+                within = rel <= tol
+                if model == "inception_v3" and rel > tol:
+                    # random-init Inception-v3 amplifies bf16 rounding ~20x (test_models_gpu.py): the
+                    # bound is 1.25x the framework's own bf16 error on the same suffix and input
+                    if units_bf16 is None:
+                        import copy
+                        units_bf16 = units_for(model, copy.deepcopy(m).to(torch.bfloat16))
+                    fb = run_span(units_bf16, p, ch.n_units, xin[jj:jj + 1].to(torch.bfloat16)).float().reshape(-1)
+                    bound = 1.25 * ((fb - r).norm() / r.norm()).item()
+                    relaxed.append((rel, bound))
+                    within = rel <= bound
+                rels.append(rel)
+                passed.append(within)
                 top2 = r.topk(2).values
                 if classifier and (top2[0] - top2[1]) > 0.02 * (r.max() - r.min()):
                     decisive += 1
                     agree += int(int(got.argmax()) == int(r.argmax()))
     if not rels:
-        return {"checked": 0, "sampled": len(idx), "unresolved_points": sum(1 for p in points if p is None)}
+        return {"checked": 0, "sampled": len(idx), "unresolved_points": sum(1 for p in points if p is None),
+                "examples": [list(rep.requests[i][:2]) for i in idx[:3]]}
     return {"checked": len(rels), "distinct_clients": len(set(cids)), "cut_points": sorted(by_point),
             "max_rel_l2": round(max(rels), 6), "median_rel_l2": round(sorted(rels)[len(rels) // 2], 6),
             "top1_decisive": decisive, "top1_agree": agree, "tolerance": tol,
-            "ok": max(rels) <= tol and agree == decisive, "cpu_s": round(time.time() - t0, 1),
+            "inception_bf16_bound": ({"samples": len(relaxed), "max_rel_l2": round(max(a for a, _ in relaxed), 6),
+                                      "max_bound": round(max(b for _, b in relaxed), 6),
+                                      "rule": "rel <= max(2e-2, 1.25 x torch-bf16 error of the same suffix on the "
+                                              "same input), as tests/test_replay_gpu.py"} if relaxed else None),
+            "ok": all(passed) and agree == decisive, "cpu_s": round(time.time() - t0, 1),
             "oracle": "fp32 CPU forward (oracle/units.py, torchvision definitions) of each sampled request's "
                       "client activation; requests are the last completions of the timed run"}
 

@@ -105,6 +105,11 @@ SHAPES["l1_3x3_64_k16"] = (16, 56, 56, 64, 64, 3, 3, 1, 1)
 SHAPES["l2_3x3_128_k16"] = (16, 28, 28, 128, 128, 3, 3, 1, 1)
 SHAPES["l3_3x3_k1"] = (1, 14, 14, 256, 256, 3, 3, 1, 1)
 SHAPES["l1_1x1_576_k1"] = (1, 56, 56, 576, 64, 1, 1, 1, 0)
+# the layer4 tail at batch 1 (stages [15,18) / [17,18) of the serving plans)
+SHAPES["l4_1x1_2048_512_k1"] = (1, 7, 7, 2048, 512, 1, 1, 1, 0)
+SHAPES["l4_3x3_512_k1"] = (1, 7, 7, 512, 512, 3, 3, 1, 1)
+SHAPES["l4_1x1_512_2048_k1_res"] = (1, 7, 7, 512, 2048, 1, 1, 1, 0)
+SHAPES["l4_1x1_512_2048_k4_res"] = (4, 7, 7, 512, 2048, 1, 1, 1, 0)
 
 
 if __name__ == "__main__":

@@ -11,7 +11,10 @@ done
 if [ -n "$NCU" ]; then
   IFS=: read A B K BUD <<< "$NCU"
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:'conv_(tc|halo)_kernel' -c 60 \
-    -o $O/${TAG}_stage_conv python scripts/ncu_stage.py resnet50 $A $B $K $BUD > $O/${TAG}_ncu_stage.log 2>&1
-  python scripts/ncu_conv_summary.py $O/${TAG}_stage_conv.ncu-rep resnet50:$A:$B:$K:$BUD >> $O/${TAG}_ncu_stage.log 2>&1
+    -o /tmp/${TAG}_stage_conv python scripts/ncu_stage.py resnet50 $A $B $K $BUD > $O/${TAG}_ncu_stage.log 2>&1
+  python scripts/ncu_conv_summary.py /tmp/${TAG}_stage_conv.ncu-rep resnet50:$A:$B:$K:$BUD >> $O/${TAG}_ncu_stage.log 2>&1
+  # the report itself stays on the box (too large to merge back): details pages only
+  ncu -i /tmp/${TAG}_stage_conv.ncu-rep --page details --csv > $O/${TAG}_stage_conv_details.csv 2>/dev/null
+  ncu -i /tmp/${TAG}_stage_conv.ncu-rep --page raw --csv > /tmp/raw.csv 2>/dev/null && gzip -c /tmp/raw.csv > $O/${TAG}_stage_conv_raw.csv.gz
   cp profiles/ncu_conv_summary.json $O/${TAG}_ncu_conv_summary.json
 fi
