@@ -294,7 +294,8 @@ def run_ours(args):
             return serve(self.dep, self.clients, horizon, ctx=ctx, instances=self.instances, **extra,
                          ingress=self.pin() if host else self.dev_in,
                          ingress_from_host=(args.e2e_ingress if host else False), egress_to_host=host,
-                         max_inflight=self.max_inflight(), drain_s=drain, sample_outputs=sample)
+                         max_inflight=self.max_inflight(), drain_s=drain, sample_outputs=sample,
+                         lane_priority=1 if args.lane_priority == "time" else 0)
 
         def max_inflight(self):
             """Device slots: at least --max-inflight, and 1.5x the requests an SLO's worth of
@@ -959,6 +960,9 @@ def main():
     ap.add_argument("--e2e-ingress", choices=("zero_copy", "dma"), default="dma",
                     help="e2e host ingress: a copy-engine DMA of each request into a device slot at arrival "
                          "(default), or the gather reading pinned host memory over PCIe (zero_copy)")
+    ap.add_argument("--lane-priority", choices=("time", "uniform"), default="uniform",
+                    help="stream priority of each stage's batches: uniform (default) or by expected batch time "
+                         "(short tail spans first)")
     ap.add_argument("--placement", choices=("replicas", "plan"), default="replicas",
                     help="N > 1: an independent fleet per GPU (default), or one fleet planned and placed across "
                          "the N GPUs (run_placed)")

@@ -33,7 +33,8 @@ extern "C" {
 /* v2: stages carry their element type (fp32 execution mode), gx_stage_run_async runs on a caller
  * stream and records a caller event, gx_serve_cfg.result_rows sizes the output ring.
  * v3: on-device top-1 (K9: gx_stage_run_top1, gx_serve_cfg.top1, gx_serve_top1_for); GX_I32 token
- *     ids and the GX_OP_EMBED op (K8: BERT fragments entering at boundary 0). */
+ *     ids and the GX_OP_EMBED op (K8: BERT fragments entering at boundary 0); stream-priority lanes
+ *     (gx_serve_cfg.lane_priority). */
 #define GX_ABI_VERSION 3
 
 #if defined(__GNUC__)
@@ -301,8 +302,14 @@ typedef struct gx_serve_cfg {
                              measured; 0 = stop at the horizon like the reference                */
   int32_t top1;           /* GX_TOP1_*: the final stage's scatter also writes each request's
                              argmax (classifier chains; K9), into a ring like the logits          */
-  int32_t reserved2;
+  int32_t lane_priority;  /* GX_LANE_PRIO_*: stream priority of each stage's batches (WALL)     */
 } gx_serve_cfg;
+
+/* GX_LANE_PRIO_UNIFORM (default): every batch at the default stream priority.  GX_LANE_PRIO_BY_TIME:
+ * stages whose full batch is expected to take < 300 us / < 2 ms / longer on their SM budget run on
+ * high / middle / low priority streams (measured on the ResNet-50 fleets: no gain for the short
+ * stages, whose latency is not SM placement, and slower long stages; profiles/r02_lane_priority.log). */
+enum { GX_LANE_PRIO_UNIFORM = 0, GX_LANE_PRIO_BY_TIME = 1 };
 
 enum { GX_TOP1_NONE = 0, GX_TOP1_WITH_LOGITS = 1, GX_TOP1_ONLY = 2 /* no logits kept: egress is 4 B/request */ };
 

@@ -28,6 +28,8 @@ NVCC_FLAGS = [
 # variables (scripts/ A/B experiments on a scratch copy); never the shipped library
 if os.environ.get("GX_BUILD_DEV") == "1":
     NVCC_FLAGS.append("-DGX_DEV_KNOBS")
+    # compile-time experiment switches (e.g. -DGX_EPI_WAIT=0), development builds only
+    NVCC_FLAGS.extend(os.environ.get("GX_EXTRA_NVCC", "").split())
 
 
 def nvcc() -> str:

@@ -81,6 +81,7 @@ struct Batch {
   int dev = -1;  // device-table index the batch runs on
   std::vector<int> reqs;
   int ev = -1;           // completion event (pool of `dev`)
+  int ev0 = -1;          // GX_SERVE_DEBUG: event recorded ahead of the batch's first command
   double t_disp = 0.0;   // wall ms at dispatch (diagnostics)
   int lane = -1;         // stream-pool lane the batch runs on
 };
@@ -95,8 +96,10 @@ struct Stage {
   std::vector<int> inst_dev;  // device-table index per instance
   std::vector<char> busy;
   int out_final = 0;
+  int prio_class = 0;       // stream-priority class of its batches (0 = highest; see lane_class)
+  double expected_us = 0.0;  // roofline time of one full batch on an instance's SM budget
   // wall-clock diagnostics (GX_SERVE_DEBUG): observed dispatch->completion time per batch
-  double obs_ms = 0.0, plan_ms = 0.0;
+  double obs_ms = 0.0, plan_ms = 0.0, exec_ms = 0.0;  // exec: GPU time from the batch's first command
   int64_t obs_n = 0, obs_k = 0;
 };
 
@@ -130,6 +133,7 @@ struct Route {
 struct DevRes {
   int device = 0;
   std::vector<cudaStream_t> pool;
+  std::vector<int> pool_cls;      // priority class of each lane
   std::vector<int> pool_n;        // batches in flight per lane
   std::vector<double> pool_last;  // wall ms of the lane's last dispatch
   std::vector<cudaStream_t> copy_streams;
@@ -174,6 +178,8 @@ struct gx_serve {
   double host_dispatch_ms = 0.0, host_copy_ms = 0.0;  // diagnostics (GX_SERVE_DEBUG)
   int64_t loop_iters = 0;
   size_t max_inflight_seen = 0;
+  int n_classes = 1;  // stream-priority classes (GX_LANE_PRIO_*)
+  bool dbg_timing = false;  // GX_SERVE_DEBUG: timing events around each batch (diagnostics only)
   std::chrono::steady_clock::time_point t0;
 
   bool gpu() const { return cfg.clock != GX_CLOCK_VIRTUAL; }
@@ -223,7 +229,7 @@ struct gx_serve {
     if (r.free_events.empty()) {
       if (int rc = set_device(d)) return rc;
       cudaEvent_t ev = nullptr;
-      GX_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      GX_CUDA(cudaEventCreateWithFlags(&ev, dbg_timing ? cudaEventDefault : cudaEventDisableTiming));
       r.events.push_back(ev);
       r.free_events.push_back(static_cast<int>(r.events.size()) - 1);
     }
@@ -364,12 +370,21 @@ int gx_serve::dispatch_gpu(int si, int bi) {
   void* dst[64];
   int32_t* t1[64];
   int channels = 0;
-  // an idle lane if there is one, else the lane with the fewest / oldest batches in flight
-  int lane = 0;
-  for (int i = 1; i < static_cast<int>(dr.pool.size()); ++i)
-    if (dr.pool_n[i] < dr.pool_n[lane] || (dr.pool_n[i] == dr.pool_n[lane] && dr.pool_last[i] < dr.pool_last[lane]))
+  // an idle lane of the stage's priority class if there is one, else the class's lane with the
+  // fewest / oldest batches in flight
+  int lane = -1;
+  for (int i = 0; i < static_cast<int>(dr.pool.size()); ++i) {
+    if (dr.pool_cls[i] != st.prio_class) continue;
+    if (lane < 0 || dr.pool_n[i] < dr.pool_n[lane] ||
+        (dr.pool_n[i] == dr.pool_n[lane] && dr.pool_last[i] < dr.pool_last[lane]))
       lane = i;
+  }
+  if (lane < 0) return fail(GX_EINTERNAL, "no stream lane for the stage's priority class");
   cudaStream_t sm = dr.pool[lane];
+  if (dbg_timing) {
+    if (int e = take_event(d, &b.ev0)) return e;
+    GX_CUDA(cudaEventRecord(dr.events[b.ev0], sm));
+  }
   for (int i = 0; i < k; ++i) {
     Req& r = reqs[b.reqs[i]];
     if (r.h2d_ev >= 0) {  // (cross-device event waits are allowed)
@@ -597,6 +612,14 @@ int gx_serve::run() {
           inflight[i] = inflight.back();
           inflight.pop_back();
           dr.pool_n[b.lane] -= 1;
+          if (b.ev0 >= 0) {
+            float ms = 0.0f;
+            if (cudaEventElapsedTime(&ms, dr.events[b.ev0], dr.events[b.ev]) == cudaSuccess)
+              stages[b.stage].exec_ms += ms;
+            cudaGetLastError();
+            dr.free_events.push_back(b.ev0);
+            b.ev0 = -1;
+          }
           dr.free_events.push_back(b.ev);
           b.ev = -1;
           if (now <= limit) {
@@ -659,8 +682,9 @@ int gx_serve::run() {
     for (size_t i = 0; i < stages.size(); ++i) {
       const Stage& st = stages[i];
       if (!st.obs_n) continue;
-      fprintf(stderr, "[serve] stage %zu: batches=%lld mean_k=%.2f obs=%.3fms plan=%.3fms ratio=%.2f busy=%.0f%%\n", i,
-              static_cast<long long>(st.obs_n), double(st.obs_k) / st.obs_n, st.obs_ms / st.obs_n,
+      fprintf(stderr, "[serve] stage %zu: cls=%d exp=%.0fus batches=%lld mean_k=%.2f obs=%.3fms gpu=%.3fms plan=%.3fms ratio=%.2f busy=%.0f%%\n", i,
+              st.prio_class, st.expected_us,
+              static_cast<long long>(st.obs_n), double(st.obs_k) / st.obs_n, st.obs_ms / st.obs_n, st.exec_ms / st.obs_n,
               st.plan_ms / st.obs_n, st.obs_ms / std::max(1e-9, st.plan_ms),
               100.0 * st.obs_ms / std::max(1e-9, wall_ms * st.instances));
     }
@@ -697,11 +721,20 @@ int create_gpu_resources(gx_serve* s) {
     for (int i = cfg.max_inflight - 1; i >= 0; --i) r.free_slots.push_back(i);
     // more lanes than the 32 hardware queues: the least-loaded-lane choice then spreads in-flight
     // batches over every queue (measured: 30 lanes -> p99 205 ms, 64 -> 101 ms at 1536 clients)
+    // lanes split over the priority classes in use; class c streams get priority greatest + c
+    // (lower value = scheduled first when CTAs wait for SMs)
     const int lanes = std::max(1, dev().serve_streams);
-    for (int i = 0; i < lanes; ++i) {
-      cudaStream_t q = nullptr;
-      GX_CUDA(cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking));
-      r.pool.push_back(q);
+    int least = 0, greatest = 0;
+    GX_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    for (int c = 0; c < s->n_classes; ++c) {
+      const int n = std::max(1, lanes / s->n_classes + (c < lanes % s->n_classes ? 1 : 0));
+      const int prio = std::min(least, greatest + c);
+      for (int i = 0; i < n; ++i) {
+        cudaStream_t q = nullptr;
+        GX_CUDA(cudaStreamCreateWithPriority(&q, cudaStreamNonBlocking, prio));
+        r.pool.push_back(q);
+        r.pool_cls.push_back(c);
+      }
     }
     r.pool_n.assign(r.pool.size(), 0);
     r.pool_last.assign(r.pool.size(), 0.0);
@@ -742,6 +775,34 @@ int create_gpu_resources(gx_serve* s) {
   return GX_OK;
 }
 
+// Stream priorities by expected batch time (GX_LANE_PRIO_BY_TIME): the roofline time of one full
+// batch on the instance's SM budget (tensor peak or the per-SM L2 feed per op, plus a launch
+// allowance).  Short stages (the tail spans planned at batch 1-2) go to the highest-priority lanes:
+// when the GPU's SMs are all held by persistent grids, their CTAs are placed first as SMs free up,
+// instead of queueing behind long batches (shortest-job-first at the block scheduler).
+double expected_batch_us(const gx_stage* g, int k) {
+  double us = 0.0;
+  const double sm = std::max(1, g->sm_budget);
+  for (int oi : g->ops) {
+    double f = 0.0, b = 0.0;
+    gx::op_work(g->m->ops[oi], g->m->tensors.data(), k, &f, &b);
+    us += std::max(f / (sm * 11.2e6), b / (sm * 1.7e5)) + 3.0;  // 11.2 TFLOP/s and ~170 GB/s per SM
+  }
+  return us;
+}
+
+void classify_stages(gx_serve* s) {
+  s->n_classes = 1;
+  for (Stage& x : s->stages) {
+    x.prio_class = 0;
+    x.expected_us = x.inst.empty() ? 0.0 : expected_batch_us(x.inst[0], x.batch);
+  }
+  if (s->cfg.lane_priority != GX_LANE_PRIO_BY_TIME) return;
+  // three classes: < 300 us, < 2 ms, longer
+  for (Stage& x : s->stages) x.prio_class = x.expected_us < 300.0 ? 0 : x.expected_us < 2000.0 ? 1 : 2;
+  s->n_classes = 3;
+}
+
 int device_of_pointer(const void* p, int fallback) {
   cudaPointerAttributes at;
   if (p && cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeDevice) return at.device;
@@ -760,6 +821,7 @@ int gx_serve_create(gx_ctx* ctx, int n_stages, const gx_serve_stage* st, int n_r
   s->ctx = ctx;
   s->cfg = *cfg;
   const bool gpu_clock = cfg->clock != GX_CLOCK_VIRTUAL;
+  s->dbg_timing = cfg->clock == GX_CLOCK_WALL && getenv("GX_SERVE_DEBUG") != nullptr;  // diagnostics only
   s->gpus.push_back(gpu_clock ? ctx->device : 0);
   for (int i = 0; i < n_stages; ++i) {
     Stage x;
@@ -894,6 +956,7 @@ int gx_serve_create(gx_ctx* ctx, int n_stages, const gx_serve_stage* st, int n_r
                                  " bytes a route needs (ingress copy or intermediate boundary)");
     }
     if (s->cfg.result_rows <= 0) s->cfg.result_rows = cfg->max_inflight;
+    classify_stages(s);
     if (cfg->top1 < GX_TOP1_NONE || cfg->top1 > GX_TOP1_ONLY) {
       delete s;
       return fail(GX_EINVAL, "top1 must be GX_TOP1_NONE, GX_TOP1_WITH_LOGITS or GX_TOP1_ONLY");
