@@ -232,7 +232,8 @@ def run_ours(args):
             self.clients = [ClientView.from_doc(c) for c in wl["clients"]]
             self.instances = []
             for d in self.deps:  # each deployment gets its planned shares on the whole GPU
-                it = iter(ctx.sm_budgets([(s.share, s.instances) for s in d.stages], work_conserving=not strict))
+                it = iter(ctx.sm_budgets([(s.share, s.instances) for s in d.stages], work_conserving=not strict,
+                                         capacity=int(round(99 * args.sm_oversubscribe))))
                 self.instances += [[StageInstance(dm, s.start, s.end, s.batch, next(it)) for _ in range(s.instances)]
                                    for s in d.stages]
             keys = sorted({(cid, r.point) for d in self.deps for cid, r in d.routes.items()})
@@ -295,7 +296,7 @@ def run_ours(args):
                          ingress=self.pin() if host else self.dev_in,
                          ingress_from_host=(args.e2e_ingress if host else False), egress_to_host=host,
                          max_inflight=self.max_inflight(), drain_s=drain, sample_outputs=sample,
-                         lane_priority=1 if args.lane_priority == "time" else 0)
+                         lane_policy={"split": 0, "least": 1, "time": 2, "earliest": 3}[args.lanes])
 
         def max_inflight(self):
             """Device slots: at least --max-inflight, and 1.5x the requests an SLO's worth of
@@ -960,9 +961,13 @@ def main():
     ap.add_argument("--e2e-ingress", choices=("zero_copy", "dma"), default="dma",
                     help="e2e host ingress: a copy-engine DMA of each request into a device slot at arrival "
                          "(default), or the gather reading pinned host memory over PCIe (zero_copy)")
-    ap.add_argument("--lane-priority", choices=("time", "uniform"), default="uniform",
-                    help="stream priority of each stage's batches: uniform (default) or by expected batch time "
-                         "(short tail spans first)")
+    ap.add_argument("--sm-oversubscribe", type=float, default=3.0,
+                    help="work-conserving SM budgets may sum to this multiple of the GPU's SMs (at most 32 "
+                         "batches execute at once, one per hardware queue: budgets summing to 1x leave SMs idle)")
+    ap.add_argument("--lanes", choices=("split", "least", "time", "earliest"), default="split",
+                    help="stream-lane policy (graft_exec.h GX_LANE_*): one lane per hardware queue with queues "
+                         "reserved for short stages (default), least-loaded of 64 lanes, the same with priorities "
+                         "by expected batch time, or one lane per hardware queue, earliest free")
     ap.add_argument("--placement", choices=("replicas", "plan"), default="replicas",
                     help="N > 1: an independent fleet per GPU (default), or one fleet planned and placed across "
                          "the N GPUs (run_placed)")

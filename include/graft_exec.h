@@ -34,7 +34,7 @@ extern "C" {
  * stream and records a caller event, gx_serve_cfg.result_rows sizes the output ring.
  * v3: on-device top-1 (K9: gx_stage_run_top1, gx_serve_cfg.top1, gx_serve_top1_for); GX_I32 token
  *     ids and the GX_OP_EMBED op (K8: BERT fragments entering at boundary 0); stream-priority lanes
- *     (gx_serve_cfg.lane_priority). */
+ *     (gx_serve_cfg.lane_policy). */
 #define GX_ABI_VERSION 3
 
 #if defined(__GNUC__)
@@ -302,14 +302,22 @@ typedef struct gx_serve_cfg {
                              measured; 0 = stop at the horizon like the reference                */
   int32_t top1;           /* GX_TOP1_*: the final stage's scatter also writes each request's
                              argmax (classifier chains; K9), into a ring like the logits          */
-  int32_t lane_priority;  /* GX_LANE_PRIO_*: stream priority of each stage's batches (WALL)     */
+  int32_t lane_policy;    /* GX_LANE_*: how batches are placed on the stream lanes (WALL)        */
 } gx_serve_cfg;
 
-/* GX_LANE_PRIO_UNIFORM (default): every batch at the default stream priority.  GX_LANE_PRIO_BY_TIME:
- * stages whose full batch is expected to take < 300 us / < 2 ms / longer on their SM budget run on
- * high / middle / low priority streams (measured on the ResNet-50 fleets: no gain for the short
- * stages, whose latency is not SM placement, and slower long stages; profiles/r02_lane_priority.log). */
-enum { GX_LANE_PRIO_UNIFORM = 0, GX_LANE_PRIO_BY_TIME = 1 };
+/* A device has CUDA_DEVICE_MAX_CONNECTIONS = 32 hardware queues; a batch is a chain of dependent
+ * kernels, so two batches on one queue run one after the other (false serialisation) and at most 32
+ * batches execute at once.  Lane policies:
+ * GX_LANE_SPLIT (default): one lane per hardware queue, 4 of them reserved for short stages (expected
+ *   batch time < 150 us on their SM budget: the tail spans planned at batch 1-2), the rest for the
+ *   others; within its pool a batch takes the lane expected to free first (each lane's queued work
+ *   is tracked from the stages' measured batch times).
+ * GX_LANE_LEAST_LOADED: 64 lanes; an idle lane, else the one with the fewest batches in flight.
+ * GX_LANE_PRIO_BY_TIME: the same with three stream priorities by expected batch time (< 300 us /
+ *   < 2 ms / longer; measured: no gain, profiles/r02_lane_priority.log).
+ * GX_LANE_EARLIEST: one lane per hardware queue, earliest expected free lane, no reserved queues.
+ * (Measurements: profiles/r02_lanes_oversubscribe.log.) */
+enum { GX_LANE_SPLIT = 0, GX_LANE_LEAST_LOADED = 1, GX_LANE_PRIO_BY_TIME = 2, GX_LANE_EARLIEST = 3 };
 
 enum { GX_TOP1_NONE = 0, GX_TOP1_WITH_LOGITS = 1, GX_TOP1_ONLY = 2 /* no logits kept: egress is 4 B/request */ };
 

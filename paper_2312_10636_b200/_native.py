@@ -22,7 +22,7 @@ GX_OPF_COUNT_INCLUDE_PAD, GX_OPF_NO_HALO, GX_OPF_FC_SIMT = 1, 2, 4
 GX_CLOCK_VIRTUAL, GX_CLOCK_WALL, GX_CLOCK_REPLAY = 0, 1, 2
 GX_EXEC_GRAPH, GX_EXEC_SPAN = 0, 1
 GX_TOP1_NONE, GX_TOP1_WITH_LOGITS, GX_TOP1_ONLY = 0, 1, 2
-GX_LANE_PRIO_UNIFORM, GX_LANE_PRIO_BY_TIME = 0, 1
+GX_LANE_SPLIT, GX_LANE_LEAST_LOADED, GX_LANE_PRIO_BY_TIME, GX_LANE_EARLIEST = 0, 1, 2, 3
 
 
 class GxTensor(C.Structure):
@@ -78,7 +78,7 @@ class GxServeCfg(C.Structure):
                 ("record_dispatch", C.c_int32), ("ingress_from_host", C.c_int32),
                 ("egress_to_host", C.c_int32), ("slot_bytes", C.c_int64),
                 ("max_inflight", C.c_int32), ("warmup_requests_skip", C.c_int32), ("result_rows", C.c_int64),
-                ("drain_ms", C.c_double), ("top1", C.c_int32), ("lane_priority", C.c_int32)]
+                ("drain_ms", C.c_double), ("top1", C.c_int32), ("lane_policy", C.c_int32)]
 
 
 _lib = None

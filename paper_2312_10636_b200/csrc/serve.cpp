@@ -84,6 +84,7 @@ struct Batch {
   int ev0 = -1;          // GX_SERVE_DEBUG: event recorded ahead of the batch's first command
   double t_disp = 0.0;   // wall ms at dispatch (diagnostics)
   int lane = -1;         // stream-pool lane the batch runs on
+  double t_start_est = 0.0;  // GX_LANE_EARLIEST: when the lane was expected to start it (wall ms)
 };
 
 struct Stage {
@@ -98,6 +99,7 @@ struct Stage {
   int out_final = 0;
   int prio_class = 0;       // stream-priority class of its batches (0 = highest; see lane_class)
   double expected_us = 0.0;  // roofline time of one full batch on an instance's SM budget
+  double est_ms = 0.0;       // GX_LANE_EARLIEST: running estimate of one batch's time on its lane
   // wall-clock diagnostics (GX_SERVE_DEBUG): observed dispatch->completion time per batch
   double obs_ms = 0.0, plan_ms = 0.0, exec_ms = 0.0;  // exec: GPU time from the batch's first command
   int64_t obs_n = 0, obs_k = 0;
@@ -136,6 +138,7 @@ struct DevRes {
   std::vector<int> pool_cls;      // priority class of each lane
   std::vector<int> pool_n;        // batches in flight per lane
   std::vector<double> pool_last;  // wall ms of the lane's last dispatch
+  std::vector<double> pool_free;  // GX_LANE_EARLIEST: expected wall ms the lane's queued work ends
   std::vector<cudaStream_t> copy_streams;
   int64_t n_copies = 0;
   void* slots = nullptr;
@@ -373,11 +376,23 @@ int gx_serve::dispatch_gpu(int si, int bi) {
   // an idle lane of the stage's priority class if there is one, else the class's lane with the
   // fewest / oldest batches in flight
   int lane = -1;
-  for (int i = 0; i < static_cast<int>(dr.pool.size()); ++i) {
-    if (dr.pool_cls[i] != st.prio_class) continue;
-    if (lane < 0 || dr.pool_n[i] < dr.pool_n[lane] ||
-        (dr.pool_n[i] == dr.pool_n[lane] && dr.pool_last[i] < dr.pool_last[lane]))
-      lane = i;
+  if (cfg.lane_policy == GX_LANE_EARLIEST || cfg.lane_policy == GX_LANE_SPLIT) {
+    // the lane (= hardware queue) of the stage's pool expected to free first; ties -> fewer in flight
+    for (int i = 0; i < static_cast<int>(dr.pool.size()); ++i) {
+      if (dr.pool_cls[i] != st.prio_class) continue;
+      const double fi = std::max(b.t_disp, dr.pool_free[i]);
+      const double fl = lane < 0 ? 0.0 : std::max(b.t_disp, dr.pool_free[lane]);
+      if (lane < 0 || fi < fl - 1e-9 || (fi <= fl + 1e-9 && dr.pool_n[i] < dr.pool_n[lane])) lane = i;
+    }
+    b.t_start_est = std::max(b.t_disp, dr.pool_free[lane]);
+    dr.pool_free[lane] = b.t_start_est + st.est_ms;
+  } else {
+    for (int i = 0; i < static_cast<int>(dr.pool.size()); ++i) {
+      if (dr.pool_cls[i] != st.prio_class) continue;
+      if (lane < 0 || dr.pool_n[i] < dr.pool_n[lane] ||
+          (dr.pool_n[i] == dr.pool_n[lane] && dr.pool_last[i] < dr.pool_last[lane]))
+        lane = i;
+    }
   }
   if (lane < 0) return fail(GX_EINTERNAL, "no stream lane for the stage's priority class");
   cudaStream_t sm = dr.pool[lane];
@@ -612,6 +627,13 @@ int gx_serve::run() {
           inflight[i] = inflight.back();
           inflight.pop_back();
           dr.pool_n[b.lane] -= 1;
+          if (cfg.lane_policy == GX_LANE_EARLIEST || cfg.lane_policy == GX_LANE_SPLIT) {
+            // the batch ran from about max(dispatch, expected start) to now: refine the stage's estimate
+            Stage& xs = stages[b.stage];
+            const double took = now - b.t_start_est;
+            if (took > 0.0) xs.est_ms += 0.1 * (took - xs.est_ms);
+            if (dr.pool_n[b.lane] == 0) dr.pool_free[b.lane] = now;
+          }
           if (b.ev0 >= 0) {
             float ms = 0.0f;
             if (cudaEventElapsedTime(&ms, dr.events[b.ev0], dr.events[b.ev]) == cudaSuccess)
@@ -693,6 +715,9 @@ int gx_serve::run() {
 }
 
 namespace {
+constexpr int kSplitShortLanes = 4;      // GX_LANE_SPLIT: queues reserved for short stages
+constexpr double kSplitShortUs = 150.0;  // GX_LANE_SPLIT: a stage is short below this expected batch time
+
 // GPU-clock resources: per device a stream pool, copy streams, a slot pool; peer access between
 // every pair of devices the plan spans (batches gather activations produced on another GPU).
 int create_gpu_resources(gx_serve* s) {
@@ -723,12 +748,18 @@ int create_gpu_resources(gx_serve* s) {
     // batches over every queue (measured: 30 lanes -> p99 205 ms, 64 -> 101 ms at 1536 clients)
     // lanes split over the priority classes in use; class c streams get priority greatest + c
     // (lower value = scheduled first when CTAs wait for SMs)
-    const int lanes = std::max(1, dev().serve_streams);
+    // GX_LANE_EARLIEST: one lane per hardware queue (the DMA copy stream takes one of the 32)
+    const bool per_queue = cfg.lane_policy == GX_LANE_EARLIEST || cfg.lane_policy == GX_LANE_SPLIT;
+    const int lanes = per_queue ? (cfg.ingress_from_host == GX_INGRESS_DMA ? 31 : 32) : std::max(1, dev().serve_streams);
     int least = 0, greatest = 0;
     GX_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
     for (int c = 0; c < s->n_classes; ++c) {
-      const int n = std::max(1, lanes / s->n_classes + (c < lanes % s->n_classes ? 1 : 0));
-      const int prio = std::min(least, greatest + c);
+      int n = std::max(1, lanes / s->n_classes + (c < lanes % s->n_classes ? 1 : 0));
+      int prio = std::min(least, greatest + c);
+      if (cfg.lane_policy == GX_LANE_SPLIT && s->n_classes == 2) {  // short stages: kSplitShortLanes queues
+        n = c == 0 ? kSplitShortLanes : lanes - kSplitShortLanes;
+        prio = 0;
+      }
       for (int i = 0; i < n; ++i) {
         cudaStream_t q = nullptr;
         GX_CUDA(cudaStreamCreateWithPriority(&q, cudaStreamNonBlocking, prio));
@@ -738,6 +769,7 @@ int create_gpu_resources(gx_serve* s) {
     }
     r.pool_n.assign(r.pool.size(), 0);
     r.pool_last.assign(r.pool.size(), 0.0);
+    r.pool_free.assign(r.pool.size(), 0.0);
     // one FIFO copy stream: arrival order is deadline order, and concurrent copies only share
     // the PCIe link (measured at 1152 clients: p99 88 ms with 1 stream, 205-220 ms with 4 or 16)
     const int ncopy = cfg.ingress_from_host == GX_INGRESS_DMA ? std::max(1, dev().copy_streams) : 0;
@@ -797,7 +829,23 @@ void classify_stages(gx_serve* s) {
     x.prio_class = 0;
     x.expected_us = x.inst.empty() ? 0.0 : expected_batch_us(x.inst[0], x.batch);
   }
-  if (s->cfg.lane_priority != GX_LANE_PRIO_BY_TIME) return;
+  for (Stage& x : s->stages) x.est_ms = 1.5e-3 * x.expected_us;  // refined by measured batch times
+  if (s->cfg.lane_policy == GX_LANE_SPLIT) {
+    // short stages (tail spans at batch 1-2) get hardware queues of their own, so they never wait
+    // behind a long batch that shares their queue; everything else shares the remaining queues
+    bool any_short = false, any_long = false;
+    for (Stage& x : s->stages) {
+      x.prio_class = x.expected_us < kSplitShortUs ? 0 : 1;
+      (x.prio_class == 0 ? any_short : any_long) = true;
+    }
+    if (!any_short || !any_long) {  // one kind of stage: every queue serves it
+      for (Stage& x : s->stages) x.prio_class = 0;
+      return;
+    }
+    s->n_classes = 2;
+    return;
+  }
+  if (s->cfg.lane_policy != GX_LANE_PRIO_BY_TIME) return;
   // three classes: < 300 us, < 2 ms, longer
   for (Stage& x : s->stages) x.prio_class = x.expected_us < 300.0 ? 0 : x.expected_us < 2000.0 ? 1 : 2;
   s->n_classes = 3;

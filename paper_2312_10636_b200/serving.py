@@ -158,7 +158,7 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
           egress_to_host: bool = False, slot_bytes: int = 0, max_inflight: int = 4096,
           planner: str | None = None, plan_latency=None, return_outputs: bool = False,
           epochs: list | None = None, result_rows: int = 0, sample_outputs: int = 0,
-          drain_s: float = 0.0, top1: int = 0, lane_priority: int = 0) -> ServeReport:
+          drain_s: float = 0.0, top1: int = 0, lane_policy: int = 0) -> ServeReport:
     """Run one plan for one horizon.
 
     latency: callable (StageSpec, k) -> ms for the virtual clock (None -> wall clock).
@@ -177,8 +177,9 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
     [n, elems] fp32) — output spot-checks of long serving runs.
     top1: GX_TOP1_* (0 none, 1 logits + top-1, 2 top-1 only): the final stage's scatter also writes
     each request's argmax (K9, classifier chains); report.top1 = int32 per request (-1: none).
-    lane_priority: GX_LANE_PRIO_* (0: every batch at the default stream priority, 1: stages with short
-    expected batches on high-priority streams).
+    lane_policy: GX_LANE_* (graft_exec.h): 0 one lane per hardware queue with 4 queues reserved for
+    short stages (default), 1 least-loaded of 64 lanes, 2 the same with stream priorities by expected
+    batch time, 3 one lane per hardware queue, earliest expected free lane.
     plan_latency: optional (StageSpec, k) -> ms the plan assumed; on the wall clock it is only
     compared with the observed batch times in the GX_SERVE_DEBUG summary.
     epochs: plan transitions under churn, one entry per epoch (Deployment / None = keep /
@@ -294,7 +295,7 @@ def serve(deployment: Deployment, clients: list[ClientView], horizon_s: float, *
     cfg.result_rows = result_rows
     cfg.drain_ms = drain_s * 1000.0 if wall else 0.0
     cfg.top1 = int(top1)
-    cfg.lane_priority = int(lane_priority)
+    cfg.lane_policy = int(lane_policy)
     L = N.lib()
     h = C.c_void_p()
     ctx_handle = ctx.handle if ctx is not None else C.c_void_p(0)
