@@ -46,7 +46,7 @@ CONFIGS = {
     "resnet50": ("resnet50", None, METRIC,
                  "resnet50 re-aligned fragment groups, {n} clients x {rps} rps per GPU, 8 cut points, plan from the "
                  "reference planner on the measured B200 profile table, SM-share partitioning"),
-    "vgg16_churn": ("vgg16", "vgg16_churn_s2", "SLO-met requests/sec (p99<=SLO) for VGG-16 fragment groups under "
+    "vgg16_churn": ("vgg16", "vgg16_churn", "SLO-met requests/sec (p99<=SLO) for VGG-16 fragment groups under "
                     "partition-point churn",
                     "vgg16 fragment groups under network-trace-driven partition-point churn: {n} clients x {rps} rps "
                     "per GPU on a fast/slow bandwidth trace (half out of phase), re-partitioned and re-planned by "
@@ -384,7 +384,7 @@ def run_ours(args):
             res = one_run(fleet, host, sample)
         return fleet, res, first
 
-    all_wl = _workloads(args.plans or args.model, all_plans=args.plans is None)
+    all_wl = _workloads(args.plans or args.model, all_plans=args.all_plans)
     sample = 256 if (rank == 0 and not args.no_cpu_baseline) else 0
     with ClockSampler(local) as clk:
         if args.clients is not None:
@@ -837,7 +837,7 @@ def cpu_serving_rate(model, budget_s=40.0, horizon_s=3.0, tag=None):
     m = torch_model(model)
     units = units_for(model, m)
     chain = build_chain(model, module=m)
-    wl = (_workloads(tag) if tag else _workloads(model) or _workloads(model, all_plans=True))[0]
+    wl = (_workloads(tag, all_plans=True) if tag else _workloads(model) or _workloads(model, all_plans=True))[0]
     first = next(e for e in wl["epochs"] if e["kind"] == "deploy") if "epochs" in wl else wl
     dep = deploy(first["plan"], first["fragments"])
     # clients in descending id order: the cut mix cycles from the cheapest suffix (cut 17) down to
@@ -974,6 +974,7 @@ def main():
     args = ap.parse_args()
     model, tag, args.metric, args.workload = CONFIGS[args.config]
     args.model = args.model or model
+    args.all_plans = args.plans is None  # the config's plan families (load-calibrated tables, merge thresholds)
     args.plans = args.plans or tag
     if args.warmup < 3:
         args.warmup = 3

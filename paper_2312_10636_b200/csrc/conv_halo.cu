@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
       }
       for (int i = 0; i < 2; ++i) {
         mbar_init(&sp.tfull[i], 1);
-        mbar_init(&sp.tempty[i], 256);
+        mbar_init(&sp.tempty[i], 8);  // one arrival per epilogue warp
       }
       for (int i = 0; i < S_; ++i) {
         mbar_init(&sp.bfull[i], 1);
@@ -291,7 +291,8 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&sp.tempty[acc]);
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&sp.tempty[acc]);  // one arrival per warp
     }
   }
   pdl_launch_dependents();

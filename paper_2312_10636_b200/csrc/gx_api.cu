@@ -188,21 +188,31 @@ bool encode_tmap_halo_bf16(CUtensorMap* map, const void* base, int C, int W, int
 int elem_size(int dtype) { return dtype == GX_BF16 ? 2 : 4; }  // GX_F32, GX_I32: 4 bytes
 int64_t tensor_elems(const gx_tensor& t) { return static_cast<int64_t>(t.H) * t.W * t.C; }
 
+// N tile width: the persistent grid runs min(tiles, budget) CTAs, so the makespan of the busiest
+// CTA is ceil(tiles / grid) tiles of (BN + a fixed per-tile cost of ~64 accumulator columns: the A
+// operand fetch and the epilogue start).  Candidates: multiples of 64 (the fast epilogue paths)
+// and divisors of Cout that are multiples of 16 (Inception 320 / 384 / 448 -> 160 / 192 / 224,
+// the 1000-way FC); the cheapest makespan wins, wider tiles on ties.  (A pure halving rule left
+// the ResNet head at 5 tiles on 2 or 4 SMs: 3 / 2 waves.)
 static int pick_bn(int Cout, int m_tiles, int sm_budget, int cap) {
-  int bn;
-  if (Cout <= cap) {
-    bn = Cout;
-  } else {
-    bn = cap;
-    // prefer a tile width that divides Cout (Inception 320/384/448 -> 160/192/224)
-    for (int cand = cap; cand >= 64; cand -= 16)
-      if (Cout % cand == 0) {
-        bn = cand;
-        break;
-      }
-  }
-  while (m_tiles * ((Cout + bn - 1) / bn) < sm_budget && bn > 64 && (bn / 2) % 16 == 0) bn /= 2;
-  return bn;
+  const int budget = std::max(1, sm_budget);
+  int best = 0;
+  int64_t best_t = 0;
+  auto consider = [&](int bn) {
+    if (bn < 16 || bn > cap || bn > ((Cout + 15) / 16) * 16) return;
+    const int64_t tiles = static_cast<int64_t>(m_tiles) * ((Cout + bn - 1) / bn);
+    const int64_t grid = std::min<int64_t>(tiles, budget);
+    const int64_t t = (tiles + grid - 1) / grid * (bn + 64);
+    if (best == 0 || t < best_t || (t == best_t && bn > best)) {
+      best = bn;
+      best_t = t;
+    }
+  };
+  for (int bn = 64; bn <= cap; bn += 64) consider(bn);
+  for (int bn = 16; bn <= cap; bn += 16)
+    if (Cout % bn == 0) consider(bn);
+  if (Cout < 64) consider(((Cout + 15) / 16) * 16);
+  return best > 0 ? best : std::min(cap, ((Cout + 15) / 16) * 16);
 }
 
 static uint32_t tmem_cols_for(int bn) {

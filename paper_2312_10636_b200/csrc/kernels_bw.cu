@@ -366,7 +366,7 @@ __global__ void pool_kernel(int mode, const __nv_bfloat16* __restrict__ x, int N
 // row's three taps once into a row value (max or sum) and each output from three row values:
 // 3*(T+2) loads for T outputs instead of 9*T, so the nine-fold tap reuse no longer has to come
 // from L1/L2 (the per-output kernel was L2->SM bound at 0.26 of HBM on 35x35x288).
-constexpr int kPoolStrip = 8;
+constexpr int kPoolStrip = 6;
 __global__ void pool3s1_kernel(int mode, const __nv_bfloat16* __restrict__ x, int N, int H, int W, int C, int x_ld,
                                __nv_bfloat16* __restrict__ y, int Ho, int Wo, int y_ld, int y_coff, int ph, int pw,
                                int count_include_pad) {
@@ -389,17 +389,23 @@ __global__ void pool3s1_kernel(int mode, const __nv_bfloat16* __restrict__ x, in
     for (int s = 0; s < 3; ++s) ncols += (w0 + s >= 0 && w0 + s < W) ? 1 : 0;
     float rv[T + 2][8];
     bool rok[T + 2];
+    // every tap of the strip is loaded before any is combined: 3 (T + 2) independent 16-byte loads
+    // in flight per thread (the per-row load-then-combine order left ~3, latency-bound at 0.28 of HBM)
+    uint4 raw[T + 2][3];
 #pragma unroll
     for (int j = 0; j < T + 2; ++j) {
       const int hi = ho0 - ph + j;
       rok[j] = hi >= 0 && hi < H && ho0 + j - 2 < Ho;  // rows past the strip's last output unused
       const int hc = min(max(hi, 0), H - 1);
-      uint4 v[3];
 #pragma unroll
       for (int s = 0; s < 3; ++s) {
         const int wc = min(max(w0 + s, 0), W - 1);
-        v[s] = __ldg(reinterpret_cast<const uint4*>(x + ((static_cast<int64_t>(n) * H + hc) * W + wc) * x_ld) + c8);
+        raw[j][s] = __ldg(reinterpret_cast<const uint4*>(x + ((static_cast<int64_t>(n) * H + hc) * W + wc) * x_ld) + c8);
       }
+    }
+#pragma unroll
+    for (int j = 0; j < T + 2; ++j) {
+      const uint4* v = raw[j];
 #pragma unroll
       for (int e = 0; e < 8; ++e) rv[j][e] = ident;
 #pragma unroll
@@ -454,28 +460,36 @@ __global__ void pool3s1_kernel(int mode, const __nv_bfloat16* __restrict__ x, in
   }
 }
 
-// Global average pool: [N, HW, C] -> [N, C].  A block owns (sample, 256 channels): lane = 8
-// channels (a warp reads 512 contiguous bytes of one pixel), the 8 warps stride the HW pixels with
-// independent loads in flight, then the 8 partial sums are reduced through shared memory.  (The
-// former one-thread-per-8-channels kernel walked all HW pixels serially: 49 dependent loads.)
+// Global average pool: [N, HW, C] -> [N, C].  A warp owns one (sample, 256 channels) item: lane =
+// 8 channels (the warp reads 512 contiguous bytes of one pixel) and walks the HW pixels with 8
+// independent 16-byte loads in flight per lane, accumulating in fp32 registers; no shared memory
+// and no block barriers, so the 8 warps of a block stream 8 items concurrently.  (Round 1 split
+// one item over the 8 warps and reduced through shared memory: two barriers per item, 0.55 of HBM.)
 constexpr int kGapWarps = 8;
 __global__ void __launch_bounds__(kGapWarps * 32) gap_kernel(const __nv_bfloat16* __restrict__ x, int N, int HW,
                                                             int C, __nv_bfloat16* __restrict__ y) {
-  __shared__ float part[kGapWarps][32][9];  // +1 pad: lane-strided rows hit distinct banks
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const int cv = C / 8;
   const int groups = (cv + 31) / 32;
   const float inv = 1.0f / HW;
-  for (int64_t item = blockIdx.x; item < static_cast<int64_t>(N) * groups; item += gridDim.x) {
+  const int64_t items = static_cast<int64_t>(N) * groups;
+  const int64_t wstride = static_cast<int64_t>(gridDim.x) * kGapWarps;
+  for (int64_t item = static_cast<int64_t>(blockIdx.x) * kGapWarps + (threadIdx.x >> 5); item < items;
+       item += wstride) {
     const int n = static_cast<int>(item / groups);
     const int c8 = static_cast<int>(item % groups) * 32 + lane;
+    if (c8 >= cv) continue;
+    const uint4* base = reinterpret_cast<const uint4*>(x + static_cast<int64_t>(n) * HW * C) + c8;
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    if (c8 < cv) {
-      const uint4* base = reinterpret_cast<const uint4*>(x + static_cast<int64_t>(n) * HW * C) + c8;
-#pragma unroll 4
-      for (int p = warp; p < HW; p += kGapWarps) {
-        const uint4 v = ldg_stream(base + static_cast<int64_t>(p) * cv);
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    constexpr int U = 8;
+    for (int p0 = 0; p0 < HW; p0 += U) {
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        v[u] = p0 + u < HW ? ldg_stream(base + static_cast<int64_t>(p0 + u) * cv) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const float2 f = unpack_bf16x2(w[j]);
@@ -484,25 +498,12 @@ __global__ void __launch_bounds__(kGapWarps * 32) gap_kernel(const __nv_bfloat16
         }
       }
     }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) part[warp][lane][j] = acc[j];
-    __syncthreads();
-    if (warp == 0 && c8 < cv) {
-      float s[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        s[j] = 0.0f;
-#pragma unroll
-        for (int w = 0; w < kGapWarps; ++w) s[j] += part[w][lane][j];
-      }
-      uint4 o;
-      o.x = pack_bf16x2(s[0] * inv, s[1] * inv);
-      o.y = pack_bf16x2(s[2] * inv, s[3] * inv);
-      o.z = pack_bf16x2(s[4] * inv, s[5] * inv);
-      o.w = pack_bf16x2(s[6] * inv, s[7] * inv);
-      reinterpret_cast<uint4*>(y + static_cast<int64_t>(n) * C)[c8] = o;
-    }
-    __syncthreads();
+    uint4 o;
+    o.x = pack_bf16x2(acc[0] * inv, acc[1] * inv);
+    o.y = pack_bf16x2(acc[2] * inv, acc[3] * inv);
+    o.z = pack_bf16x2(acc[4] * inv, acc[5] * inv);
+    o.w = pack_bf16x2(acc[6] * inv, acc[7] * inv);
+    reinterpret_cast<uint4*>(y + static_cast<int64_t>(n) * C)[c8] = o;
   }
 }
 
@@ -645,25 +646,36 @@ __global__ void copy_channels_kernel(const __nv_bfloat16* __restrict__ x, int64_
   const int cv = C / 8;
   const int total = static_cast<int>(pixels * cv);  // < 2^31 (launcher)
   const int stride = gridDim.x * blockDim.x;
+  // (pixel, vector) of the thread's element advanced incrementally: one division per thread, none
+  // per element (a 32-bit division by the runtime vector count per 16-byte element made the copy
+  // issue-bound at 0.62 of HBM)
+  const int dp = stride / cv, dr = stride - dp * cv;
+  int i0 = blockIdx.x * blockDim.x + threadIdx.x;
+  int p0 = i0 / cv, r0 = i0 - p0 * cv;
   // 4 independent 16-byte loads in flight per thread, then the 4 stores
-  for (int i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < total; i0 += 4 * stride) {
+  for (; i0 < total; i0 += 4 * stride) {
     uint4 v[4];
+    int pp[4], rr[4];
+    int p = p0, r = r0;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int i = i0 + u * stride;
-      if (i < total) {
-        const int p = i / cv;
-        v[u] = ldg_stream(reinterpret_cast<const uint4*>(x + static_cast<int64_t>(p) * x_ld + x_coff) + (i - p * cv));
+      pp[u] = p;
+      rr[u] = r;
+      if (i0 + u * stride < total)
+        v[u] = ldg_stream(reinterpret_cast<const uint4*>(x + static_cast<int64_t>(p) * x_ld + x_coff) + r);
+      p += dp;
+      r += dr;
+      if (r >= cv) {
+        r -= cv;
+        ++p;
       }
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i = i0 + u * stride;
-      if (i < total) {
-        const int p = i / cv;
-        reinterpret_cast<uint4*>(y + static_cast<int64_t>(p) * y_ld + y_coff)[i - p * cv] = v[u];
-      }
-    }
+    for (int u = 0; u < 4; ++u)
+      if (i0 + u * stride < total)
+        reinterpret_cast<uint4*>(y + static_cast<int64_t>(pp[u]) * y_ld + y_coff)[rr[u]] = v[u];
+    p0 = p;
+    r0 = r;
   }
 }
 
@@ -760,8 +772,8 @@ cudaError_t launch_pool(int mode, const __nv_bfloat16* x, int N, int H, int W, i
 
 cudaError_t launch_gap(const __nv_bfloat16* x, int N, int HW, int C, __nv_bfloat16* y, int grid, cudaStream_t s) {
   if (C & 7) return cudaErrorInvalidValue;
-  gap_kernel<<<grid_for(static_cast<int64_t>(N) * ((C / 8 + 31) / 32), 1, grid), kGapWarps * 32, 0, s>>>(x, N, HW,
-                                                                                                       C, y);
+  gap_kernel<<<grid_for(static_cast<int64_t>(N) * ((C / 8 + 31) / 32), kGapWarps, grid), kGapWarps * 32, 0, s>>>(
+      x, N, HW, C, y);
   return cudaGetLastError();
 }
 

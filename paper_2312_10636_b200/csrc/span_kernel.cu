@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       }
       for (int i = 0; i < 2; ++i) {
         mbar_init(&tfull[i], 1);
-        mbar_init(&tempty[i], 256);
+        mbar_init(&tempty[i], 8);  // one arrival per epilogue warp
         mbar_init(&rfull[i], 1);
       }
       mbar_init(bfull, 1);
@@ -398,7 +398,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           }
         }
         tc_fence_before();
-        mbar_arrive(&tempty[acc]);
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(&tempty[acc]);  // one arrival per warp
         if (has_res) {
           named_bar_sync(1, 256);  // all epilogue threads are done with this residual slot
           if (leader && tt + L.has_res < ntile) issue_res(tt + L.has_res);

@@ -7,7 +7,8 @@ everything offloaded when fast, cut after the conv blocks when slow), re-plans w
 against the measured B200 VGG-16 table (x2, the load calibration of the ResNet fleets) and deploys
 the new plan while the old stages drain.  Recorded per epoch with the golden recorder
 (scripts/make_golden.py RecordingSim): the deployment (plan + merged fragments) or keep /
-infeasible.  -> tests/golden/workload/vgg16_churn_s2_c<N>.json, served by scripts/bench_configs.py
+infeasible.  -> tests/golden/workload/vgg16_churn_s<scale>_c<N>.json, served by
+`bench.py --config vgg16_churn` on the wall clock with the route switches at each REPLAN.
 on the wall clock with the route switches at each REPLAN.
 
 (Inception-v3 and BERT-base fleets come from scripts/make_workload.py, MODEL_CFG.)
@@ -90,14 +91,21 @@ def vgg16_churn(n_clients: int):
            "clients": [ClientView.from_reference(c).to_doc() for c in sorted(sc.clients, key=lambda c: c.client_id)],
            "reference_summary": {"generated": rep.generated, "completed": rep.completed, "dropped": rep.dropped,
                                  "p99": rep.latency_p99_ms}}
-    path = OUT / f"vgg16_churn_s2_c{n_clients}.json"
-    path.write_text(json.dumps(out, separators=(",", ":")) + "\n")
     kinds = [e["kind"] for e in sim.epoch_log]
+    if all(k == "infeasible" for k in kinds):
+        print(f"vgg16 churn clients={n_clients}: every epoch infeasible at scale {SCALE:g}; not written")
+        return
+    path = OUT / f"vgg16_churn_s{SCALE:g}_c{n_clients}.json"
+    path.write_text(json.dumps(out, separators=(",", ":")) + "\n")
     print(f"vgg16 churn clients={n_clients}: epochs={kinds} reference generated={rep.generated} "
           f"completed={rep.completed} dropped={rep.dropped}")
 
 
 if __name__ == "__main__":
+    if "--scale" in sys.argv:
+        i = sys.argv.index("--scale")
+        SCALE = float(sys.argv[i + 1])
+        del sys.argv[i:i + 2]
     sizes = [int(x) for x in sys.argv[1].split(",")] if len(sys.argv) > 1 else [128, 256, 512]
     for n in sizes:
         vgg16_churn(n)

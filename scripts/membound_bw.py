@@ -118,7 +118,6 @@ def main():
           lambda: N.check(N.lib().gx_scatter(ctx.handle, k, C.c_void_p(dst.data_ptr()), N.GX_BF16, pix * cc, op_,
                                              N.GX_BF16, 0, C.c_void_p(s.cuda_stream)), "gx_scatter"))
     # FC weight streaming at batch 1 (VGG-16 fc6: 25088 -> 4096, 205 MB of weights), both paths
-    import os
     K, O = 25088, 4096
     blob = WeightBlob()
     w_off = blob.add_bf16(torch.randn(O, K) * 0.01)
@@ -126,13 +125,10 @@ def main():
     wfc = torch.from_numpy(blob.bytes()).cuda()
     x = torch.randn(1, 7, 7, 512, device="cuda").to(bf)
     y = torch.empty(1, O, dtype=bf, device="cuda")
-    op = N.make_op(N.GX_OP_FC, 0, 1, Cin=K, Cout=O, w_off=w_off, b_off=b_off)
-    for path in ("tcgen05", "simt"):
-        if path == "simt":
-            os.environ["GX_FC_SIMT"] = "1"
+    for path, flags in (("tcgen05", 0), ("simt", N.GX_OPF_FC_SIMT)):  # the op flag selects the path
+        op = N.make_op(N.GX_OP_FC, 0, 1, Cin=K, Cout=O, w_off=w_off, b_off=b_off, flags=flags)
         timed(f"fc_{path}", "25088->4096 k=1 (VGG fc6)", K * O * 2 + O * 4 + K * 2 + O * 2,
-              lambda: run_op(op, [x, y], [tensor_desc(7, 7, 512), tensor_desc(1, 1, O)], wfc, 1))
-    os.environ.pop("GX_FC_SIMT", None)
+              lambda op=op: run_op(op, [x, y], [tensor_desc(7, 7, 512), tensor_desc(1, 1, O)], wfc, 1))
     if args.out:
         with open(args.out, "w", newline="") as f:
             w = csv.DictWriter(f, fieldnames=list(rows[0].keys()))

@@ -34,6 +34,8 @@ print(f"  tile: MMA acc-free interval median {np.median(np.diff(mt[:nt])):.0f} c
       f"median {np.median(np.diff(epi[:nt,0])):.0f}; epilogue drain (start->end) median "
       f"{np.median(epi[:nt,1]-epi[:nt,0]):.0f}")
 print(f"  epilogue start - MMA acc-free (same tile) median {np.median(epi[:nt,0]-mt[:nt]):.0f} clk")
+for i in range(min(nk, 12)):
+    print(f"  kb {i:3d}: prod_empty_exit {kb[i,0]-t0:8d}  mma_full_exit {kb[i,1]-t0:8d}  mma_commit {kb[i,2]-t0:8d}")
 for t in range(min(nt, 12)):
     print(f"  tile {t:3d}: mma_acc_free {mt[t]-t0:8d}  epi_start {epi[t,0]-t0:8d}  epi_end {epi[t,1]-t0:8d}"
           f"  store {epi[t,2]-t0 if epi[t,2] else -1:8d}")
