@@ -296,7 +296,7 @@ def run_ours(args):
                          ingress=self.pin() if host else self.dev_in,
                          ingress_from_host=(args.e2e_ingress if host else False), egress_to_host=host,
                          max_inflight=self.max_inflight(), drain_s=drain, sample_outputs=sample,
-                         lane_policy={"split": 0, "least": 1, "time": 2, "earliest": 3}[args.lanes])
+                         lane_policy={"split": 0, "least": 1, "time": 2, "earliest": 3, "edf": 4}[args.lanes])
 
         def max_inflight(self):
             """Device slots: at least --max-inflight, and 1.5x the requests an SLO's worth of
@@ -401,7 +401,7 @@ def run_ours(args):
     # threshold): first the value fleet itself, then down the family to the fleets whose PCIe
     # demand fits the link (fleets above ~85% of it queue on the copy engine without bound)
     family = [w for w in all_wl if _family(w) == _family(wl)]
-    e2e_cands = [w for w in family if _fkey(w) < _fkey(wl) and _h2d_gbs(w) <= 0.85 * PCIE_GBS]
+    e2e_cands = [w for w in family if _fkey(w) < _fkey(wl) and _h2d_gbs(w) <= 0.92 * PCIE_GBS]
     res_e2e = one_run(fleet, True)
     e2e_on_value = res_e2e
     e2e_fleet = fleet
@@ -452,6 +452,21 @@ def run_ours(args):
     sustained, burst, hbm, src = _peaks()
     achieved = conv_flops / (conv_ms * 1e-3) / 1e12
     peak_scaled = burst * inst.sm_budget / ctx.sm_count
+    # attainable time per conv on its SM budget: the tensor peak or the per-SM L2<->SM data path,
+    # whichever binds (profiles/r02_sm_feed_probe.log: bulk reads 86 B/clk, stores 31.5 B/clk, a
+    # concurrent read + write stream ~25 B/clk each), reads = inputs + weights + residual, writes =
+    # the output; the K=64 1x1 convs of layer1/2 write 2 bytes per 128 FLOP and sit on the write path
+    first_op = chain.unit_first_op[st.start]
+    clk_hz = 1.965e9
+    att_s = 0.0
+    for o in convs:
+        op = chain.ops[first_op + o["op"]]
+        H, W, Cc, dt = chain.tensors[op.out]
+        wbytes = st.batch * H * W * (op.Cout or Cc) * (4 if dt == N.GX_F32 else 2)
+        rbytes = max(0.0, o["bytes"] - wbytes)
+        t_tc = o["flops"] / (burst * 1e12 * inst.sm_budget / ctx.sm_count)
+        t_mem = max(rbytes / 86.0, wbytes / 31.5, (rbytes + wbytes) / 50.0) / inst.sm_budget / clk_hz
+        att_s += max(t_tc, t_mem)
     span_flops = st.batch * sum(chain.unit_flops[st.start:st.end])
     traffic = None
     ncu_path = ROOT / "profiles" / "ncu_conv_summary.json"
@@ -524,6 +539,10 @@ def run_ours(args):
                                    f"on {inst.sm_budget} SMs (busiest stage, planned share {st.share}%)",
                          "achieved": round(achieved, 2), "peak": round(peak_scaled, 2), "unit": "TFLOP/s",
                          "frac": round(achieved / peak_scaled, 4), "traffic": traffic,
+                         "attainable": {"frac": round(att_s / (conv_ms * 1e-3), 4),
+                                        "us": round(att_s * 1e6, 1), "measured_us": round(conv_ms * 1000, 1),
+                                        "model": "per conv max(FLOPs / tensor peak x budget/148, per-SM data "
+                                                 "path: reads/86, writes/31.5, (reads+writes)/50 B/clk x budget)"},
                          "avg_launch_us": round(conv_ms * 1000 / max(1, len(convs)), 2),
                          "flops_per_launch": round(conv_flops / max(1, len(convs))),
                          "peak_source": f"{src} bf16_tflops burst ({burst}) x {inst.sm_budget}/{ctx.sm_count} SMs",
@@ -964,7 +983,7 @@ def main():
     ap.add_argument("--sm-oversubscribe", type=float, default=3.0,
                     help="work-conserving SM budgets may sum to this multiple of the GPU's SMs (at most 32 "
                          "batches execute at once, one per hardware queue: budgets summing to 1x leave SMs idle)")
-    ap.add_argument("--lanes", choices=("split", "least", "time", "earliest"), default="split",
+    ap.add_argument("--lanes", choices=("split", "least", "time", "earliest", "edf"), default="split",
                     help="stream-lane policy (graft_exec.h GX_LANE_*): one lane per hardware queue with queues "
                          "reserved for short stages (default), least-loaded of 64 lanes, the same with priorities "
                          "by expected batch time, or one lane per hardware queue, earliest free")

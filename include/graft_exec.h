@@ -316,8 +316,10 @@ typedef struct gx_serve_cfg {
  * GX_LANE_PRIO_BY_TIME: the same with three stream priorities by expected batch time (< 300 us /
  *   < 2 ms / longer; measured: no gain, profiles/r02_lane_priority.log).
  * GX_LANE_EARLIEST: one lane per hardware queue, earliest expected free lane, no reserved queues.
+ * GX_LANE_EDF: the split pools with at most one batch per hardware queue; a batch that finds no idle
+ *   lane of its pool is held by the host and launched earliest-deadline-first when one frees.
  * (Measurements: profiles/r02_lanes_oversubscribe.log.) */
-enum { GX_LANE_SPLIT = 0, GX_LANE_LEAST_LOADED = 1, GX_LANE_PRIO_BY_TIME = 2, GX_LANE_EARLIEST = 3 };
+enum { GX_LANE_SPLIT = 0, GX_LANE_LEAST_LOADED = 1, GX_LANE_PRIO_BY_TIME = 2, GX_LANE_EARLIEST = 3, GX_LANE_EDF = 4 };
 
 enum { GX_TOP1_NONE = 0, GX_TOP1_WITH_LOGITS = 1, GX_TOP1_ONLY = 2 /* no logits kept: egress is 4 B/request */ };
 

@@ -22,7 +22,7 @@ GX_OPF_COUNT_INCLUDE_PAD, GX_OPF_NO_HALO, GX_OPF_FC_SIMT = 1, 2, 4
 GX_CLOCK_VIRTUAL, GX_CLOCK_WALL, GX_CLOCK_REPLAY = 0, 1, 2
 GX_EXEC_GRAPH, GX_EXEC_SPAN = 0, 1
 GX_TOP1_NONE, GX_TOP1_WITH_LOGITS, GX_TOP1_ONLY = 0, 1, 2
-GX_LANE_SPLIT, GX_LANE_LEAST_LOADED, GX_LANE_PRIO_BY_TIME, GX_LANE_EARLIEST = 0, 1, 2, 3
+GX_LANE_SPLIT, GX_LANE_LEAST_LOADED, GX_LANE_PRIO_BY_TIME, GX_LANE_EARLIEST, GX_LANE_EDF = 0, 1, 2, 3, 4
 
 
 class GxTensor(C.Structure):

@@ -507,6 +507,65 @@ __global__ void __launch_bounds__(kGapWarps * 32) gap_kernel(const __nv_bfloat16
   }
 }
 
+// GAP for few items (the batch-1..4 tails of a serving plan): one item per block, its 8 warps split
+// the HW pixels (one load per warp per pixel row of the walk, all in flight) and reduce through
+// shared memory; the per-warp kernel above would leave all but a handful of warps idle and walk 49
+// pixels in 7 dependent rounds.
+__global__ void __launch_bounds__(kGapWarps * 32) gap_split_kernel(const __nv_bfloat16* __restrict__ x, int N, int HW,
+                                                                  int C, __nv_bfloat16* __restrict__ y) {
+  __shared__ float part[kGapWarps][32][9];  // +1 pad: lane-strided rows hit distinct banks
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cv = C / 8;
+  const int groups = (cv + 31) / 32;
+  const float inv = 1.0f / HW;
+  for (int64_t item = blockIdx.x; item < static_cast<int64_t>(N) * groups; item += gridDim.x) {
+    const int n = static_cast<int>(item / groups);
+    const int c8 = static_cast<int>(item % groups) * 32 + lane;
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (c8 < cv) {
+      const uint4* base = reinterpret_cast<const uint4*>(x + static_cast<int64_t>(n) * HW * C) + c8;
+      constexpr int U = 8;
+      for (int p0 = warp; p0 < HW; p0 += kGapWarps * U) {
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int pp = p0 + u * kGapWarps;
+          v[u] = pp < HW ? ldg_stream(base + static_cast<int64_t>(pp) * cv) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 f = unpack_bf16x2(w[j]);
+            acc[2 * j] += f.x;
+            acc[2 * j + 1] += f.y;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) part[warp][lane][j] = acc[j];
+    __syncthreads();
+    if (warp == 0 && c8 < cv) {
+      float t[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        t[j] = 0.0f;
+#pragma unroll
+        for (int w = 0; w < kGapWarps; ++w) t[j] += part[w][lane][j];
+      }
+      uint4 o;
+      o.x = pack_bf16x2(t[0] * inv, t[1] * inv);
+      o.y = pack_bf16x2(t[2] * inv, t[3] * inv);
+      o.z = pack_bf16x2(t[4] * inv, t[5] * inv);
+      o.w = pack_bf16x2(t[6] * inv, t[7] * inv);
+      reinterpret_cast<uint4*>(y + static_cast<int64_t>(n) * C)[c8] = o;
+    }
+    __syncthreads();
+  }
+}
+
 // Skinny FC at small batch (weight-streaming, HBM-bound): y[n][o] = x[n] . w[o] + b[o].
 // Block = 8 warps; warp w owns OPW consecutive output features; lanes stride K in 16-byte
 // vectors.  The batch rows are staged in shared memory one K-chunk at a time (each weight byte is
@@ -772,8 +831,11 @@ cudaError_t launch_pool(int mode, const __nv_bfloat16* x, int N, int H, int W, i
 
 cudaError_t launch_gap(const __nv_bfloat16* x, int N, int HW, int C, __nv_bfloat16* y, int grid, cudaStream_t s) {
   if (C & 7) return cudaErrorInvalidValue;
-  gap_kernel<<<grid_for(static_cast<int64_t>(N) * ((C / 8 + 31) / 32), kGapWarps, grid), kGapWarps * 32, 0, s>>>(
-      x, N, HW, C, y);
+  const int64_t items = static_cast<int64_t>(N) * ((C / 8 + 31) / 32);
+  if (items < 4 * static_cast<int64_t>(grid))  // few items: one block per item, warps split the pixels
+    gap_split_kernel<<<grid_for(items, 1, grid), kGapWarps * 32, 0, s>>>(x, N, HW, C, y);
+  else
+    gap_kernel<<<grid_for(items, kGapWarps, grid), kGapWarps * 32, 0, s>>>(x, N, HW, C, y);
   return cudaGetLastError();
 }
 

@@ -171,6 +171,7 @@ struct gx_serve {
   std::vector<Batch> batches;
   std::vector<int> free_batches;
   std::vector<int> inflight;  // batch ids in flight (WALL)
+  std::vector<int> pending;   // GX_LANE_EDF: batches decided but held until a lane of their pool is idle
   void* results = nullptr;  // fp32 outputs ring (context device) or mapped pinned host
   int32_t* top1s = nullptr;  // GX_TOP1_*: int32 argmax ring, same rows and memory kind as `results`
   int64_t result_elems = 0;
@@ -249,6 +250,13 @@ struct gx_serve {
   int complete(int ri, double now);
   int pick_instance(Stage& st, const Batch& b) const;
   int dispatch_gpu(int si, int bi);
+  bool lane_idle(int dev, int cls) const {
+    const DevRes& dr = devs[dev];
+    for (size_t i = 0; i < dr.pool.size(); ++i)
+      if (dr.pool_cls[i] == cls && dr.pool_n[i] == 0) return true;
+    return false;
+  }
+  int launch_pending();
   int run();
 };
 
@@ -376,7 +384,10 @@ int gx_serve::dispatch_gpu(int si, int bi) {
   // an idle lane of the stage's priority class if there is one, else the class's lane with the
   // fewest / oldest batches in flight
   int lane = -1;
-  if (cfg.lane_policy == GX_LANE_EARLIEST || cfg.lane_policy == GX_LANE_SPLIT) {
+  if (cfg.lane_policy == GX_LANE_EDF) {
+    for (int i = 0; i < static_cast<int>(dr.pool.size()) && lane < 0; ++i)
+      if (dr.pool_cls[i] == st.prio_class && dr.pool_n[i] == 0) lane = i;
+  } else if (cfg.lane_policy == GX_LANE_EARLIEST || cfg.lane_policy == GX_LANE_SPLIT) {
     // the lane (= hardware queue) of the stage's pool expected to free first; ties -> fewer in flight
     for (int i = 0; i < static_cast<int>(dr.pool.size()); ++i) {
       if (dr.pool_cls[i] != st.prio_class) continue;
@@ -456,6 +467,34 @@ int gx_serve::dispatch_gpu(int si, int bi) {
   return GX_OK;
 }
 
+// GX_LANE_EDF: every hardware queue runs at most one batch; batches that find no idle lane of their
+// pool wait here and are launched earliest-deadline-first (the earliest deadline among their
+// requests) as lanes free, instead of queueing FIFO behind whatever batch holds a hardware queue.
+int gx_serve::launch_pending() {
+  while (!pending.empty()) {
+    int best = -1;
+    double best_dl = 0.0;
+    for (size_t i = 0; i < pending.size(); ++i) {
+      const Batch& b = batches[pending[i]];
+      if (!lane_idle(b.dev, stages[b.stage].prio_class)) continue;
+      double dl = 1e300;
+      for (int ri : b.reqs) dl = std::min(dl, reqs[ri].deadline);
+      if (best < 0 || dl < best_dl) {
+        best = static_cast<int>(i);
+        best_dl = dl;
+      }
+    }
+    if (best < 0) return GX_OK;
+    const int bi = pending[best];
+    pending.erase(pending.begin() + best);
+    const double t_a = now_wall();
+    int rc = dispatch_gpu(batches[bi].stage, bi);
+    host_dispatch_ms += now_wall() - t_a;
+    if (rc != GX_OK) return rc;
+  }
+  return GX_OK;
+}
+
 int gx_serve::service(int si, double now) {
   Stage& st = stages[si];
   auto& q = st.queue;
@@ -513,6 +552,10 @@ int gx_serve::service(int si, double now) {
     } else {
       const double t_a = now_wall();
       b.t_disp = t_a;
+      if (cfg.lane_policy == GX_LANE_EDF && !lane_idle(b.dev, st.prio_class)) {
+        pending.push_back(bi);  // launched by launch_pending when a lane of its pool frees
+        continue;
+      }
       int rc = dispatch_gpu(si, bi);
       host_dispatch_ms += now_wall() - t_a;
       if (rc != GX_OK) return rc;
@@ -627,7 +670,8 @@ int gx_serve::run() {
           inflight[i] = inflight.back();
           inflight.pop_back();
           dr.pool_n[b.lane] -= 1;
-          if (cfg.lane_policy == GX_LANE_EARLIEST || cfg.lane_policy == GX_LANE_SPLIT) {
+          if (cfg.lane_policy == GX_LANE_EARLIEST || cfg.lane_policy == GX_LANE_SPLIT ||
+              cfg.lane_policy == GX_LANE_EDF) {
             // the batch ran from about max(dispatch, expected start) to now: refine the stage's estimate
             Stage& xs = stages[b.stage];
             const double took = now - b.t_start_est;
@@ -658,6 +702,7 @@ int gx_serve::run() {
           return cuda_fail(q, "batch completion");
         }
       }
+      if (rc == GX_OK && !pending.empty()) rc = launch_pending();
       if (rc != GX_OK) break;
       while (!heap.empty() && heap.top().t <= now && heap.top().t <= limit + kEps && rc == GX_OK) {
         Ev e = heap.top();
@@ -689,7 +734,7 @@ int gx_serve::run() {
         }
       }
       if (rc != GX_OK) break;
-      if (now > horizon && inflight.empty() && (now > limit || heap.empty() || heap.top().t > limit + kEps)) break;
+      if (now > horizon && inflight.empty() && pending.empty() && (now > limit || heap.empty() || heap.top().t > limit + kEps)) break;
       if (now > limit + 60000.0) return fail(GX_EINTERNAL, "wall-clock serving did not drain");
     }
   }
@@ -749,14 +794,15 @@ int create_gpu_resources(gx_serve* s) {
     // lanes split over the priority classes in use; class c streams get priority greatest + c
     // (lower value = scheduled first when CTAs wait for SMs)
     // GX_LANE_EARLIEST: one lane per hardware queue (the DMA copy stream takes one of the 32)
-    const bool per_queue = cfg.lane_policy == GX_LANE_EARLIEST || cfg.lane_policy == GX_LANE_SPLIT;
+    const bool per_queue = cfg.lane_policy == GX_LANE_EARLIEST || cfg.lane_policy == GX_LANE_SPLIT ||
+                           cfg.lane_policy == GX_LANE_EDF;
     const int lanes = per_queue ? (cfg.ingress_from_host == GX_INGRESS_DMA ? 31 : 32) : std::max(1, dev().serve_streams);
     int least = 0, greatest = 0;
     GX_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
     for (int c = 0; c < s->n_classes; ++c) {
       int n = std::max(1, lanes / s->n_classes + (c < lanes % s->n_classes ? 1 : 0));
       int prio = std::min(least, greatest + c);
-      if (cfg.lane_policy == GX_LANE_SPLIT && s->n_classes == 2) {  // short stages: kSplitShortLanes queues
+      if ((cfg.lane_policy == GX_LANE_SPLIT || cfg.lane_policy == GX_LANE_EDF) && s->n_classes == 2) {  // short stages: kSplitShortLanes queues
         n = c == 0 ? kSplitShortLanes : lanes - kSplitShortLanes;
         prio = 0;
       }
@@ -830,7 +876,7 @@ void classify_stages(gx_serve* s) {
     x.expected_us = x.inst.empty() ? 0.0 : expected_batch_us(x.inst[0], x.batch);
   }
   for (Stage& x : s->stages) x.est_ms = 1.5e-3 * x.expected_us;  // refined by measured batch times
-  if (s->cfg.lane_policy == GX_LANE_SPLIT) {
+  if (s->cfg.lane_policy == GX_LANE_SPLIT || s->cfg.lane_policy == GX_LANE_EDF) {
     // short stages (tail spans at batch 1-2) get hardware queues of their own, so they never wait
     // behind a long batch that shares their queue; everything else shares the remaining queues
     bool any_short = false, any_long = false;

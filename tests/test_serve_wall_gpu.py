@@ -201,3 +201,22 @@ def test_stage_top1_entry_matches_logits_argmax():
     with pytest.raises(ValidationError):
         StageInstance(dm, 2, 6, max_batch=2, sm_budget=4).run_top1(xs[:1])
     del context
+
+
+@pytest.mark.parametrize("lane_policy", [1, 2, 3])
+def test_wall_clock_lane_policies_keep_outputs(lane_policy):
+    """Every stream-lane policy (graft_exec.h GX_LANE_*: least-loaded, priorities by expected time,
+    earliest-free per hardware queue; the default split policy is covered above) serves the same
+    requests to the same logits: lanes change when a batch runs, never what it computes."""
+    from paper_2312_10636_b200.serving import serve
+
+    dep, clients, ctx, instances, dev_in, host_in, expected, keep = _setup()
+    rep = serve(dep, clients, 0.25, ctx=ctx, instances=instances, ingress=dev_in, max_inflight=4096,
+                result_rows=16384, return_outputs=True, drain_s=0.5, lane_policy=lane_policy)
+    ok = np.array([r[4] == "completed" for r in rep.requests])
+    assert rep.generated == rep.completed + rep.dropped + rep.in_flight and ok.sum() > 300
+    ids = [r[0] for r in rep.requests]
+    got = torch.from_numpy(rep.outputs[ok])
+    ref = torch.stack([expected[ids[i]] for i in np.nonzero(ok)[0]])
+    assert ((got - ref).norm(dim=1) / ref.norm(dim=1)).max().item() < 2e-2
+    del keep
