@@ -156,10 +156,11 @@ def test_pool(mode, R, stride, pad):
     assert _rel(y.float().cpu(), ref) < 1e-2
 
 
-def test_gap_and_fc():
+@pytest.mark.parametrize("k,H", [(5, 7), (700, 7), (3, 8)])  # few items (block per item) / many (warp per item)
+def test_gap_and_fc(k, H):
     g = torch.Generator().manual_seed(2)
-    k, HW, Cc, O = 5, 49, 2048, 1000
-    x = torch.randn(k, 7, 7, Cc, generator=g).to(torch.bfloat16)
+    HW, Cc, O = H * H, 2048, 1000
+    x = torch.randn(k, H, H, Cc, generator=g).to(torch.bfloat16)
     w = torch.randn(O, Cc, generator=g) / Cc ** 0.5
     b = torch.randn(O, generator=g)
     pooled_ref = x.float().mean(dim=(1, 2))
@@ -168,7 +169,7 @@ def test_gap_and_fc():
     b_off = blob.add_f32(b)
     wdev = torch.from_numpy(blob.bytes()).cuda()
     pooled = torch.empty(k, Cc, dtype=torch.bfloat16, device="cuda")
-    run_op(N.make_op(N.GX_OP_GAP, 0, 1), [x.cuda(), pooled], [tensor_desc(7, 7, Cc), tensor_desc(1, 1, Cc)], wdev, k)
+    run_op(N.make_op(N.GX_OP_GAP, 0, 1), [x.cuda(), pooled], [tensor_desc(H, H, Cc), tensor_desc(1, 1, Cc)], wdev, k)
     logits = torch.empty(k, O, dtype=torch.float32, device="cuda")
     run_op(N.make_op(N.GX_OP_FC, 0, 1, Cin=Cc, Cout=O, w_off=w_off, b_off=b_off), [pooled, logits],
            [tensor_desc(1, 1, Cc), tensor_desc(1, 1, O, N.GX_F32)], wdev, k)
