@@ -349,9 +349,199 @@ cudaError_t launch_layernorm(const __nv_bfloat16* x, const __nv_bfloat16* res, i
   return cudaGetLastError();
 }
 
+// K6 on the 5th-gen tensor cores (S <= 128, head dim 64: BERT-base).  One CTA of 4 warps owns one
+// (request, head) item at a time, persistent over the items:
+//   TMA     Q and K tiles ([128 rows][64] bf16, 128-byte swizzle) straight into the MMA layout;
+//           V is transposed by the threads into V^T ([2 key blocks][64 d][64 keys], same swizzle);
+//   MMA 1   S = Q K^T : M=128 queries, N=128 keys, K=64  (4 x tcgen05.mma, fp32 in TMEM cols 0-127);
+//           the softmax reads S out completely before MMA 2 writes O over its first 64 columns, and P
+//           takes the shared memory of Q and K: 48 KB and 128 TMEM columns per CTA, 4 items per SM;
+//   softmax thread q = TMEM lane q owns query row q: two passes over its 128 scores (row max, then
+//           exp2 / row sum), P = bf16 probabilities written to shared memory as the next A operand;
+//   MMA 2   O = P V   : M=128, N=64, K=128 keys  (8 x tcgen05.mma, TMEM cols 0-63);
+//   epilogue O / rowsum -> bf16 -> out.  Keys >= S are masked; queries >= S are not stored.
+// One elected thread issues each MMA group and commits it to an mbarrier the 128 threads wait on.
+constexpr int kAttnTcThreads = 128;
+constexpr uint32_t kAttnTcSmem = 1024 + 16384 * 3 + 64;  // Q|K (then P) + V^T + barriers: 4 CTAs per SM
+
+__device__ __forceinline__ void tma_load_2d_attn(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
+          "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void fence_async_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// byte offset of element (row, col) of a [rows][64] bf16 tile with the 128-byte swizzle
+__device__ __forceinline__ uint32_t sw128_off(int row, int col) {
+  return static_cast<uint32_t>(row) * 128u + ((((col >> 3) ^ (row & 7)) & 7) << 4) + (col & 7) * 2;
+}
+
+__global__ void __launch_bounds__(kAttnTcThreads, 4)
+    attention_tc_kernel(const __grid_constant__ CUtensorMap qkmap, const __nv_bfloat16* __restrict__ qkv, int N, int S,
+                        int heads, int hidden, float scale_log2, __nv_bfloat16* __restrict__ out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;               // [128][64]
+  uint8_t* sK = sQ + 16384;         // [128][64]
+  uint8_t* sP = smem;               // [2][128][64]: P overwrites Q and K once S = Q K^T is in TMEM
+  uint8_t* sVt = sK + 16384;        // [2][64][64]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sVt + 16384);  // qk_full, s_full, o_full
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 3);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int i = 0; i < 3; ++i) mbar_init(&bars[i], 1);
+      fence_barrier_init();
+      tma_prefetch_desc(&qkmap);
+    }
+    __syncwarp();
+    tmem_alloc(tslot, 128);  // S (128 columns), then O (64) over it
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+  const int64_t row_ld = 3 * static_cast<int64_t>(hidden);
+  const uint32_t idesc_s = umma_idesc_bf16(128, 128), idesc_o = umma_idesc_bf16(128, 64);
+  pdl_wait();
+  uint32_t ph = 0;
+  for (int it = blockIdx.x; it < N * heads; it += gridDim.x, ph ^= 1) {
+    const int n = it / heads, h = it - n * heads;
+    if (tid == 0) {
+      mbar_arrive_expect_tx(&bars[0], 32768u);
+      tma_load_2d_attn(sQ, &qkmap, &bars[0], h * 64, n * S);
+      tma_load_2d_attn(sK, &qkmap, &bars[0], hidden + h * 64, n * S);
+    }
+    {  // V^T: thread t transposes key t's 64 values (zero rows past S)
+      const int key = tid;
+      uint4 v[8];
+      const uint4* src = reinterpret_cast<const uint4*>(qkv + (static_cast<int64_t>(n) * S + key) * row_ld + 2 * hidden +
+                                                        h * 64);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = key < S ? __ldcg(src + j) : make_uint4(0, 0, 0, 0);
+      uint8_t* vt = sVt + (key >> 6) * 8192;
+      const int kc = key & 63;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v[j]);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          *reinterpret_cast<__nv_bfloat16*>(vt + sw128_off(j * 8 + q, kc)) = e[q];
+      }
+    }
+    fence_async_shared();
+    __syncthreads();
+    if (tid == 0) {  // S = Q K^T
+      mbar_wait(&bars[0], ph);
+      tc_fence_after();
+      const uint64_t qd = umma_desc_sw128(sQ), kd = umma_desc_sw128(sK);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) umma_bf16(tmem, qd + 2 * kk, kd + 2 * kk, idesc_s, kk != 0);
+      umma_commit(&bars[1]);
+    }
+    mbar_wait(&bars[1], ph);
+    tc_fence_after();
+    // softmax of row q over the valid keys: pass 1 max, pass 2 exp2 + sum + P (bf16) to smem
+    const int q = tid;
+    float mx = -INFINITY;
+    for (int c = 0; c < 128; c += 16) {
+      uint32_t r[16];
+      tmem_ld16(tmem + lane_base + c, r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (c + j < S) mx = fmaxf(mx, __uint_as_float(r[j]));
+    }
+    const float mscaled = mx * scale_log2;
+    float sum = 0.0f;
+    for (int c = 0; c < 128; c += 16) {
+      uint32_t r[16];
+      tmem_ld16(tmem + lane_base + c, r);
+      tmem_ld_wait();
+      float pr[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        pr[j] = c + j < S ? exp2f(__uint_as_float(r[j]) * scale_log2 - mscaled) : 0.0f;
+        sum += pr[j];
+      }
+      uint8_t* pt = sP + (c >> 6) * 16384;
+      const int cc = c & 63;
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        uint4 o;
+        o.x = pack_bf16x2(pr[8 * hh + 0], pr[8 * hh + 1]);
+        o.y = pack_bf16x2(pr[8 * hh + 2], pr[8 * hh + 3]);
+        o.z = pack_bf16x2(pr[8 * hh + 4], pr[8 * hh + 5]);
+        o.w = pack_bf16x2(pr[8 * hh + 6], pr[8 * hh + 7]);
+        *reinterpret_cast<uint4*>(pt + sw128_off(q, cc + 8 * hh)) = o;
+      }
+    }
+    fence_async_shared();
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {  // O = P V
+      tc_fence_after();
+#pragma unroll
+      for (int kb = 0; kb < 2; ++kb) {
+        const uint64_t pd = umma_desc_sw128(sP + kb * 16384), vd = umma_desc_sw128(sVt + kb * 8192);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) umma_bf16(tmem, pd + 2 * kk, vd + 2 * kk, idesc_o, (kb | kk) != 0);
+      }
+      umma_commit(&bars[2]);
+    }
+    mbar_wait(&bars[2], ph);
+    tc_fence_after();
+    {  // tcgen05.ld is warp-collective: every lane loads, only rows q < S are stored
+      const float inv = 1.0f / sum;
+      uint4* dst = reinterpret_cast<uint4*>(out + (static_cast<int64_t>(n) * S + q) * hidden + h * 64);
+#pragma unroll
+      for (int c = 0; c < 64; c += 16) {
+        uint32_t r[16];
+        tmem_ld16(tmem + lane_base + c, r);
+        tmem_ld_wait();
+        if (q >= S) continue;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          uint4 o;
+          o.x = pack_bf16x2(__uint_as_float(r[8 * hh + 0]) * inv, __uint_as_float(r[8 * hh + 1]) * inv);
+          o.y = pack_bf16x2(__uint_as_float(r[8 * hh + 2]) * inv, __uint_as_float(r[8 * hh + 3]) * inv);
+          o.z = pack_bf16x2(__uint_as_float(r[8 * hh + 4]) * inv, __uint_as_float(r[8 * hh + 5]) * inv);
+          o.w = pack_bf16x2(__uint_as_float(r[8 * hh + 6]) * inv, __uint_as_float(r[8 * hh + 7]) * inv);
+          dst[(c >> 3) + hh] = o;
+        }
+      }
+    }
+    tc_fence_before();
+    __syncthreads();  // TMEM and the smem tiles are reused by the next item
+  }
+  pdl_launch_dependents();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 128);
+  }
+}
+
 cudaError_t launch_attention(const __nv_bfloat16* qkv, int N, int S, int heads, int dh, __nv_bfloat16* out, int grid,
                              cudaStream_t s) {
   if (dh != 64 || S < 1 || S > 512) return cudaErrorInvalidValue;
+  if (S <= 128) {  // tcgen05 path (BERT-base: S = 128)
+    static bool tc_configured = false;
+    if (!tc_configured) {
+      cudaFuncSetAttribute(attention_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnTcSmem);
+      tc_configured = true;
+    }
+    CUtensorMap map;
+    if (!encode_tmap_2d_bf16(&map, qkv, 3ull * heads * dh, static_cast<uint64_t>(N) * S, 3ull * heads * dh * 2, 64,
+                             128))
+      return cudaErrorInvalidValue;
+    int blocks = N * heads;
+    if (blocks > grid / 2) blocks = std::max(1, grid / 2);  // grid = budget x 8: <= 4 CTAs per budget SM
+    const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(dh));
+    attention_tc_kernel<<<blocks, kAttnTcThreads, kAttnTcSmem, s>>>(map, qkv, N, S, heads, heads * dh, scale_log2,
+                                                                    out);
+    return cudaGetLastError();
+  }
   const int SP = (S + 63) & ~63;
   const size_t smem = (static_cast<size_t>(SP) * (dh + 8) + static_cast<size_t>(dh) * (SP + 8)) * 2;
   static bool configured = false;
