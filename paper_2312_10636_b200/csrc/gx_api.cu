@@ -350,7 +350,7 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
     for (int kk = want; kk >= 2 && a.kps == 1 && !a.res_mma; --kk) {
       int nres2 = 0;
       if (tma && kk <= 3 && a.num_kb >= kk &&
-          conv_pick_stages(a.BN, a.num_kb, epi_res || a.ystore, a.Cout, &nres2, kk, bres_bytes) >= 3)
+          conv_pick_stages(a.BN, a.num_kb, epi_res || a.ystore, a.Cout, &nres2, kk, bres_bytes) >= (a.m_tiles == 1 ? 2 : 3))
         a.kps = kk;
     }
   }

@@ -206,6 +206,7 @@ struct gx_serve {
   uint32_t flag_seq = 0;
   size_t max_inflight_seen = 0;
   int n_classes = 1;  // stream-priority classes (GX_LANE_PRIO_*)
+  int short_lanes = 4;  // GX_LANE_SPLIT / EDF: hardware queues of the short-stage pool
   bool dbg_timing = false;  // GX_SERVE_DEBUG: timing events around each batch (diagnostics only)
   std::chrono::steady_clock::time_point t0;
 
@@ -789,9 +790,9 @@ int gx_serve::run() {
   wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   if (cfg.clock == GX_CLOCK_WALL && getenv("GX_SERVE_DEBUG")) {  // diagnostics only: prints, changes nothing
     fprintf(stderr,
-            "[serve] wall=%.0fms batches=%lld host_copy=%.0fms host_dispatch=%.0fms (%.1fus/batch) host_busy=%.0fms "
+            "[serve] short_lanes=%d wall=%.0fms batches=%lld host_copy=%.0fms host_dispatch=%.0fms (%.1fus/batch) host_busy=%.0fms "
             "event_poll=%.0fms loop_iters=%lld max_inflight=%zu gpus=%zu remote_gathers=%lld\n",
-            wall_ms, static_cast<long long>(n_batches), host_copy_ms, host_dispatch_ms,
+            short_lanes, wall_ms, static_cast<long long>(n_batches), host_copy_ms, host_dispatch_ms,
             n_batches ? 1000.0 * host_dispatch_ms / n_batches : 0.0, busy_ms, poll_ms, static_cast<long long>(loop_iters),
             max_inflight_seen, gpus.size(), static_cast<long long>(remote_gathers));
     for (size_t i = 0; i < stages.size(); ++i) {
@@ -808,7 +809,6 @@ int gx_serve::run() {
 }
 
 namespace {
-constexpr int kSplitShortLanes = 4;      // GX_LANE_SPLIT: queues reserved for short stages
 constexpr double kSplitShortUs = 150.0;  // GX_LANE_SPLIT: a stage is short below this expected batch time
 
 // GPU-clock resources: per device a stream pool, copy streams, a slot pool; peer access between
@@ -851,7 +851,7 @@ int create_gpu_resources(gx_serve* s) {
       int n = std::max(1, lanes / s->n_classes + (c < lanes % s->n_classes ? 1 : 0));
       int prio = std::min(least, greatest + c);
       if ((cfg.lane_policy == GX_LANE_SPLIT || cfg.lane_policy == GX_LANE_EDF) && s->n_classes == 2) {  // short stages: kSplitShortLanes queues
-        n = c == 0 ? kSplitShortLanes : lanes - kSplitShortLanes;
+        n = c == 0 ? s->short_lanes : lanes - s->short_lanes;
         prio = 0;
       }
       for (int i = 0; i < n; ++i) {
@@ -951,6 +951,30 @@ void classify_stages(gx_serve* s) {
       for (Stage& x : s->stages) x.prio_class = 0;
       return;
     }
+    // queues for the short pool from its expected occupancy: each stage's request rate (the clients
+    // routed through it, any epoch), / batch, x ~3x its roofline batch time; twice that plus one
+    // queue, 2..16 (the tail stages of a 3072-client ResNet-50 plan keep ~3 queues busy)
+    std::vector<double> rate(s->stages.size(), 0.0);
+    for (const Client& c : s->clients) {
+      std::vector<int> rs = c.epoch_route;
+      if (rs.empty()) rs.push_back(c.route);
+      std::vector<char> seen(s->stages.size(), 0);
+      for (int ri : rs) {
+        if (ri < 0) continue;
+        const Route& rt = s->routes[ri];
+        for (int j = 0; j < rt.n_stages; ++j)
+          if (!seen[rt.stage[j]]) {
+            seen[rt.stage[j]] = 1;
+            rate[rt.stage[j]] += c.rate;
+          }
+      }
+    }
+    double busy = 0.0;
+    for (size_t i = 0; i < s->stages.size(); ++i) {
+      const Stage& x = s->stages[i];
+      if (x.prio_class == 0) busy += rate[i] / x.batch * std::max(50.0, 3.0 * x.expected_us) * 1e-6;
+    }
+    s->short_lanes = std::min(16, std::max(2, static_cast<int>(std::ceil(2.0 * busy)) + 1));
     s->n_classes = 2;
     return;
   }
