@@ -308,11 +308,12 @@ typedef struct gx_serve_cfg {
 /* A device has CUDA_DEVICE_MAX_CONNECTIONS = 32 hardware queues; a batch is a chain of dependent
  * kernels, so two batches on one queue run one after the other (false serialisation) and at most 32
  * batches execute at once.  Lane policies:
- * GX_LANE_SPLIT (default): one lane per hardware queue, a pool of them reserved for short stages
- *   (expected batch time < 150 us on their SM budget: the tail spans planned at batch 1-2), sized
- *   from those stages' expected queue occupancy (request rate / batch x batch time; 2-16 queues),
- *   the rest for the others; within its pool a batch takes the lane expected to free first (each
- *   lane's queued work is tracked from the stages' measured batch times).
+ * GX_LANE_SPLIT (default): one lane per hardware queue; stages whose full batch is expected to take
+ *   < 150 us on their SM budget (the tail spans at batch 1-2) get a group of queues of their own,
+ *   sized from their expected occupancy (request rate / batch x batch time: twice that plus one,
+ *   2-16 queues), so they never queue behind a long batch; the other stages share the rest; within
+ *   its group a batch takes the lane expected to free first (each lane's queued work is tracked
+ *   from the stages' measured batch times).
  * GX_LANE_LEAST_LOADED: 64 lanes; an idle lane, else the one with the fewest batches in flight.
  * GX_LANE_PRIO_BY_TIME: the same with three stream priorities by expected batch time (< 300 us /
  *   < 2 ms / longer; measured: no gain, profiles/r02_lane_priority.log).

@@ -206,7 +206,8 @@ struct gx_serve {
   uint32_t flag_seq = 0;
   size_t max_inflight_seen = 0;
   int n_classes = 1;  // stream-priority classes (GX_LANE_PRIO_*)
-  int short_lanes = 4;  // GX_LANE_SPLIT / EDF: hardware queues of the short-stage pool
+  int short_lanes = 4;  // GX_LANE_SPLIT / EDF: hardware queues of the first (shortest) pool
+  std::vector<int> class_lanes;  // GX_LANE_SPLIT / EDF: hardware queues per stage group
   bool dbg_timing = false;  // GX_SERVE_DEBUG: timing events around each batch (diagnostics only)
   std::chrono::steady_clock::time_point t0;
 
@@ -789,10 +790,12 @@ int gx_serve::run() {
   }
   wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   if (cfg.clock == GX_CLOCK_WALL && getenv("GX_SERVE_DEBUG")) {  // diagnostics only: prints, changes nothing
+    std::string groups;
+    for (int q : class_lanes) groups += (groups.empty() ? "" : "/") + std::to_string(q);
     fprintf(stderr,
-            "[serve] short_lanes=%d wall=%.0fms batches=%lld host_copy=%.0fms host_dispatch=%.0fms (%.1fus/batch) host_busy=%.0fms "
+            "[serve] lane_groups=%s wall=%.0fms batches=%lld host_copy=%.0fms host_dispatch=%.0fms (%.1fus/batch) host_busy=%.0fms "
             "event_poll=%.0fms loop_iters=%lld max_inflight=%zu gpus=%zu remote_gathers=%lld\n",
-            short_lanes, wall_ms, static_cast<long long>(n_batches), host_copy_ms, host_dispatch_ms,
+            groups.empty() ? "-" : groups.c_str(), wall_ms, static_cast<long long>(n_batches), host_copy_ms, host_dispatch_ms,
             n_batches ? 1000.0 * host_dispatch_ms / n_batches : 0.0, busy_ms, poll_ms, static_cast<long long>(loop_iters),
             max_inflight_seen, gpus.size(), static_cast<long long>(remote_gathers));
     for (size_t i = 0; i < stages.size(); ++i) {
@@ -809,7 +812,10 @@ int gx_serve::run() {
 }
 
 namespace {
-constexpr double kSplitShortUs = 150.0;  // GX_LANE_SPLIT: a stage is short below this expected batch time
+constexpr double kSplitShortUs = 150.0;    // GX_LANE_SPLIT: group bounds on a stage's expected batch time
+// a middle group (bound 1.5 ms) measured worse: the long stages carry most of the GPU time and need
+// most of the queues (profiles/r02_lanes_oversubscribe.log), so medium batches share the long group
+constexpr double kSplitMediumUs = 1e30;
 
 // GPU-clock resources: per device a stream pool, copy streams, a slot pool; peer access between
 // every pair of devices the plan spans (batches gather activations produced on another GPU).
@@ -850,8 +856,9 @@ int create_gpu_resources(gx_serve* s) {
     for (int c = 0; c < s->n_classes; ++c) {
       int n = std::max(1, lanes / s->n_classes + (c < lanes % s->n_classes ? 1 : 0));
       int prio = std::min(least, greatest + c);
-      if ((cfg.lane_policy == GX_LANE_SPLIT || cfg.lane_policy == GX_LANE_EDF) && s->n_classes == 2) {  // short stages: kSplitShortLanes queues
-        n = c == 0 ? s->short_lanes : lanes - s->short_lanes;
+      if ((cfg.lane_policy == GX_LANE_SPLIT || cfg.lane_policy == GX_LANE_EDF) &&
+          static_cast<int>(s->class_lanes.size()) == s->n_classes) {  // queues per stage group
+        n = s->class_lanes[c];
         prio = 0;
       }
       for (int i = 0; i < n; ++i) {
@@ -940,20 +947,10 @@ void classify_stages(gx_serve* s) {
   }
   for (Stage& x : s->stages) x.est_ms = 1.5e-3 * x.expected_us;  // refined by measured batch times
   if (s->cfg.lane_policy == GX_LANE_SPLIT || s->cfg.lane_policy == GX_LANE_EDF) {
-    // short stages (tail spans at batch 1-2) get hardware queues of their own, so they never wait
-    // behind a long batch that shares their queue; everything else shares the remaining queues
-    bool any_short = false, any_long = false;
-    for (Stage& x : s->stages) {
-      x.prio_class = x.expected_us < kSplitShortUs ? 0 : 1;
-      (x.prio_class == 0 ? any_short : any_long) = true;
-    }
-    if (!any_short || !any_long) {  // one kind of stage: every queue serves it
-      for (Stage& x : s->stages) x.prio_class = 0;
-      return;
-    }
-    // queues for the short pool from its expected occupancy: each stage's request rate (the clients
-    // routed through it, any epoch), / batch, x ~3x its roofline batch time; twice that plus one
-    // queue, 2..16 (the tail stages of a 3072-client ResNet-50 plan keep ~3 queues busy)
+    // stages grouped by expected batch time (< 150 us: the tail spans at batch 1-2; < 1.5 ms; longer),
+    // each group with hardware queues of its own, so a batch never waits in a queue behind a batch
+    // of a much longer kind; queues per group follow the group's expected occupancy: per stage its
+    // request rate (the clients routed through it, any epoch) / batch x ~3x its roofline batch time
     std::vector<double> rate(s->stages.size(), 0.0);
     for (const Client& c : s->clients) {
       std::vector<int> rs = c.epoch_route;
@@ -969,13 +966,43 @@ void classify_stages(gx_serve* s) {
           }
       }
     }
-    double busy = 0.0;
+    double occ[3] = {0.0, 0.0, 0.0};
     for (size_t i = 0; i < s->stages.size(); ++i) {
-      const Stage& x = s->stages[i];
-      if (x.prio_class == 0) busy += rate[i] / x.batch * std::max(50.0, 3.0 * x.expected_us) * 1e-6;
+      Stage& x = s->stages[i];
+      x.prio_class = x.expected_us < kSplitShortUs ? 0 : x.expected_us < kSplitMediumUs ? 1 : 2;
+      occ[x.prio_class] += rate[i] / x.batch * std::max(50.0, 3.0 * x.expected_us) * 1e-6;
     }
-    s->short_lanes = std::min(16, std::max(2, static_cast<int>(std::ceil(2.0 * busy)) + 1));
-    s->n_classes = 2;
+    // compact the classes in use to 0..n-1
+    int remap[3] = {-1, -1, -1}, n = 0;
+    std::vector<int> used;
+    for (const Stage& x : s->stages) used.push_back(x.prio_class);
+    for (int c = 0; c < 3; ++c)
+      if (std::find(used.begin(), used.end(), c) != used.end()) remap[c] = n++;
+    for (Stage& x : s->stages) x.prio_class = remap[x.prio_class];
+    s->n_classes = n;
+    s->class_lanes.assign(n, 0);
+    const int lanes = s->cfg.ingress_from_host == GX_INGRESS_DMA ? 31 : 32;
+    // the shorter groups get twice their expected occupancy plus one queue (headroom: their
+    // batches are many and latency-critical), the longest group the rest (at least 8)
+    int given = 0, last = -1;
+    for (int c = 0; c < 3; ++c)
+      if (remap[c] >= 0) last = c;
+    for (int c = 0; c < 3; ++c) {
+      if (remap[c] < 0 || c == last) continue;
+      const int q = std::min(16, std::max(2, static_cast<int>(std::ceil(2.0 * occ[c])) + 1));
+      s->class_lanes[remap[c]] = q;
+      given += q;
+    }
+    s->class_lanes[remap[last]] = lanes - given;
+    while (s->class_lanes[remap[last]] < 8) {  // keep >= 8 for the longest group: trim the others
+      int big = -1;
+      for (int c = 0; c < n; ++c)
+        if (c != remap[last] && (big < 0 || s->class_lanes[c] > s->class_lanes[big])) big = c;
+      if (big < 0 || s->class_lanes[big] <= 2) break;
+      --s->class_lanes[big];
+      ++s->class_lanes[remap[last]];
+    }
+    s->short_lanes = s->class_lanes[0];
     return;
   }
   if (s->cfg.lane_policy != GX_LANE_PRIO_BY_TIME) return;
