@@ -203,10 +203,10 @@ def test_stage_top1_entry_matches_logits_argmax():
     del context
 
 
-@pytest.mark.parametrize("lane_policy", [1, 2, 3])
+@pytest.mark.parametrize("lane_policy", [1, 2, 3, 4])
 def test_wall_clock_lane_policies_keep_outputs(lane_policy):
     """Every stream-lane policy (graft_exec.h GX_LANE_*: least-loaded, priorities by expected time,
-    earliest-free per hardware queue; the default split policy is covered above) serves the same
+    earliest-free per hardware queue, host-held EDF; the default split policy is covered above) serves the same
     requests to the same logits: lanes change when a batch runs, never what it computes."""
     from paper_2312_10636_b200.serving import serve
 
