@@ -980,7 +980,7 @@ def main():
     ap.add_argument("--e2e-ingress", choices=("zero_copy", "dma"), default="dma",
                     help="e2e host ingress: a copy-engine DMA of each request into a device slot at arrival "
                          "(default), or the gather reading pinned host memory over PCIe (zero_copy)")
-    ap.add_argument("--sm-oversubscribe", type=float, default=3.0,
+    ap.add_argument("--sm-oversubscribe", type=float, default=4.0,
                     help="work-conserving SM budgets may sum to this multiple of the GPU's SMs (at most 32 "
                          "batches execute at once, one per hardware queue: budgets summing to 1x leave SMs idle)")
     ap.add_argument("--lanes", choices=("split", "least", "time", "earliest", "edf"), default="split",
