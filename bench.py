@@ -51,11 +51,11 @@ CONFIGS = {
                     "vgg16 fragment groups under network-trace-driven partition-point churn: {n} clients x {rps} rps "
                     "per GPU on a fast/slow bandwidth trace (half out of phase), re-partitioned and re-planned by "
                     "the reference every 2-s epoch, plan transitions served on the wall clock"),
-    "inception_v3": ("inception_v3", "inception_v3_s2_m0", "SLO-met requests/sec (p99<=SLO) for re-aligned "
+    "inception_v3": ("inception_v3", "inception_v3", "SLO-met requests/sec (p99<=SLO) for re-aligned "
                      "Inception-v3 groups",
                      "inception_v3 multi-branch re-aligned fragment groups (ragged gather across concat "
                      "boundaries), {n} clients x {rps} rps per GPU, 8 cut points at the Mixed blocks"),
-    "bert_base": ("bert_base", "bert_base_s2_m0", "SLO-met requests/sec (p99<=SLO) for re-aligned BERT-base "
+    "bert_base": ("bert_base", "bert_base", "SLO-met requests/sec (p99<=SLO) for re-aligned BERT-base "
                   "encoder groups, seq 128",
                   "bert_base encoder fragments split at layer boundaries (cuts 0/3/6/9), seq 128, {n} clients x "
                   "{rps} rps per GPU, shared-suffix GEMM batching"),
