@@ -72,6 +72,10 @@ extern "C" {
 #define GX_OPF_COUNT_INCLUDE_PAD 1 /* avg pool: divisor counts padding (PyTorch default)            */
 #define GX_OPF_NO_HALO 2           /* conv: skip the halo-tile kernel, use the im2col TMA path       */
 #define GX_OPF_FC_SIMT 4           /* FC: CUDA-core weight-streaming kernel instead of tcgen05       */
+#define GX_OPF_DS 8                /* CONV (1x1/1, bf16): in2 is a bottleneck block's input and the op
+                                      also computes its 1x1 downsample (stride = reserved) in the same
+                                      GEMM, K concatenated: y = act(W [in | in2 strided] + b); weights
+                                      [Cout][Cin + C(in2)], bias = both BN-folded biases summed      */
 
 /* activation codes for GX_OP_CONV / GX_OP_LINEAR / GX_OP_FC epilogues */
 #define GX_ACT_NONE 0
@@ -107,7 +111,7 @@ typedef struct gx_op {
   int64_t w_off, b_off, w2_off, w3_off;
   float eps;            /* layernorm epsilon                               */
   int32_t ph_hi, pw_hi; /* conv bottom/right padding; -1 = same as ph / pw  */
-  int32_t reserved;
+  int32_t reserved;     /* GX_OPF_DS: stride of the fused downsample (1 or 2) */
 } gx_op;
 
 typedef struct gx_ctx gx_ctx;     /* one per GPU: device, SM count, driver entry points    */

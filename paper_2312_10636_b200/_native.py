@@ -18,7 +18,7 @@ GX_BF16, GX_F32, GX_I32 = 0, 1, 2
 (GX_OP_CONV, GX_OP_MAXPOOL, GX_OP_AVGPOOL, GX_OP_GAP, GX_OP_FC, GX_OP_LINEAR, GX_OP_LAYERNORM,
  GX_OP_ATTENTION, GX_OP_EMBED, GX_OP_COPY, GX_OP_FLATTEN_NCHW) = range(1, 12)
 GX_ACT_NONE, GX_ACT_RELU, GX_ACT_GELU = 0, 1, 2
-GX_OPF_COUNT_INCLUDE_PAD, GX_OPF_NO_HALO, GX_OPF_FC_SIMT = 1, 2, 4
+GX_OPF_COUNT_INCLUDE_PAD, GX_OPF_NO_HALO, GX_OPF_FC_SIMT, GX_OPF_DS = 1, 2, 4, 8
 GX_CLOCK_VIRTUAL, GX_CLOCK_WALL, GX_CLOCK_REPLAY = 0, 1, 2
 GX_EXEC_GRAPH, GX_EXEC_SPAN = 0, 1
 GX_TOP1_NONE, GX_TOP1_WITH_LOGITS, GX_TOP1_ONLY = 0, 1, 2
@@ -43,13 +43,13 @@ class GxOp(C.Structure):
 
 def make_op(kind, in_, out, in2=-1, out_coff=0, act=GX_ACT_NONE, R=1, S=1, sh=1, sw=1, ph=0, pw=0,
             Cin=0, Cout=0, heads=0, flags=0, w_off=-1, b_off=-1, w2_off=-1, w3_off=-1, eps=0.0, ph_hi=-1,
-            pw_hi=-1):
+            pw_hi=-1, reserved=0):
     op = GxOp()
     op.kind, op.in_, op.in2, op.out, op.out_coff, op.act = kind, in_, in2, out, out_coff, act
     op.R, op.S, op.sh, op.sw, op.ph, op.pw = R, S, sh, sw, ph, pw
     op.Cin, op.Cout, op.heads, op.flags = Cin, Cout, heads, flags
     op.w_off, op.b_off, op.w2_off, op.w3_off, op.eps = w_off, b_off, w2_off, w3_off, eps
-    op.ph_hi, op.pw_hi = ph_hi, pw_hi
+    op.ph_hi, op.pw_hi, op.reserved = ph_hi, pw_hi, reserved
     return op
 
 

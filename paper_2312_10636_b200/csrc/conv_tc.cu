@@ -227,6 +227,7 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
     if (issuer) {
       if (do_b && !a.wsw) tma_prefetch_desc(WM);
       if (do_a) tma_prefetch_desc(AM);
+      if (do_a && a.ds) tma_prefetch_desc(RM);
     }
     const bool loadB = do_b && !skipB && !bres;  // bres: the weights were loaded once, below
     const uint32_t tx = (do_a && !skipA ? kATileBytes : 0u) + (loadB ? b_bytes : 0u);
@@ -281,7 +282,17 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
           // residual x identity block: A = residual columns [nb0 + 64*(kb - num_kb), +64)
           if (issuer && !skipA) tma_load_2d(sa, RM, &sp.full[st], n_blk * BN + (kb - a.num_kb) * 64, m_blk * kBM);
         } else if (do_a) {
-          if (a.a2d) {
+          if (a.ds && kb >= a.kb_split) {
+            // fused downsample (GX_OPF_DS): these k-blocks are the block input's channels at the
+            // output pixels (2D map at stride 1, 1x1 im2col map at the downsample stride)
+            const int cds = (kb - a.kb_split) * kBK;
+            if (issuer && !skipA) {
+              if (a.ds_stride == 1)
+                tma_load_2d(sa, RM, &sp.full[st], cds, m_blk * kBM);
+              else
+                tma_load_im2col_4d(sa, RM, &sp.full[st], cds, wc * a.ds_stride, hc * a.ds_stride, nimg, 0, 0);
+            }
+          } else if (a.a2d) {
             // 1x1 / stride 1 / no padding: A is the plain [M, C] activation matrix
             if (issuer && !skipA) tma_load_2d(sa, AM, &sp.full[st], kb * kBK, m_blk * kBM);
           } else {

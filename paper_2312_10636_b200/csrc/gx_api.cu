@@ -256,6 +256,19 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
   a.pw = gemm1x1 ? 0 : op.pw;
   a.K = R * S * op.Cin;
   a.num_kb = (a.K + kBK - 1) / kBK;
+  const bool ds = (op.flags & GX_OPF_DS) != 0;
+  if (ds) {
+    // the expand 1x1 and the block's 1x1 downsample as one GEMM: K = [in's channels | in2's]
+    if (op.kind != GX_OP_CONV || R != 1 || S != 1 || op.sh != 1 || op.sw != 1 || op.ph != 0 || op.pw != 0 ||
+        op.in2 < 0 || op.Cin % 64 != 0 || op.Cin != ti.C || T[op.in2].C % 64 != 0 || T[op.in2].dtype != GX_BF16 ||
+        op.reserved < 1 || T[op.in2].H != to.H * op.reserved || T[op.in2].W != to.W * op.reserved || for_span)
+      return fail(GX_EINVAL, "fused downsample needs a 1x1/1 conv and a 1x1 downsample over 64-channel blocks");
+    a.K = op.Cin + T[op.in2].C;
+    a.num_kb = a.K / kBK;
+    a.ds = 1;
+    a.kb_split = op.Cin / kBK;
+    a.ds_stride = op.reserved;
+  }
   a.M = k * a.Ho * a.Wo;
   a.Cout = op.Cout;
   a.m_tiles = (a.M + kBM - 1) / kBM;
@@ -309,8 +322,8 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
   a.n_tiles = (a.Cout + a.BN - 1) / a.BN;
   a.num_tiles = a.m_tiles * a.n_tiles;
   a.bias = reinterpret_cast<const float*>(wbase + op.b_off);
-  a.res = op.in2 >= 0 ? static_cast<const __nv_bfloat16*>(ptrs[op.in2]) : nullptr;
-  a.res_ld = op.in2 >= 0 ? T[op.in2].C : 0;
+  a.res = op.in2 >= 0 && !ds ? static_cast<const __nv_bfloat16*>(ptrs[op.in2]) : nullptr;
+  a.res_ld = op.in2 >= 0 && !ds ? T[op.in2].C : 0;
   a.y = ptrs[op.out];
   a.y_ld = to.C;
   a.y_coff = op.out_coff;
@@ -389,6 +402,16 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
   if (a.res && !encode_tmap_2d_bf16(&out->rmap, a.res, a.res_ld, a.M, static_cast<uint64_t>(a.res_ld) * 2, 64,
                                     (a.wstore && !a.res_mma) ? 32 : kBM))
     return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for the residual: " + g_last_encode);
+  if (ds) {  // rmap = the downsample's A operand: in2 at the output pixels (x stride)
+    const gx_tensor& tx = T[op.in2];
+    const void* xb = ptrs[op.in2];
+    const bool ok = a.ds_stride == 1
+                        ? encode_tmap_2d_bf16(&out->rmap, xb, tx.C, a.M, static_cast<uint64_t>(tx.C) * 2, kBK, kBM)
+                        : encode_tmap_im2col_bf16(&out->rmap, xb, tx.C, tx.W, tx.H, k, 0, 0, 0, 0, a.ds_stride,
+                                                  a.ds_stride, 64);
+    if (!ok) return fail(GX_ECUDA, "tensor map encode failed for the fused downsample input: " + g_last_encode);
+    if (!a.tma_a || !a.a2d) return fail(GX_EINVAL, "fused downsample needs the 2D TMA A path");
+  }
   out->grid = std::min(a.num_tiles, std::max(1, sm_budget));
   a.gmaps = nullptr;
   if (dev().gmaps) {  // experiment: maps in global memory (leaks one small buffer per plan)
@@ -413,11 +436,15 @@ void op_work(const gx_op& op, const gx_tensor* T, int k, double* flops, double* 
     case GX_OP_CONV:
     case GX_OP_LINEAR: {
       const int R = op.kind == GX_OP_LINEAR ? 1 : op.R, S = op.kind == GX_OP_LINEAR ? 1 : op.S;
-      const double K = static_cast<double>(R) * S * op.Cin;
+      double K = static_cast<double>(R) * S * op.Cin;
+      if (op.flags & GX_OPF_DS) {  // + the fused downsample: in2 read once at the output pixels
+        K += T[op.in2].C;
+        b = out_px * T[op.in2].C * es_in;
+      }
       f = 2.0 * out_px * op.Cout * K;
-      b = in_px * op.Cin * es_in + static_cast<double>(op.Cout) * K * es_in + op.Cout * 4.0 +
-          out_px * op.Cout * es_out;
-      if (op.in2 >= 0) b += out_px * op.Cout * es_in;
+      b += in_px * op.Cin * es_in + static_cast<double>(op.Cout) * K * es_in + op.Cout * 4.0 +
+           out_px * op.Cout * es_out;
+      if (op.in2 >= 0 && !(op.flags & GX_OPF_DS)) b += out_px * op.Cout * es_in;
       break;
     }
     case GX_OP_MAXPOOL:
@@ -467,6 +494,7 @@ int launch_op_f32(const gx_op& op, const gx_tensor* T, void* const* ptrs, const 
   const gx_tensor& ti = T[op.in];
   const gx_tensor& to = T[op.out];
   if (to.dtype != GX_F32) return fail(GX_EINVAL, "fp32 op writes a non-fp32 tensor");
+  if (op.flags & GX_OPF_DS) return fail(GX_EINVAL, "fp32 chains take the unfused downsample");
   const float* x = static_cast<const float*>(ptrs[op.in]);
   float* y = static_cast<float*>(ptrs[op.out]);
   switch (op.kind) {

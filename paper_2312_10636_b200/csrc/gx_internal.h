@@ -78,6 +78,9 @@ struct ConvArgs {
                        // once and stay in smem; with res_mma the residual is added by N=64 MMAs into
                        // the accumulator's 64-column slices against one resident 64x64 identity block
   uint32_t idesc64;    // instruction descriptor of those M=128, N=64 MMAs
+  int ds;              // GX_OPF_DS: k-blocks >= kb_split take A from the block input (rmap): a 2D map
+  int kb_split;        // over [M][Cx] (ds_stride 1) or a 1x1 im2col map at the downsample stride
+  int ds_stride;
 };
 constexpr int kConvThreads = 320;  // span kernel: 4 A-producer warps, TMA warp, MMA warp, 4 epilogue warps
 // conv_tc: warps 0-3 cp.async A producers (or epilogue when TMA builds A), 4 A/B TMA, 5 MMA,

@@ -41,8 +41,8 @@ unsigned long long* debug_trace_buffer();
 // identity k-blocks appended to the op's pre-swizzled weights (the epilogue then has no residual
 // traffic), when the op's planning confirms the 2D A path (plan_conv).
 inline bool res_through_mma(const gx_op& op) {
-  return op.kind == GX_OP_CONV && op.in2 >= 0 && op.R == 1 && op.S == 1 && op.sh == 1 && op.sw == 1 && op.ph == 0 &&
-         op.pw == 0 && op.Cout % 64 == 0 && op.Cin % 64 == 0;
+  return op.kind == GX_OP_CONV && op.in2 >= 0 && !(op.flags & GX_OPF_DS) && op.R == 1 && op.S == 1 && op.sh == 1 &&
+         op.sw == 1 && op.ph == 0 && op.pw == 0 && op.Cout % 64 == 0 && op.Cin % 64 == 0;
 }
 // FC (GX_OP_FC) on the tcgen05 GEMM path: the flattened per-sample input is a [k, K] row-major A
 // operand (1x1 conv on a 1x1 image with Cin = K), the [Cout][K] weights the B operand.  Needs whole

@@ -273,7 +273,8 @@ cudaError_t build_bulk_weights(gx_model* m, const uint8_t* blob) {
     const gx_op& op = m->ops[i];
     if (!is_tc_op(op, m->tensors.data())) continue;
     const int R = op.kind != GX_OP_CONV ? 1 : op.R, S = op.kind != GX_OP_CONV ? 1 : op.S;
-    const size_t kpad = (static_cast<size_t>(R) * S * op.Cin + 63) / 64 * 64;
+    const size_t kpad = (static_cast<size_t>(R) * S * op.Cin + 63) / 64 * 64 +
+                        ((op.flags & GX_OPF_DS) ? static_cast<size_t>(m->tensors[op.in2].C) : 0);
     m->wsw_off[i] = static_cast<int64_t>(total);
     total += (kpad + (res_through_mma(op) ? op.Cout : 0)) * op.Cout * 2;
   }
@@ -284,7 +285,8 @@ cudaError_t build_bulk_weights(gx_model* m, const uint8_t* blob) {
     if (m->wsw_off[i] < 0) continue;
     const gx_op& op = m->ops[i];
     const int R = op.kind != GX_OP_CONV ? 1 : op.R, S = op.kind != GX_OP_CONV ? 1 : op.S;
-    const size_t kpad = (static_cast<size_t>(R) * S * op.Cin + 63) / 64 * 64;
+    const size_t kpad = (static_cast<size_t>(R) * S * op.Cin + 63) / 64 * 64 +
+                        ((op.flags & GX_OPF_DS) ? static_cast<size_t>(m->tensors[op.in2].C) : 0);
     const size_t nkb = kpad / 64;
     const uint8_t* src = blob + op.w_off;  // [Cout][kpad] bf16
     uint8_t* dst = h.data() + m->wsw_off[i];

@@ -164,6 +164,29 @@ class ChainBuilder:
         self._flops += flops if flops is not None else 2.0 * Ho * Wo * cout * cin * R * S
         return out
 
+    def conv_ds(self, t, conv: nn.Conv2d, bn: nn.BatchNorm2d, x, ds_conv: nn.Conv2d, ds_bn: nn.BatchNorm2d,
+                relu=True):
+        """A bottleneck's expand 1x1 conv and its block's 1x1 downsample as ONE GEMM (GX_OPF_DS): K is
+        [t's channels | x's channels at the downsample's stride], weights [W3 | Wds], bias b3 + bds; the
+        downsample's output (the residual) is never written or read back."""
+        w3, b3 = self.folded(conv, bn)
+        wd, bd = self.folded(ds_conv, ds_bn)
+        H, W, Ct, _ = self.shape(t)
+        Hx, Wx, Cx, _ = self.shape(x)
+        stride = ds_conv.stride[0]
+        assert conv.kernel_size == (1, 1) and ds_conv.kernel_size == (1, 1) and conv.stride == (1, 1)
+        assert (Hx + stride - 1) // stride == H and Ct % 64 == 0 and Cx % 64 == 0
+        cout = w3.shape[0]
+        out = self.tensor(H, W, cout)
+        w = torch.cat([pack_conv_weight(w3), pack_conv_weight(wd)], dim=1)
+        w_off = self.add_weight(w)
+        b_off = self.c.blob.add_f32(b3 + bd)
+        self.c.ops.append(N.make_op(N.GX_OP_CONV, t, out, in2=x, act=N.GX_ACT_RELU if relu else N.GX_ACT_NONE,
+                                    Cin=Ct, Cout=cout, w_off=w_off, b_off=b_off, flags=N.GX_OPF_DS,
+                                    reserved=stride))
+        self._flops += 2.0 * H * W * cout * (Ct + Cx)
+        return out
+
     def s2d_stem(self, conv: nn.Conv2d, bn: nn.BatchNorm2d | None, image_hw: int, relu=True):
         """A 7x7 stride-2 pad-3 stem as the equivalent 4x4 stride-1 conv over the 2x2
         space-to-depth image (channel (dy*2+dx)*3 + c), padding (2, 2, 1, 1).
@@ -285,8 +308,11 @@ def torch_model(name: str, seed: int = 0) -> nn.Module:
 # chain builders
 # ---------------------------------------------------------------------------------------------
 
-def _resnet_chain(name: str, m, dtype=BF16) -> UnitChain:
+def _resnet_chain(name: str, m, dtype=BF16, fuse_downsample: bool | None = None) -> UnitChain:
+    """fuse_downsample (default: bf16 chains): each bottleneck's downsample 1x1 is computed inside its
+    expand conv's GEMM (GX_OPF_DS) instead of as an op whose output is the residual."""
     b = ChainBuilder(name, dtype)
+    fuse = dtype == BF16 if fuse_downsample is None else fuse_downsample
     # boundary 0: the 3-channel 224x224 image, rearranged by the gather into 2x2 space-to-depth
     # blocks (112x112x16) so the 7x7/2 stem runs as a 4x4/1 conv with 32-byte im2col pixels
     y = b.s2d_stem(m.conv1, m.bn1, 224)
@@ -295,12 +321,16 @@ def _resnet_chain(name: str, m, dtype=BF16) -> UnitChain:
         for blk in layer:
             b.begin_unit(y)
             idn = y
-            if blk.downsample is not None:
+            bottleneck = hasattr(blk, "conv3")
+            if blk.downsample is not None and not (bottleneck and fuse):
                 idn = b.conv(y, blk.downsample[0], blk.downsample[1], relu=False)
-            if hasattr(blk, "conv3"):  # bottleneck
+            if bottleneck:
                 t = b.conv(y, blk.conv1, blk.bn1, relu=True)
                 t = b.conv(t, blk.conv2, blk.bn2, relu=True)
-                y = b.conv(t, blk.conv3, blk.bn3, relu=True, residual=idn)
+                if blk.downsample is not None and fuse:
+                    y = b.conv_ds(t, blk.conv3, blk.bn3, y, blk.downsample[0], blk.downsample[1])
+                else:
+                    y = b.conv(t, blk.conv3, blk.bn3, relu=True, residual=idn)
             else:  # basic block
                 t = b.conv(y, blk.conv1, blk.bn1, relu=True)
                 y = b.conv(t, blk.conv2, blk.bn2, relu=True, residual=idn)
@@ -444,12 +474,15 @@ def _inception_chain(m, dtype=BF16) -> UnitChain:
     return b.finish(out)
 
 
-def build_chain(name: str, seed: int = 0, module: nn.Module | None = None, dtype: int = BF16) -> UnitChain:
+def build_chain(name: str, seed: int = 0, module: nn.Module | None = None, dtype: int = BF16,
+                fuse_downsample: bool | None = None) -> UnitChain:
     """The unit chain of `name` with its parameters; dtype F32 builds the fp32 execution mode (same
-    units, boundaries and weights, every tensor fp32)."""
+    units, boundaries and weights, every tensor fp32).  fuse_downsample: ResNet bottlenecks compute
+    the downsample inside the expand GEMM (default for bf16 chains; the span kernel and the fp32
+    kernels take the unfused form)."""
     m = module if module is not None else torch_model(name, seed)
     if name in ("resnet50", "resnet18"):
-        return _resnet_chain(name, m, dtype)
+        return _resnet_chain(name, m, dtype, fuse_downsample)
     if name == "vgg16":
         return _vgg16_chain(m, dtype)
     if name == "inception_v3":

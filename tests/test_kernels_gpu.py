@@ -381,3 +381,36 @@ def test_gather_ex_space_to_depth_bit_exact(f, c_src, c_dst, H, dst_f32):
                                  3, C.c_void_p(torch.cuda.current_stream().cuda_stream)))
     torch.cuda.synchronize()
     assert torch.equal(out.cpu(), ref.to(dt))
+
+
+@pytest.mark.parametrize("k,H,Ct,Cx,Cout,stride,budget", [
+    (3, 56, 64, 64, 256, 1, 4),      # layer1 block 0 (downsample at stride 1)
+    (2, 28, 128, 256, 512, 2, 6),    # layer2 block 0: block input 56x56x256 at stride 2
+    (1, 7, 512, 1024, 2048, 2, 3),   # layer4 block 0 at batch 1
+    (5, 14, 256, 512, 1024, 2, 148),
+])
+def test_conv_fused_downsample_matches_torch(k, H, Ct, Cx, Cout, stride, budget):
+    """GX_OPF_DS: a bottleneck's expand 1x1 and its block's 1x1 downsample as one K-concatenated
+    GEMM, y = relu(W3 t + Wd x[::s, ::s] + b3 + bd), against the two convs in fp32."""
+    g = torch.Generator().manual_seed(11)
+    t = torch.randn(k, H, H, Ct, generator=g).to(torch.bfloat16)
+    x = torch.randn(k, H * stride, H * stride, Cx, generator=g).to(torch.bfloat16)
+    w3 = torch.randn(Cout, Ct, 1, 1, generator=g) / Ct ** 0.5
+    wd = torch.randn(Cout, Cx, 1, 1, generator=g) / Cx ** 0.5
+    b = torch.randn(Cout, generator=g) * 0.1
+    ref = (F.conv2d(t.float().permute(0, 3, 1, 2), w3.to(torch.bfloat16).float()) +
+           F.conv2d(x.float().permute(0, 3, 1, 2), wd.to(torch.bfloat16).float(), stride=stride) +
+           b.view(1, -1, 1, 1)).clamp_min(0).permute(0, 2, 3, 1)
+    blob = WeightBlob()
+    w_off = blob.add_bf16(torch.cat([pack_conv_weight(w3), pack_conv_weight(wd)], dim=1))
+    b_off = blob.add_f32(b)
+    wdev = torch.from_numpy(blob.bytes()).cuda()
+    y = torch.full((k, H, H, Cout), float("nan"), dtype=torch.bfloat16, device="cuda")
+    op = N.make_op(N.GX_OP_CONV, 0, 1, in2=2, act=N.GX_ACT_RELU, Cin=Ct, Cout=Cout, w_off=w_off, b_off=b_off,
+                   flags=N.GX_OPF_DS, reserved=stride)
+    run_op(op, [t.cuda(), y, x.cuda()],
+           [tensor_desc(H, H, Ct), tensor_desc(H, H, Cout), tensor_desc(H * stride, H * stride, Cx)], wdev, k, budget)
+    torch.cuda.synchronize()
+    got = y.float().cpu()
+    assert torch.isfinite(got).all()
+    assert _rel(got, ref) < 1.5e-2

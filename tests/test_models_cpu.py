@@ -62,7 +62,9 @@ def test_fp32_chain_mirrors_bf16_chain(name):
     tensor fp32 and weights stored fp32 (twice the bf16 bytes for conv / linear / FC weights)."""
     from paper_2312_10636_b200 import _native as N
     m = torch_model(name)
-    a = build_chain(name, module=m)
+    # (bf16 ResNet-50 chains fuse each downsample into its expand GEMM; the fp32 mode keeps it apart)
+    a = build_chain(name, module=m, fuse_downsample=False) if name in ("resnet18", "resnet50") else \
+        build_chain(name, module=m)
     b = build_chain(name, module=m, dtype=N.GX_F32)
     assert b.dtype == N.GX_F32 and a.dtype == N.GX_BF16
     assert a.boundary == b.boundary and a.unit_first_op == b.unit_first_op
@@ -88,3 +90,18 @@ def test_bert_boundary_zero_ships_token_ids():
     assert chain.payload_bytes(0) == 512 and chain.payload_bytes(6) == 393216
     assert chain.ops[chain.unit_first_op[0]].kind == N.GX_OP_EMBED
     assert chain.model_spec_doc()["input_bytes"] == 512
+
+
+def test_fused_downsample_chain_keeps_units():
+    """The fused ResNet-50 chain (GX_OPF_DS) has the unfused chain's units, boundary shapes, payloads
+    and FLOPs, with four ops fewer (one per stage's first bottleneck)."""
+    from paper_2312_10636_b200 import _native as N
+    m = torch_model("resnet50")
+    a = build_chain("resnet50", module=m)
+    b = build_chain("resnet50", module=m, fuse_downsample=False)
+    assert a.n_units == b.n_units and len(a.ops) == len(b.ops) - 4
+    assert [a.boundary_shape(p) for p in range(a.n_units + 1)] == [b.boundary_shape(p) for p in range(b.n_units + 1)]
+    assert [round(f) for f in a.unit_flops] == [round(f) for f in b.unit_flops]
+    ds = [o for o in a.ops if o.flags & N.GX_OPF_DS]
+    assert [(o.Cin, a.tensors[o.in2][2], o.Cout, o.reserved) for o in ds] == [
+        (64, 64, 256, 1), (128, 256, 512, 2), (256, 512, 1024, 2), (512, 1024, 2048, 2)]

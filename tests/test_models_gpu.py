@@ -125,8 +125,10 @@ def test_span_kernel_matches_per_op_path(budget):
     graph path compute the same span.  The per-op path sums the wide 3x3 convs in halo order and
     adds the expand convs' residual inside the MMA, so the two agree to bf16 rounding, and both
     agree with the fp32 oracle."""
-    from paper_2312_10636_b200.engine import StageInstance
-    m, chain, dm = _setup("resnet50")
+    from paper_2312_10636_b200.engine import DeviceModel, StageInstance
+    m, _chain, _dm = _setup("resnet50")
+    chain = build_chain("resnet50", module=m, fuse_downsample=False)  # the span kernel takes unfused ops
+    dm = DeviceModel(chain)
     x = torch.randn(3, 3, 224, 224, generator=torch.Generator().manual_seed(5))
     inp = _inputs(x)
     ref = StageInstance(dm, 0, chain.n_units, max_batch=4, sm_budget=budget).run(inp, src_channels=3)
