@@ -402,6 +402,11 @@ def run_ours(args):
     # demand fits the link (fleets above ~85% of it queue on the copy engine without bound)
     family = [w for w in all_wl if _family(w) == _family(wl)]
     e2e_cands = [w for w in family if _fkey(w) < _fkey(wl) and _h2d_gbs(w) <= 0.92 * PCIE_GBS]
+    if not e2e_cands:  # the value fleet's family has no fleet within the link: the nearest family that does
+        fams = sorted({_family(w) for w in all_wl if _h2d_gbs(w) <= 0.92 * PCIE_GBS},
+                      key=lambda f: (abs(f[0] - _family(wl)[0]), abs(f[1] - _family(wl)[1])))
+        if fams:
+            e2e_cands = [w for w in all_wl if _family(w) == fams[0] and _h2d_gbs(w) <= 0.92 * PCIE_GBS]
     res_e2e = one_run(fleet, True)
     e2e_on_value = res_e2e
     e2e_fleet = fleet
