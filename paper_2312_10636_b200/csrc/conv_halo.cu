@@ -10,6 +10,11 @@
 // at nine row offsets, and each input pixel crosses L2->SM
 // once per M tile instead of nine times.
 //
+// Images wider than a tile (Inception's 147x147 stem convs) are cut into column tiles: an M tile is
+// BH output rows x WT output columns of one image, its halo (BH + R - 1) x (WT + S - 1) input pixels
+// with pitch Wp = WT + S - 1, and the same row-offset trick holds inside the tile.  RB = 64: the
+// 32-channel inputs (SWIZZLE_64B rows), two taps per weight k-block, two K=16 MMAs per tap.
+//
 // Roles (352 threads): warp 4 halo producer, warp 10 weight producer (bulk copies of the
 // pre-swizzled [kb][Cout][64] tiles, kb = tap*Cin/64 + cb), one elected lane of warp 5 issues the
 // MMAs, warps 0-3 and 6-9 run the epilogue (bias, ReLU, bf16, row-remapped stores).
@@ -62,9 +67,11 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
   const int S_ = a.stages;
   const int BN = a.BN;
   const uint32_t b_bytes = static_cast<uint32_t>(BN) * 128u;
-  const int Wp = a.hWp, BH = a.hBH, TPI = a.hTPI;
+  const int Wp = a.hWp, BH = a.hBH, TPI = a.hTPI, WT = a.hWT, CT = a.hCT;
   const int CB = RB == 128 ? a.Cin / 64 : 1;
-  const int NKB = RB == 128 ? 9 : a.R;  // weight k-blocks per channel block
+  // weight k-blocks per channel block: one per tap (128-byte rows), per filter row (the 32-byte
+  // s2d stem), per pair of taps (64-byte rows: 32 channels)
+  const int NKB = RB == 128 ? 9 : RB == 32 ? a.R : (a.R * a.S + 1) / 2;
   const uint32_t hbytes = static_cast<uint32_t>(Wp * (BH + a.R - 1) * RB);
   // one N tile and one channel block (the stem; layer1's 56x56x64 3x3): the NKB weight k-blocks
   // are loaded once into ring slots 0..NKB-1 and stay resident.  Every tile would otherwise
@@ -73,7 +80,7 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
   const bool resident = a.n_tiles == 1 && S_ >= NKB && CB == 1 && !(a.dbg & 32);  // GX_CONV_DBG=32: ring as before
   // the stem's halo is ~15 KB and one tile's MMAs take ~0.3 us: four buffers keep enough TMA loads
   // in flight to cover their latency
-  constexpr int NH = RB == 32 ? 4 : 2;
+  constexpr int NH = RB == 128 ? 2 : 4;
   constexpr uint32_t HB = 2u * kHaloBytes / NH;
   HaloSmem sp;
   sp.halo = smem;
@@ -124,12 +131,13 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
     uint32_t hph = 0;
     for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
       const int m_blk = tile / a.n_tiles;
-      const int n = m_blk / TPI, h0 = (m_blk % TPI) * BH;
+      const int n = m_blk / (TPI * CT), rc = m_blk % (TPI * CT);
+      const int h0 = (rc / CT) * BH, c0 = (rc % CT) * WT;
       for (int cb = 0; cb < CB; ++cb) {
         mbar_wait(&sp.hempty[hs], hph ^ 1);
         if (issuer) {
           mbar_arrive_expect_tx(&sp.hfull[hs], hbytes);
-          tma_load_4d(sp.halo + hs * HB, &hmap, &sp.hfull[hs], cb * 64, -a.pw, h0 - a.ph, n);
+          tma_load_4d(sp.halo + hs * HB, &hmap, &sp.hfull[hs], cb * 64, c0 - a.pw, h0 - a.ph, n);
         }
         __syncwarp();
         if (++hs == NH) {
@@ -207,6 +215,21 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
               for (int kk = 0; kk < 4; ++kk)
                 umma_bf16(d, ad + 2 * kk, bd + 2 * kk, a.idesc, (cb | tap | kk) != 0);
             }
+          } else if (RB == 64) {
+            // k-block `tap` holds taps 2*tap and 2*tap+1 (32 channels each): two K=16 MMAs per tap,
+            // A = the halo started r*Wp + s pixel rows later (64-byte rows, SWIZZLE_64B)
+            if (issuer) {
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int t9 = 2 * tap + h;
+                if (t9 >= a.R * a.S) break;
+                const int r = t9 / a.S, s = t9 - r * a.S;
+#pragma unroll
+                for (int kk = 0; kk < 2; ++kk)
+                  umma_bf16(d, umma_desc_kmajor(hbase + static_cast<uint32_t>(r * Wp + s) * 64u, 32, 0) + 2 * kk,
+                            bd + 2 * (2 * h + kk), a.idesc, (tap | h | kk) != 0);
+              }
+            }
           } else if (issuer) {
             // k-block `tap` = filter row r; its K slice s (32 bytes) is tap (r, s), whose A operand
             // is the halo started r*Wp + s pixel rows later (SWIZZLE_32B on absolute address bits,
@@ -240,7 +263,7 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
     const int q = warp & 3;
     const int half = warp < 4 ? 1 : 0;
     const int row = q * 32 + lane;  // virtual row u of the tile
-    const int i = row / Wp, j = row - (row / Wp) * Wp;
+    const int i = row / Wp, j = row - (row / Wp) * Wp;  // output (h0 + i, c0 + j) of the tile
     if (warp == 6 && lane == 0) {
       mbar_arrive_expect_tx(sp.biasbar, static_cast<uint32_t>(a.Cout) * 4u);
       bulk_load(sp.bias, a.bias, static_cast<uint32_t>(a.Cout) * 4u, sp.biasbar);
@@ -249,8 +272,9 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
     int t = 0;
     for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++t) {
       const int m_blk = tile / a.n_tiles, n_blk = tile % a.n_tiles;
-      const int n = m_blk / TPI, h = (m_blk % TPI) * BH + i;
-      const bool row_ok = i < BH && j < a.W && h < a.H;
+      const int n = m_blk / (TPI * CT), rc = m_blk % (TPI * CT);
+      const int h = (rc / CT) * BH + i, w = (rc % CT) * WT + j;
+      const bool row_ok = i < BH && j < WT && h < a.Ho && w < a.Wo;
       const int nb0 = n_blk * BN;
       const int ncols = min(BN, a.Cout - nb0);
       const int acc = t & 1;
@@ -259,7 +283,7 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
       const uint32_t tbase = tmem_base + acc * acc_stride + (static_cast<uint32_t>(q * 32) << 16);
       const uint32_t bias_s = smem_u32(sp.bias + nb0);
       __nv_bfloat16* yrow = static_cast<__nv_bfloat16*>(a.y) +
-                            ((static_cast<size_t>(n) * a.H + h) * a.W + j) * a.y_ld + a.y_coff + nb0;
+                            ((static_cast<size_t>(n) * a.Ho + h) * a.Wo + w) * a.y_ld + a.y_coff + nb0;
       for (int c = half * 16; c < BN; c += 32) {
         uint32_t v[16];
         tmem_ld16(tbase + c, v);
@@ -325,6 +349,8 @@ cudaError_t launch_conv_halo(const CUtensorMap& wmap, const CUtensorMap& hmap, c
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(conv_halo_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(conv_halo_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    if (e != cudaSuccess) return e;
     configured = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -338,6 +364,7 @@ cudaError_t launch_conv_halo(const CUtensorMap& wmap, const CUtensorMap& hmap, c
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
   if (a.hRB == 32) return cudaLaunchKernelEx(&cfg, conv_halo_kernel<32>, wmap, hmap, a);
+  if (a.hRB == 64) return cudaLaunchKernelEx(&cfg, conv_halo_kernel<64>, wmap, hmap, a);
   return cudaLaunchKernelEx(&cfg, conv_halo_kernel<128>, wmap, hmap, a);
 }
 

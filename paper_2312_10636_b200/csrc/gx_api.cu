@@ -180,7 +180,8 @@ bool encode_tmap_halo_bf16(CUtensorMap* map, const void* base, int C, int W, int
                        1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, box_c == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE,
+            box_c == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : box_c == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -279,16 +280,39 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
   // MMA per tap, 128 // (W + 3) output rows per tile
   const bool halo32 = R == 4 && S == 4 && a.ph == 2 && a.pw == 2 && op.ph_hi == 1 && op.pw_hi == 1 && op.Cin == 16 &&
                       ti.W + 3 <= kBM && !dev().no_halo32;
-  if (!for_span && op.kind == GX_OP_CONV && (halo128 || halo32) && a.sh == 1 && a.sw == 1 && op.Cin == ti.C &&
-      a.Ho == ti.H && a.Wo == ti.W && op.in2 < 0 && to.dtype == GX_BF16 && !dev().no_halo &&
-      !(op.flags & GX_OPF_NO_HALO)) {
-    const int Wp = ti.W + (halo32 ? 3 : 2);
+  // 3x3 / stride 1 / pad 0 or 1 on images wider than a tile row (Inception's 147x147 stem convs) or
+  // over 32 channels: column tiles of WT output columns, 64-byte halo rows for 32 channels
+  const bool sym01 = a.ph == a.pw && a.ph <= 1 && (op.ph_hi < 0 || op.ph_hi == a.ph) && (op.pw_hi < 0 || op.pw_hi == a.pw);
+  const bool halo_wide = !halo128 && R == 3 && S == 3 && sym01 && (op.Cin % 64 == 0 || op.Cin == 32) && ti.W >= 28 &&
+                         a.Wo >= 28;
+  if (!for_span && op.kind == GX_OP_CONV && (halo128 || halo32 || halo_wide) && a.sh == 1 && a.sw == 1 &&
+      op.Cin == ti.C && (halo_wide || (a.Ho == ti.H && a.Wo == ti.W)) && op.in2 < 0 && to.dtype == GX_BF16 &&
+      !dev().no_halo && !(op.flags & GX_OPF_NO_HALO)) {
+    int WT = a.Wo, Wp = ti.W + (halo32 ? 3 : 2), BH = std::min(ti.H, kBM / Wp);
+    if (halo_wide) {
+      // the column-tile width with the fewest tiles: BH = 128 / (WT + 2) rows per tile, the halo
+      // ((BH + 2) x (WT + 2) pixels) within one 256-row halo buffer
+      int64_t best = INT64_MAX;
+      for (int wt = 16; wt <= std::min(62, a.Wo); ++wt) {
+        const int bh = std::min(a.Ho, kBM / (wt + 2));
+        if (bh < 1 || (bh + 2) * (wt + 2) > 256) continue;
+        const int64_t tiles = static_cast<int64_t>((a.Ho + bh - 1) / bh) * ((a.Wo + wt - 1) / wt);
+        if (tiles < best) {
+          best = tiles;
+          WT = wt;
+          BH = bh;
+        }
+      }
+      Wp = WT + 2;
+    }
     a.halo = 1;
     a.hWp = Wp;
-    a.hRB = halo32 ? 32 : 128;
-    a.hBH = std::min(ti.H, kBM / Wp);
-    a.hTPI = (ti.H + a.hBH - 1) / a.hBH;
-    a.m_tiles = k * a.hTPI;
+    a.hRB = halo32 ? 32 : op.Cin == 32 ? 64 : 128;
+    a.hBH = BH;
+    a.hWT = halo_wide ? WT : a.Wo;
+    a.hCT = (a.Wo + a.hWT - 1) / a.hWT;
+    a.hTPI = (a.Ho + a.hBH - 1) / a.hBH;
+    a.m_tiles = k * a.hTPI * a.hCT;
     a.BN = pick_bn(op.Cout, a.m_tiles, sm_budget, bn_cap);
     a.n_tiles = (a.Cout + a.BN - 1) / a.BN;
     a.num_tiles = a.m_tiles * a.n_tiles;
@@ -309,7 +333,7 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
     memset(&out->ymap, 0, sizeof(out->ymap));
     if (!encode_tmap_2d_bf16(&out->wmap, wbase + op.w_off, kpad, op.Cout, static_cast<uint64_t>(kpad) * 2, kBK, a.BN))
       return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for conv weights: " + g_last_encode);
-    if (!encode_tmap_halo_bf16(&out->amap, a.x, ti.C, ti.W, ti.H, k, Wp, a.hBH + R - 1, halo32 ? 16 : 64))
+    if (!encode_tmap_halo_bf16(&out->amap, a.x, ti.C, ti.W, ti.H, k, Wp, a.hBH + R - 1, halo32 ? 16 : a.hRB / 2))
       return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for the conv halo");
     if (a.stages < 2) return fail(GX_EINVAL, "halo conv: shared memory too small for the weight ring");
     out->grid = std::min(a.num_tiles, std::max(1, sm_budget));

@@ -73,7 +73,8 @@ struct ConvArgs {
                        // (rmap, box 64 x 128), B = identity blocks at kb = num_kb + col/64 (wsw)
   int halo;            // 3x3/s1/p1 wide-image conv on conv_halo_kernel (amap = the 4D halo map)
   int hBH, hTPI;       // halo: output rows per M tile, M tiles per image
-  int hWp, hRB;        // halo: padded row pitch (W + left + right pad), bytes per halo pixel row (128 | 32)
+  int hWp, hRB;        // halo: row pitch of a tile's halo (WT + S - 1), bytes per halo pixel row (128 | 64 | 32)
+  int hWT, hCT;        // halo: output columns per tile, column tiles per image row
   int bres;            // B resident: the CTA's num_kb weight k-blocks (its N tile is fixed) are bulk-loaded
                        // once and stay in smem; with res_mma the residual is added by N=64 MMAs into
                        // the accumulator's 64-column slices against one resident 64x64 identity block

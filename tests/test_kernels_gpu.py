@@ -86,6 +86,12 @@ def _conv_case(k, H, W, Cin, Cout, R, S, stride, pad, residual, relu, cin_pad=No
         (3, 28, 28, 128, 128, 3, 3, 1, 1, False, True),       # layer2 3x3 (BH=4)
         (2, 35, 35, 64, 96, 3, 3, 1, 1, False, True),         # Inception 35x35 (BH=3, last tile short)
         (2, 30, 30, 128, 192, 3, 3, 1, 1, False, False),      # W+2 = 32, BN not a power of two
+        # wide halo (column tiles) and 32-channel halo rows
+        (2, 147, 147, 32, 64, 3, 3, 1, 1, False, True),       # Inception Conv2d_2b (RB 64, column tiles)
+        (1, 149, 149, 32, 32, 3, 3, 1, 0, False, True),       # Inception Conv2d_2a, unpadded
+        (2, 112, 112, 128, 128, 3, 3, 1, 1, False, True),     # VGG-16 conv2 (RB 128, column tiles)
+        (1, 224, 224, 64, 64, 3, 3, 1, 1, False, True),       # VGG-16 conv1_2
+        (3, 40, 40, 32, 48, 3, 3, 1, 1, False, False),        # 32 channels, whole rows
     ],
 )
 def test_conv_matches_torch(k, H, W, Cin, Cout, R, S, stride, pad, residual, relu):
