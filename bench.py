@@ -597,7 +597,7 @@ def run_placed(args):
 
         def build(wl):
             dep = deploy(wl["plan"], wl["fragments"])
-            inst = placed_instances(dep, models)
+            inst = placed_instances(dep, models, capacity=int(round(99 * args.sm_oversubscribe)))
             clients = [ClientView.from_doc(c) for c in wl["clients"]]
             ingress, keep = {}, []
             for cid in sorted(c.client_id for c in clients if c.client_id in dep.routes):

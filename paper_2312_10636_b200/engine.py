@@ -59,11 +59,12 @@ def _gx_dtype(t: torch.Tensor) -> int:
     return {torch.float32: N.GX_F32, torch.bfloat16: N.GX_BF16, torch.int32: N.GX_I32}[t.dtype]
 
 
-def placed_instances(dep, models: dict, work_conserving: bool = True) -> list:
+def placed_instances(dep, models: dict, work_conserving: bool = True, capacity: int = 99) -> list:
     """Executor instances of a deployment placed across the GPUs of one box: instance i of stage s
     runs on GPU s.gpus[i] (the plan's placement, placement.py:24-70; None = GPU 0).  `models` maps
     a plan GPU index to the DeviceModel resident on it.  SM budgets are assigned per GPU from the
-    shares of the instances placed on that GPU (Context.sm_budgets)."""
+    shares of the instances placed on that GPU (Context.sm_budgets; `capacity` > 100 oversubscribes,
+    DESIGN.md §6.1)."""
     per_gpu = {}
     for si, s in enumerate(dep.stages):
         for i, g in enumerate(s.gpus if s.gpus is not None else (0,) * s.instances):
@@ -72,7 +73,8 @@ def placed_instances(dep, models: dict, work_conserving: bool = True) -> list:
     for g, lst in per_gpu.items():
         if g not in models:
             raise ValidationError(f"plan places instances on GPU {g} but no model is resident there")
-        bs = models[g].ctx.sm_budgets([(share, 1) for _si, _i, share in lst], work_conserving=work_conserving)
+        bs = models[g].ctx.sm_budgets([(share, 1) for _si, _i, share in lst], capacity=capacity,
+                                      work_conserving=work_conserving)
         for (si, i, _share), b in zip(lst, bs):
             budget[(si, i)] = (g, b)
     out = []
