@@ -466,8 +466,8 @@ def run_ours(args):
     att_s = 0.0
     for o in convs:
         op = chain.ops[first_op + o["op"]]
-        H, W, Cc, dt = chain.tensors[op.out]
-        wbytes = st.batch * H * W * (op.Cout or Cc) * (4 if dt == N.GX_F32 else 2)
+        oh, ow, oc, dt = chain.tensors[op.out]  # (not W / H: W is the warm-up window count)
+        wbytes = st.batch * oh * ow * (op.Cout or oc) * (4 if dt == N.GX_F32 else 2)
         rbytes = max(0.0, o["bytes"] - wbytes)
         t_tc = o["flops"] / (burst * 1e12 * inst.sm_budget / ctx.sm_count)
         t_mem = max(rbytes / 86.0, wbytes / 31.5, (rbytes + wbytes) / 50.0) / inst.sm_budget / clk_hz

@@ -25,6 +25,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--no-torch", action="store_true", help="skip the PyTorch reference rows")
     args = ap.parse_args()
 
     import torch
@@ -129,6 +130,20 @@ def main():
         op = N.make_op(N.GX_OP_FC, 0, 1, Cin=K, Cout=O, w_off=w_off, b_off=b_off, flags=flags)
         timed(f"fc_{path}", "25088->4096 k=1 (VGG fc6)", K * O * 2 + O * 4 + K * 2 + O * 2,
               lambda op=op: run_op(op, [x, y], [tensor_desc(7, 7, 512), tensor_desc(1, 1, O)], wfc, 1))
+    # the same traffic through PyTorch's own kernels (library ceilings on this box, not ours): a
+    # plain copy, a strided slice copy, a channels-last max pool and a spatial sum
+    if not args.no_torch:
+        a = torch.randn(1024, 35, 35, 64, device="cuda").to(bf)
+        b = torch.empty_like(a)
+        timed("torch_copy", "contiguous 1024x35x35x64 bf16", a.numel() * 4, lambda: b.copy_(a))
+        y = torch.empty(1024, 35, 35, 288, dtype=bf, device="cuda")
+        timed("torch_slice", "35x35x64 -> slice of 288, k=1024", a.numel() * 4, lambda: y[..., 96:160].copy_(a))
+        x = torch.randn(128, 64, 112, 112, device="cuda").to(bf).to(memory_format=torch.channels_last)
+        timed("torch_maxpool", "3x3/2 112x112x64 k=128 (NHWC)", x.numel() * 2 + x.numel() // 2,
+              lambda: torch.nn.functional.max_pool2d(x, 3, 2, 1))
+        g = torch.randn(1024, 7, 7, 2048, device="cuda").to(bf)
+        timed("torch_gap", "7x7x2048 k=1024 (sum dim 1,2)", g.numel() * 2 + 1024 * 2048 * 2,
+              lambda: g.sum(dim=(1, 2)))
     if args.out:
         with open(args.out, "w", newline="") as f:
             w = csv.DictWriter(f, fieldnames=list(rows[0].keys()))
