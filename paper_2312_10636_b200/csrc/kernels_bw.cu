@@ -364,14 +364,19 @@ __global__ void pool_kernel(int mode, const __nv_bfloat16* __restrict__ x, int N
 // 3x3 / stride-1 pooling (Inception's branch_pool avg pools, and max): a thread owns a vertical
 // strip of kPoolStrip outputs at one (column, 8 channels) and slides down it, combining each input
 // row's three taps once into a row value (max or sum) and each output from three row values:
-// 3*(T+2) loads for T outputs instead of 9*T, so the nine-fold tap reuse no longer has to come
-// from L1/L2 (the per-output kernel was L2->SM bound at 0.26 of HBM on 35x35x288).
+// 3*(T+2) loads for T outputs instead of 9*T.  Rows stream through a register ring with the loads
+// of row j+1 issued before row j is combined (6 loads in flight, <= 85 registers: 3 blocks of 256
+// per SM), and every address is one 32-bit offset from a per-thread base (round 1 held all 24
+// taps and did the 64-bit index math per tap: 127 registers, 2 blocks per SM, issue-bound at 0.41
+// of HBM).  The combine order is unchanged: row = ((id + t0) + t1) + t2, out = ((id + r0) + r1) + r2.
 constexpr int kPoolStrip = 6;
-__global__ void pool3s1_kernel(int mode, const __nv_bfloat16* __restrict__ x, int N, int H, int W, int C, int x_ld,
-                               __nv_bfloat16* __restrict__ y, int Ho, int Wo, int y_ld, int y_coff, int ph, int pw,
-                               int count_include_pad) {
+__global__ void __launch_bounds__(256, 3) pool3s1_kernel(int mode, const __nv_bfloat16* __restrict__ x, int N, int H,
+                                                        int W, int C, int x_ld, __nv_bfloat16* __restrict__ y,
+                                                        int Ho, int Wo, int y_ld, int y_coff, int ph, int pw,
+                                                        int count_include_pad) {
   constexpr int T = kPoolStrip;
   const int cv = C / 8;
+  const int ldv = x_ld / 8;  // pixel pitch in 16-byte vectors
   const int strips = (Ho + T - 1) / T;
   const int total = N * strips * Wo * cv;  // < 2^31 (launcher)
   const float ident = mode == 0 ? -INFINITY : 0.0f;
@@ -384,61 +389,63 @@ __global__ void pool3s1_kernel(int mode, const __nv_bfloat16* __restrict__ x, in
     const int n = p / strips;
     const int ho0 = st * T;
     const int w0 = wo - pw;
+    const uint4* base = reinterpret_cast<const uint4*>(x + static_cast<int64_t>(n) * H * W * x_ld) + c8;
+    int co[3];
+    bool cok[3];
     int ncols = 0;
 #pragma unroll
-    for (int s = 0; s < 3; ++s) ncols += (w0 + s >= 0 && w0 + s < W) ? 1 : 0;
-    float rv[T + 2][8];
-    bool rok[T + 2];
-    // every tap of the strip is loaded before any is combined: 3 (T + 2) independent 16-byte loads
-    // in flight per thread (the per-row load-then-combine order left ~3, latency-bound at 0.28 of HBM)
-    uint4 raw[T + 2][3];
-#pragma unroll
-    for (int j = 0; j < T + 2; ++j) {
-      const int hi = ho0 - ph + j;
-      rok[j] = hi >= 0 && hi < H && ho0 + j - 2 < Ho;  // rows past the strip's last output unused
-      const int hc = min(max(hi, 0), H - 1);
-#pragma unroll
-      for (int s = 0; s < 3; ++s) {
-        const int wc = min(max(w0 + s, 0), W - 1);
-        raw[j][s] = __ldg(reinterpret_cast<const uint4*>(x + ((static_cast<int64_t>(n) * H + hc) * W + wc) * x_ld) + c8);
-      }
+    for (int s = 0; s < 3; ++s) {
+      cok[s] = w0 + s >= 0 && w0 + s < W;
+      ncols += cok[s] ? 1 : 0;
+      co[s] = min(max(w0 + s, 0), W - 1) * ldv;
     }
+    const int rstep = W * ldv;
+    uint4 raw[2][3];
+    float rv[3][8];
+    auto load_row = [&](int j) {
+      const int ro = min(max(ho0 - ph + j, 0), H - 1) * rstep;
+#pragma unroll
+      for (int s = 0; s < 3; ++s) raw[j % 2][s] = __ldg(base + ro + co[s]);
+    };
+    load_row(0);
 #pragma unroll
     for (int j = 0; j < T + 2; ++j) {
-      const uint4* v = raw[j];
+      if (j + 1 < T + 2) load_row(j + 1);
+      float* r = rv[j % 3];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) rv[j][e] = ident;
+      for (int e = 0; e < 8; ++e) r[e] = ident;
 #pragma unroll
       for (int s = 0; s < 3; ++s) {
-        if (w0 + s < 0 || w0 + s >= W) continue;
-        const uint32_t w[4] = {v[s].x, v[s].y, v[s].z, v[s].w};
+        if (!cok[s]) continue;
+        const uint4 v = raw[j % 2][s];
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const float2 f = unpack_bf16x2(w[q]);
           if (mode == 0) {
-            rv[j][2 * q] = fmaxf(rv[j][2 * q], f.x);
-            rv[j][2 * q + 1] = fmaxf(rv[j][2 * q + 1], f.y);
+            r[2 * q] = fmaxf(r[2 * q], f.x);
+            r[2 * q + 1] = fmaxf(r[2 * q + 1], f.y);
           } else {
-            rv[j][2 * q] += f.x;
-            rv[j][2 * q + 1] += f.y;
+            r[2 * q] += f.x;
+            r[2 * q + 1] += f.y;
           }
         }
       }
-    }
-#pragma unroll
-    for (int t = 0; t < T; ++t) {
+      const int t = j - 2;
       const int ho = ho0 + t;
-      if (ho >= Ho) break;
+      if (j < 2 || ho >= Ho) continue;
       float acc[8];
       int nrows = 0;
 #pragma unroll
       for (int e = 0; e < 8; ++e) acc[e] = ident;
 #pragma unroll
-      for (int r = 0; r < 3; ++r) {
-        if (!rok[t + r]) continue;
+      for (int rr = 0; rr < 3; ++rr) {
+        const int hi = ho - ph + rr;
+        if (hi < 0 || hi >= H) continue;
         ++nrows;
+        const float* rw = rv[(t + rr) % 3];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) acc[e] = mode == 0 ? fmaxf(acc[e], rv[t + r][e]) : acc[e] + rv[t + r][e];
+        for (int e = 0; e < 8; ++e) acc[e] = mode == 0 ? fmaxf(acc[e], rw[e]) : acc[e] + rw[e];
       }
       if (mode == 1) {
         int div = nrows * ncols;
@@ -455,18 +462,69 @@ __global__ void pool3s1_kernel(int mode, const __nv_bfloat16* __restrict__ x, in
       o.y = pack_bf16x2(acc[2], acc[3]);
       o.z = pack_bf16x2(acc[4], acc[5]);
       o.w = pack_bf16x2(acc[6], acc[7]);
-      *reinterpret_cast<uint4*>(y + ((static_cast<int64_t>(n) * Ho + ho) * Wo + wo) * y_ld + y_coff + 8 * c8) = o;
+      *reinterpret_cast<uint4*>(y + (static_cast<int64_t>(n) * Ho + ho) * Wo * y_ld + wo * y_ld + y_coff + 8 * c8) = o;
     }
   }
 }
 
+// 3x3 max pool at any stride (the ResNet stem 3x3/2, Inception's 3x3/2 reductions): the nine taps
+// are loaded from clamped coordinates (a clamped tap is another pixel of the same window, and max
+// is idempotent, so no tap needs a predicate) and combined as packed bf16x2 maxima (exact: the
+// result is one of the inputs), 4 HMNMX2 per tap instead of 8 unpacks + 8 FMNMX; addresses are
+// 32-bit offsets from a per-sample base.  Round 1's generic kernel was issue-bound at 0.61 of HBM.
+__global__ void __launch_bounds__(256) maxpool3_kernel(const __nv_bfloat16* __restrict__ x, int N, int H, int W,
+                                                       int C, int x_ld, __nv_bfloat16* __restrict__ y, int Ho, int Wo,
+                                                       int y_ld, int y_coff, int sh, int sw, int ph, int pw) {
+  const int cv = C / 8;
+  const int ldv = x_ld / 8;
+  const int total = N * Ho * Wo * cv;  // < 2^31 (launcher)
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int c8 = i % cv;
+    int p = i / cv;
+    const int wo = p % Wo;
+    p /= Wo;
+    const int ho = p % Ho;
+    const int n = p / Ho;
+    const uint4* base = reinterpret_cast<const uint4*>(x + static_cast<int64_t>(n) * H * W * x_ld) + c8;
+    int ro[3], co[3];
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      ro[t] = min(max(ho * sh - ph + t, 0), H - 1) * W * ldv;
+      co[t] = min(max(wo * sw - pw + t, 0), W - 1) * ldv;
+    }
+    uint4 v[9];
+#pragma unroll
+    for (int t = 0; t < 9; ++t) v[t] = __ldg(base + ro[t / 3] + co[t % 3]);
+    __nv_bfloat162 m[4];
+    m[0] = *reinterpret_cast<const __nv_bfloat162*>(&v[0].x);
+    m[1] = *reinterpret_cast<const __nv_bfloat162*>(&v[0].y);
+    m[2] = *reinterpret_cast<const __nv_bfloat162*>(&v[0].z);
+    m[3] = *reinterpret_cast<const __nv_bfloat162*>(&v[0].w);
+#pragma unroll
+    for (int t = 1; t < 9; ++t) {
+      m[0] = __hmax2(m[0], *reinterpret_cast<const __nv_bfloat162*>(&v[t].x));
+      m[1] = __hmax2(m[1], *reinterpret_cast<const __nv_bfloat162*>(&v[t].y));
+      m[2] = __hmax2(m[2], *reinterpret_cast<const __nv_bfloat162*>(&v[t].z));
+      m[3] = __hmax2(m[3], *reinterpret_cast<const __nv_bfloat162*>(&v[t].w));
+    }
+    uint4 o;
+    o.x = *reinterpret_cast<const uint32_t*>(&m[0]);
+    o.y = *reinterpret_cast<const uint32_t*>(&m[1]);
+    o.z = *reinterpret_cast<const uint32_t*>(&m[2]);
+    o.w = *reinterpret_cast<const uint32_t*>(&m[3]);
+    *reinterpret_cast<uint4*>(y + (static_cast<int64_t>(n) * Ho + ho) * Wo * y_ld + wo * y_ld + y_coff + 8 * c8) = o;
+  }
+}
+
 // Global average pool: [N, HW, C] -> [N, C].  A warp owns one (sample, 256 channels) item: lane =
-// 8 channels (the warp reads 512 contiguous bytes of one pixel) and walks the HW pixels with 8
+// 8 channels (the warp reads 512 contiguous bytes of one pixel) and walks the HW pixels with 4
 // independent 16-byte loads in flight per lane, accumulating in fp32 registers; no shared memory
-// and no block barriers, so the 8 warps of a block stream 8 items concurrently.  (Round 1 split
-// one item over the 8 warps and reduced through shared memory: two barriers per item, 0.55 of HBM.)
+// and no block barriers, so the 8 warps of a block stream 8 items concurrently.  At <= 32
+// registers 8 blocks fit per SM, so a 1024-sample batch (8192 items) is resident in one wave; with
+// 8 loads in flight (40 registers, 6 blocks per SM) 15% of the items ran as a second, near-empty
+// wave (0.62 of HBM).  (Round 1 split one item over the 8 warps through shared memory: 0.55.)
 constexpr int kGapWarps = 8;
-__global__ void __launch_bounds__(kGapWarps * 32) gap_kernel(const __nv_bfloat16* __restrict__ x, int N, int HW,
+__global__ void __launch_bounds__(kGapWarps * 32, 8) gap_kernel(const __nv_bfloat16* __restrict__ x, int N, int HW,
                                                             int C, __nv_bfloat16* __restrict__ y) {
   const int lane = threadIdx.x & 31;
   const int cv = C / 8;
@@ -481,7 +539,7 @@ __global__ void __launch_bounds__(kGapWarps * 32) gap_kernel(const __nv_bfloat16
     if (c8 >= cv) continue;
     const uint4* base = reinterpret_cast<const uint4*>(x + static_cast<int64_t>(n) * HW * C) + c8;
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    constexpr int U = 8;
+    constexpr int U = 4;  // <= 32 registers: 8 blocks (64 warps) per SM, every item resident in one wave
     for (int p0 = 0; p0 < HW; p0 += U) {
       uint4 v[U];
 #pragma unroll
@@ -820,7 +878,10 @@ cudaError_t launch_pool(int mode, const __nv_bfloat16* x, int N, int H, int W, i
     const int64_t strips = static_cast<int64_t>(N) * ((Ho + kPoolStrip - 1) / kPoolStrip) * Wo * (C / 8);
     pool3s1_kernel<<<grid_for(strips, 256, grid), 256, 0, s>>>(mode, x, N, H, W, C, x_ld, y, Ho, Wo, y_ld, y_coff, ph,
                                                                pw, count_include_pad);
-  } else if (R == 3 && S == 3)
+  } else if (R == 3 && S == 3 && mode == 0 && (x_ld & 7) == 0)
+    maxpool3_kernel<<<grid_for(work, 256, grid), 256, 0, s>>>(x, N, H, W, C, x_ld, y, Ho, Wo, y_ld, y_coff, sh, sw, ph,
+                                                              pw);
+  else if (R == 3 && S == 3)
     pool_kernel<3><<<grid_for(work, 256, grid), 256, 0, s>>>(mode, x, N, H, W, C, x_ld, y, Ho, Wo, y_ld, y_coff, R, S,
                                                              sh, sw, ph, pw, count_include_pad);
   else

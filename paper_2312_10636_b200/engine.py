@@ -169,8 +169,12 @@ class StageInstance:
         n = n.value
         ms, fl, by, kd = (C.c_float * n)(), (C.c_double * n)(), (C.c_double * n)(), (C.c_int32 * n)()
         N.check(L.gx_stage_profile_ops(self.handle, k, iters, n, ms, fl, by, kd), "gx_stage_profile_ops")
-        return [{"op": i, "kind": int(kd[i]), "ms": float(ms[i]), "flops": float(fl[i]), "bytes": float(by[i])}
-                for i in range(n)]
+        # logical FLOPs of convs with zero-padded channels (UnitChain.op_flops_scale)
+        chain = self.model.chain
+        first = chain.unit_first_op[self.start]
+        scale = [getattr(chain, "op_flops_scale", {}).get(first + i, 1.0) for i in range(n)]
+        return [{"op": i, "kind": int(kd[i]), "ms": float(ms[i]), "flops": float(fl[i]) * scale[i],
+                 "bytes": float(by[i])} for i in range(n)]
 
     def kernel_count(self, k: int) -> int:
         n = C.c_int()

@@ -38,6 +38,10 @@ class UnitChain:
     unit_flops: list = field(default_factory=list)  # per-sample FLOPs of each unit
     tensor_s2d: dict = field(default_factory=dict)  # tensor id -> space-to-depth factor (stride-2 stems)
     dtype: int = BF16  # compute element type (F32: the fp32 execution mode)
+    # op index -> logical / executed FLOPs of a conv whose channels are zero-padded (the stem's
+    # 3 -> 8 input, Inception's 48 / 96 / 160-channel intermediates stored at 64 / 128 / 192): the
+    # roofline tables count the logical FLOPs only
+    op_flops_scale: dict = field(default_factory=dict)
 
     @property
     def n_units(self) -> int:
@@ -135,33 +139,46 @@ class ChainBuilder:
         return w, b
 
     def conv(self, x, conv: nn.Conv2d, bn: nn.BatchNorm2d | None, relu=True, residual=-1, out=-1, out_coff=0,
-             cin_pad=None):
+             cin_pad=None, cout_pad=None):
         w, b = self.folded(conv, bn)
         sh, sw = conv.stride
         ph, pw = conv.padding
-        return self.conv_w(x, w, b, (sh, sw), (ph, pw, ph, pw), relu, residual, out, out_coff, cin_pad)
+        return self.conv_w(x, w, b, (sh, sw), (ph, pw, ph, pw), relu, residual, out, out_coff, cin_pad,
+                           cout_pad=cout_pad)
 
-    def conv_w(self, x, w, b, stride, pad, relu=True, residual=-1, out=-1, out_coff=0, cin_pad=None, flops=None):
-        """Conv from explicit (folded) weights; pad = (top, left, bottom, right)."""
+    def conv_w(self, x, w, b, stride, pad, relu=True, residual=-1, out=-1, out_coff=0, cin_pad=None, flops=None,
+               cout_pad=None):
+        """Conv from explicit (folded) weights; pad = (top, left, bottom, right).  cout_pad: the output
+        tensor (a new one) stores cout_pad >= Cout channels, the extra ones zero (zero weights and
+        bias); a conv reading a tensor with more channels than its weights have zero-pads its Cin."""
         H, W, Cx, _ = self.shape(x)
         cout, cin, R, S = w.shape
         sh, sw = stride
         ph, pw, ph_hi, pw_hi = pad
         Ho = (H + ph + ph_hi - R) // sh + 1
         Wo = (W + pw + pw_hi - S) // sw + 1
-        cin_pad = cin_pad or cin
+        logical = flops if flops is not None else 2.0 * Ho * Wo * cout * cin * R * S
+        cin_pad = cin_pad or (Cx if Cx > cin else cin)
         assert cin_pad <= Cx, (cin_pad, Cx)
+        if cout_pad and cout_pad > cout:
+            assert out < 0
+            w = torch.nn.functional.pad(w, (0, 0, 0, 0, 0, 0, 0, cout_pad - cout))
+            b = torch.nn.functional.pad(b, (0, cout_pad - cout))
+            cout = cout_pad
         if out < 0:
             out = self.tensor(Ho, Wo, cout)
         else:
             assert self.shape(out)[:2] == (Ho, Wo), (self.shape(out), Ho, Wo)
+        executed = 2.0 * Ho * Wo * cout * cin_pad * R * S
+        if executed != logical:
+            self.c.op_flops_scale[len(self.c.ops)] = logical / executed
         w_off = self.add_weight(pack_conv_weight(w, cin_pad))
         b_off = self.c.blob.add_f32(b)
         self.c.ops.append(N.make_op(N.GX_OP_CONV, x, out, in2=residual, out_coff=out_coff,
                                     act=N.GX_ACT_RELU if relu else N.GX_ACT_NONE, R=R, S=S, sh=sh, sw=sw, ph=ph,
                                     pw=pw, Cin=cin_pad, Cout=cout, w_off=w_off, b_off=b_off,
                                     ph_hi=ph_hi if ph_hi != ph else -1, pw_hi=pw_hi if pw_hi != pw else -1))
-        self._flops += flops if flops is not None else 2.0 * Ho * Wo * cout * cin * R * S
+        self._flops += logical
         return out
 
     def conv_ds(self, t, conv: nn.Conv2d, bn: nn.BatchNorm2d, x, ds_conv: nn.Conv2d, ds_bn: nn.BatchNorm2d,
@@ -378,6 +395,19 @@ def _basic(b, x, bc, out=-1, out_coff=0):
     return b.conv(x, bc.conv, bc.bn, relu=True, out=out, out_coff=out_coff)
 
 
+def _mid(b, x, bc):
+    """A conv whose output only feeds the next conv of its branch (Inception's 48 / 96 / 160-channel
+    intermediates): in the bf16 chain it is stored with its channels zero-padded to a multiple of 64,
+    so the consumer's im2col TMA moves 128-byte pixel rows (64 channels per row) instead of 32 / 64-
+    byte rows of 16 / 32 channels (the TMA row rate, not the tensor pipe, bounded those convs at
+    0.18-0.29 of the budget-scaled peak), and 3x3/s1/p1 consumers qualify for the halo kernel.  The
+    padding channels are exact zeros (zero weights and bias, ReLU(0) = 0), so results are unchanged
+    up to the consumer's summation order."""
+    c = bc.conv.out_channels
+    pad = -(-c // 64) * 64 if b.dtype == BF16 and c % 64 else None
+    return b.conv(x, bc.conv, bc.bn, relu=True, cout_pad=pad)
+
+
 def _inception_chain(m, dtype=BF16) -> UnitChain:
     b = ChainBuilder("inception_v3", dtype)
     x = b.tensor(299, 299, 8)
@@ -405,10 +435,10 @@ def _inception_chain(m, dtype=BF16) -> UnitChain:
         pf = blk.branch_pool.conv.out_channels
         out = cat(H, W, 64 + 64 + 96 + pf)
         _basic(b, y, blk.branch1x1, out, 0)
-        t = _basic(b, y, blk.branch5x5_1)
+        t = _mid(b, y, blk.branch5x5_1)
         _basic(b, t, blk.branch5x5_2, out, 64)
         t = _basic(b, y, blk.branch3x3dbl_1)
-        t = _basic(b, t, blk.branch3x3dbl_2)
+        t = _mid(b, t, blk.branch3x3dbl_2)
         _basic(b, t, blk.branch3x3dbl_3, out, 128)
         t = b.pool(y, "avg", 3, 1, 1)
         _basic(b, t, blk.branch_pool, out, 224)
@@ -420,7 +450,7 @@ def _inception_chain(m, dtype=BF16) -> UnitChain:
     out = cat(Ho, Wo, 384 + 96 + Cc)
     _basic(b, y, blk.branch3x3, out, 0)
     t = _basic(b, y, blk.branch3x3dbl_1)
-    t = _basic(b, t, blk.branch3x3dbl_2)
+    t = _mid(b, t, blk.branch3x3dbl_2)
     _basic(b, t, blk.branch3x3dbl_3, out, 384)
     b.pool(y, "max", 3, 2, 0, out=out, out_coff=480)
     y = out
@@ -429,13 +459,13 @@ def _inception_chain(m, dtype=BF16) -> UnitChain:
         H, W, _, _ = b.shape(y)
         out = cat(H, W, 768)
         _basic(b, y, blk.branch1x1, out, 0)
-        t = _basic(b, y, blk.branch7x7_1)
-        t = _basic(b, t, blk.branch7x7_2)
+        t = _mid(b, y, blk.branch7x7_1)
+        t = _mid(b, t, blk.branch7x7_2)
         _basic(b, t, blk.branch7x7_3, out, 192)
-        t = _basic(b, y, blk.branch7x7dbl_1)
-        t = _basic(b, t, blk.branch7x7dbl_2)
-        t = _basic(b, t, blk.branch7x7dbl_3)
-        t = _basic(b, t, blk.branch7x7dbl_4)
+        t = _mid(b, y, blk.branch7x7dbl_1)
+        t = _mid(b, t, blk.branch7x7dbl_2)
+        t = _mid(b, t, blk.branch7x7dbl_3)
+        t = _mid(b, t, blk.branch7x7dbl_4)
         _basic(b, t, blk.branch7x7dbl_5, out, 384)
         t = b.pool(y, "avg", 3, 1, 1)
         _basic(b, t, blk.branch_pool, out, 576)

@@ -68,15 +68,22 @@ def test_fp32_chain_mirrors_bf16_chain(name):
     b = build_chain(name, module=m, dtype=N.GX_F32)
     assert b.dtype == N.GX_F32 and a.dtype == N.GX_BF16
     assert a.boundary == b.boundary and a.unit_first_op == b.unit_first_op
-    assert [t[:3] for t in a.tensors] == [t[:3] for t in b.tensors]
+    # (bf16 Inception stores its 48 / 96 / 160-channel branch intermediates zero-padded to a multiple
+    # of 64 channels, models._mid; never a boundary tensor)
+    def padded(x, y):
+        return x == y or x == -(-y // 64) * 64
+
+    assert [t[:2] for t in a.tensors] == [t[:2] for t in b.tensors]
+    assert all(padded(ta[2], tb[2]) for ta, tb in zip(a.tensors, b.tensors))
+    assert all(a.tensors[t][2] == b.tensors[t][2] for t in a.boundary)
     # (BERT's boundary 0 holds int32 token ids in both modes: the K8 embedding's input)
     assert all(t[3] == N.GX_F32 or (t[3] == N.GX_I32 and i == b.boundary[0]) for i, t in enumerate(b.tensors))
     # bf16 chains: only the chain output may be fp32
     assert all(t[3] == N.GX_BF16 or i == a.boundary[-1] or (t[3] == N.GX_I32 and i == a.boundary[0])
                for i, t in enumerate(a.tensors))
     assert [a.payload_bytes(p) for p in range(a.n_units + 1)] == [b.payload_bytes(p) for p in range(b.n_units + 1)]
-    assert [(o.kind, o.in_, o.out, o.Cin, o.Cout) for o in a.ops] == [(o.kind, o.in_, o.out, o.Cin, o.Cout)
-                                                                        for o in b.ops]
+    assert [(o.kind, o.in_, o.out) for o in a.ops] == [(o.kind, o.in_, o.out) for o in b.ops]
+    assert all(padded(oa.Cin, ob.Cin) and padded(oa.Cout, ob.Cout) for oa, ob in zip(a.ops, b.ops))
     assert b.blob.size > 1.8 * a.blob.size
 
 
