@@ -82,8 +82,13 @@ def main():
             t = o["ms"] * 1e-3
             tf = o["flops"] / t / 1e12 if t > 0 else 0.0
             gb = o["bytes"] / t / 1e9 if t > 0 else 0.0
-            t_tc = o["flops"] / (tc_peak * scale * 1e12)
-            mem_peak = min(hbm_peak, SM_FEED_GBS * budget)
+            # persistent tensor-core kernels (conv / linear / FC) run on `budget` CTAs = SMs; attention
+            # launches up to 4 CTAs per budget SM and the bandwidth kernels budget x 8 blocks of 256
+            # threads, which the block scheduler spreads over up to 4x / 8x as many SMs (a budget is a
+            # grid size, not an SM partition)
+            spread = budget if o["kind"] in (1, 5, 6) else min(sms, (4 if o["kind"] == 8 else 8) * budget)
+            t_tc = o["flops"] / (tc_peak * spread / sms * 1e12)
+            mem_peak = min(hbm_peak, SM_FEED_GBS * spread)
             t_hbm = o["bytes"] / (mem_peak * 1e9)
             frac = max(t_tc, t_hbm) / t if t > 0 else 0.0
             frac_w += frac * o["ms"]
@@ -95,7 +100,7 @@ def main():
                          "roofline_us": round(max(t_tc, t_hbm) * 1e6, 2), "frac": round(frac, 3)})
         print(f"# span [{a},{b}) k={k} budget={budget} SMs: graph {whole * 1000:.1f} us, sum of ops "
               f"{tot_ms * 1000:.1f} us over {len(ops)} ops, time-weighted roofline frac "
-              f"{frac_w / max(tot_ms, 1e-12):.3f} (peaks {src}: {tc_peak} TF/s x {budget}/{sms}; memory min({hbm_peak}, {SM_FEED_GBS} x {budget}) GB/s)",
+              f"{frac_w / max(tot_ms, 1e-12):.3f} (peaks {src}: {tc_peak} TF/s x {budget}/{sms}; memory min({hbm_peak}, {SM_FEED_GBS} x SMs touched: budget, or 8 x budget for the bandwidth kernels) GB/s)",
               flush=True)
         by_kind = {}
         for r in rows[-len(ops):]:
