@@ -25,6 +25,7 @@ namespace gx {
 
 namespace {
 constexpr int kATileBytes = kBM * kBK * 2;
+constexpr int kMaxStages = 32;  // pipeline stages of a short-A (a_rows < 128) weight-streaming GEMM
 constexpr int kResGroupBytes = kBM * 64 * 2;  // one 128 x 64 bf16 residual box
 
 __device__ __forceinline__ float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
@@ -102,8 +103,11 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
   sp.sA = smem;
   // KPS: k-blocks per pipeline stage (TMA mode): one barrier round trip per KPS*64 of K
   const bool bres = a.bres != 0;
-  const uint32_t sa_bytes = KPS * kATileBytes, sb_bytes = bres ? 0u : KPS * b_bytes;
-  sp.sB = sp.sA + static_cast<size_t>(S_) * sa_bytes;
+  // A tile stride: 128 rows, or a single short M tile's live rows (a.a_rows); the region keeps a
+  // full tile's worth past the last stage so the MMA's 128-row reads stay inside the allocation
+  const uint32_t a_tile = static_cast<uint32_t>(a.a_rows) * 128u;
+  const uint32_t sa_bytes = KPS * a_tile, sb_bytes = bres ? 0u : KPS * b_bytes;
+  sp.sB = sp.sA + static_cast<size_t>(S_) * sa_bytes + (kATileBytes - a_tile);
   sp.sBres = sp.sB + static_cast<size_t>(S_) * sb_bytes;
   sp.sIdent = sp.sBres + static_cast<size_t>(a.num_kb) * b_bytes;
   sp.sRes = sp.sBres + bres_alloc(a.bres, a.num_kb, BN, a.res_mma);
@@ -230,7 +234,7 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
       if (do_a && a.ds) tma_prefetch_desc(RM);
     }
     const bool loadB = do_b && !skipB && !bres;  // bres: the weights were loaded once, below
-    const uint32_t tx = (do_a && !skipA ? kATileBytes : 0u) + (loadB ? b_bytes : 0u);
+    const uint32_t tx = (do_a && !skipA ? a_tile : 0u) + (loadB ? b_bytes : 0u);
     if (do_b && bres && issuer) {
       // every tile of this CTA has the same N tile (planned so): its num_kb weight k-blocks, and
       // with res_mma the 64x64 identity block (rows 0..63 of identity k-block num_kb), once
@@ -276,7 +280,7 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
         }
         for (int j = 0; j < nk; ++j) {
         const int kb = kb0 + j;
-        uint8_t* const sa = sp.sA + st * sa_bytes + j * kATileBytes;
+        uint8_t* const sa = sp.sA + st * sa_bytes + j * a_tile;
         uint8_t* const sb = sp.sB + static_cast<size_t>(st) * sb_bytes + j * b_bytes;
         if (do_a && kb >= a.num_kb) {
           // residual x identity block: A = residual columns [nb0 + 64*(kb - num_kb), +64)
@@ -355,7 +359,7 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
         const int nk = min(KPS, nkb_tile - kb0);
         for (int jj = 0; jj < nk; ++jj) {
         const int kb = kb0 + jj;
-        const uint32_t abase = smem_u32(sp.sA + st * sa_bytes + jj * kATileBytes);
+        const uint32_t abase = smem_u32(sp.sA + st * sa_bytes + jj * a_tile);
         const uint64_t bd = bres ? umma_desc_sw128(sp.sBres + static_cast<size_t>(min(kb, a.num_kb - 1)) * b_bytes)
                                  : umma_desc_sw128(sp.sB + static_cast<size_t>(st) * sb_bytes + jj * b_bytes);
         if (bres && kb >= a.num_kb) {
@@ -638,22 +642,26 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
 }
 }  // namespace
 
-size_t conv_smem_bytes(int BN, int stages, int num_kb, int nres, int Cout, int kps, size_t bres_bytes) {
-  return 1024 + static_cast<size_t>(stages) * kps * (kATileBytes + (bres_bytes ? 0 : BN * 128)) + bres_bytes +
+size_t conv_smem_bytes(int BN, int stages, int num_kb, int nres, int Cout, int kps, size_t bres_bytes, int a_rows) {
+  const size_t a_tile = static_cast<size_t>(a_rows) * 128;
+  return 1024 + static_cast<size_t>(stages) * kps * (a_tile + (bres_bytes ? 0 : BN * 128)) + (kATileBytes - a_tile) +
+         bres_bytes +
          static_cast<size_t>(nres) * res_groups(BN) * kResGroupBytes + bias_alloc(Cout) + (2 * stages + 26) * 8 + 16 +
          static_cast<size_t>(num_kb) * 8 * sizeof(int2);
 }
 
 // Pipeline depth and residual slots that fit in ~220 KB: prefer >= 3 stages with a double-
 // buffered residual, else a single residual slot.
-int conv_pick_stages(int BN, int num_kb, bool res, int Cout, int* nres_out, int kps, size_t bres_bytes) {
+int conv_pick_stages(int BN, int num_kb, bool res, int Cout, int* nres_out, int kps, size_t bres_bytes, int a_rows) {
   const size_t budget = 220 * 1024;
-  const size_t per_stage = static_cast<size_t>(kps) * (kATileBytes + (bres_bytes ? 0 : BN * 128)) + 16;
+  const size_t per_stage = static_cast<size_t>(kps) * (static_cast<size_t>(a_rows) * 128 + (bres_bytes ? 0 : BN * 128)) +
+                           16;
   int best_s = 2, best_r = res ? 1 : 0;
   for (int nres = res ? 2 : 0; nres >= (res ? 1 : 0); --nres) {
-    const size_t fixed = conv_smem_bytes(BN, 0, num_kb, nres, Cout, kps, bres_bytes);
+    const size_t fixed = conv_smem_bytes(BN, 0, num_kb, nres, Cout, kps, bres_bytes, a_rows);
     int s = budget > fixed ? static_cast<int>((budget - fixed) / per_stage) : 0;
-    if (s > 8) s = 8;
+    const int cap = a_rows < kBM ? kMaxStages : 8;  // short A tiles: weight streaming wants depth
+    if (s > cap) s = cap;
     // short-K convs (the bottleneck expand 1x1s) are epilogue-bound: with the per-warp epilogue the next tile's residual/staging slot must be free while this
     // tile's epilogue runs; for K <= 128 one operand stage keeps the MMA ahead of the epilogue
     const int kb_short = dev().res2_kb;  // measured neutral: off
@@ -682,8 +690,8 @@ cudaError_t launch_conv(const CUtensorMap& wmap, const CUtensorMap& amap, const 
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);
   cfg.blockDim = dim3(kConvTcThreads, 1, 1);
-  cfg.dynamicSmemBytes =
-      conv_smem_bytes(a.BN, a.stages, a.num_kb, a.nres, a.Cout, a.kps, bres_alloc(a.bres, a.num_kb, a.BN, a.res_mma));
+  cfg.dynamicSmemBytes = conv_smem_bytes(a.BN, a.stages, a.num_kb, a.nres, a.Cout, a.kps,
+                                         bres_alloc(a.bres, a.num_kb, a.BN, a.res_mma), a.a_rows);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

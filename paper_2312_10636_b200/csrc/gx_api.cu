@@ -380,6 +380,16 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
   const size_t bres_bytes = a.bres ? static_cast<size_t>(a.num_kb) * a.BN * 128 + (a.res_mma ? 8192 : 0) : 0;
   // two k-blocks per pipeline stage halve the barrier round trips per unit of K; worth it when the
   // per-k-block MMA time (2*BN cycles) is below the ~500-cycle stage round trip and >= 3 stages fit
+  a.cpl = (op.Cin % 64 == 0) ? 64 : (op.Cin % 32 == 0) ? 32 : (op.Cin % 16 == 0) ? 16 : 8;
+  a.tma_a = !dev().no_tma_im2col;
+  a.a2d = a.tma_a && a.R == 1 && a.S == 1 && a.sh == 1 && a.sw == 1 && a.ph == 0 && a.pw == 0 && a.cpl == 64 &&
+          a.Cin == ti.C && !dev().no_a2d;
+  // one M tile with fewer than 128 live rows (batch-1..2 FC and layer4 1x1 convs): the A box holds
+  // only those rows and the pipeline stages are packed at that stride (the MMA's other rows read
+  // whatever follows in smem; their outputs are never stored), so a weight-streaming GEMM keeps up
+  // to 32 stages of B in flight instead of 8 stages of mostly zero-filled 16 KB A tiles (a batch-1
+  // FC streamed weights at 0.22 of HBM)
+  a.a_rows = (a.a2d && !ds && !for_span && !a.res_mma && a.m_tiles == 1 && a.M < kBM) ? (a.M + 7) & ~7 : kBM;
   a.kps = 1;
   {
     const bool tma = !dev().no_tma_im2col;
@@ -387,12 +397,13 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
     for (int kk = want; kk >= 2 && a.kps == 1 && !a.res_mma; --kk) {
       int nres2 = 0;
       if (tma && kk <= 3 && a.num_kb >= kk &&
-          conv_pick_stages(a.BN, a.num_kb, epi_res || a.ystore, a.Cout, &nres2, kk, bres_bytes) >= (a.m_tiles == 1 ? 2 : 3))
+          conv_pick_stages(a.BN, a.num_kb, epi_res || a.ystore, a.Cout, &nres2, kk, bres_bytes, a.a_rows) >=
+              (a.m_tiles == 1 ? 2 : 3))
         a.kps = kk;
     }
   }
   a.stages = conv_pick_stages(a.BN, a.num_kb + (a.res_mma ? a.BN / 64 : 0), epi_res || a.ystore, a.Cout, &a.nres,
-                              a.kps, bres_bytes);
+                              a.kps, bres_bytes, a.a_rows);
   if (const int st = dev().stages) {
     if (st >= 1 && st <= a.stages) a.stages = st;
   }
@@ -412,12 +423,8 @@ int plan_conv(const gx_op& op, const gx_tensor* T, void* const* ptrs, const uint
     return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for the conv output: " + g_last_encode);
   if (!encode_tmap_2d_bf16(&out->wmap, wbase + op.w_off, kpad, op.Cout, static_cast<uint64_t>(kpad) * 2, kBK, a.BN))
     return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for conv weights: " + g_last_encode);
-  a.cpl = (op.Cin % 64 == 0) ? 64 : (op.Cin % 32 == 0) ? 32 : (op.Cin % 16 == 0) ? 16 : 8;
-  a.tma_a = !dev().no_tma_im2col;
-  a.a2d = a.tma_a && a.R == 1 && a.S == 1 && a.sh == 1 && a.sw == 1 && a.ph == 0 && a.pw == 0 && a.cpl == 64 &&
-          a.Cin == ti.C && !dev().no_a2d;
   if (a.a2d) {
-    if (!encode_tmap_2d_bf16(&out->amap, a.x, ti.C, a.M, static_cast<uint64_t>(ti.C) * 2, kBK, kBM))
+    if (!encode_tmap_2d_bf16(&out->amap, a.x, ti.C, a.M, static_cast<uint64_t>(ti.C) * 2, kBK, a.a_rows))
       return fail(GX_ECUDA, "cuTensorMapEncodeTiled failed for conv input: " + g_last_encode);
   } else if (a.tma_a && !encode_tmap_im2col_bf16(&out->amap, a.x, ti.C, ti.W, ti.H, k, -a.pw, -a.ph,
                                                  (op.pw_hi >= 0 ? op.pw_hi : a.pw) - (a.S - 1),

@@ -82,6 +82,9 @@ struct ConvArgs {
   int ds;              // GX_OPF_DS: k-blocks >= kb_split take A from the block input (rmap): a 2D map
   int kb_split;        // over [M][Cx] (ds_stride 1) or a 1x1 im2col map at the downsample stride
   int ds_stride;
+  int a_rows;  // a2d: rows per A load; a single M tile with M < 128 (FC / 1x1 convs at batch 1-2)
+               // loads only its live rows, the MMA's other rows read stale smem whose outputs are
+               // never stored (row i of the product depends on row i of A only)
 };
 constexpr int kConvThreads = 320;  // span kernel: 4 A-producer warps, TMA warp, MMA warp, 4 epilogue warps
 // conv_tc: warps 0-3 cp.async A producers (or epilogue when TMA builds A), 4 A/B TMA, 5 MMA,
@@ -90,8 +93,11 @@ constexpr int kConvTcThreads = 352;
 constexpr int kBM = 128;
 constexpr int kBK = 64;
 // bres_bytes: resident weight (+ identity) bytes; stages then hold only the A operand
-size_t conv_smem_bytes(int BN, int stages, int num_kb, int nres, int Cout, int kps = 1, size_t bres_bytes = 0);
-int conv_pick_stages(int BN, int num_kb, bool res, int Cout, int* nres_out, int kps = 1, size_t bres_bytes = 0);
+// a_rows < kBM: A tiles packed at a_rows x 128 bytes per k-block (ConvArgs::a_rows)
+size_t conv_smem_bytes(int BN, int stages, int num_kb, int nres, int Cout, int kps = 1, size_t bres_bytes = 0,
+                       int a_rows = kBM);
+int conv_pick_stages(int BN, int num_kb, bool res, int Cout, int* nres_out, int kps = 1, size_t bres_bytes = 0,
+                     int a_rows = kBM);
 // wmap: weights [Cout][Kpad]; amap: im2col map of the input (tma_a); rmap: residual [M][res_ld];
 // ymap: output [M][y_ld] (ystore).
 cudaError_t launch_conv(const CUtensorMap& wmap, const CUtensorMap& amap, const CUtensorMap& rmap,

@@ -136,6 +136,13 @@ def test_conv_bounded_sm_budget_and_concat_offset():
     assert _rel(got, ref) < 1.5e-2
 
 
+@pytest.mark.parametrize("k,residual", [(1, False), (1, True), (2, True), (3, False)])
+def test_conv_1x1_single_short_tile(k, residual):
+    """layer4 1x1 convs at batch 1-3 (M = 49k < 128): the A box holds only the live rows."""
+    got, ref = _conv_case(k, 7, 7, 512, 2048, 1, 1, 1, 0, residual, True, sm_budget=6)
+    assert _rel(got, ref) < 1.5e-2
+
+
 def test_conv_large_m_persistent():
     got, ref = _conv_case(8, 56, 56, 256, 64, 1, 1, 1, 0, False, True, sm_budget=20)
     assert _rel(got, ref) < 1.5e-2
