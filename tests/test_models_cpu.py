@@ -112,3 +112,27 @@ def test_fused_downsample_chain_keeps_units():
     ds = [o for o in a.ops if o.flags & N.GX_OPF_DS]
     assert [(o.Cin, a.tensors[o.in2][2], o.Cout, o.reserved) for o in ds] == [
         (64, 64, 256, 1), (128, 256, 512, 2), (256, 512, 1024, 2), (512, 1024, 2048, 2)]
+
+
+@pytest.mark.parametrize("name", ["resnet50", "vgg16", "inception_v3"])
+def test_padded_convs_count_logical_flops(name):
+    """Convs run on zero-padded channels (stem 3 -> 8 / s2d, Inception's 48/96/160 -> 64/128/192
+    intermediates) carry logical/executed FLOP ratios, so the executed conv/FC work scaled by them
+    adds up to the chain's logical FLOPs (what the roofline tables divide by)."""
+    from paper_2312_10636_b200 import _native as N
+    c = build_chain(name, module=torch_model(name))
+    total = 0.0
+    for i, o in enumerate(c.ops):
+        H, W, _, _ = c.tensors[o.out]
+        if o.kind == N.GX_OP_CONV:
+            k_ds = c.tensors[o.in2][2] if o.flags & N.GX_OPF_DS else 0
+            executed = 2.0 * H * W * o.Cout * (o.Cin * o.R * o.S + k_ds)
+        elif o.kind == N.GX_OP_FC:
+            executed = 2.0 * o.Cin * o.Cout
+        else:
+            continue
+        total += executed * c.op_flops_scale.get(i, 1.0)
+    assert abs(total - sum(c.unit_flops)) <= 1e-9 * total
+    if name == "inception_v3":
+        padded = [i for i, v in c.op_flops_scale.items() if i > 0]
+        assert len(padded) == 30 and all(0.69 < c.op_flops_scale[i] < 0.84 for i in padded)
