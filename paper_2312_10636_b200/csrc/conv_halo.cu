@@ -192,6 +192,16 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
     const bool issuer = elect_one();
     int hs = 0, bs = 0, t = 0;
     uint32_t hph = 0, bph = 0;
+    // descriptor bases: a tap's A / B descriptor is the base plus a 16-byte-unit offset (the start
+    // field is addr >> 4 in 14 bits, smem < 256 KB, so the add never carries out of it)
+    const uint64_t b0 = umma_desc_sw128(sp.sB);
+    const uint32_t b_step = b_bytes >> 4, row_step = static_cast<uint32_t>(Wp) * 8u;
+    if (resident) {
+      // resident weights: each slot completed phase 0 once and is never re-armed, so the NKB waits
+      // happen once here instead of once per tap of every tile
+      for (int tap = 0; tap < NKB; ++tap) mbar_wait(&sp.bfull[tap], 0u);
+      tc_fence_after();
+    }
     for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++t) {
       const int acc = t & 1;
       mbar_wait(&sp.tempty[acc], ((t >> 1) & 1) ^ 1);
@@ -201,6 +211,52 @@ __global__ void __launch_bounds__(kConvTcThreads, 1)
         mbar_wait(&sp.hfull[hs], hph);
         tc_fence_after();
         const uint32_t hbase = smem_u32(sp.halo + hs * HB);
+        if (RB == 128 && resident) {
+          // resident weights: the nine taps unrolled with (r, s) compile-time, each descriptor one
+          // 64-bit add and no barrier between taps, so the issuing thread keeps the tensor pipe fed
+          // (scripts/native/mma_probe.cu: back-to-back M128 N64 K16 MMAs run at 48 cycles; the
+          // rolled loop's per-tap division, R2UR moves and barrier wait cost ~115 per MMA).  Layer1's
+          // 56x56x64 3x3: 440 -> 284 us at k=16 on 2 SMs.  (Unrolling the weight-ring case as well
+          // measured slower: 28x28x128 3x3 286 -> 349 us; it keeps the rolled loop below.)
+          const uint64_t a0 = desc_sw128_row(hbase);
+#pragma unroll
+          for (int tap = 0; tap < 9; ++tap) {
+            const int r = tap / 3, s = tap - r * 3;
+            const uint64_t bd = b0 + static_cast<uint64_t>(static_cast<uint32_t>(tap) * b_step);
+            const uint64_t ad = a0 + static_cast<uint64_t>(static_cast<uint32_t>(r) * row_step + s * 8u);
+            if (issuer) {
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk) umma_bf16(d, ad + 2 * kk, bd + 2 * kk, a.idesc, (cb | tap | kk) != 0);
+            }
+          }
+        } else if (RB == 32 && resident) {
+          // the s2d stem (4x4 taps over 32-byte rows), same unrolled issue: k-block r holds filter
+          // row r, its four 32-byte K slices are taps (r, 0..3)
+          const uint64_t a0 = umma_desc_kmajor(hbase, 16, 0);
+#pragma unroll
+          for (int tap = 0; tap < 4; ++tap) {
+            const uint64_t bd = b0 + static_cast<uint64_t>(static_cast<uint32_t>(tap) * b_step);
+            if (issuer) {
+#pragma unroll
+              for (int s = 0; s < 4; ++s)
+                umma_bf16(d, a0 + static_cast<uint64_t>((static_cast<uint32_t>(tap) * Wp + s) * 2u), bd + 2 * s,
+                          a.idesc, (tap | s) != 0);
+            }
+          }
+        } else if (RB == 64 && resident) {
+          // 32-channel 3x3 (64-byte rows): k-block kb holds taps 2kb and 2kb + 1, two K=16 MMAs each
+          const uint64_t a0 = umma_desc_kmajor(hbase, 32, 0);
+#pragma unroll
+          for (int t9 = 0; t9 < 9; ++t9) {
+            const int r = t9 / 3, s = t9 - r * 3, kb = t9 / 2, h = t9 & 1;
+            const uint64_t bd = b0 + static_cast<uint64_t>(static_cast<uint32_t>(kb) * b_step);
+            const uint64_t ad = a0 + static_cast<uint64_t>((static_cast<uint32_t>(r) * Wp + s) * 4u);
+            if (issuer) {
+#pragma unroll
+              for (int kk = 0; kk < 2; ++kk) umma_bf16(d, ad + 2 * kk, bd + 2 * (2 * h + kk), a.idesc, (t9 | kk) != 0);
+            }
+          }
+        } else
         for (int tap = 0; tap < NKB; ++tap) {
           const int slot = resident ? tap : bs;
           // resident slots completed phase 0 once and are never re-armed: parity-0 waits pass
